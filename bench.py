@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""bench.py — DialSort histogram + reconstruct throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one pass of the whole hot path: histogram ingestion with the
+CRN, sub-histogram merge, offset scan and projection of one batch of n synthetic keys
+(resident in HBM).  N=1 runs configs[1] (c2: n=10^7 uniform keys, U=65536); N>1 (torchrun,
+one rank per GPU, NCCL) shards those n keys evenly, reduce-scatters H over NVLink and
+projects each universe slice (strong scaling).  Rank 0 prints one JSON line.
+
+Timing: W untimed warm-up steps, then K steps between a barrier + synchronize on both
+sides, CUDA events on the launching stream, max over ranks.  L2 hygiene: every step reads
+a different input copy from a rotation whose footprint exceeds 3x the 126 MB L2 (and writes
+a different output), so no step's 40 MB input is L2-resident.  `e2e` is the same metric
+through the C-ABI host-buffer call (pinned H2D copy + sort + D2H copy, every step).
+`--impl reference` times the CPU oracle (the only other place this file runs oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted keys/s (histogram+reconstruct) and % of HBM roofline, 1/2/4/8 B200"
+
+CONFIGS = {
+    "c1": dict(n=100_000, U=256, dist="uniform", desc="c1: n=1e5 uniform, U=256"),
+    "c2": dict(n=10_000_000, U=65536, dist="uniform", desc="c2: n=1e7 uniform, U=65536"),
+    "c3-zipf": dict(n=10_000_000, U=65536, dist="zipf", desc="c3: n=1e7 Zipf(1.2) permuted, U=65536"),
+    "c3-sorted": dict(n=10_000_000, U=65536, dist="sorted", desc="c3: n=1e7 sorted, U=65536"),
+    "c3-reverse": dict(n=10_000_000, U=65536, dist="reverse", desc="c3: n=1e7 reverse-sorted, U=65536"),
+    "c3-hot1": dict(n=10_000_000, U=65536, dist="hot1", desc="c3: n=1e7 uniform + 1% hot key, U=65536"),
+    "c4": dict(n=1_000_000_000, U=1 << 20, dist="uniform", desc="c4: n=1e9 uniform, U=2^20"),
+    "c5": dict(n=100_000_000, U=0, dist="int32", desc="c5: n=1e8 full-range int32, radix"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML SM clock + throttle-reason sampler (runs during the timed region)."""
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_host_input(cfg, seed):
+    import synth
+    if cfg["dist"] == "int32":
+        return synth.full_int32(cfg["n"], seed)
+    return synth.make(cfg["dist"], cfg["n"], cfg["U"], seed)
+
+
+def make_device_input(cfg, seed, dev, lo=0, count=None):
+    import torch
+    import synth
+    n = cfg["n"] if count is None else count
+    if cfg["dist"] == "uniform":
+        return synth.device_uniform(n, cfg["U"], seed, lo=lo, device=dev)
+    if cfg["dist"] == "int32":
+        return synth.device_full_int32(n, seed, lo=lo, device=dev)
+    h = make_host_input(cfg, seed)[lo:lo + n]
+    return torch.from_numpy(h).to(dev)
+
+
+def alg_bytes(cfg, G=1):
+    """Algorithmic HBM bytes of one step, all ranks: 8n + 8U at G=1,
+    Σ_g (8n/G + 8U + 8U/G) at G>1; radix 36n."""
+    n, U = cfg["n"], cfg["U"]
+    if cfg["dist"] == "int32":
+        return 36 * n
+    if G == 1:
+        return 8 * n + 8 * U
+    return G * (8 * n // G + 8 * U + 8 * U // G)
+
+
+def run_reference(args, cfg):
+    """The CPU oracle as it stands, one thread, on this host: each step = one bounded sample."""
+    import numpy as np
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    x = make_host_input(cfg, args.seed)
+    # bounded sample: at most 10^7 keys per step (c4 would take minutes per step)
+    m = min(cfg["n"], 10_000_000)
+    sample = x[:m]
+    fn = (lambda: oracle.radix_sort_i32(sample)) if cfg["dist"] == "int32" else (lambda: oracle.sort(sample, cfg["U"]))
+    for _ in range(args.warmup):
+        fn()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    sec = sum(ts) / len(ts)
+    v = m / sec
+    line = {
+        "metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": cfg["desc"], "n": cfg["n"], "U": cfg["U"], "dist": cfg["dist"], "seed": args.seed},
+        "cpu_baseline": {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {m} keys of the {args.config} input per step, oracle/oracle.c single thread"},
+        "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, seed, budget_s=10.0):
+    """Oracle timed on the host: full config input (or a 10^7-key sample), ~budget_s of work."""
+    import oracle
+    x = make_host_input(cfg, seed) if cfg["n"] <= 100_000_000 else None
+    m = min(cfg["n"], 10_000_000)
+    if x is None:
+        import synth
+        x = synth.uniform(m, cfg["U"], seed)
+    sample = x[:m]
+    fn = (lambda: oracle.radix_sort_i32(sample)) if cfg["dist"] == "int32" else (lambda: oracle.sort(sample, cfg["U"]))
+    fn()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        fn()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or reps >= 200:
+            break
+    return {"value": m * reps / el, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} x oracle sort of the first {m} keys of the {cfg['desc']} input ({el:.1f} s, 1 thread)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=20260321)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2605_16667_b200 as dsl
+    from paper_2605_16667_b200.sharded import sharded_sort
+
+    n, U = cfg["n"], cfg["U"]
+    radix = cfg["dist"] == "int32"
+    G = world
+    if G > 1 and (radix or U % G):
+        raise SystemExit("multi-GPU bench supports the bounded-universe configs with U % G == 0")
+    lo, hi = rank * n // G, (rank + 1) * n // G
+    n_loc = hi - lo
+    ctx = dsl.Context(local, max_n=n_loc, max_U=max(U, 256))
+
+    # ---- inputs: rotation of R copies so that no step's input is L2-resident ------------
+    L2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    step_bytes = 8 * n_loc + 8 * max(U, 1)
+    R = max(2, min(16, -(-3 * L2 // step_bytes)))
+    if 8 * n_loc * R > 40 * (1 << 30):
+        R = 2
+    base = make_device_input(cfg, args.seed, dev, lo=lo, count=n_loc)
+    ins = [base] + [base.clone() for _ in range(R - 1)]
+    cap = n_loc if G == 1 else min(n, 2 * n_loc + (1 << 20))
+    outs = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(R)]
+    torch.cuda.synchronize()
+
+    def step(i):
+        j = i % R
+        if radix:
+            ctx.sort_int32(ins[j], out=outs[j])
+        elif G == 1:
+            ctx.sort(ins[j], U, out=outs[j])
+        else:
+            sharded_sort(ins[j], U, capacity=cap, ctx=ctx, out=outs[j])
+
+    # ---- correctness gate before timing (bit-exact vs oracle at N=1) -----------------------
+    verified = None
+    step(0)
+    ctx.sync()
+    if G == 1 and n <= 100_000_000:
+        import oracle
+        xh = make_host_input(cfg, args.seed)
+        ref = oracle.radix_sort_i32(xh) if radix else oracle.sort(xh, U)
+        verified = bool(np.array_equal(outs[0][:n].cpu().numpy(), ref))
+        if not verified:
+            raise SystemExit("bench: GPU output differs from the oracle")
+
+    # ---- warm-up + timed region ------------------------------------------------------------
+    stream = torch.cuda.current_stream(dev)
+    for i in range(args.warmup):
+        step(i)
+    ctx.sync()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ctx.sync()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if G > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n / (ms_step * 1e-3)
+    if radix:
+        launches_per_step = 6
+    elif G == 1:
+        launches_per_step = 3 if U <= 98304 else 4
+    else:
+        launches_per_step = (3 if U <= 98304 else 4) + 2 - 1  # hist(+reduce) then scan+expand
+    peak, peak_kind = load_peaks()
+
+    # ---- per-kernel live timing (separate pass: event pairs disable the PDL overlap) -------
+    ctx.profile(True)
+    prof_steps = min(args.steps, 200)
+    for i in range(prof_steps):
+        step(i)
+    torch.cuda.synchronize()
+    ctx.profile(False)
+    recs = ctx.profile_read()
+    per = {}
+    for name, t in recs:
+        per.setdefault(name, []).append(t)
+    kern_avg = {k: sum(v) / len(v) for k, v in per.items()}
+    kern_share = {k: sum(v) for k, v in per.items()}
+    tot = sum(kern_share.values()) or 1.0
+    dom = max(kern_share, key=kern_share.get) if kern_share else None
+    # algorithmic bytes per launch of each kernel
+    kb = {
+        "k_hist_smem32": 4 * n_loc, "k_hist_smem16": 4 * n_loc, "k_hist_global": 4 * n_loc,
+        "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_reduce_scan": 8 * max(U // G, 1),
+        "k_radix_pass": 8 * n_loc, "k_radix_hist4": 4 * n_loc, "k_zero": 4 * U,
+    }
+    roof = None
+    if dom:
+        ach = kb.get(dom, 0) / (kern_avg[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "alg_bytes_per_launch": kb.get(dom, 0), "avg_ms": kern_avg[dom],
+                "share_of_step": kern_share[dom] / tot,
+                "kernels_ms": {k: round(v, 5) for k, v in kern_avg.items()}}
+    step_alg = alg_bytes(cfg, G)
+    step_roof = {"alg_bytes": step_alg, "achieved_gbs": step_alg / (ms_step * 1e-3) / 1e9,
+                 "frac_of_measured": step_alg / (ms_step * 1e-3) / 1e9 / peak,
+                 "frac_of_8tbs": step_alg / (ms_step * 1e-3) / 1e9 / 8000.0}
+
+    # ---- e2e: host buffers through the C ABI ----------------------------------------------
+    e2e = None
+    if not args.no_e2e and G == 1:
+        xh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        xh.copy_(ins[0][:n].cpu())
+        oh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        for _ in range(3):
+            ctx.sort_host(xh, U, oh)
+        k2 = max(3, min(args.steps, 50))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k2):
+            ctx.sort_host(xh, U, oh)
+        b.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / k2
+        dev_ms = a.elapsed_time(b) / k2
+        e2e = {"value": n / max(wall, dev_ms * 1e-3), "unit": "keys/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 4 * n, "ms_per_step": max(wall * 1e3, dev_ms), "api": "dialsort_sort_host"}
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.seed)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": n, "U": U, "dist": cfg["dist"], "seed": args.seed,
+                       "parallelism": f"dp{G}: keys sharded, H reduce-scatter (NCCL), per-slice projection"
+                       if G > 1 else "single GPU",
+                       "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)"},
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

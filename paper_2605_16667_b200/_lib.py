@@ -1,0 +1,75 @@
+"""ctypes loader for libdialsort.so (the C ABI declared in include/dialsort.h).
+
+Argument marshalling only: every step of the method runs in the CUDA kernels behind the
+C ABI.  There is no fallback: if the shared library is missing or fails to load, importing
+this module raises, so a GPU run can never silently use another implementation.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_DIR, "libdialsort.so")
+
+# dialsort_status
+OK, E_INVALID_ARG, E_KEY_RANGE, E_SIZE, E_OVERFLOW, E_CUDA, E_NOMEM = 0, 1, 2, 3, 4, 5, 7
+
+EXPORTS = (
+    "dialsort_status_string", "dialsort_last_error", "dialsort_version",
+    "dialsort_ctx_create", "dialsort_ctx_destroy", "dialsort_sync",
+    "dialsort_histogram_async", "dialsort_reconstruct_async", "dialsort_sort_async",
+    "dialsort_sort_int32_async", "dialsort_histogram", "dialsort_reconstruct",
+    "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host",
+    "dialsort_range_count_async", "dialsort_crn_resolve_async",
+    "dialsort_profile_enable", "dialsort_profile_read", "dialsort_kernel_name",
+)
+
+
+class ErrorInfo(ctypes.Structure):
+    _fields_ = [
+        ("bad_count", ctypes.c_uint64),
+        ("first_bad_index", ctypes.c_uint64),
+        ("first_bad_key", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+        ("last_total", ctypes.c_uint64),
+    ]
+
+
+def load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the DialSort product path has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, u64, u32, i32, ci = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int
+    sig = {
+        "dialsort_status_string": ([ci], ctypes.c_char_p),
+        "dialsort_last_error": ([], ctypes.c_char_p),
+        "dialsort_version": ([], ci),
+        "dialsort_ctx_create": ([ci, u64, u32, ctypes.POINTER(P)], ci),
+        "dialsort_ctx_destroy": ([P], ci),
+        "dialsort_sync": ([P, P, ctypes.POINTER(ErrorInfo)], ci),
+        "dialsort_histogram_async": ([P, P, u64, u32, P, P], ci),
+        "dialsort_reconstruct_async": ([P, P, u32, i32, P, u64, ci, P, P], ci),
+        "dialsort_sort_async": ([P, P, u64, u32, P, P, P], ci),
+        "dialsort_sort_int32_async": ([P, P, u64, P, P], ci),
+        "dialsort_histogram": ([P, u64, u32, P], ci),
+        "dialsort_reconstruct": ([P, u32, P, u64], ci),
+        "dialsort_sort": ([P, u64, u32, P], ci),
+        "dialsort_sort_int32": ([P, u64, P], ci),
+        "dialsort_sort_host": ([P, P, u64, u32, P, P], ci),
+        "dialsort_range_count_async": ([P, P, u32, u32, u32, P, P], ci),
+        "dialsort_crn_resolve_async": ([P, P, P, u64, P, P, P], ci),
+        "dialsort_profile_enable": ([P, ci], ci),
+        "dialsort_profile_read": ([P, ci, P, P], ci),
+        "dialsort_kernel_name": ([ci], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = load()

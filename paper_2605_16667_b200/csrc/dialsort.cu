@@ -1,0 +1,640 @@
+// dialsort.cu — C ABI (include/dialsort.h) and launch logic of the B200 DialSort hot path.
+//
+// Host side only decides paths, sizes grids and enqueues kernels; every step of the method
+// runs in the kernels of ds_hist.cuh / ds_scan.cuh / ds_expand.cuh / ds_radix.cuh.
+// All launches use programmatic dependent launch (PDL) so each kernel's launch overlaps
+// its predecessor's tail; every kernel calls griddepcontrol.wait before touching its
+// inputs, which keeps stream order exact.
+#include "../../include/dialsort.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ds_common.cuh"
+#include "ds_expand.cuh"
+#include "ds_hist.cuh"
+#include "ds_radix.cuh"
+#include "ds_scan.cuh"
+
+using namespace ds;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define DS_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(DIALSORT_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+enum KernelId {
+  KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_REDUCE_SCAN, KID_EXPAND,
+  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_COUNT
+};
+const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
+                                             "k_reduce_scan", "k_expand", "k_radix_hist4", "k_radix_pass",
+                                             "k_range_count", "k_crn_resolve"};
+
+// Per-context launch profiler (off by default): an event pair around each launch.
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // 2 per record
+  std::vector<int> ids;
+  size_t used = 0;
+};
+thread_local Profiler* g_prof = nullptr;  // set by the API entry for the ctx in use
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  Profiler* P = g_prof;
+  if (P && P->on) {
+    if (2 * P->used + 2 > P->ev.size()) {
+      for (int i = 0; i < 512; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        P->ev.push_back(e);
+      }
+    }
+    cudaEventRecord(P->ev[2 * P->used], s);
+    cudaError_t r = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    cudaEventRecord(P->ev[2 * P->used + 1], s);
+    P->ids.push_back(kid);
+    P->used++;
+    return r;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
+
+// A device buffer that only grows (reallocation happens outside any timed region: the first
+// call with a larger size; callers size the context at create to avoid it).
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want, bool zero = false) {
+    if (want <= bytes && p) return DIALSORT_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    want = want < 256 ? 256 : want;
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DIALSORT_E_NOMEM, "cudaMalloc of " + std::to_string(want) + " bytes failed");
+    }
+    if (zero && cudaMemset(p, 0, want) != cudaSuccess) return fail(DIALSORT_E_CUDA, "cudaMemset failed");
+    bytes = want;
+    return DIALSORT_OK;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct dialsort_ctx_s {
+  int device = 0;
+  int nsm = 148;
+  uint32_t epoch = 0;
+  DBuf partials, P, lb_status, tfb, ws_total, ovfH, status, stage, Hglob, radix_tmp, radix_hist, radix_lb,
+      scratch64;
+  DevStatus* host_status = nullptr;  // pinned mirror
+  Profiler prof;
+};
+
+namespace {
+
+int ctx_init(dialsort_ctx c) {
+  DS_CUDA(cudaSetDevice(c->device));
+  cudaDeviceProp prop;
+  DS_CUDA(cudaGetDeviceProperties(&prop, c->device));
+  c->nsm = prop.multiProcessorCount;
+  int rc;
+  if ((rc = c->status.ensure(sizeof(DevStatus), true))) return rc;
+  DS_CUDA(cudaMallocHost(&c->host_status, sizeof(DevStatus)));
+  DevStatus clean = {};
+  clean.first_bad = ~0ull;
+  clean.ovf_epoch = ~0u;
+  DS_CUDA(cudaMemcpy(c->status.p, &clean, sizeof(clean), cudaMemcpyHostToDevice));
+  if ((rc = c->ws_total.ensure(64, true))) return rc;
+  if ((rc = c->scratch64.ensure(64, true))) return rc;
+  DS_CUDA(cudaFuncSetAttribute(k_hist_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(4 * round_up((kSmem16MaxBins + 1) / 2, 8))));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(4 * round_up(kSmem32MaxBins, 8))));
+  radix_configure();
+  return DIALSORT_OK;
+}
+
+// Bumps the call epoch (tags look-back statuses and the packed-overflow flag).  On wrap of
+// the 24-bit status tag the look-back array is cleared so a stale tag can never match.
+uint32_t next_epoch(dialsort_ctx c, cudaStream_t s) {
+  c->epoch = (c->epoch + 1) & 0xffffffu;
+  if (c->epoch == 0) {
+    if (c->lb_status.p) cudaMemsetAsync(c->lb_status.p, 0, c->lb_status.bytes, s);
+    c->epoch = 1;
+  }
+  // radix tags are (4*epoch + pass) mod 2^24: clear their array whenever those wrap
+  if ((c->epoch & 0x3fffffu) == 0 && c->radix_lb.p) cudaMemsetAsync(c->radix_lb.p, 0, c->radix_lb.bytes, s);
+  return c->epoch;
+}
+
+int check_keys_arg(const void* p, uint64_t n) {
+  if (n > 0xffffffffull) return fail(DIALSORT_E_INVALID_ARG, "n exceeds 2^32-1");
+  if (n > 0 && p == nullptr) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer with n > 0");
+  if (reinterpret_cast<uintptr_t>(p) & 3u) return fail(DIALSORT_E_INVALID_ARG, "pointer not 4-byte aligned");
+  return DIALSORT_OK;
+}
+int check_U(uint32_t U) {
+  if (U == 0 || U > 0x80000000u) return fail(DIALSORT_E_INVALID_ARG, "U must be in [1, 2^31]");
+  return DIALSORT_OK;
+}
+
+enum class HistPath { Smem32, Smem16, Global };
+HistPath choose_path(uint32_t U) {
+  if (U <= kSmem32MaxBins) return HistPath::Smem32;
+  if (U <= kSmem16MaxBins) return HistPath::Smem16;
+  return HistPath::Global;
+}
+
+struct HistPlan {
+  HistPath path;
+  uint32_t W = 0, ldw = 0, C = 0, threads = 0;
+  size_t smem = 0;
+};
+
+int plan_hist(dialsort_ctx c, uint64_t n, uint32_t U, HistPlan& hp) {
+  hp.path = choose_path(U);
+  if (hp.path == HistPath::Global) return DIALSORT_OK;
+  const bool pack = hp.path == HistPath::Smem16;
+  hp.W = pack ? (U + 1) / 2 : U;
+  hp.ldw = (uint32_t)round_up(hp.W, 8);
+  hp.smem = 4ull * hp.ldw;
+  hp.threads = pack ? 1024 : 512;
+  int occ = 1;
+  if (pack)
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_smem<true>, hp.threads, hp.smem));
+  else
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_smem<false>, hp.threads, hp.smem));
+  if (occ < 1) occ = 1;
+  const uint64_t n4 = n / 4 + 1;
+  const uint64_t per_cta_min = (uint64_t)hp.threads * kHistUnroll * 2;  // >= 2 unrolled rounds
+  uint64_t want = cdiv(n4, per_cta_min);
+  uint64_t cap = (uint64_t)c->nsm * occ;
+  hp.C = (uint32_t)(want < cap ? (want ? want : 1) : cap);
+  return DIALSORT_OK;
+}
+
+// Enqueue histogram ingestion; on return either (smem paths) partial rows are pending in
+// c->partials with plan hp, or (global path) Hdst holds H.
+int enqueue_ingest(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, const HistPlan& hp,
+                   uint32_t* Hdst, uint32_t epoch, cudaStream_t s) {
+  int rc;
+  DevStatus* st = c->status.as<DevStatus>();
+  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  if (hp.path == HistPath::Global) {
+    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, Hdst, (uint64_t)U));
+    uint64_t want = cdiv(n / 4 + 1, 256ull * kHistUnroll);
+    uint64_t cap = (uint64_t)c->nsm * 8;
+    uint32_t grid = (uint32_t)(want < cap ? (want ? want : 1) : cap);
+    DS_CUDA(launch_k(KID_HIST_GLOBAL, k_hist_global, dim3(grid), dim3(256), 0, s, keys, n, U, Hdst, st));
+    return DIALSORT_OK;
+  }
+  if ((rc = c->partials.ensure(4ull * hp.C * hp.ldw))) return rc;
+  if (hp.path == HistPath::Smem16)
+    DS_CUDA(launch_k(KID_HIST_SMEM16, k_hist_smem<true>, dim3(hp.C), dim3(hp.threads), hp.smem, s, keys, n, U, hp.W, hp.ldw,
+                   c->partials.as<uint32_t>(), c->ovfH.as<uint32_t>(), st, epoch));
+  else
+    DS_CUDA(launch_k(KID_HIST_SMEM32, k_hist_smem<false>, dim3(hp.C), dim3(hp.threads), hp.smem, s, keys, n, U, hp.W, hp.ldw,
+                   c->partials.as<uint32_t>(), c->ovfH.as<uint32_t>(), st, epoch));
+  return DIALSORT_OK;
+}
+
+// Enqueue merge (+ optional scan / projection).  For C == 0, Hsrc is read.
+int enqueue_reduce_scan(dialsort_ctx c, const HistPlan* hp, const uint32_t* Hsrc, uint32_t U,
+                        uint32_t* Hout, bool do_scan, uint64_t cap, bool exact, uint64_t* d_total,
+                        uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a = {};
+  const bool smem = hp && hp->path != HistPath::Global;
+  a.partials = smem ? c->partials.as<uint32_t>() : nullptr;
+  a.C = smem ? hp->C : 0;
+  a.ldw = smem ? hp->ldw : 0;
+  a.pack16 = smem && hp->path == HistPath::Smem16;
+  a.Hsrc = Hsrc;
+  a.ovfH = smem ? c->ovfH.as<uint32_t>() : nullptr;
+  a.ovfH_mut = a.ovfH ? c->ovfH.as<uint32_t>() : nullptr;
+  a.U = U;
+  a.Hout = Hout;
+  a.do_scan = do_scan;
+  const uint32_t bins_per_tile = a.pack16 ? 2 * kScanWords : kScanWords;
+  const uint32_t ntiles = (uint32_t)cdiv(U, bins_per_tile);
+  const uint64_t ntiles_out = cap ? cdiv(cap, kExpandTile) : 1;
+  if (do_scan) {
+    if ((rc = c->P.ensure(4ull * (U + 1)))) return rc;
+    if ((rc = c->lb_status.ensure(8ull * ntiles, true))) return rc;
+    if ((rc = c->tfb.ensure(4ull * ntiles_out))) return rc;
+  }
+  a.P = c->P.as<uint32_t>();
+  a.status = c->lb_status.as<uint64_t>();
+  a.tfb = c->tfb.as<uint32_t>();
+  a.T = kExpandTile;
+  a.ntiles_out = ntiles_out;
+  a.n_expected = cap;
+  a.exact = exact;
+  a.d_total = d_total;
+  a.ws_total = c->ws_total.as<uint64_t>();
+  a.st = c->status.as<DevStatus>();
+  a.epoch = epoch;
+  DS_CUDA(launch_k(KID_REDUCE_SCAN, k_reduce_scan, dim3(ntiles), dim3(kScanThreads), 0, s, a));
+  return DIALSORT_OK;
+}
+
+int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, int32_t* out, cudaStream_t s) {
+  if (cap == 0) return DIALSORT_OK;
+  const uint64_t ntiles_out = cdiv(cap, kExpandTile);
+  if (ntiles_out > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "output too large");
+  DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3((uint32_t)ntiles_out), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
+                 c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out));
+  return DIALSORT_OK;
+}
+
+// Host-side enqueue of DialSort-Radix: K7 once, then K8 for p = 0..3 ping-ponging tmp/out.
+int radix_enqueue(int nsm, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, DBuf& hist, DBuf& lb,
+                  uint32_t epoch, cudaStream_t s) {
+  const uint64_t ntiles = (n + kRadixTile - 1) / kRadixTile;
+  if (ntiles > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "n too large for radix");
+  int rc;
+  if ((rc = hist.ensure(4 * 1024 + 64))) return rc;
+  if ((rc = lb.ensure(8ull * ntiles * 256, true))) return rc;
+  uint32_t* gh = hist.as<uint32_t>();
+  uint32_t* ctrs = gh + 1024;
+  uint64_t* st = lb.as<uint64_t>();
+  cudaError_t e;
+  if ((e = launch_k(KID_ZERO, k_zero, dim3(1), dim3(256), 0, s, gh, (uint64_t)1024)) != cudaSuccess)
+    return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
+  uint64_t want = (n / 4 + 1 + 512 * 4 - 1) / (512 * 4);
+  uint32_t grid = (uint32_t)(want < (uint64_t)nsm * 2 ? want : (uint64_t)nsm * 2);
+  if ((e = launch_k(KID_RADIX_HIST4, k_radix_hist4, dim3(grid), dim3(512), 0, s, keys, n, gh, ctrs)) != cudaSuccess)
+    return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(keys);
+  uint32_t* bufs[2] = {reinterpret_cast<uint32_t*>(tmp), reinterpret_cast<uint32_t*>(out)};
+  for (int p = 0; p < 4; ++p) {
+    uint32_t* dst = bufs[p & 1];
+    const uint32_t tag = (epoch * 4u + (uint32_t)p) & 0xffffffu;
+    if ((e = launch_k(KID_RADIX_PASS, k_radix_pass, dim3((uint32_t)ntiles), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst, n, p,
+                    (const uint32_t*)gh, st, ctrs + p, tag)) != cudaSuccess)
+      return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
+    src = dst;
+  }
+  return DIALSORT_OK;
+}
+
+// Makes `c`'s profiler the active one for launches made by this thread during an API call.
+struct ProfScope {
+  Profiler* prev;
+  explicit ProfScope(dialsort_ctx c) : prev(g_prof) { g_prof = c ? &c->prof : nullptr; }
+  ~ProfScope() { g_prof = prev; }
+};
+
+std::mutex g_default_mu;
+std::map<int, dialsort_ctx> g_default;
+
+int default_ctx(dialsort_ctx* out) {
+  int dev = 0;
+  DS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_default_mu);
+  auto it = g_default.find(dev);
+  if (it != g_default.end()) {
+    *out = it->second;
+    return DIALSORT_OK;
+  }
+  dialsort_ctx c = nullptr;
+  int rc = dialsort_ctx_create(dev, 0, 0, &c);
+  if (rc) return rc;
+  g_default[dev] = c;
+  *out = c;
+  return DIALSORT_OK;
+}
+
+bool ranges_overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + nb && b0 < a0 + na;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dialsort_status_string(int s) {
+  switch (s) {
+    case DIALSORT_OK: return "ok";
+    case DIALSORT_E_INVALID_ARG: return "invalid argument";
+    case DIALSORT_E_KEY_RANGE: return "key outside [0,U)";
+    case DIALSORT_E_SIZE: return "size mismatch (sum(H) vs n)";
+    case DIALSORT_E_OVERFLOW: return "count overflow";
+    case DIALSORT_E_CUDA: return "CUDA error";
+    case DIALSORT_E_NOMEM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+const char* dialsort_last_error(void) { return g_last_error.c_str(); }
+int dialsort_version(void) { return 100; }
+
+int dialsort_ctx_create(int device, uint64_t max_n, uint32_t max_U, dialsort_ctx* out) {
+  if (!out) return fail(DIALSORT_E_INVALID_ARG, "out is NULL");
+  dialsort_ctx c = new dialsort_ctx_s();
+  c->device = device;
+  int rc = ctx_init(c);
+  if (!rc && max_U) {
+    HistPlan hp;
+    if (!(rc = plan_hist(c, max_n ? max_n : (1u << 20), max_U, hp)) && hp.path != HistPath::Global)
+      rc = c->partials.ensure(4ull * hp.C * hp.ldw);
+    if (!rc) rc = c->P.ensure(4ull * (max_U + 1));
+    if (!rc) rc = c->lb_status.ensure(8ull * cdiv(max_U, kScanWords) + 64, true);
+    if (!rc) rc = c->ovfH.ensure(4ull * max_U, true);
+  }
+  if (!rc && max_n) rc = c->tfb.ensure(4ull * (cdiv(max_n, kExpandTile) + 1));
+  if (rc) {
+    dialsort_ctx_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return DIALSORT_OK;
+}
+
+int dialsort_ctx_destroy(dialsort_ctx c) {
+  if (!c) return DIALSORT_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (DBuf* b : {&c->partials, &c->P, &c->lb_status, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hglob,
+                  &c->radix_tmp, &c->radix_hist, &c->radix_lb, &c->scratch64})
+    b->release();
+  if (c->host_status) cudaFreeHost(c->host_status);
+  for (cudaEvent_t e : c->prof.ev) cudaEventDestroy(e);
+  delete c;
+  return DIALSORT_OK;
+}
+
+int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info* info) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(cudaMemcpyAsync(c->host_status, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  DS_CUDA(cudaStreamSynchronize(s));
+  DevStatus h = *c->host_status;
+  DevStatus clean = {};
+  clean.first_bad = ~0ull;
+  clean.ovf_epoch = h.ovf_epoch;
+  clean.last_total = h.last_total;
+  if (h.bad_count || h.flags) DS_CUDA(cudaMemcpy(c->status.p, &clean, sizeof(clean), cudaMemcpyHostToDevice));
+  if (info) {
+    info->bad_count = h.bad_count;
+    info->first_bad_index = h.bad_count ? (h.first_bad >> 32) : ~0ull;
+    info->first_bad_key = h.bad_count ? (int32_t)(uint32_t)(h.first_bad & 0xffffffffu) : 0;
+    info->flags = h.flags;
+    info->last_total = h.last_total;
+  }
+  if (h.bad_count) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%llu key(s) outside [0,U); first at index %llu (key %d)",
+             (unsigned long long)h.bad_count, (unsigned long long)(h.first_bad >> 32),
+             (int32_t)(uint32_t)(h.first_bad & 0xffffffffu));
+    return fail(DIALSORT_E_KEY_RANGE, buf);
+  }
+  if (h.flags & FLAG_OVERFLOW) return fail(DIALSORT_E_OVERFLOW, "sum(H) >= 2^32");
+  if (h.flags & FLAG_SIZE)
+    return fail(DIALSORT_E_SIZE, "sum(H) = " + std::to_string(h.last_total) + " does not match n / capacity");
+  return DIALSORT_OK;
+}
+
+int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H,
+                             dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
+  if (!H) return fail(DIALSORT_E_INVALID_ARG, "H is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c, s);
+  if (n == 0) {
+    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
+    return DIALSORT_OK;
+  }
+  HistPlan hp;
+  if ((rc = plan_hist(c, n, U, hp))) return rc;
+  if ((rc = enqueue_ingest(c, keys, n, U, hp, H, epoch, s))) return rc;
+  if (hp.path != HistPath::Global)
+    if ((rc = enqueue_reduce_scan(c, &hp, nullptr, U, H, false, 0, false, nullptr, epoch, s))) return rc;
+  return DIALSORT_OK;
+}
+
+int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int32_t key_base, int32_t* out,
+                               uint64_t cap, int exact, uint64_t* d_total, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(out, cap))) return rc;
+  if (!H) return fail(DIALSORT_E_INVALID_ARG, "H is NULL");
+  if ((int64_t)key_base + (int64_t)U - 1 > 0x7fffffffll)
+    return fail(DIALSORT_E_INVALID_ARG, "key_base + U - 1 exceeds INT32_MAX");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c, s);
+  if ((rc = enqueue_reduce_scan(c, nullptr, H, U, nullptr, true, cap, exact != 0, d_total, epoch, s))) return rc;
+  return enqueue_expand(c, U, cap, key_base, out, s);
+}
+
+int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, int32_t* out, uint32_t* H_out,
+                        dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(out, n))) return rc;
+  if (n && out != keys && ranges_overlap(keys, 4 * n, out, 4 * n))
+    return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c, s);
+  if (n == 0) {
+    if (H_out) DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H_out, (uint64_t)U));
+    return DIALSORT_OK;
+  }
+  HistPlan hp;
+  if ((rc = plan_hist(c, n, U, hp))) return rc;
+  uint32_t* Hg = nullptr;
+  if (hp.path == HistPath::Global) {
+    if (H_out) {
+      Hg = H_out;
+    } else {
+      if ((rc = c->Hglob.ensure(4ull * U))) return rc;
+      Hg = c->Hglob.as<uint32_t>();
+    }
+  }
+  if ((rc = enqueue_ingest(c, keys, n, U, hp, Hg, epoch, s))) return rc;
+  if (hp.path == HistPath::Global) {
+    if ((rc = enqueue_reduce_scan(c, nullptr, Hg, U, nullptr, true, n, true, nullptr, epoch, s))) return rc;
+  } else {
+    if ((rc = enqueue_reduce_scan(c, &hp, nullptr, U, H_out, true, n, true, nullptr, epoch, s))) return rc;
+  }
+  return enqueue_expand(c, U, n, 0, out, s);
+}
+
+int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(out, n))) return rc;
+  if (n && out != keys && ranges_overlap(keys, 4 * n, out, 4 * n))
+    return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c, s);
+  if (n == 0) return DIALSORT_OK;
+  if ((rc = c->radix_tmp.ensure(4ull * n + 16))) return rc;
+  return radix_enqueue(c->nsm, keys, n, out, c->radix_tmp.as<int32_t>(), c->radix_hist, c->radix_lb, epoch, s);
+}
+
+int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, uint32_t a, uint32_t b,
+                               uint64_t* d_result, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U))) return rc;
+  if (!H || !d_result) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
+  if (a > b || b >= U) return fail(DIALSORT_E_INVALID_ARG, "need 0 <= a <= b < U");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(1), dim3(32), 0, s, reinterpret_cast<uint32_t*>(d_result), (uint64_t)2));
+  uint64_t len = (uint64_t)b - a + 1;
+  uint32_t grid = (uint32_t)(cdiv(len, 1024) < (uint64_t)c->nsm * 4 ? cdiv(len, 1024) : (uint64_t)c->nsm * 4);
+  DS_CUDA(launch_k(KID_RANGE_COUNT, k_range_count, dim3(grid), dim3(256), 0, s, H, a, b,
+                 reinterpret_cast<unsigned long long*>(d_result)));
+  return DIALSORT_OK;
+}
+
+int dialsort_profile_enable(dialsort_ctx c, int enable) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  c->prof.on = enable != 0;
+  return DIALSORT_OK;
+}
+
+int dialsort_profile_read(dialsort_ctx c, int max, int* ids, float* ms) {
+  if (!c) return -fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  int n = 0;
+  for (size_t i = 0; i < c->prof.used && n < max; ++i, ++n) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->prof.ev[2 * i], c->prof.ev[2 * i + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      t = -1.f;
+    }
+    if (ids) ids[n] = c->prof.ids[i];
+    if (ms) ms[n] = t;
+  }
+  c->prof.used = 0;
+  c->prof.ids.clear();
+  return n;
+}
+
+const char* dialsort_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kKernelNames[id] : "?"; }
+
+int dialsort_crn_resolve_async(dialsort_ctx c, const int32_t* lane_keys, const uint32_t* active, uint64_t n_batches,
+                               int32_t* out_keys, uint32_t* out_counts, dialsort_stream_t stream) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if (n_batches == 0) return DIALSORT_OK;
+  if (!lane_keys || !active || !out_keys || !out_counts) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  uint64_t grid = cdiv(n_batches * 32, 256);
+  if (grid > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "too many batches");
+  DS_CUDA(launch_k(KID_CRN, k_crn_resolve, dim3((uint32_t)grid), dim3(256), 0, s, lane_keys, active, n_batches, out_keys,
+                 out_counts));
+  return DIALSORT_OK;
+}
+
+// ---- synchronous forms ----------------------------------------------------------------------
+int dialsort_histogram(const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H) {
+  dialsort_ctx c;
+  int rc = default_ctx(&c);
+  if (rc) return rc;
+  if ((rc = dialsort_histogram_async(c, keys, n, U, H, nullptr))) return rc;
+  return dialsort_sync(c, nullptr, nullptr);
+}
+int dialsort_reconstruct(const uint32_t* H, uint32_t U, int32_t* out, uint64_t n) {
+  dialsort_ctx c;
+  int rc = default_ctx(&c);
+  if (rc) return rc;
+  if ((rc = dialsort_reconstruct_async(c, H, U, 0, out, n, 1, nullptr, nullptr))) return rc;
+  return dialsort_sync(c, nullptr, nullptr);
+}
+int dialsort_sort(const int32_t* keys, uint64_t n, uint32_t U, int32_t* out) {
+  dialsort_ctx c;
+  int rc = default_ctx(&c);
+  if (rc) return rc;
+  if ((rc = dialsort_sort_async(c, keys, n, U, out, nullptr, nullptr))) return rc;
+  return dialsort_sync(c, nullptr, nullptr);
+}
+int dialsort_sort_int32(const int32_t* keys, uint64_t n, int32_t* out) {
+  dialsort_ctx c;
+  int rc = default_ctx(&c);
+  if (rc) return rc;
+  if ((rc = dialsort_sort_int32_async(c, keys, n, out, nullptr))) return rc;
+  return dialsort_sync(c, nullptr, nullptr);
+}
+
+int dialsort_sort_host(dialsort_ctx c, const int32_t* keys_host, uint64_t n, uint32_t U, int32_t* out_host,
+                       dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(keys_host, n)) || (rc = check_keys_arg(out_host, n))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  if (n == 0) return DIALSORT_OK;
+  if ((rc = c->stage.ensure(4ull * n + 16))) return rc;
+  int32_t* d = c->stage.as<int32_t>();
+  DS_CUDA(cudaMemcpyAsync(d, keys_host, 4ull * n, cudaMemcpyHostToDevice, s));
+  if (U == 0)
+    rc = dialsort_sort_int32_async(c, d, n, d, stream);
+  else
+    rc = dialsort_sort_async(c, d, n, U, d, nullptr, stream);
+  if (rc) return rc;
+  DS_CUDA(cudaMemcpyAsync(out_host, d, 4ull * n, cudaMemcpyDeviceToHost, s));
+  return dialsort_sync(c, stream, nullptr);
+}
+
+}  // extern "C"

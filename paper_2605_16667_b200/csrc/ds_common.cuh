@@ -1,0 +1,159 @@
+// ds_common.cuh — shared device helpers of the DialSort CUDA path (sm_100a only).
+// Nothing here is shared with oracle/ (the two are independent by construction).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef __CUDACC__
+#error "CUDA only"
+#endif
+
+namespace ds {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+// Deferred device error state of one context (dialsort_sync reads and clears it).
+struct DevStatus {
+  unsigned long long bad_count;   // keys outside [0,U)
+  unsigned long long first_bad;   // min over bad keys of (index << 32) | (uint32)key
+  unsigned long long last_total;  // ΣH of the most recent scan
+  unsigned int flags;             // bit0 size error, bit1 overflow
+  unsigned int ovf_epoch;         // epoch of the last call whose packed-u16 histogram overflowed
+};
+constexpr unsigned FLAG_SIZE = 1u, FLAG_OVERFLOW = 2u;
+
+__device__ __forceinline__ void record_bad(DevStatus* st, uint64_t idx, uint32_t key) {
+  atomicAdd(&st->bad_count, 1ull);
+  atomicMin(&st->first_bad, (unsigned long long)((idx << 32) | (uint64_t)key));
+}
+
+// Programmatic dependent launch (PDL): wait for the producer grid / let dependents launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Streaming 128-bit loads/stores (keys are read once; outputs written once).
+__device__ __forceinline__ int4 ld_stream4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream4(int4* p, int4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+
+// Fire-and-forget global add (RED.ADD.U32 in SASS).
+__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- the warp CRN (def:crn_level P:896-915, lem:crn P:951-962) ----------------------------
+// Multiset reading R1: the active lanes `mask` are grouped by equal key with one
+// equality-only instruction (MATCH.ANY); the lowest lane of each group is its leader and
+// carries the group's total count.  Returns the group mask of the calling lane.
+// Must be called by exactly the lanes in `mask`.
+__device__ __forceinline__ uint32_t crn_group(uint32_t mask, uint32_t key) {
+  return __match_any_sync(mask, key);
+}
+__device__ __forceinline__ bool crn_is_leader(uint32_t group) {
+  return (threadIdx.x & 31) == (uint32_t)(__ffs(group) - 1);
+}
+
+// Block-wide reductions / scans (blockDim multiple of 32, <= 1024).
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red /* >= 32 slots */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T r = lane < nw ? red[lane] : T(0);
+  r = warp_sum(r);
+  return r;
+}
+
+// Inclusive warp scan.
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Exclusive block scan; returns the exclusive prefix of the calling thread and the block total.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T& total, T* red /* >= 33 slots */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T inc = warp_incl_scan(v);
+  __syncthreads();
+  if (lane == 31) red[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < nw ? red[lane] : T(0);
+    T wi = warp_incl_scan(w);
+    red[lane] = wi - w;  // exclusive warp offsets
+    if (lane == 31) red[32] = wi;
+  }
+  __syncthreads();
+  total = red[32];
+  return red[warp] + inc - v;
+}
+
+// Decoupled look-back tile status: [epoch:24 | flag:2 | value:38].
+constexpr uint64_t LB_VALUE_BITS = 38;
+constexpr uint64_t LB_VALUE_MASK = (1ull << LB_VALUE_BITS) - 1;
+constexpr uint64_t LB_FLAG_AGG = 1, LB_FLAG_INC = 2;
+__device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint64_t flag, uint64_t value) {
+  value = value > LB_VALUE_MASK ? LB_VALUE_MASK : value;
+  return ((uint64_t)(epoch & 0xffffffu) << 40) | (flag << LB_VALUE_BITS) | value;
+}
+__device__ __forceinline__ void lb_store(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_load(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Warp-cooperative look-back for tile `tile` (> 0), called by all 32 lanes of one warp.
+// Returns the exclusive prefix of the tile (sum of all preceding tile aggregates).
+__device__ __forceinline__ uint64_t lookback(const uint64_t* status, uint32_t tile, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;  // newest predecessor not yet consumed
+  const uint32_t ep = epoch & 0xffffffu;
+  while (base >= 0) {
+    int64_t t = base - lane;  // lane 0 = nearest predecessor
+    uint64_t s = 0;
+    uint32_t flag = LB_FLAG_INC;  // lanes past tile 0 behave like an inclusive 0
+    if (t >= 0) {
+      do {
+        s = lb_load(status + t);
+        flag = ((uint32_t)(s >> 40) == ep) ? (uint32_t)((s >> LB_VALUE_BITS) & 3) : 0u;
+      } while (flag == 0);
+    }
+    uint64_t val = (t >= 0) ? (s & LB_VALUE_MASK) : 0;
+    uint32_t inc_mask = __ballot_sync(FULL, flag == LB_FLAG_INC);
+    int first_inc = __ffs(inc_mask) - 1;  // nearest predecessor with an inclusive prefix
+    uint64_t contrib = (inc_mask == 0 || lane <= first_inc) ? val : 0;
+    excl += warp_sum(contrib);
+    if (inc_mask) break;
+    base -= 32;
+  }
+  return excl;
+}
+
+}  // namespace ds
