@@ -295,9 +295,9 @@ def main():
     if radix:
         launches_per_step = 6
     elif G == 1:
-        launches_per_step = 3 if U <= 98304 else 4
+        launches_per_step = 2 if U <= 98304 else 4           # fused hist+merge+scan, expand
     else:
-        launches_per_step = (3 if U <= 98304 else 4) + 2 - 1  # hist(+reduce) then scan+expand
+        launches_per_step = (1 if U <= 98304 else 2) + 2     # local hist; scan + expand
     peak, peak_kind = load_peaks()
 
     # ---- per-kernel live timing (separate pass: event pairs disable the PDL overlap) -------
@@ -318,7 +318,7 @@ def main():
     # algorithmic bytes per launch of each kernel
     kb = {
         "k_hist_smem32": 4 * n_loc, "k_hist_smem16": 4 * n_loc, "k_hist_global": 4 * n_loc,
-        "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_reduce_scan": 8 * max(U // G, 1),
+        "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),
         "k_radix_pass": 8 * n_loc, "k_radix_hist4": 4 * n_loc, "k_zero": 4 * U,
     }
     roof = None

@@ -129,6 +129,10 @@ int dialsort_profile_enable(dialsort_ctx ctx, int enable);
  * the last read into the host arrays; returns the record count (or -status on error). */
 int dialsort_profile_read(dialsort_ctx ctx, int max, int* kernel_ids, float* ms);
 const char* dialsort_kernel_name(int kernel_id);
+/* Debug: with DIALSORT_PHASE_TIMING=1 in the environment at context creation, the fused
+ * histogram kernel records %globaltimer phase stamps (max over CTAs); this copies the 8
+ * phase times in ns relative to the earliest CTA start into out8 (host) and resets them. */
+int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out8);
 
 /* ---- test entry: the warp CRN primitive on explicit lane batches ---------------------- */
 /* lane_keys: int32[32*n_batches]; active: uint32[n_batches] lane masks.  For each batch, the

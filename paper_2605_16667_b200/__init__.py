@@ -161,6 +161,13 @@ class Context:
             _check(-n)
         return [(_L.dialsort_kernel_name(int(i)).decode(), float(t)) for i, t in zip(ids[:n], ms[:n])]
 
+    def debug_phase_ns(self):
+        """Phase stamps of the fused kernel (DIALSORT_PHASE_TIMING=1), ns from the first CTA start."""
+        import numpy as np
+        out = np.zeros(8, dtype=np.uint64)
+        _check(_L.dialsort_debug_phase_ns(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out.tolist()
+
     def crn_resolve(self, lane_keys: torch.Tensor, active: torch.Tensor):
         """Warp CRN test entry: (leader keys, leader counts) per 32-lane batch."""
         nb = active.numel()

@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -41,11 +43,11 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum KernelId {
-  KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_REDUCE_SCAN, KID_EXPAND,
+  KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND,
   KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
-                                             "k_reduce_scan", "k_expand", "k_radix_hist4", "k_radix_pass",
+                                             "k_scan", "k_expand", "k_radix_hist4", "k_radix_pass",
                                              "k_range_count", "k_crn_resolve"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
@@ -89,6 +91,8 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+constexpr size_t kSmemBudget = 227 * 1024 - 1024;  // dynamic smem per CTA (static smem aside)
+
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
 
@@ -126,10 +130,11 @@ struct dialsort_ctx_s {
   int device = 0;
   int nsm = 148;
   uint32_t epoch = 0;
-  DBuf partials, P, lb_status, tfb, ws_total, ovfH, status, stage, Hglob, radix_tmp, radix_hist, radix_lb,
-      scratch64;
+  DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, radix_tmp, radix_hist, radix_lb;
   DevStatus* host_status = nullptr;  // pinned mirror
   Profiler prof;
+  int expand_occ = 4, scan_occ = 2;
+  PhaseTimes* pt = nullptr;  // debug phase timing (DIALSORT_PHASE_TIMING=1)
 };
 
 namespace {
@@ -147,23 +152,30 @@ int ctx_init(dialsort_ctx c) {
   clean.ovf_epoch = ~0u;
   DS_CUDA(cudaMemcpy(c->status.p, &clean, sizeof(clean), cudaMemcpyHostToDevice));
   if ((rc = c->ws_total.ensure(64, true))) return rc;
-  if ((rc = c->scratch64.ensure(64, true))) return rc;
-  DS_CUDA(cudaFuncSetAttribute(k_hist_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(4 * round_up((kSmem16MaxBins + 1) / 2, 8))));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(4 * round_up(kSmem32MaxBins, 8))));
+  if ((rc = c->gridbar.ensure(64, true))) return rc;
+  if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
+  int occ = 0;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kExpandThreads, 0));
+  c->expand_occ = occ > 0 ? occ : 1;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan, kTileBins, 0));
+  c->scan_occ = occ > 0 ? (occ > 4 ? 4 : occ) : 1;
+  const char* e = getenv("DIALSORT_PHASE_TIMING");
+  if (e && e[0] == '1') {
+    DS_CUDA(cudaMalloc(&c->pt, sizeof(PhaseTimes)));
+    PhaseTimes init = {};
+    init.start_min = ~0ull;
+    DS_CUDA(cudaMemcpy(c->pt, &init, sizeof(init), cudaMemcpyHostToDevice));
+  }
   return DIALSORT_OK;
 }
 
-// Bumps the call epoch (tags look-back statuses and the packed-overflow flag).  On wrap of
-// the 24-bit status tag the look-back array is cleared so a stale tag can never match.
+// Bumps the call epoch (tags the packed-overflow flag and the radix look-back statuses).
 uint32_t next_epoch(dialsort_ctx c, cudaStream_t s) {
   c->epoch = (c->epoch + 1) & 0xffffffu;
-  if (c->epoch == 0) {
-    if (c->lb_status.p) cudaMemsetAsync(c->lb_status.p, 0, c->lb_status.bytes, s);
-    c->epoch = 1;
-  }
+  if (c->epoch == 0) c->epoch = 1;
   // radix tags are (4*epoch + pass) mod 2^24: clear their array whenever those wrap
   if ((c->epoch & 0x3fffffu) == 0 && c->radix_lb.p) cudaMemsetAsync(c->radix_lb.p, 0, c->radix_lb.bytes, s);
   return c->epoch;
@@ -187,86 +199,19 @@ HistPath choose_path(uint32_t U) {
   return HistPath::Global;
 }
 
-struct HistPlan {
-  HistPath path;
-  uint32_t W = 0, ldw = 0, C = 0, threads = 0;
-  size_t smem = 0;
-};
-
-int plan_hist(dialsort_ctx c, uint64_t n, uint32_t U, HistPlan& hp) {
-  hp.path = choose_path(U);
-  if (hp.path == HistPath::Global) return DIALSORT_OK;
-  const bool pack = hp.path == HistPath::Smem16;
-  hp.W = pack ? (U + 1) / 2 : U;
-  hp.ldw = (uint32_t)round_up(hp.W, 8);
-  hp.smem = 4ull * hp.ldw;
-  hp.threads = pack ? 1024 : 512;
-  int occ = 1;
-  if (pack)
-    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_smem<true>, hp.threads, hp.smem));
-  else
-    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_smem<false>, hp.threads, hp.smem));
-  if (occ < 1) occ = 1;
-  const uint64_t n4 = n / 4 + 1;
-  const uint64_t per_cta_min = (uint64_t)hp.threads * kHistUnroll * 2;  // >= 2 unrolled rounds
-  uint64_t want = cdiv(n4, per_cta_min);
-  uint64_t cap = (uint64_t)c->nsm * occ;
-  hp.C = (uint32_t)(want < cap ? (want ? want : 1) : cap);
-  return DIALSORT_OK;
-}
-
-// Enqueue histogram ingestion; on return either (smem paths) partial rows are pending in
-// c->partials with plan hp, or (global path) Hdst holds H.
-int enqueue_ingest(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, const HistPlan& hp,
-                   uint32_t* Hdst, uint32_t epoch, cudaStream_t s) {
+// Common scan arguments (workspace pointers, output tiling, size check).
+int fill_scan_args(dialsort_ctx c, ScanArgs& a, uint32_t U, bool do_scan, uint64_t cap, bool exact, uint64_t* d_total,
+                   uint32_t epoch) {
   int rc;
-  DevStatus* st = c->status.as<DevStatus>();
-  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
-  if (hp.path == HistPath::Global) {
-    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, Hdst, (uint64_t)U));
-    uint64_t want = cdiv(n / 4 + 1, 256ull * kHistUnroll);
-    uint64_t cap = (uint64_t)c->nsm * 8;
-    uint32_t grid = (uint32_t)(want < cap ? (want ? want : 1) : cap);
-    DS_CUDA(launch_k(KID_HIST_GLOBAL, k_hist_global, dim3(grid), dim3(256), 0, s, keys, n, U, Hdst, st));
-    return DIALSORT_OK;
-  }
-  if ((rc = c->partials.ensure(4ull * hp.C * hp.ldw))) return rc;
-  if (hp.path == HistPath::Smem16)
-    DS_CUDA(launch_k(KID_HIST_SMEM16, k_hist_smem<true>, dim3(hp.C), dim3(hp.threads), hp.smem, s, keys, n, U, hp.W, hp.ldw,
-                   c->partials.as<uint32_t>(), c->ovfH.as<uint32_t>(), st, epoch));
-  else
-    DS_CUDA(launch_k(KID_HIST_SMEM32, k_hist_smem<false>, dim3(hp.C), dim3(hp.threads), hp.smem, s, keys, n, U, hp.W, hp.ldw,
-                   c->partials.as<uint32_t>(), c->ovfH.as<uint32_t>(), st, epoch));
-  return DIALSORT_OK;
-}
-
-// Enqueue merge (+ optional scan / projection).  For C == 0, Hsrc is read.
-int enqueue_reduce_scan(dialsort_ctx c, const HistPlan* hp, const uint32_t* Hsrc, uint32_t U,
-                        uint32_t* Hout, bool do_scan, uint64_t cap, bool exact, uint64_t* d_total,
-                        uint32_t epoch, cudaStream_t s) {
-  int rc;
-  ScanArgs a = {};
-  const bool smem = hp && hp->path != HistPath::Global;
-  a.partials = smem ? c->partials.as<uint32_t>() : nullptr;
-  a.C = smem ? hp->C : 0;
-  a.ldw = smem ? hp->ldw : 0;
-  a.pack16 = smem && hp->path == HistPath::Smem16;
-  a.Hsrc = Hsrc;
-  a.ovfH = smem ? c->ovfH.as<uint32_t>() : nullptr;
-  a.ovfH_mut = a.ovfH ? c->ovfH.as<uint32_t>() : nullptr;
-  a.U = U;
-  a.Hout = Hout;
-  a.do_scan = do_scan;
-  const uint32_t bins_per_tile = a.pack16 ? 2 * kScanWords : kScanWords;
-  const uint32_t ntiles = (uint32_t)cdiv(U, bins_per_tile);
   const uint64_t ntiles_out = cap ? cdiv(cap, kExpandTile) : 1;
   if (do_scan) {
     if ((rc = c->P.ensure(4ull * (U + 1)))) return rc;
-    if ((rc = c->lb_status.ensure(8ull * ntiles, true))) return rc;
     if ((rc = c->tfb.ensure(4ull * ntiles_out))) return rc;
   }
+  a.U = U;
+  a.do_scan = do_scan;
   a.P = c->P.as<uint32_t>();
-  a.status = c->lb_status.as<uint64_t>();
+  a.range_tot = c->range_tot.as<uint64_t>();
   a.tfb = c->tfb.as<uint32_t>();
   a.T = kExpandTile;
   a.ntiles_out = ntiles_out;
@@ -275,17 +220,76 @@ int enqueue_reduce_scan(dialsort_ctx c, const HistPlan* hp, const uint32_t* Hsrc
   a.d_total = d_total;
   a.ws_total = c->ws_total.as<uint64_t>();
   a.st = c->status.as<DevStatus>();
+  a.bar = c->gridbar.as<GridBar>();
   a.epoch = epoch;
-  DS_CUDA(launch_k(KID_REDUCE_SCAN, k_reduce_scan, dim3(ntiles), dim3(kScanThreads), 0, s, a));
+  a.pt = c->pt;
+  return DIALSORT_OK;
+}
+
+// Histogram of keys into H; when do_scan, also P / tfb for a projection of `cap` outputs.
+// Smem paths: one fused co-resident kernel.  Global path: zero + L2 ingest + k_scan.
+int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, bool do_scan,
+                      uint64_t cap, uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a = {};
+  if ((rc = fill_scan_args(c, a, U, do_scan, cap, true, nullptr, epoch))) return rc;
+  const HistPath path = choose_path(U);
+  if (path == HistPath::Global) {
+    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, H, (uint64_t)U));
+    const uint64_t want = cdiv(n / 4 + 1, 256ull * kHistUnroll);
+    const uint64_t capg = (uint64_t)c->nsm * 8;
+    const uint32_t grid = (uint32_t)(want < capg ? (want ? want : 1) : capg);
+    DS_CUDA(launch_k(KID_HIST_GLOBAL, k_hist_global, dim3(grid), dim3(256), 0, s, keys, n, U, H, a.st));
+    if (!do_scan) return DIALSORT_OK;
+    a.Hsrc = H;
+    const uint64_t ntiles = cdiv(U, kTileBins);
+    const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
+    DS_CUDA(launch_k(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
+    return DIALSORT_OK;
+  }
+  const bool pack = path == HistPath::Smem16;
+  const uint32_t W = pack ? (U + 1) / 2 : U;
+  const uint32_t ldw = (uint32_t)round_up(W, 8);
+  const size_t smem = std::max<size_t>(4ull * ldw, 32 * 1024);
+  const uint64_t n4 = n / 4 + 1;
+  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);  // >= 2 load batches per CTA
+  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
+  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
+  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  a.partials = c->partials.as<uint32_t>();
+  a.C = C;
+  a.ldw = ldw;
+  a.pack16 = pack;
+  a.ovfH = c->ovfH.as<uint32_t>();
+  a.H = H;
+  if (pack)
+    DS_CUDA(launch_k(KID_HIST_SMEM16, k_hist_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a));
+  else
+    DS_CUDA(launch_k(KID_HIST_SMEM32, k_hist_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a));
+  return DIALSORT_OK;
+}
+
+// Scan of a caller histogram (reconstruct API).
+int enqueue_scan(dialsort_ctx c, const uint32_t* H, uint32_t U, uint64_t cap, bool exact, uint64_t* d_total,
+                 uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a = {};
+  if ((rc = fill_scan_args(c, a, U, true, cap, exact, d_total, epoch))) return rc;
+  a.Hsrc = H;
+  const uint64_t ntiles = cdiv(U, kTileBins);
+  const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
+  DS_CUDA(launch_k(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
   return DIALSORT_OK;
 }
 
 int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, int32_t* out, cudaStream_t s) {
   if (cap == 0) return DIALSORT_OK;
   const uint64_t ntiles_out = cdiv(cap, kExpandTile);
-  if (ntiles_out > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "output too large");
-  DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3((uint32_t)ntiles_out), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
-                 c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out));
+  const uint64_t wave = (uint64_t)c->nsm * c->expand_occ;  // persistent grid: one wave
+  const uint32_t grid = (uint32_t)(ntiles_out < wave ? ntiles_out : wave);
+  DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3(grid), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
+                   c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out,
+                   c->pt));
   return DIALSORT_OK;
 }
 
@@ -378,12 +382,14 @@ int dialsort_ctx_create(int device, uint64_t max_n, uint32_t max_U, dialsort_ctx
   c->device = device;
   int rc = ctx_init(c);
   if (!rc && max_U) {
-    HistPlan hp;
-    if (!(rc = plan_hist(c, max_n ? max_n : (1u << 20), max_U, hp)) && hp.path != HistPath::Global)
-      rc = c->partials.ensure(4ull * hp.C * hp.ldw);
+    const HistPath path = choose_path(max_U);
+    if (path != HistPath::Global) {
+      const uint64_t W = path == HistPath::Smem16 ? (max_U + 1) / 2 : max_U;
+      rc = c->partials.ensure(4ull * c->nsm * round_up(W, 8));
+    }
     if (!rc) rc = c->P.ensure(4ull * (max_U + 1));
-    if (!rc) rc = c->lb_status.ensure(8ull * cdiv(max_U, kScanWords) + 64, true);
     if (!rc) rc = c->ovfH.ensure(4ull * max_U, true);
+    if (!rc) rc = c->Hws.ensure(4ull * max_U);
   }
   if (!rc && max_n) rc = c->tfb.ensure(4ull * (cdiv(max_n, kExpandTile) + 1));
   if (rc) {
@@ -398,10 +404,11 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   if (!c) return DIALSORT_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  for (DBuf* b : {&c->partials, &c->P, &c->lb_status, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hglob,
-                  &c->radix_tmp, &c->radix_hist, &c->radix_lb, &c->scratch64})
+  for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
+                  &c->range_tot, &c->gridbar, &c->radix_tmp, &c->radix_hist, &c->radix_lb})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
+  if (c->pt) cudaFree(c->pt);
   for (cudaEvent_t e : c->prof.ev) cudaEventDestroy(e);
   delete c;
   return DIALSORT_OK;
@@ -409,7 +416,6 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
 
 int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info* info) {
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
   DS_CUDA(cudaMemcpyAsync(c->host_status, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
@@ -454,12 +460,7 @@ int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, ui
     DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
     return DIALSORT_OK;
   }
-  HistPlan hp;
-  if ((rc = plan_hist(c, n, U, hp))) return rc;
-  if ((rc = enqueue_ingest(c, keys, n, U, hp, H, epoch, s))) return rc;
-  if (hp.path != HistPath::Global)
-    if ((rc = enqueue_reduce_scan(c, &hp, nullptr, U, H, false, 0, false, nullptr, epoch, s))) return rc;
-  return DIALSORT_OK;
+  return enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s);
 }
 
 int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int32_t key_base, int32_t* out,
@@ -474,7 +475,7 @@ int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, in
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
   const uint32_t epoch = next_epoch(c, s);
-  if ((rc = enqueue_reduce_scan(c, nullptr, H, U, nullptr, true, cap, exact != 0, d_total, epoch, s))) return rc;
+  if ((rc = enqueue_scan(c, H, U, cap, exact != 0, d_total, epoch, s))) return rc;
   return enqueue_expand(c, U, cap, key_base, out, s);
 }
 
@@ -493,23 +494,12 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     if (H_out) DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H_out, (uint64_t)U));
     return DIALSORT_OK;
   }
-  HistPlan hp;
-  if ((rc = plan_hist(c, n, U, hp))) return rc;
-  uint32_t* Hg = nullptr;
-  if (hp.path == HistPath::Global) {
-    if (H_out) {
-      Hg = H_out;
-    } else {
-      if ((rc = c->Hglob.ensure(4ull * U))) return rc;
-      Hg = c->Hglob.as<uint32_t>();
-    }
+  uint32_t* H = H_out;
+  if (!H) {
+    if ((rc = c->Hws.ensure(4ull * U))) return rc;
+    H = c->Hws.as<uint32_t>();
   }
-  if ((rc = enqueue_ingest(c, keys, n, U, hp, Hg, epoch, s))) return rc;
-  if (hp.path == HistPath::Global) {
-    if ((rc = enqueue_reduce_scan(c, nullptr, Hg, U, nullptr, true, n, true, nullptr, epoch, s))) return rc;
-  } else {
-    if ((rc = enqueue_reduce_scan(c, &hp, nullptr, U, H_out, true, n, true, nullptr, epoch, s))) return rc;
-  }
+  if ((rc = enqueue_hist_scan(c, keys, n, U, H, true, n, epoch, s))) return rc;
   return enqueue_expand(c, U, n, 0, out, s);
 }
 
@@ -570,6 +560,21 @@ int dialsort_profile_read(dialsort_ctx c, int max, int* ids, float* ms) {
 }
 
 const char* dialsort_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kKernelNames[id] : "?"; }
+
+// Debug: phase times (ns, relative to the earliest fused-kernel CTA start) of the most recent
+// calls since the last read; zeros unless DIALSORT_PHASE_TIMING=1 at context creation.
+int dialsort_debug_phase_ns(dialsort_ctx c, uint64_t* out8) {
+  if (!c || !out8) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < 8; ++i) out8[i] = 0;
+  if (!c->pt) return DIALSORT_OK;
+  PhaseTimes h;
+  DS_CUDA(cudaMemcpy(&h, c->pt, sizeof(h), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 8; ++i) out8[i] = h.t[i] > h.start_min ? h.t[i] - h.start_min : 0;
+  PhaseTimes init = {};
+  init.start_min = ~0ull;
+  DS_CUDA(cudaMemcpy(c->pt, &init, sizeof(init), cudaMemcpyHostToDevice));
+  return DIALSORT_OK;
+}
 
 int dialsort_crn_resolve_async(dialsort_ctx c, const int32_t* lane_keys, const uint32_t* active, uint64_t n_batches,
                                int32_t* out_keys, uint32_t* out_counts, dialsort_stream_t stream) {

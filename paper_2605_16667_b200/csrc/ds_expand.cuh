@@ -1,80 +1,102 @@
 // ds_expand.cuh — the ordered projection ("geometric read"), eq:projection:
-// for k = 0..U-1 emit key_base + k exactly H[k] times.  Output-tile-centric: CTA t owns
-// output positions [t*T, (t+1)*T), looks up its first bin in tfb (written by k_reduce_scan),
-// stages the prefix window P[k_lo .. k_hi+1] in shared memory and writes every position
-// exactly once with 128-bit streaming stores.  Balanced by construction, whatever the skew
-// (a Zipf hot key spanning 240 tiles is written by 240 CTAs).
+// for k = 0..U-1 emit key_base + k exactly H[k] times.
+//
+// Output-tile-centric and persistent: CTA c processes output tiles t = c, c + G, ... of
+// kExpandTile positions.  For tile [p0, p1) the first bin k_lo comes from tfb[t] (written by
+// k_reduce_scan); every later bin k whose start P[k] falls inside the tile adds one "bin
+// start" mark at P[k] - p0 in a shared-memory count array; an inclusive scan of the marks
+// then gives, for every position p, key(p) = key_base + k_lo + #{starts <= p}.  Marks are
+// counts, not flags, so empty bins (equal starts) need no special case, and the cost is
+// O(T + #bins) per tile with no per-position search and no divergence.  The finished tile
+// leaves shared memory through 128-bit streaming stores, each warp instruction writing 512
+// contiguous bytes.  Balanced by construction whatever the skew: a Zipf hot key spanning
+// many tiles is written by many CTAs.
 #pragma once
 #include "ds_common.cuh"
 
 namespace ds {
 
-constexpr int kExpandThreads = 256;
-constexpr uint32_t kExpandTile = 8192;    // positions per CTA (multiple of 4)
-constexpr uint32_t kExpandWindow = 2048;  // bins staged per smem chunk
+constexpr int kExpandThreads = 512;
+constexpr uint32_t kExpandTile = 8192;                                // positions per tile
+constexpr uint32_t kExpandQuads = kExpandTile / 4;                    // 2048 int4
+constexpr uint32_t kExpandPerThread = kExpandQuads / kExpandThreads;  // 4 quads (16 positions)
 
-// Largest i in [0, m) with sP[i] <= q, given sP[0] <= q < sP[m].
-__device__ __forceinline__ uint32_t window_search(const uint32_t* sP, uint32_t m, uint32_t q) {
-  uint32_t lo = 0, len = m;
-  while (len > 1) {
-    uint32_t half = len >> 1;
-    if (sP[lo + half] <= q) lo += half;
-    len -= half;
-  }
-  return lo;
-}
+// XOR swizzle of quad index q so that both access patterns are bank-conflict free:
+// thread-contiguous (thread t owns quads 4t..4t+3) and warp-contiguous (quad j by lane j).
+__device__ __forceinline__ uint32_t swz(uint32_t q) { return q ^ ((q >> 3) & 7u); }
 
-__global__ void __launch_bounds__(kExpandThreads) k_expand(const uint32_t* __restrict__ P, uint32_t U,
+__global__ void __launch_bounds__(kExpandThreads, 4) k_expand(const uint32_t* __restrict__ P, uint32_t U,
                                                            const uint32_t* __restrict__ tfb,
                                                            uint64_t ntiles, const uint64_t* ws_total,
                                                            uint64_t cap, int32_t key_base,
-                                                           int32_t* __restrict__ out) {
-  __shared__ uint32_t sP[kExpandWindow + 1];
+                                                           int32_t* __restrict__ out, PhaseTimes* pt) {
+  __shared__ __align__(16) uint32_t M[kExpandTile];
+  __shared__ uint32_t red[34];
   pdl_wait();
+  phase_mark(pt, 7);  // earliest expand start recorded as t[7] max; see dialsort_debug_phase_ns
   const uint64_t total = *ws_total;
-  const uint64_t nw = total < cap ? total : cap;  // positions to write
-  const uint64_t t = blockIdx.x;
-  const uint64_t p0 = t * kExpandTile;
-  if (p0 >= nw) return;
-  const uint64_t p1 = (p0 + kExpandTile < nw) ? p0 + kExpandTile : nw;
-  const uint32_t k_lo = tfb[t];
-  const uint32_t k_hi = (t + 1 < ntiles && (t + 1) * kExpandTile < nw) ? tfb[t + 1] : U - 1;
+  const uint32_t nw = (uint32_t)(total < cap ? total : cap);  // positions to write (< 2^32)
+  const uint64_t ntw = ((uint64_t)nw + kExpandTile - 1) / kExpandTile;
+  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  const uint64_t pol = l2_evict_first_policy();
+  uint4* M4 = reinterpret_cast<uint4*>(M);
 
-  // Output alignment: positions [p0, p0 + head) scalar, then 16-byte aligned quads.
-  const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(out) >> 2) & 3u);
-  const uint32_t head = mis ? 4 - mis : 0;  // same for every tile (T % 4 == 0)
-
-  for (uint64_t c0 = k_lo; c0 <= k_hi; c0 += kExpandWindow) {
-    const uint32_t m = (uint32_t)((k_hi + 1 - c0) < kExpandWindow ? (k_hi + 1 - c0) : kExpandWindow);
+  for (uint64_t t = blockIdx.x; t < ntw; t += gridDim.x) {
+    const uint32_t p0 = (uint32_t)(t * kExpandTile);
+    const uint32_t p1 = (nw - p0 > kExpandTile) ? p0 + kExpandTile : nw;
+    const uint32_t k_lo = tfb[t];
+    const uint32_t k_hi = (t + 1 < ntiles && (uint64_t)p0 + kExpandTile < nw) ? tfb[t + 1] : U - 1;
+    // 1. clear the marks
+#pragma unroll
+    for (uint32_t j = 0; j < kExpandPerThread; ++j) M4[threadIdx.x + j * kExpandThreads] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i <= m; i += blockDim.x) sP[i] = __ldcg(P + c0 + i);
-    __syncthreads();
-    // Positions this chunk covers within the tile.
-    const uint64_t lo = sP[0] > p0 ? sP[0] : p0;
-    const uint64_t hi = sP[m] < p1 ? sP[m] : p1;
-    if (lo >= hi) continue;
-    const int32_t kb = key_base + (int32_t)c0;
-    // Scalar edges: [lo, a0) and [a1, hi) where a0/a1 are quad-aligned output positions.
-    uint64_t a0 = lo + ((head + 4 - (uint32_t)(lo & 3)) & 3);  // first q >= lo, q ≡ head (mod 4)
-    if (a0 > hi) a0 = hi;
-    uint64_t a1 = a0 + ((hi - a0) & ~3ull);
-    for (uint64_t q = lo + threadIdx.x; q < a0; q += blockDim.x)
-      out[q] = kb + (int32_t)window_search(sP, m, (uint32_t)q);
-    for (uint64_t q = a1 + threadIdx.x; q < hi; q += blockDim.x)
-      out[q] = kb + (int32_t)window_search(sP, m, (uint32_t)q);
-    // Aligned quads.
-    for (uint64_t q = a0 + 4 * (uint64_t)threadIdx.x; q < a1; q += 4 * (uint64_t)blockDim.x) {
-      uint32_t i = window_search(sP, m, (uint32_t)q);
-      int4 v;
-      v.x = kb + (int32_t)i;
-      while (sP[i + 1] <= q + 1) ++i;
-      v.y = kb + (int32_t)i;
-      while (sP[i + 1] <= q + 2) ++i;
-      v.z = kb + (int32_t)i;
-      while (sP[i + 1] <= q + 3) ++i;
-      v.w = kb + (int32_t)i;
-      st_stream4(reinterpret_cast<int4*>(out + q), v);
+    // 2. one mark per bin start inside the tile (P[k] > p0 for every k > k_lo)
+    for (uint64_t k = (uint64_t)k_lo + 1 + threadIdx.x; k <= k_hi; k += kExpandThreads) {
+      const uint32_t b = __ldcg(P + k);
+      if (b < p1) {
+        const uint32_t w = b - p0;
+        atomicAdd(&M[(swz(w >> 2) << 2) | (w & 3u)], 1u);
+      }
     }
+    __syncthreads();
+    // 3. inclusive scan of the marks -> keys (thread t owns positions 16t .. 16t+15)
+    uint4 v[kExpandPerThread];
+#pragma unroll
+    for (uint32_t j = 0; j < kExpandPerThread; ++j) {
+      v[j] = M4[swz(kExpandPerThread * threadIdx.x + j)];
+      v[j].y += v[j].x;
+      v[j].z += v[j].y;
+      v[j].w += v[j].z;
+    }
+#pragma unroll
+    for (uint32_t j = 1; j < kExpandPerThread; ++j) {
+      v[j].x += v[j - 1].w; v[j].y += v[j - 1].w; v[j].z += v[j - 1].w; v[j].w += v[j - 1].w;
+    }
+    uint32_t tile_marks;
+    const uint32_t ex = block_excl_scan<uint32_t>(v[kExpandPerThread - 1].w, tile_marks, red);
+    const uint32_t base = (uint32_t)key_base + k_lo + ex;
+#pragma unroll
+    for (uint32_t j = 0; j < kExpandPerThread; ++j)
+      M4[swz(kExpandPerThread * threadIdx.x + j)] =
+          make_uint4(base + v[j].x, base + v[j].y, base + v[j].z, base + v[j].w);
+    __syncthreads();
+    // 4. copy out: lane-contiguous quads, 512 contiguous bytes per warp instruction
+#pragma unroll
+    for (uint32_t j = 0; j < kExpandPerThread; ++j) {
+      const uint32_t qd = threadIdx.x + j * kExpandThreads;
+      const uint32_t q = p0 + 4 * qd;
+      if (q >= p1) continue;
+      const uint4 x = M4[swz(qd)];
+      if (aligned && q + 4 <= p1) {
+        st_stream4(reinterpret_cast<int4*>(out + q), make_int4((int)x.x, (int)x.y, (int)x.z, (int)x.w), pol);
+      } else {
+        out[q] = (int)x.x;
+        if (q + 1 < p1) out[q + 1] = (int)x.y;
+        if (q + 2 < p1) out[q + 2] = (int)x.z;
+        if (q + 3 < p1) out[q + 3] = (int)x.w;
+      }
+    }
+    __syncthreads();  // M is reused by the next tile
   }
   pdl_trigger();
 }

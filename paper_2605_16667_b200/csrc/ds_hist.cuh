@@ -14,29 +14,13 @@
 // the merge is not free: the L2 path, and the smem16 overflow fallback.
 #pragma once
 #include "ds_common.cuh"
+#include "ds_scan.cuh"
 
 namespace ds {
 
 constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
-constexpr int kHistUnroll = 4;              // int4 loads in flight per thread
-
-__device__ __forceinline__ uint32_t packed_word(uint32_t k) { return k >> 1; }
-__device__ __forceinline__ uint32_t packed_inc(uint32_t k) { return (k & 1u) ? 65536u : 1u; }
-
-template <bool PACK16>
-__device__ __forceinline__ void ingest_smem(uint32_t* h, uint32_t k, uint32_t U, uint64_t idx,
-                                            DevStatus* st, uint32_t& valid) {
-  if (k < U) {
-    if (PACK16)
-      atomicAdd(h + packed_word(k), packed_inc(k));
-    else
-      atomicAdd(h + k, 1u);
-    ++valid;
-  } else {
-    record_bad(st, idx, k);
-  }
-}
+constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
 
 // Key layout shared by every pass over `keys`: `head` scalars before the first 16-byte
 // boundary, `n4` aligned int4 vectors, `tail` scalars.  CTA 0 takes the head, the last CTA
@@ -58,42 +42,61 @@ __host__ __device__ inline KeySpan make_span(const int32_t* keys, uint64_t n) {
   return s;
 }
 
-// Visit every key this CTA owns: f(key, index).
-template <typename F>
-__device__ __forceinline__ void for_each_key(const KeySpan& s, F&& f) {
-  const uint64_t T = blockDim.x, G = gridDim.x;
-  if (blockIdx.x == 0 && threadIdx.x < s.head) f((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
+// Visit this CTA's keys as int4 groups: f4(v, int4 index of v), plus scalars f1(key, index)
+// for the unaligned head (CTA 0) and tail (last CTA).  32-bit vector indices (n4 < 2^30);
+// software-pipelined: the next batch of kHistUnroll vectors is in flight while the current
+// batch is ingested, so the load queue never drains between batches.
+template <typename F4, typename F1>
+__device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1) {
+  const uint32_t T = blockDim.x, G = gridDim.x;
+  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
   if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
     uint64_t i = s.head + 4 * s.n4 + threadIdx.x;
-    f((uint32_t)s.keys[i], i);
+    f1((uint32_t)s.keys[i], i);
   }
-  const int4* body = s.body();
-  const uint64_t stride = G * T;
-  uint64_t i = blockIdx.x * T + threadIdx.x;
-  for (; i + (kHistUnroll - 1) * stride < s.n4; i += kHistUnroll * stride) {
-    int4 v[kHistUnroll];
+  const uint64_t pol = l2_evict_first_policy();
+  const int4* __restrict__ body = s.body();
+  // Grid-stride over vectors (all SMs sweep the array together: measured faster than
+  // contiguous per-CTA ranges with an up-front L2 bulk prefetch, 10 vs 12.7 us at c2).
+  const uint32_t n4 = (uint32_t)s.n4, stride = G * T;
+  uint32_t i = blockIdx.x * T + threadIdx.x;
+  int4 a[kHistUnroll];
 #pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) v[u] = ld_stream4(body + i + u * stride);
+  for (int u = 0; u < kHistUnroll; ++u)
+    a[u] = (i + u * stride < n4) ? ld_stream4(body + i + u * stride, pol) : make_int4(0, 0, 0, 0);
+  while (i < n4) {
+    const uint32_t in = i + kHistUnroll * stride;
+    int4 b[kHistUnroll];
 #pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      uint64_t b = s.head + 4 * (i + u * stride);
-      f((uint32_t)v[u].x, b);
-      f((uint32_t)v[u].y, b + 1);
-      f((uint32_t)v[u].z, b + 2);
-      f((uint32_t)v[u].w, b + 3);
-    }
-  }
-  for (; i < s.n4; i += stride) {
-    int4 v = ld_stream4(body + i);
-    uint64_t b = s.head + 4 * i;
-    f((uint32_t)v.x, b);
-    f((uint32_t)v.y, b + 1);
-    f((uint32_t)v.z, b + 2);
-    f((uint32_t)v.w, b + 3);
+    for (int u = 0; u < kHistUnroll; ++u)
+      b[u] = (in + u * stride < n4) ? ld_stream4(body + in + u * stride, pol) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u)
+      if (i + u * stride < n4) f4(a[u], i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) a[u] = b[u];
+    i = in;
   }
 }
 
-// Global-path ingestion of one key batch position with the warp CRN.  All 32 lanes call it
+// Slow path of an int4 group holding at least one key outside [0,U): ingest the valid keys
+// one by one and record the bad ones (never taken on valid input; kept out of line).
+template <bool PACK16>
+__device__ __noinline__ uint32_t ingest4_checked(uint32_t* h, int4 v, uint64_t idx0, uint32_t U, DevStatus* st) {
+  uint32_t k[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+  uint32_t bad = 0;
+  for (int j = 0; j < 4; ++j) {
+    if (k[j] < U) {
+      if (PACK16) atomicAdd(h + (k[j] >> 1), 1u << ((k[j] & 1u) << 4));
+      else atomicAdd(h + k[j], 1u);
+    } else {
+      record_bad(st, idx0 + j, k[j]);
+      ++bad;
+    }
+  }
+  return bad;
+}
+
 // (the predicate `valid` marks lanes that carry a key; absent lanes never enter the CRN).
 __device__ __forceinline__ void crn_red(uint32_t* H, uint32_t k, bool valid) {
   uint32_t mask = __ballot_sync(FULL, valid);
@@ -139,57 +142,112 @@ __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
     }
   }
 }
+__device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
+                                                    uint32_t U, DevStatus* st, uint32_t epoch) {
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
+  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
+}
 
-// ---- shared-memory paths -----------------------------------------------------------------
-// partials: row r = CTA r, W words per row (W = U for u32, ceil(U/2) packed), row stride
-// `ldw` = W rounded up to a multiple of 8 words; dynamic smem = 4*ldw bytes.  ovfH: uint32[U], zero on entry, used only by the fallback.
+// ---- shared-memory paths: ingestion + merge + scan in one co-resident grid ------------------
+// Phase 0: CTA c ingests its keys into a private shared-memory histogram (uint32, or packed
+//          2 x 16-bit with exact overflow detection) and writes it as partial row c
+//          (plain coalesced stores; no zeroing of H, no global atomics).
+// Phase A: after a grid barrier, CTA c merges the rows of its contiguous range of 512-bin
+//          tiles into H (ds_scan.cuh merge_tile) and its range total.
+// Phase B: after a second barrier, offsets from the range totals and the tile scans give P
+//          and the expand index tfb (skipped for the histogram-only API).
+// One CTA per SM (1024 threads); the grid (<= #SMs) is co-resident by construction.
+// Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
 template <bool PACK16>
-__global__ void __launch_bounds__(1024) k_hist_smem(const int32_t* __restrict__ keys, uint64_t n,
-                                                    uint32_t U, uint32_t W, uint32_t ldw,
-                                                    uint32_t* __restrict__ partials,
-                                                    uint32_t* __restrict__ ovfH, DevStatus* st,
-                                                    uint32_t epoch) {
+__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a) {
   extern __shared__ __align__(16) uint32_t sh_hist[];
-  __shared__ unsigned long long red64[33];
+  __shared__ uint64_t red64[34];
   pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
+  phase_mark(a.pt, -1);
+  const uint32_t U = a.U, ldw = a.ldw;
 
-  // K1: zero the private histogram (vectorised; ldw = W rounded up to 8 words, the padding
-  // stays zero so k_reduce_scan may read whole 8-word groups).
+  // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
+  // merge may read whole uint4 groups).
   const uint32_t W4 = ldw / 4;
   uint4* h4 = reinterpret_cast<uint4*>(sh_hist);
   for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
+  // Ingestion (eq:ingestion): one shared atomic per key; equal addresses inside one warp
+  // instruction are merged by the shared-memory atomic unit (the CRN's equality merge).
   const KeySpan s = make_span(keys, n);
-  uint32_t valid = 0;
-  for_each_key(s, [&](uint32_t k, uint64_t idx) { ingest_smem<PACK16>(sh_hist, k, U, idx, st, valid); });
-  pdl_trigger();
+  DevStatus* st = a.st;
+  uint32_t seen = 0, bad = 0;
+  // packed word of key k: k >> 1 (byte offset (2k) & ~3); increment 1 or 65536
+  auto add16 = [&](uint32_t k) {
+    atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh_hist) + ((k << 1) & ~3u)), 1u + (k & 1u) * 65535u);
+  };
+  auto f4 = [&](int4 v, uint32_t i4) {
+    seen += 4;
+    if (umax4(v) < U) {
+      if (PACK16) {
+        add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
+      } else {
+        atomicAdd(sh_hist + (uint32_t)v.x, 1u);
+        atomicAdd(sh_hist + (uint32_t)v.y, 1u);
+        atomicAdd(sh_hist + (uint32_t)v.z, 1u);
+        atomicAdd(sh_hist + (uint32_t)v.w, 1u);
+      }
+    } else {
+      bad += ingest4_checked<PACK16>(sh_hist, v, s.head + 4 * (uint64_t)i4, U, st);
+    }
+  };
+  auto f1 = [&](uint32_t k, uint64_t idx) {
+    seen += 1;
+    if (k < U) {
+      if (PACK16) add16(k);
+      else atomicAdd(sh_hist + k, 1u);
+    } else {
+      record_bad(st, idx, k);
+      ++bad;
+    }
+  };
+  for_each_key4(s, f4, f1);
+  phase_mark(a.pt, 0);
   __syncthreads();
+  phase_mark(a.pt, 1);
 
-  uint32_t* row = partials + (uint64_t)blockIdx.x * ldw;
-  uint4* row4 = reinterpret_cast<uint4*>(row);
+  // Flush the private histogram as partial row blockIdx.x.
+  uint4* row4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * ldw);
   if (!PACK16) {
-    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = h4[i];
-    return;
+    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) __stcg(row4 + i, h4[i]);
+  } else {
+    // Packed counters: a 16-bit field that wrapped loses >= 65535 from the field sum
+    // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.
+    unsigned long long fsum = 0;
+    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) {
+      const uint4 w = h4[i];
+      fsum += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
+              (w.w & 0xffffu) + (w.w >> 16);
+      __stcg(row4 + i, w);
+    }
+    const uint64_t tot = block_sum<uint64_t>(fsum, red64);
+    const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
+    if (tot != nvalid) hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch);
   }
-  // Packed counters: a 16-bit field that wrapped loses >= 65535 from the field sum
-  // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.
-  unsigned long long fsum = 0;
-  for (uint32_t i = threadIdx.x; i < ldw; i += blockDim.x) {
-    uint32_t w = sh_hist[i];
-    fsum += (w & 0xffffu) + (w >> 16);
-  }
-  unsigned long long tot = block_sum<unsigned long long>(fsum, red64);
-  unsigned long long nvalid = block_sum<unsigned long long>((unsigned long long)valid, red64);
-  if (tot == nvalid) {
-    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = h4[i];
-    return;
-  }
-  // Fallback (a key occurred >= 65536 times in this CTA's share): zero the row and re-ingest
-  // this CTA's keys into ovfH through the warp CRN + L2 atomics.  Exact, slow, rare.
-  for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
-  if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
-  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
+  phase_mark(a.pt, 2);
+  grid_barrier(a.bar);  // every row (and any fallback contribution) is in L2
+  phase_mark(a.pt, 3);
+
+  // Phase A: merge this CTA's tile range.
+  const bool use_ovf = ld_acquire_u32(&st->ovf_epoch) == a.epoch;
+  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
+  uint32_t tb0, tb1;
+  my_tiles(ntiles, tb0, tb1);
+  uint64_t range = 0;
+  for (uint32_t t = tb0; t < tb1; ++t) range += merge_tile(a, t, use_ovf, sh_hist, red64);
+  phase_mark(a.pt, 4);
+  // Phase B: offsets + scan -> P, tfb.
+  if (a.do_scan) scan_phase_b(a, a.H, tb0, tb1, range, red64);
+  phase_mark(a.pt, 5);
+  pdl_trigger();
 }
 
 // ---- L2 path -----------------------------------------------------------------------------

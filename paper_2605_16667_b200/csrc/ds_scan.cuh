@@ -1,132 +1,182 @@
-// ds_scan.cuh — sub-histogram merge + the GPU's write-offset scan.
+// ds_scan.cuh — sub-histogram merge and the GPU's write-offset scan.
 //
-// k_reduce_scan sums the per-CTA partial rows written by k_hist_smem (the additive merge,
-// lem:crn lifted to whole histograms) into H, and — when a projection follows —
-// computes the exclusive prefix P[k] = Σ_{j<k} H[j] with a single-pass decoupled look-back
-// across bin tiles.  P is the parallel write-offset step north_star asks for; the paper's
-// own substrates need no prefix sum because they emit sequentially.
-// It also emits the output-tile index `tfb` (tile t's first position t*T lies in bin
-// tfb[t]) that lets each expand CTA find its bins in O(1).
+// The merge sums the per-CTA partial histogram rows written by the ingestion phase (the
+// additive merge, lem:crn lifted to whole histograms) into H.  The scan computes
+// the exclusive prefix P[k] = Σ_{j<k} H[j]: the parallel write-offset step north_star asks
+// for (the paper's own substrates emit sequentially and need no prefix sum, P:13-14,
+// P:2013-2016).  It also emits the output-tile index `tfb` (tile t's first position t*T
+// lies in bin tfb[t]) that gives each expand CTA its first bin in O(1).
+//
+// Both run inside persistent, co-resident grids as a two-level reduce-then-scan separated by
+// grid barriers — no decoupled look-back chain: every CTA owns a contiguous range of 512-bin
+// tiles; phase A writes H for its range and its range total; phase B derives its range
+// offset from all range totals (<= a few hundred values) and scans its tiles into P.
 #pragma once
 #include "ds_common.cuh"
 
 namespace ds {
 
-constexpr int kScanThreads = 512;
-constexpr int kScanWords = 256;  // partial-row words per tile (512 bins packed, 256 bins u32)
+constexpr uint32_t kTileBins = 512;  // bins per scan tile
+
+// Sense-reversing grid barrier for a co-resident grid (all CTAs participate every time).
+// Self-resetting: `count` returns to 0 at every barrier, `gen` only grows.
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(GridBar* gb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire_u32(&gb->gen);
+    unsigned old;
+    // arrive with release semantics (orders this CTA's prior writes, made visible to thread 0
+    // by __syncthreads, before the arrival), observe the release with acquire loads
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&gb->count) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&gb->count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&gb->gen) : "memory");
+    } else {
+      while (ld_acquire_u32(&gb->gen) == g) {
+      }
+    }
+  }
+  __syncthreads();
+}
 
 struct ScanArgs {
-  const uint32_t* partials;  // [C][ldw] rows, or nullptr when C == 0
+  const uint32_t* partials;  // [C][ldw] rows (C > 0), or nullptr
   uint32_t C, ldw;
-  int pack16;                // partial words hold 2 x 16-bit bins
-  const uint32_t* Hsrc;      // C == 0: read H from here
-  const uint32_t* ovfH;      // added (and cleared) iff st->ovf_epoch == epoch
-  uint32_t* ovfH_mut;
+  int pack16;                // partial words hold 2 x 16-bit bins (2w, 2w+1)
+  const uint32_t* Hsrc;      // C == 0: H is read from here
+  uint32_t* ovfH;            // packed-overflow side histogram (added and cleared if flagged)
   uint32_t U;
-  uint32_t* Hout;            // nullable: write merged H
+  uint32_t* H;               // C > 0: merged H written here (user H or workspace)
   int do_scan;
-  uint32_t* P;               // [U+1] exclusive prefix (do_scan)
-  uint64_t* status;          // [num tiles] look-back status
-  uint32_t* tfb;             // [ntiles_out] first bin of each output tile (do_scan)
-  uint64_t T;                // output tile size (positions)
-  uint64_t ntiles_out;
+  uint32_t* P;               // [U+1] exclusive prefix
+  uint64_t* range_tot;       // [gridDim] per-CTA range totals
+  uint32_t* tfb;             // [ntiles_out] first bin of each output tile
+  uint64_t T, ntiles_out;
   uint64_t n_expected;       // exact: ΣH must equal; else capacity
   int exact;
   uint64_t* d_total;         // nullable, receives ΣH
   uint64_t* ws_total;        // workspace scalar read by k_expand
   DevStatus* st;
+  GridBar* bar;
   uint32_t epoch;
+  PhaseTimes* pt;            // nullable debug timing
 };
 
-__global__ void __launch_bounds__(kScanThreads) k_reduce_scan(ScanArgs a) {
-  __shared__ uint32_t part[kScanThreads / 32][2 * kScanWords];  // per-warp bin sums (32 KB)
-  __shared__ uint64_t red[34];
-  __shared__ uint64_t s_excl;
-  pdl_wait();
+// Tiles [tb0, tb1) of CTA b in a grid of G over ntiles (contiguous ranges).
+__device__ __forceinline__ void my_tiles(uint32_t ntiles, uint32_t& tb0, uint32_t& tb1) {
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  tb0 = (uint32_t)((uint64_t)ntiles * b / G);
+  tb1 = (uint32_t)((uint64_t)ntiles * (b + 1) / G);
+}
 
-  const uint32_t tile = blockIdx.x;
-  const uint32_t bins_per_tile = a.pack16 ? 2 * kScanWords : kScanWords;
-  const uint64_t bin0 = (uint64_t)tile * bins_per_tile;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool use_ovf = a.ovfH != nullptr && *(volatile unsigned*)&a.st->ovf_epoch == a.epoch;
-
-  // ---- merge: H[bin0 + j] for j < bins_per_tile; thread j owns bin j -------------------
-  uint64_t hval = 0;
-  if (a.C > 0) {
-    // Warp w sums rows w, w+nw, ...; lane l covers words [8l, 8l+8) of the tile.
-    const uint64_t word0 = (uint64_t)tile * kScanWords + 8 * lane;
-    uint32_t acc[16];
+// Phase A for one tile: H[tile] = Σ_rows partial[row][tile] (+ ovfH), written to a.H.
+// Returns the tile total (valid in every thread).  scratch: >= (blockDim/64)*2 KB of smem.
+__device__ __forceinline__ uint64_t merge_tile(const ScanArgs& a, uint32_t tile, bool use_ovf, uint32_t* scratch,
+                                               uint64_t* red) {
+  const uint32_t words = a.pack16 ? kTileBins / 2 : kTileBins;  // partial words per tile
+  const uint32_t lanes_per_row = words / 4;                      // one uint4 per lane per row
+  const uint32_t ngroups = blockDim.x / lanes_per_row;
+  const uint32_t grp = threadIdx.x / lanes_per_row, l = threadIdx.x % lanes_per_row;
+  const uint32_t Wtot = a.pack16 ? (a.U + 1) / 2 : a.U;
+  const uint64_t word0 = (uint64_t)tile * words + 4 * l;
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (grp < ngroups && word0 < Wtot) {
+    const uint32_t* base = a.partials + word0;
+    for (uint32_t r0 = grp; r0 < a.C; r0 += 8 * ngroups) {
+      uint4 x[8];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0;
-    const uint32_t Wtot = a.pack16 ? (a.U + 1) / 2 : a.U;
-    if (word0 < Wtot) {
-      for (uint32_t r = warp; r < a.C; r += nw) {
-        const uint4* p = reinterpret_cast<const uint4*>(a.partials + (uint64_t)r * a.ldw + word0);
-        uint4 x0 = __ldcg(p), x1 = __ldcg(p + 1);
-        uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t r = r0 + u * ngroups;
+        x[u] = r < a.C ? __ldcg(reinterpret_cast<const uint4*>(base + (uint64_t)r * a.ldw)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
         if (a.pack16) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) { acc[2 * j] += w[j] & 0xffffu; acc[2 * j + 1] += w[j] >> 16; }
+          acc[0] += x[u].x & 0xffffu; acc[1] += x[u].x >> 16; acc[2] += x[u].y & 0xffffu; acc[3] += x[u].y >> 16;
+          acc[4] += x[u].z & 0xffffu; acc[5] += x[u].z >> 16; acc[6] += x[u].w & 0xffffu; acc[7] += x[u].w >> 16;
         } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] += w[j];
+          acc[0] += x[u].x; acc[1] += x[u].y; acc[2] += x[u].z; acc[3] += x[u].w;
         }
       }
     }
-    const int per = a.pack16 ? 16 : 8;
-    for (int j = 0; j < per; ++j) part[warp][per * lane + j] = acc[j];
-    __syncthreads();
-    if (threadIdx.x < bins_per_tile) {
-      uint64_t sum = 0;
-      for (int w = 0; w < nw; ++w) sum += part[w][threadIdx.x];
-      hval = sum;
-    }
   }
-  const uint64_t bin = bin0 + threadIdx.x;
-  const bool own = threadIdx.x < bins_per_tile && bin < a.U;
-  if (own) {
-    if (a.C == 0) hval = a.Hsrc[bin];
-    if (use_ovf) {
-      hval += a.ovfH[bin];
-      a.ovfH_mut[bin] = 0;  // consumed: ovfH is zero again for the next call
-    }
-  } else {
-    hval = 0;
-  }
-  if (own && a.Hout) a.Hout[bin] = (uint32_t)(hval > 0xffffffffull ? 0xffffffffull : hval);
-  if (!a.do_scan) {
-    pdl_trigger();
-    return;
-  }
-
-  // ---- tile scan + decoupled look-back ---------------------------------------------------
-  uint64_t tile_total;
-  uint64_t excl_in_tile = block_excl_scan<uint64_t>(hval, tile_total, red);
-  if (warp == 0) {
-    uint64_t excl = 0;
-    if (tile == 0) {
-      if (lane == 0) lb_store(a.status, lb_pack(a.epoch, LB_FLAG_INC, tile_total));
-    } else {
-      if (lane == 0) lb_store(a.status + tile, lb_pack(a.epoch, LB_FLAG_AGG, tile_total));
-      excl = lookback(a.status, tile, a.epoch);
-      if (lane == 0) lb_store(a.status + tile, lb_pack(a.epoch, LB_FLAG_INC, excl + tile_total));
-    }
-    if (lane == 0) s_excl = excl;
+  // cross-group reduction through shared memory: scratch[g][bin]
+  __syncthreads();
+  if (grp < ngroups) {
+    uint32_t* dst = scratch + grp * kTileBins + (a.pack16 ? 8 * l : 4 * l);
+    reinterpret_cast<uint4*>(dst)[0] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+    if (a.pack16) reinterpret_cast<uint4*>(dst)[1] = make_uint4(acc[4], acc[5], acc[6], acc[7]);
   }
   __syncthreads();
-  const uint64_t pk = s_excl + excl_in_tile;  // P[bin]
+  uint64_t tile_sum = 0;
+  for (uint32_t j = threadIdx.x; j < kTileBins; j += blockDim.x) {
+    const uint64_t bin = (uint64_t)tile * kTileBins + j;
+    if (bin >= a.U) break;
+    uint32_t h = 0;
+    for (uint32_t g = 0; g < ngroups; ++g) h += scratch[g * kTileBins + j];
+    if (use_ovf) {
+      h += a.ovfH[bin];
+      a.ovfH[bin] = 0;  // consumed: ovfH is zero again for the next call
+    }
+    a.H[bin] = h;
+    tile_sum += h;
+  }
+  return block_sum<uint64_t>(tile_sum, red);
+}
+
+// Sum of H over one tile (phase A when H is given).
+__device__ __forceinline__ uint64_t sum_tile(const uint32_t* H, uint32_t U, uint32_t tile, uint64_t* red) {
+  uint64_t s = 0;
+  for (uint32_t j = threadIdx.x; j < kTileBins; j += blockDim.x) {
+    const uint64_t bin = (uint64_t)tile * kTileBins + j;
+    if (bin < U) s += __ldcg(H + bin);
+  }
+  return block_sum<uint64_t>(s, red);
+}
+
+// Phase B for one tile: P[bin] = offset + exclusive prefix within the tile; tfb scatter.
+// Requires blockDim.x >= kTileBins.  Returns offset + tile total.
+__device__ __forceinline__ uint64_t scan_tile(const ScanArgs& a, const uint32_t* H, uint32_t tile, uint64_t offset,
+                                              uint64_t* red) {
+  const uint64_t bin = (uint64_t)tile * kTileBins + threadIdx.x;
+  const bool own = threadIdx.x < kTileBins && bin < a.U;
+  const uint64_t h = own ? __ldcg(H + bin) : 0;
+  uint64_t tile_total;
+  const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
   if (own) {
+    const uint64_t pk = offset + ex;
     a.P[bin] = (uint32_t)pk;
-    // Output tiles whose first position t*T falls in [pk, pk + hval) start in this bin.
-    if (hval > 0) {
-      uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + hval - 1) / a.T;
-      if (t1 >= a.ntiles_out) t1 = a.ntiles_out - 1;
+    if (h > 0) {  // output tiles whose first position t*T falls in [pk, pk + h) start in this bin
+      const uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + h - 1) / a.T;
       for (uint64_t t = t0; t <= t1 && t < a.ntiles_out; ++t) a.tfb[t] = (uint32_t)bin;
     }
   }
-  const uint32_t ntiles = (a.U + bins_per_tile - 1) / bins_per_tile;
-  if (tile == ntiles - 1 && threadIdx.x == 0) {
-    const uint64_t total = s_excl + tile_total;
+  return offset + tile_total;
+}
+
+// Phase B for a co-resident grid (called by every CTA, all threads), after phase A left
+// `range` = this CTA's range total.
+__device__ __forceinline__ void scan_phase_b(const ScanArgs& a, const uint32_t* H, uint32_t tb0, uint32_t tb1,
+                                             uint64_t range, uint64_t* red) {
+  if (threadIdx.x == 0) a.range_tot[blockIdx.x] = range;
+  grid_barrier(a.bar);
+  phase_mark(a.pt, 6);
+  // this CTA's offset = Σ range totals of lower CTAs
+  uint64_t s = 0;
+  for (uint32_t j = threadIdx.x; j < blockIdx.x; j += blockDim.x) s += __ldcg(a.range_tot + j);
+  uint64_t off = block_sum<uint64_t>(s, red);
+  for (uint32_t t = tb0; t < tb1; ++t) off = scan_tile(a, H, t, off, red);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const uint64_t total = off;
     a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
     unsigned flags = 0;
     if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
@@ -136,6 +186,18 @@ __global__ void __launch_bounds__(kScanThreads) k_reduce_scan(ScanArgs a) {
     if (a.d_total) *a.d_total = total;
     *a.ws_total = total;
   }
+}
+
+// Standalone scan of a given H (global path, reconstruct API): persistent co-resident grid.
+__global__ void __launch_bounds__(kTileBins) k_scan(ScanArgs a) {
+  __shared__ uint64_t red[34];
+  pdl_wait();
+  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
+  uint32_t tb0, tb1;
+  my_tiles(ntiles, tb0, tb1);
+  uint64_t range = 0;
+  for (uint32_t t = tb0; t < tb1; ++t) range += sum_tile(a.Hsrc, a.U, t, red);
+  scan_phase_b(a, a.Hsrc, tb0, tb1, range, red);
   pdl_trigger();
 }
 

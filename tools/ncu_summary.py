@@ -1,0 +1,26 @@
+"""Summarise an ncu report: time, DRAM bytes, throughput, occupancy, top stall reasons."""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units = rows[0], rows[1]
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smsp__inst_executed_op_shared_atom.sum",
+        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_sector_hit_rate.pct", "lts__t_bytes.sum"]
+for r in rows[2:]:
+    print("==", r[hdr.index("Kernel Name")][:70])
+    for k in keys:
+        if k in hdr and r[hdr.index(k)] not in ("", "n/a"):
+            print(f"   {k:60s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
+    st = [(h, float(v)) for h, v in zip(hdr, r)
+          if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")
+          and v not in ("", "n/a")]
+    st.sort(key=lambda x: -x[1])
+    print("   stalls:", ", ".join(f"{h[34:-23]}={v:.2f}" for h, v in st[:6]))
