@@ -91,7 +91,7 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-constexpr size_t kSmemBudget = 227 * 1024 - 1024;  // dynamic smem per CTA (static smem aside)
+constexpr size_t kSmemBudget = 227 * 1024 - 2048;  // dynamic smem per CTA (static smem <= 2 KB)
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -130,7 +130,8 @@ struct dialsort_ctx_s {
   int device = 0;
   int nsm = 148;
   uint32_t epoch = 0;
-  DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, radix_tmp, radix_hist, radix_lb;
+  DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
+      radix_lb;
   DevStatus* host_status = nullptr;  // pinned mirror
   Profiler prof;
   int expand_occ = 4, scan_occ = 2;
@@ -256,6 +257,8 @@ int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
   if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
   if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  if ((rc = c->tsums.ensure(4ull * C * cdiv(U, kTileBins)))) return rc;
+  a.tsums = c->tsums.as<uint32_t>();
   a.partials = c->partials.as<uint32_t>();
   a.C = C;
   a.ldw = ldw;
@@ -405,7 +408,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
-                  &c->range_tot, &c->gridbar, &c->radix_tmp, &c->radix_hist, &c->radix_lb})
+                  &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt) cudaFree(c->pt);

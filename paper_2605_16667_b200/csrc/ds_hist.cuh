@@ -42,10 +42,8 @@ __host__ __device__ inline KeySpan make_span(const int32_t* keys, uint64_t n) {
   return s;
 }
 
-// Visit this CTA's keys as int4 groups: f4(v, int4 index of v), plus scalars f1(key, index)
-// for the unaligned head (CTA 0) and tail (last CTA).  32-bit vector indices (n4 < 2^30);
-// software-pipelined: the next batch of kHistUnroll vectors is in flight while the current
-// batch is ingested, so the load queue never drains between batches.
+// Visit this CTA's keys as int4 vectors f4(v, vector index), plus scalars f1(key, index) for
+// the unaligned head (CTA 0) and tail (last CTA).  32-bit vector indices (n4 < 2^30).
 template <typename F4, typename F1>
 __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1) {
   const uint32_t T = blockDim.x, G = gridDim.x;
@@ -58,6 +56,8 @@ __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1
   const int4* __restrict__ body = s.body();
   // Grid-stride over vectors (all SMs sweep the array together: measured faster than
   // contiguous per-CTA ranges with an up-front L2 bulk prefetch, 10 vs 12.7 us at c2).
+  // Software pipeline: the next batch is requested before the current one is ingested
+  // (measured faster than ping-pong / refill-after-consume variants, 10 vs 14 us at c2).
   const uint32_t n4 = (uint32_t)s.n4, stride = G * T;
   uint32_t i = blockIdx.x * T + threadIdx.x;
   int4 a[kHistUnroll];
@@ -97,6 +97,21 @@ __device__ __noinline__ uint32_t ingest4_checked(uint32_t* h, int4 v, uint64_t i
   return bad;
 }
 
+// Error path of the hot loop: re-read this thread's vectors and ingest, key by key, those
+// that hold an out-of-range key (the hot loop skipped them whole); returns #bad keys.
+template <bool PACK16>
+__device__ __noinline__ uint32_t ingest_deferred(uint32_t* h, const KeySpan& s, uint32_t U, DevStatus* st) {
+  const uint32_t stride = gridDim.x * blockDim.x, n4 = (uint32_t)s.n4;
+  const int4* body = s.body();
+  uint32_t bad = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int4 v = body[i];
+    if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)i, U, st);
+  }
+  return bad;
+}
+
+// Global-path ingestion of one key batch position with the warp CRN.  All 32 lanes call it
 // (the predicate `valid` marks lanes that carry a key; absent lanes never enter the CRN).
 __device__ __forceinline__ void crn_red(uint32_t* H, uint32_t k, bool valid) {
   uint32_t mask = __ballot_sync(FULL, valid);
@@ -179,24 +194,24 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
   // instruction are merged by the shared-memory atomic unit (the CRN's equality merge).
   const KeySpan s = make_span(keys, n);
   DevStatus* st = a.st;
-  uint32_t seen = 0, bad = 0;
-  // packed word of key k: k >> 1 (byte offset (2k) & ~3); increment 1 or 65536
+  uint32_t seen = 0, bad = 0, deferred = 0;
+  // packed word of key k: k >> 1 at byte offset (2k) & ~3; increment 1 or 65536
   auto add16 = [&](uint32_t k) {
-    atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh_hist) + ((k << 1) & ~3u)), 1u + (k & 1u) * 65535u);
+    atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh_hist) + ((k + k) & ~3u)), 1u + (k & 1u) * 65535u);
   };
-  auto f4 = [&](int4 v, uint32_t i4) {
-    seen += 4;
+  auto add32 = [&](uint32_t k) { atomicAdd(sh_hist + k, 1u); };
+  // Hot loop: a vector whose keys are all in [0,U) is ingested directly; a vector with an
+  // out-of-range key is deferred to an out-of-loop checked pass (error path only), which
+  // keeps calls and spills out of the loop body.
+  auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
       if (PACK16) {
         add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
       } else {
-        atomicAdd(sh_hist + (uint32_t)v.x, 1u);
-        atomicAdd(sh_hist + (uint32_t)v.y, 1u);
-        atomicAdd(sh_hist + (uint32_t)v.z, 1u);
-        atomicAdd(sh_hist + (uint32_t)v.w, 1u);
+        add32((uint32_t)v.x); add32((uint32_t)v.y); add32((uint32_t)v.z); add32((uint32_t)v.w);
       }
     } else {
-      bad += ingest4_checked<PACK16>(sh_hist, v, s.head + 4 * (uint64_t)i4, U, st);
+      deferred = 1;
     }
   };
   auto f1 = [&](uint32_t k, uint64_t idx) {
@@ -210,43 +225,73 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
     }
   };
   for_each_key4(s, f4, f1);
+  {
+    // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
+    const uint32_t stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n4 = (uint32_t)s.n4;
+    const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
+    seen += 4 * cnt;
+  }
+  if (deferred) bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
 
-  // Flush the private histogram as partial row blockIdx.x.
+  // Flush the private histogram as partial row blockIdx.x, and this row's per-tile sums
+  // (tsums[tile][row]) so that, after one barrier, every CTA knows its scan offsets.
+  // Warp w flushes whole tiles w, w+32, ... (64 or 128 uint4 each): coalesced 512-byte
+  // stores and one warp reduction per tile.
   uint4* row4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * ldw);
-  if (!PACK16) {
-    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) __stcg(row4 + i, h4[i]);
-  } else {
-    // Packed counters: a 16-bit field that wrapped loses >= 65535 from the field sum
-    // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.
-    unsigned long long fsum = 0;
-    for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) {
-      const uint4 w = h4[i];
-      fsum += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
-              (w.w & 0xffffu) + (w.w >> 16);
-      __stcg(row4 + i, w);
+  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
+  constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
+  const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  unsigned long long fsum = 0;
+  for (uint32_t t = threadIdx.x >> 5; t < ntiles; t += nwarps) {
+    uint32_t v = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < q_per_tile; j += 32) {
+      const uint32_t i = t * q_per_tile + j + lane;
+      if (i < W4) {
+        const uint4 w = h4[i];
+        __stcg(row4 + i, w);
+        if (PACK16)
+          v += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
+               (w.w & 0xffffu) + (w.w >> 16);
+        else
+          v += w.x + w.y + w.z + w.w;
+      }
     }
-    const uint64_t tot = block_sum<uint64_t>(fsum, red64);
+    v = warp_sum(v);
+    fsum += v;
+    if (lane == 0) __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
+  }
+  // (uint4 beyond the last tile are padding zeros and are never read by the merge)
+  if (PACK16) {
+    // Packed counters: a 16-bit field that wrapped loses >= 65535 from the field sum
+    // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.  On overflow the
+    // fallback zeroes the row and the CTA's tile sums are ignored (use_ovf path below).
+    const uint64_t tot = block_sum<uint64_t>(lane == 0 ? fsum : 0ull, red64);  // warp totals, once per warp
     const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
     if (tot != nvalid) hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch);
   }
   phase_mark(a.pt, 2);
-  grid_barrier(a.bar);  // every row (and any fallback contribution) is in L2
+  grid_barrier(a.bar);  // every row, tile sum (and any fallback contribution) is in L2
   phase_mark(a.pt, 3);
 
-  // Phase A: merge this CTA's tile range.
+  // Merge + scan this CTA's tile range.
   const bool use_ovf = ld_acquire_u32(&st->ovf_epoch) == a.epoch;
-  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
   uint32_t tb0, tb1;
   my_tiles(ntiles, tb0, tb1);
-  uint64_t range = 0;
-  for (uint32_t t = tb0; t < tb1; ++t) range += merge_tile(a, t, use_ovf, sh_hist, red64);
+  if (a.do_scan && !use_ovf) {
+    merge_scan_range(a, tb0, tb1, false, sh_hist, red64);  // one barrier in total
+  } else {
+    // histogram-only API, or a packed-counter overflow somewhere (tile sums incomplete):
+    // merge, then offsets from range totals after a second barrier
+    uint64_t range = 0;
+    for (uint32_t t = tb0; t < tb1; ++t) range += merge_tile(a, t, use_ovf, sh_hist, red64);
+    if (a.do_scan) scan_phase_b(a, a.H, tb0, tb1, range, red64);
+  }
   phase_mark(a.pt, 4);
-  // Phase B: offsets + scan -> P, tfb.
-  if (a.do_scan) scan_phase_b(a, a.H, tb0, tb1, range, red64);
-  phase_mark(a.pt, 5);
   pdl_trigger();
 }
 

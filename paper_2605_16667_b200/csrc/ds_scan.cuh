@@ -69,6 +69,7 @@ struct ScanArgs {
   GridBar* bar;
   uint32_t epoch;
   PhaseTimes* pt;            // nullable debug timing
+  uint32_t* tsums;           // [C][ntiles] per-row tile sums (fused path), or nullptr
 };
 
 // Tiles [tb0, tb1) of CTA b in a grid of G over ntiles (contiguous ranges).
@@ -176,6 +177,104 @@ __device__ __forceinline__ void scan_phase_b(const ScanArgs& a, const uint32_t* 
   uint64_t off = block_sum<uint64_t>(s, red);
   for (uint32_t t = tb0; t < tb1; ++t) off = scan_tile(a, H, t, off, red);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const uint64_t total = off;
+    a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
+    unsigned flags = 0;
+    if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
+    if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
+    if (flags) atomicOr(&a.st->flags, flags);
+    a.st->last_total = total;
+    if (a.d_total) *a.d_total = total;
+    *a.ws_total = total;
+  }
+}
+
+// Fused path, after the single grid barrier: this CTA's tile offset is the sum of every
+// row's tile sums over the tiles before its range (tsums, written during the flush); the
+// offset loads are issued before the partial-row loads so both share one L2 round trip,
+// and each tile is merged and scanned straight from registers (no re-read of H).
+__device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0, uint32_t tb1, bool use_ovf,
+                                                 uint32_t* scratch, uint64_t* red) {
+  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
+  // tsums is [tile][row]: the entries of tiles < tb0 are one contiguous block, read as uint4
+  // with all loads of a thread in flight together.
+  uint64_t s = 0;
+  const uint32_t cnt = a.C * tb0;
+  const uint32_t cnt4 = cnt / 4;
+  const uint4* ts4 = reinterpret_cast<const uint4*>(a.tsums);
+  for (uint32_t j0 = threadIdx.x; j0 < cnt4; j0 += 4 * blockDim.x) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = j0 + u * blockDim.x;
+      x[u] = j < cnt4 ? __ldcg(ts4 + j) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += (uint64_t)x[u].x + x[u].y + x[u].z + x[u].w;
+  }
+  for (uint32_t j = 4 * cnt4 + threadIdx.x; j < cnt; j += blockDim.x) s += __ldcg(a.tsums + j);
+  uint64_t off = block_sum<uint64_t>(s, red);
+  for (uint32_t t = tb0; t < tb1; ++t) {
+    // merge: per-group partial sums into scratch[g][bin] (as merge_tile)
+    const uint32_t words = a.pack16 ? kTileBins / 2 : kTileBins;
+    const uint32_t lanes_per_row = words / 4;
+    const uint32_t ngroups = blockDim.x / lanes_per_row;
+    const uint32_t grp = threadIdx.x / lanes_per_row, l = threadIdx.x % lanes_per_row;
+    const uint32_t Wtot = a.pack16 ? (a.U + 1) / 2 : a.U;
+    const uint64_t word0 = (uint64_t)t * words + 4 * l;
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (grp < ngroups && word0 < Wtot) {
+      const uint32_t* base = a.partials + word0;
+      for (uint32_t r0 = grp; r0 < a.C; r0 += 10 * ngroups) {  // 148 rows / 16 groups: one round
+        uint4 x[10];
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const uint32_t r = r0 + u * ngroups;
+          x[u] = r < a.C ? __ldcg(reinterpret_cast<const uint4*>(base + (uint64_t)r * a.ldw)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          if (a.pack16) {
+            acc[0] += x[u].x & 0xffffu; acc[1] += x[u].x >> 16; acc[2] += x[u].y & 0xffffu; acc[3] += x[u].y >> 16;
+            acc[4] += x[u].z & 0xffffu; acc[5] += x[u].z >> 16; acc[6] += x[u].w & 0xffffu; acc[7] += x[u].w >> 16;
+          } else {
+            acc[0] += x[u].x; acc[1] += x[u].y; acc[2] += x[u].z; acc[3] += x[u].w;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (grp < ngroups) {
+      uint32_t* dst = scratch + grp * kTileBins + (a.pack16 ? 8 * l : 4 * l);
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+      if (a.pack16) reinterpret_cast<uint4*>(dst)[1] = make_uint4(acc[4], acc[5], acc[6], acc[7]);
+    }
+    __syncthreads();
+    // thread j owns bin j of the tile: sum the groups, scan, write H and P, index tfb
+    const uint64_t bin = (uint64_t)t * kTileBins + threadIdx.x;
+    const bool own = threadIdx.x < kTileBins && bin < a.U;
+    uint32_t h = 0;
+    if (own) {
+      for (uint32_t g = 0; g < ngroups; ++g) h += scratch[g * kTileBins + threadIdx.x];
+      if (use_ovf) {
+        h += a.ovfH[bin];
+        a.ovfH[bin] = 0;
+      }
+      a.H[bin] = h;
+    }
+    uint64_t tile_total;
+    const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
+    if (own) {
+      const uint64_t pk = off + ex;
+      a.P[bin] = (uint32_t)pk;
+      if (h > 0) {
+        const uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + h - 1) / a.T;
+        for (uint64_t q = t0; q <= t1 && q < a.ntiles_out; ++q) a.tfb[q] = (uint32_t)bin;
+      }
+    }
+    off += tile_total;
+  }
+  if (tb1 == ntiles && tb1 > tb0 && threadIdx.x == 0) {
     const uint64_t total = off;
     a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
     unsigned flags = 0;
