@@ -200,12 +200,39 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
     atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh_hist) + ((k + k) & ~3u)), 1u + (k & 1u) * 65535u);
   };
   auto add32 = [&](uint32_t k) { atomicAdd(sh_hist + k, 1u); };
+  auto addn = [&](uint32_t k, uint32_t c) {  // c copies of key k (CRN output)
+    if (PACK16)
+      atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh_hist) + ((k + k) & ~3u)), c << ((k & 1u) << 4));
+    else
+      atomicAdd(sh_hist + k, c);
+  };
   // Hot loop: a vector whose keys are all in [0,U) is ingested directly; a vector with an
   // out-of-range key is deferred to an out-of-loop checked pass (error path only), which
   // keeps calls and spills out of the loop body.
+  //
+  // CRN for runs (def:crn_level, lem:crn; lane-local accumulation P:859-864): a vector of 4
+  // equal keys is one lane pair (k, 4).  When every active lane holds such a run (sorted /
+  // reverse input), the warp groups its lanes by equality — one or two distinct keys are
+  // found with a min/max reduction (REDUX) and ballots — and each group adds its total with
+  // a single atomic.  Random inputs never take this path and pay one ballot per vector.
   auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
-      if (PACK16) {
+      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
+      const uint32_t act = __activemask();
+      const uint32_t runs = __ballot_sync(act, run4);
+      if (runs == act) {
+        const uint32_t k = (uint32_t)v.x, lane = threadIdx.x & 31;
+        const uint32_t kmin = __reduce_min_sync(act, k), kmax = __reduce_max_sync(act, k);
+        const uint32_t gmin = __ballot_sync(act, k == kmin), gmax = __ballot_sync(act, k == kmax);
+        if ((gmin | gmax) == act) {  // at most two distinct keys in the warp
+          if (lane == (uint32_t)(__ffs(gmin) - 1)) addn(kmin, 4u * __popc(gmin));
+          if (kmax != kmin && lane == (uint32_t)(__ffs(gmax) - 1)) addn(kmax, 4u * __popc(gmax));
+        } else {
+          addn(k, 4u);
+        }
+      } else if (run4) {
+        addn((uint32_t)v.x, 4u);
+      } else if (PACK16) {
         add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
       } else {
         add32((uint32_t)v.x); add32((uint32_t)v.y); add32((uint32_t)v.z); add32((uint32_t)v.w);
