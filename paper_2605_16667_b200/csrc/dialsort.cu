@@ -47,7 +47,7 @@ enum KernelId {
   KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
-                                             "k_scan", "k_expand", "k_radix_hist4", "k_radix_pass",
+                                             "k_scan", "k_expand", "k_radix_hist0", "k_radix_pass",
                                              "k_range_count", "k_crn_resolve"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
@@ -134,7 +134,7 @@ struct dialsort_ctx_s {
       radix_lb;
   DevStatus* host_status = nullptr;  // pinned mirror
   Profiler prof;
-  int expand_occ = 4, scan_occ = 2;
+  int expand_occ = 4, scan_occ = 2, radix_occ = 1, radix2_occ = 1;
   PhaseTimes* pt = nullptr;  // debug phase timing (DIALSORT_PHASE_TIMING=1)
 };
 
@@ -159,6 +159,10 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
   int occ = 0;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass, kRadixThreads, sizeof(RadixSmem)));
+  c->radix_occ = occ > 0 ? occ : 1;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass2, kRadixThreads, sizeof(RadixSmem)));
+  c->radix2_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kExpandThreads, 0));
   c->expand_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan, kTileBins, 0));
@@ -177,8 +181,6 @@ int ctx_init(dialsort_ctx c) {
 uint32_t next_epoch(dialsort_ctx c, cudaStream_t s) {
   c->epoch = (c->epoch + 1) & 0xffffffu;
   if (c->epoch == 0) c->epoch = 1;
-  // radix tags are (4*epoch + pass) mod 2^24: clear their array whenever those wrap
-  if ((c->epoch & 0x3fffffu) == 0 && c->radix_lb.p) cudaMemsetAsync(c->radix_lb.p, 0, c->radix_lb.bytes, s);
   return c->epoch;
 }
 
@@ -296,32 +298,54 @@ int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, i
   return DIALSORT_OK;
 }
 
-// Host-side enqueue of DialSort-Radix: K7 once, then K8 for p = 0..3 ping-ponging tmp/out.
-int radix_enqueue(int nsm, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, DBuf& hist, DBuf& lb,
-                  uint32_t epoch, cudaStream_t s) {
-  const uint64_t ntiles = (n + kRadixTile - 1) / kRadixTile;
-  if (ntiles > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "n too large for radix");
+// Host-side enqueue of DialSort-Radix.  Default: 4 reduce-then-scan passes (k_radix_pass2,
+// co-resident grid).  DIALSORT_RADIX=onesweep selects the single-sweep variant (K7 + 4 x K8).
+bool radix_onesweep() {
+  static const bool v = [] {
+    const char* e = getenv("DIALSORT_RADIX");
+    return e && strcmp(e, "onesweep") == 0;
+  }();
+  return v;
+}
+
+int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, cudaStream_t s) {
+  if (n >= (1ull << 30)) return fail(DIALSORT_E_INVALID_ARG, "radix path supports n < 2^30 per call");
   int rc;
-  if ((rc = hist.ensure(4 * 1024 + 64))) return rc;
-  if ((rc = lb.ensure(8ull * ntiles * 256, true))) return rc;
-  uint32_t* gh = hist.as<uint32_t>();
-  uint32_t* ctrs = gh + 1024;
-  uint64_t* st = lb.as<uint64_t>();
-  cudaError_t e;
-  if ((e = launch_k(KID_ZERO, k_zero, dim3(1), dim3(256), 0, s, gh, (uint64_t)1024)) != cudaSuccess)
-    return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
-  uint64_t want = (n / 4 + 1 + 512 * 4 - 1) / (512 * 4);
-  uint32_t grid = (uint32_t)(want < (uint64_t)nsm * 2 ? want : (uint64_t)nsm * 2);
-  if ((e = launch_k(KID_RADIX_HIST4, k_radix_hist4, dim3(grid), dim3(512), 0, s, keys, n, gh, ctrs)) != cudaSuccess)
-    return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
   const uint32_t* src = reinterpret_cast<const uint32_t*>(keys);
   uint32_t* bufs[2] = {reinterpret_cast<uint32_t*>(tmp), reinterpret_cast<uint32_t*>(out)};
+  if (!radix_onesweep()) {
+    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(n, kRadixTile), (uint64_t)c->nsm * c->radix2_occ));
+    if ((rc = c->radix_hist.ensure(8ull * 256 * G + 4 * 256 + 64))) return rc;
+    Radix2Ws w;
+    w.cnt = c->radix_hist.as<uint32_t>();
+    w.pre = w.cnt + 256 * G;
+    w.total = w.pre + 256 * G;
+    w.bar = reinterpret_cast<GridBarR*>(c->gridbar.as<char>() + 32);
+    w.pt = c->pt;
+    for (int p = 0; p < 4; ++p) {
+      uint32_t* dst = bufs[p & 1];
+      DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass2, dim3(G), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
+                       (uint32_t)n, p, w));
+      src = dst;
+    }
+    return DIALSORT_OK;
+  }
+  const uint32_t ntiles = (uint32_t)cdiv(n, kRadixTile);
+  if ((rc = c->radix_hist.ensure(4 * 1024 + 64))) return rc;
+  if ((rc = c->radix_lb.ensure(2ull * 4 * 256 * ntiles + 16))) return rc;
+  RadixWs w;
+  w.ghist = c->radix_hist.as<uint32_t>();
+  w.ctrs = w.ghist + 1024;
+  w.status = c->radix_lb.as<uint32_t>();
+  w.ntiles = ntiles;
+  const uint32_t g0 = (uint32_t)std::min<uint64_t>(cdiv(n / 4 + 1, 512ull * 4), (uint64_t)c->nsm * 4);
+  DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(1), dim3(256), 0, s, w.ghist, (uint64_t)256));
+  DS_CUDA(launch_k(KID_RADIX_HIST4, k_radix_hist0, dim3(g0), dim3(512), 0, s, keys, n, w));
+  const uint32_t gp = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)c->nsm * c->radix_occ);
   for (int p = 0; p < 4; ++p) {
     uint32_t* dst = bufs[p & 1];
-    const uint32_t tag = (epoch * 4u + (uint32_t)p) & 0xffffffu;
-    if ((e = launch_k(KID_RADIX_PASS, k_radix_pass, dim3((uint32_t)ntiles), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst, n, p,
-                    (const uint32_t*)gh, st, ctrs + p, tag)) != cudaSuccess)
-      return fail(DIALSORT_E_CUDA, cudaGetErrorString(e));
+    DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass, dim3(gp), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
+                     (uint32_t)n, p, w));
     src = dst;
   }
   return DIALSORT_OK;
@@ -518,7 +542,8 @@ int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, i
   const uint32_t epoch = next_epoch(c, s);
   if (n == 0) return DIALSORT_OK;
   if ((rc = c->radix_tmp.ensure(4ull * n + 16))) return rc;
-  return radix_enqueue(c->nsm, keys, n, out, c->radix_tmp.as<int32_t>(), c->radix_hist, c->radix_lb, epoch, s);
+  (void)epoch;
+  return radix_enqueue(c, keys, n, out, c->radix_tmp.as<int32_t>(), s);
 }
 
 int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, uint32_t a, uint32_t b,
