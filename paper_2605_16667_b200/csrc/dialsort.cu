@@ -293,8 +293,8 @@ int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, i
   const uint64_t wave = (uint64_t)c->nsm * c->expand_occ;  // persistent grid: one wave
   const uint32_t grid = (uint32_t)(ntiles_out < wave ? ntiles_out : wave);
   DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3(grid), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
-                   c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out,
-                   c->pt));
+                     c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out,
+                     c->pt));
   return DIALSORT_OK;
 }
 

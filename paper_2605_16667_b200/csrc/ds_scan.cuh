@@ -213,6 +213,7 @@ __device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0
     for (int u = 0; u < 4; ++u) s += (uint64_t)x[u].x + x[u].y + x[u].z + x[u].w;
   }
   for (uint32_t j = 4 * cnt4 + threadIdx.x; j < cnt; j += blockDim.x) s += __ldcg(a.tsums + j);
+  phase_mark(a.pt, 5);  // offset loads issued (debug)
   uint64_t off = block_sum<uint64_t>(s, red);
   for (uint32_t t = tb0; t < tb1; ++t) {
     // merge: per-group partial sums into scratch[g][bin] (as merge_tile)
@@ -243,6 +244,7 @@ __device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0
         }
       }
     }
+    phase_mark(a.pt, 6);  // partial rows summed in registers (debug)
     __syncthreads();
     if (grp < ngroups) {
       uint32_t* dst = scratch + grp * kTileBins + (a.pack16 ? 8 * l : 4 * l);

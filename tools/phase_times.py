@@ -15,7 +15,7 @@ dev = torch.device("cuda:0")
 keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
 outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=cfg["U"])
-names = ["ingest", "sync", "flush", "barrier1", "merge_scan", "-", "barrier2(fallback)", "expand_start"]
+names = ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"]
 for rep in range(3):
     ctx.debug_phase_ns()
     for i in range(1):  # one isolated step (previous work drained)
