@@ -55,7 +55,7 @@ def load_peaks():
 class ClockSampler:
     """NVML SM clock + throttle-reason sampler (runs during the timed region)."""
 
-    def __init__(self, index: int, period: float = 0.005):
+    def __init__(self, index: int, period: float = 0.002):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period, self.index = period, index
         self._stop = threading.Event()
@@ -316,16 +316,25 @@ def main():
     tot = sum(kern_share.values()) or 1.0
     dom = max(kern_share, key=kern_share.get) if kern_share else None
     # algorithmic bytes per launch of each kernel
-    kb = {
-        "k_hist_smem32": 4 * n_loc, "k_hist_smem16": 4 * n_loc, "k_hist_global": 4 * n_loc,
+    kb = {  # fused ingest+merge+scan: keys read + H and P written
+        "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
         "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),
-        "k_radix_pass": 8 * n_loc, "k_radix_hist4": 4 * n_loc, "k_zero": 4 * U,
+        "k_radix_pass": 8 * n_loc, "k_radix_hist0": 4 * n_loc, "k_zero": 4 * U,
     }
+    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            tk = json.load(f)["kernels"].get(dom or "", None)
+        if tk and args.config == "c2" and G == 1:
+            traffic = tk["dram_read_bytes"] + tk["dram_write_bytes"]
+    except Exception:
+        traffic = None
     roof = None
     if dom:
         ach = kb.get(dom, 0) / (kern_avg[dom] * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                 "alg_bytes_per_launch": kb.get(dom, 0), "avg_ms": kern_avg[dom],
                 "share_of_step": kern_share[dom] / tot,
                 "kernels_ms": {k: round(v, 5) for k, v in kern_avg.items()}}
