@@ -155,8 +155,10 @@ int ctx_init(dialsort_ctx c) {
   if ((rc = c->ws_total.ensure(64, true))) return rc;
   if ((rc = c->gridbar.ensure(64, true))) return rc;
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
   int occ = 0;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass, kRadixThreads, sizeof(RadixSmem)));
@@ -200,6 +202,17 @@ HistPath choose_path(uint32_t U) {
   if (U <= kSmem32MaxBins) return HistPath::Smem32;
   if (U <= kSmem16MaxBins) return HistPath::Smem16;
   return HistPath::Global;
+}
+
+// Histogram ingestion variant: register pipeline (default) or TMA-fed ring (DIALSORT_HIST=tma,
+// kept for A/B: measured 12.7 vs 10.2 us ingest at c2 — 3 x 32 KB stages fit beside the
+// 128 KB histogram, fewer bytes in flight than 2 x 4 int4 per thread).
+bool hist_use_tma() {
+  static const bool tma = [] {
+    const char* e = getenv("DIALSORT_HIST");
+    return e && strcmp(e, "tma") == 0;
+  }();
+  return tma;
 }
 
 // Common scan arguments (workspace pointers, output tiling, size check).
@@ -253,9 +266,16 @@ int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   const bool pack = path == HistPath::Smem16;
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);
-  const size_t smem = std::max<size_t>(4ull * ldw, 32 * 1024);
+  const size_t hist_bytes = std::max<size_t>(4ull * ldw, 32 * 1024);
+  // TMA-fed ingestion only on request (DIALSORT_HIST=tma)
+  uint32_t stages = 0;
+  if (hist_use_tma()) {
+    stages = (uint32_t)std::min<size_t>(kMaxStages, (kSmemBudget - hist_bytes) / kChunkBytes);
+    if (stages < 2) stages = 0;
+  }
+  const size_t smem = hist_bytes + (size_t)stages * kChunkBytes;
   const uint64_t n4 = n / 4 + 1;
-  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);  // >= 2 load batches per CTA
+  const uint64_t want = stages ? cdiv(4 * n4, kChunkBytes / 4) : cdiv(n4, 1024ull * kHistUnroll * 2);
   const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
   if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
   if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
@@ -267,10 +287,15 @@ int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   a.pack16 = pack;
   a.ovfH = c->ovfH.as<uint32_t>();
   a.H = H;
-  if (pack)
-    DS_CUDA(launch_k(KID_HIST_SMEM16, k_hist_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a));
+  const int kid = pack ? KID_HIST_SMEM16 : KID_HIST_SMEM32;
+  if (pack && stages)
+    DS_CUDA(launch_k(kid, k_hist_fused<true, true>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
+  else if (pack)
+    DS_CUDA(launch_k(kid, k_hist_fused<true, false>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
+  else if (stages)
+    DS_CUDA(launch_k(kid, k_hist_fused<false, true>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
   else
-    DS_CUDA(launch_k(KID_HIST_SMEM32, k_hist_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a));
+    DS_CUDA(launch_k(kid, k_hist_fused<false, false>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
   return DIALSORT_OK;
 }
 

@@ -86,6 +86,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
+// (or the hint elapses) instead of spinning.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // Bulk copy of `bytes` (multiple of 16, 16-byte aligned ends) global -> shared, completing
 // on `bar` (transaction bytes), with an L2 evict-first hint: keys are streamed once.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {

@@ -21,6 +21,9 @@ namespace ds {
 constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
 constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
+constexpr uint32_t kChunkBytes = 32768;     // TMA path: 8192 keys per chunk
+constexpr uint32_t kChunkVecs = kChunkBytes / 16;
+constexpr uint32_t kMaxStages = 4;
 
 // Key layout shared by every pass over `keys`: `head` scalars before the first 16-byte
 // boundary, `n4` aligned int4 vectors, `tail` scalars.  CTA 0 takes the head, the last CTA
@@ -79,6 +82,67 @@ __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1
   }
 }
 
+// TMA-fed traversal: the aligned body is cut into kChunkBytes chunks; CTA c consumes chunks
+// c, c+G, ... through a ring of `stages` shared-memory slots filled by cp.async.bulk (one
+// elected thread issues, an mbarrier per slot signals "full", a second "empty" collects one
+// arrival per warp).  Each lane takes 2 vectors of each chunk; keys stream through the TMA
+// engine without occupying registers, so all 32 warps can issue atomics.
+
+template <typename F4, typename F1>
+__device__ __forceinline__ uint32_t for_each_key_tma(const KeySpan& s, unsigned char* ring, uint32_t stages,
+                                                 uint64_t* full_bar, uint64_t* empty_bar, F4&& f4, F1&& f1) {
+  const uint32_t G = gridDim.x;
+  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
+  if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
+    uint64_t i = s.head + 4 * s.n4 + threadIdx.x;
+    f1((uint32_t)s.keys[i], i);
+  }
+  const uint64_t nbytes = 16ull * s.n4;
+  const uint32_t nchunks = (uint32_t)((nbytes + kChunkBytes - 1) / kChunkBytes);
+  const uint32_t mine = blockIdx.x < nchunks ? (nchunks - blockIdx.x + G - 1) / G : 0;
+  const char* body = reinterpret_cast<const char*>(s.body());
+  const uint64_t pol = l2_evict_first_policy();
+  auto chunk_bytes = [&](uint32_t k) -> uint32_t {
+    const uint64_t off = (uint64_t)(blockIdx.x + k * G) * kChunkBytes;
+    const uint64_t rem = nbytes - off;
+    return (uint32_t)(rem < kChunkBytes ? rem : kChunkBytes);
+  };
+  auto issue = [&](uint32_t k) {
+    const uint32_t slot = k % stages, b = chunk_bytes(k);
+    mbar_arrive_expect_tx(&full_bar[slot], b);
+    tma_load_1d(ring + (size_t)slot * kChunkBytes, body + (uint64_t)(blockIdx.x + k * G) * kChunkBytes, b,
+                &full_bar[slot], pol);
+  };
+  if (threadIdx.x == 0)
+    for (uint32_t k = 0; k < mine && k < stages; ++k) issue(k);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t nvec = 0;
+  for (uint32_t k = 0; k < mine; ++k) {
+    const uint32_t slot = k % stages, parity = (k / stages) & 1u;
+    mbar_wait_sleep(&full_bar[slot], parity);
+    const uint32_t nv = chunk_bytes(k) / 16;
+    const int4* src = reinterpret_cast<const int4*>(ring + (size_t)slot * kChunkBytes);
+    const uint32_t v0 = warp * 64 + lane, v1 = v0 + 32;
+    const uint32_t i4 = (blockIdx.x + k * G) * (kChunkBytes / 16);
+    if (v1 < nv) {
+      const int4 x0 = src[v0], x1 = src[v1];
+      f4(x0, i4 + v0);
+      f4(x1, i4 + v1);
+      nvec += 2;
+    } else if (v0 < nv) {
+      f4(src[v0], i4 + v0);
+      nvec += 1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    if (threadIdx.x == 0 && k + stages < mine) {
+      mbar_wait_sleep(&empty_bar[slot], parity);  // every warp has read this slot
+      issue(k + stages);
+    }
+  }
+  return nvec;
+}
+
 // Slow path of an int4 group holding at least one key outside [0,U): ingest the valid keys
 // one by one and record the bad ones (never taken on valid input; kept out of line).
 template <bool PACK16>
@@ -97,16 +161,29 @@ __device__ __noinline__ uint32_t ingest4_checked(uint32_t* h, int4 v, uint64_t i
   return bad;
 }
 
-// Error path of the hot loop: re-read this thread's vectors and ingest, key by key, those
-// that hold an out-of-range key (the hot loop skipped them whole); returns #bad keys.
-template <bool PACK16>
+// Error path of the hot loop: re-read the vectors this thread owns and ingest, key by key,
+// those that hold an out-of-range key (the hot loop skipped them whole); returns #bad keys.
+// CHUNK: ownership of the TMA traversal (lane owns vectors warp*64+lane and +32 of each of its
+// CTA's chunks); otherwise the register traversal's grid stride.
+template <bool PACK16, bool CHUNK>
 __device__ __noinline__ uint32_t ingest_deferred(uint32_t* h, const KeySpan& s, uint32_t U, DevStatus* st) {
-  const uint32_t stride = gridDim.x * blockDim.x, n4 = (uint32_t)s.n4;
+  const uint32_t n4 = (uint32_t)s.n4;
   const int4* body = s.body();
   uint32_t bad = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+  auto one = [&](uint32_t i) {
     const int4 v = body[i];
     if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)i, U, st);
+  };
+  if (CHUNK) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t c = blockIdx.x; c * kChunkVecs < n4; c += gridDim.x) {
+      const uint64_t i0 = c * kChunkVecs + warp * 64 + lane;
+      if (i0 < n4) one((uint32_t)i0);
+      if (i0 + 32 < n4) one((uint32_t)(i0 + 32));
+    }
+  } else {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) one(i);
   }
   return bad;
 }
@@ -121,9 +198,10 @@ __device__ __forceinline__ void crn_red(uint32_t* H, uint32_t k, bool valid) {
   }
 }
 
-// Same traversal as for_each_key but warp-synchronous (every lane runs every iteration),
-// for the CRN paths.  f(key, index, valid).
-template <typename F>
+// The keys this CTA owns, warp-synchronously (every lane runs every iteration), for the CRN
+// paths: f(key, index, valid).  CHUNK selects the TMA traversal's ownership (whole chunks
+// c, c+G, ...), otherwise the grid stride of the register traversal.
+template <bool CHUNK = false, typename F>
 __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
   const uint64_t T = blockDim.x, G = gridDim.x;
   {
@@ -136,33 +214,35 @@ __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
     if (threadIdx.x < 32) f(v ? (uint32_t)s.keys[i] : 0u, i, v);
   }
   const int4* body = s.body();
-  const uint64_t stride = G * T;
-  const uint64_t warp_base = blockIdx.x * T + (threadIdx.x & ~31u);
-  for (uint64_t w = warp_base; w < s.n4; w += kHistUnroll * stride) {
-    int4 v[kHistUnroll];
-    bool ok[kHistUnroll];
-#pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      uint64_t i = w + (threadIdx.x & 31) + u * stride;
-      ok[u] = i < s.n4;
-      v[u] = ok[u] ? ld_stream4(body + i) : make_int4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      uint64_t b = s.head + 4 * (w + (threadIdx.x & 31) + u * stride);
-      f((uint32_t)v[u].x, b, ok[u]);
-      f((uint32_t)v[u].y, b + 1, ok[u]);
-      f((uint32_t)v[u].z, b + 2, ok[u]);
-      f((uint32_t)v[u].w, b + 3, ok[u]);
+  auto vec = [&](uint64_t i, bool ok) {
+    const int4 v = ok ? ld_stream4(body + i) : make_int4(0, 0, 0, 0);
+    const uint64_t b = s.head + 4 * i;
+    f((uint32_t)v.x, b, ok);
+    f((uint32_t)v.y, b + 1, ok);
+    f((uint32_t)v.z, b + 2, ok);
+    f((uint32_t)v.w, b + 3, ok);
+  };
+  if (CHUNK) {
+    for (uint64_t c = blockIdx.x; c * kChunkVecs < s.n4; c += G)
+      for (uint32_t j = 0; j < kChunkVecs; j += T) {
+        const uint64_t i = c * kChunkVecs + j + threadIdx.x;
+        vec(i, i < s.n4);
+      }
+  } else {
+    const uint64_t stride = G * T;
+    for (uint64_t w = blockIdx.x * T + (threadIdx.x & ~31u); w < s.n4; w += stride) {
+      const uint64_t i = w + (threadIdx.x & 31);
+      vec(i, i < s.n4);
     }
   }
 }
+template <bool CHUNK>
 __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
                                                     uint32_t U, DevStatus* st, uint32_t epoch) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
-  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
+  for_each_key_warp<CHUNK>(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
 }
 
 // ---- shared-memory paths: ingestion + merge + scan in one co-resident grid ------------------
@@ -175,10 +255,12 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 //          and the expand index tfb (skipped for the histogram-only API).
 // One CTA per SM (1024 threads); the grid (<= #SMs) is co-resident by construction.
 // Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
-template <bool PACK16>
-__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a) {
-  extern __shared__ __align__(16) uint32_t sh_hist[];
+template <bool PACK16, bool TMA>
+__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
+                                                       uint32_t stages) {
+  extern __shared__ __align__(128) uint32_t sh_hist[];
   __shared__ uint64_t red64[34];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
   phase_mark(a.pt, -1);
   const uint32_t U = a.U, ldw = a.ldw;
@@ -251,15 +333,26 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
       ++bad;
     }
   };
-  for_each_key4(s, f4, f1);
-  {
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      for (uint32_t q = 0; q < stages; ++q) {
+        mbar_init(&full_bar[q], 1);
+        mbar_init(&empty_bar[q], blockDim.x / 32);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+    seen += 4 * for_each_key_tma(s, reinterpret_cast<unsigned char*>(sh_hist) + 4ull * max(ldw, 8192u), stages,
+                                 full_bar, empty_bar, f4, f1);
+  } else {
+    for_each_key4(s, f4, f1);
     // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
     const uint32_t stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n4 = (uint32_t)s.n4;
     const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
     seen += 4 * cnt;
   }
-  if (deferred) bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
+  if (deferred) bad += ingest_deferred<PACK16, TMA>(sh_hist, s, U, st);
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
@@ -299,7 +392,7 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
     // fallback zeroes the row and the CTA's tile sums are ignored (use_ovf path below).
     const uint64_t tot = block_sum<uint64_t>(lane == 0 ? fsum : 0ull, red64);  // warp totals, once per warp
     const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
-    if (tot != nvalid) hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch);
+    if (tot != nvalid) hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
   }
   phase_mark(a.pt, 2);
   grid_barrier(a.bar);  // every row, tile sum (and any fallback contribution) is in L2
