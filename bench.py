@@ -292,12 +292,6 @@ def main():
         ms = float(t.item())
     ms_step = ms / args.steps
     value = n / (ms_step * 1e-3)
-    if radix:
-        launches_per_step = 6
-    elif G == 1:
-        launches_per_step = 2 if U <= 98304 else 4           # fused hist+merge+scan, expand
-    else:
-        launches_per_step = (1 if U <= 98304 else 2) + 2     # local hist; scan + expand
     peak, peak_kind = load_peaks()
 
     # ---- per-kernel live timing (separate pass: event pairs disable the PDL overlap) -------
@@ -308,6 +302,9 @@ def main():
     torch.cuda.synchronize()
     ctx.profile(False)
     recs = ctx.profile_read()
+    # our kernels per step, counted from the launch records of the profiled pass (the
+    # profiler records every kernel the C ABI enqueues; NCCL collectives are not ours)
+    launches_per_step = len(recs) / max(prof_steps, 1)
     per = {}
     for name, t in recs:
         per.setdefault(name, []).append(t)
@@ -316,7 +313,9 @@ def main():
     tot = sum(kern_share.values()) or 1.0
     dom = max(kern_share, key=kern_share.get) if kern_share else None
     # algorithmic bytes per launch of each kernel
-    kb = {  # fused ingest+merge+scan: keys read + H and P written
+    kb = {  # k_sort_fused = the whole step (keys read, out written, H and P written + read)
+        "k_sort_fused": 8 * n_loc + 8 * U,
+        # two-kernel pipeline: fused ingest+merge+scan (keys read + H and P written), expand
         "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
         "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),
         "k_radix_pass": 8 * n_loc, "k_radix_hist0": 4 * n_loc, "k_zero": 4 * U,
@@ -324,7 +323,9 @@ def main():
     # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        import glob
+        tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+        with open(tfiles[-1]) as f:
             tk = json.load(f)["kernels"].get(dom or "", None)
         if tk and args.config == "c2" and G == 1:
             traffic = tk["dram_read_bytes"] + tk["dram_write_bytes"]
@@ -379,7 +380,7 @@ def main():
                        if G > 1 else "single GPU",
                        "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "verified": verified,
+            "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary(), "verified": verified,
         }
         print(json.dumps(line), flush=True)
     if G > 1:

@@ -130,9 +130,14 @@ int dialsort_profile_enable(dialsort_ctx ctx, int enable);
 int dialsort_profile_read(dialsort_ctx ctx, int max, int* kernel_ids, float* ms);
 const char* dialsort_kernel_name(int kernel_id);
 /* Debug: with DIALSORT_PHASE_TIMING=1 in the environment at context creation, the fused
- * histogram kernel records %globaltimer phase stamps (max over CTAs); this copies the 8
- * phase times in ns relative to the earliest CTA start into out8 (host) and resets them. */
-int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out8);
+ * kernels record %globaltimer phase stamps; this copies 16 values in ns relative to the
+ * earliest CTA start into out16 (host): [0..7] the latest CTA's arrival at phase 0..7,
+ * [8..15] the earliest CTA's (0 = phase not reached), and resets them. */
+int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out16);
+/* Debug: raw per-CTA stamps of the most recent launches (9 per CTA: start, phase 0..7; ns
+ * after the earliest start, 0 = not reached) into out[max_ctas * 9] (host); returns the number
+ * of CTAs copied, or -status.  Reading resets the stamps (as dialsort_debug_phase_ns). */
+int dialsort_debug_phase_cta(dialsort_ctx ctx, uint64_t* out, int max_ctas);
 
 /* ---- test entry: the warp CRN primitive on explicit lane batches ---------------------- */
 /* lane_keys: int32[32*n_batches]; active: uint32[n_batches] lane masks.  For each batch, the

@@ -162,11 +162,21 @@ class Context:
         return [(_L.dialsort_kernel_name(int(i)).decode(), float(t)) for i, t in zip(ids[:n], ms[:n])]
 
     def debug_phase_ns(self):
-        """Phase stamps of the fused kernel (DIALSORT_PHASE_TIMING=1), ns from the first CTA start."""
+        """Phase stamps of the fused kernel (DIALSORT_PHASE_TIMING=1), ns from the first CTA start:
+        [latest CTA arrival at phase 0..7] + [earliest CTA arrival at phase 0..7]."""
         import numpy as np
-        out = np.zeros(8, dtype=np.uint64)
+        out = np.zeros(16, dtype=np.uint64)
         _check(_L.dialsort_debug_phase_ns(self._h, out.ctypes.data_as(ctypes.c_void_p)))
         return out.tolist()
+
+    def debug_phase_cta(self, max_ctas: int = 1024):
+        """Per-CTA phase stamps (DIALSORT_PHASE_TIMING=1): rows [start, phase 0..7] in ns."""
+        import numpy as np
+        out = np.zeros((max_ctas, 9), dtype=np.uint64)
+        n = _L.dialsort_debug_phase_cta(self._h, out.ctypes.data_as(ctypes.c_void_p), max_ctas)
+        if n < 0:
+            _check(-n)
+        return out[:n]
 
     def crn_resolve(self, lane_keys: torch.Tensor, active: torch.Tensor):
         """Warp CRN test entry: (leader keys, leader counts) per 32-lane batch."""

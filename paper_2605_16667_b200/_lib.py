@@ -23,7 +23,7 @@ EXPORTS = (
     "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host",
     "dialsort_range_count_async", "dialsort_crn_resolve_async",
     "dialsort_profile_enable", "dialsort_profile_read", "dialsort_kernel_name",
-    "dialsort_debug_phase_ns",
+    "dialsort_debug_phase_ns", "dialsort_debug_phase_cta",
 )
 
 
@@ -66,6 +66,7 @@ def load() -> ctypes.CDLL:
         "dialsort_profile_read": ([P, ci, P, P], ci),
         "dialsort_kernel_name": ([ci], ctypes.c_char_p),
         "dialsort_debug_phase_ns": ([P, P], ci),
+        "dialsort_debug_phase_cta": ([P, P, ci], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -20,6 +20,7 @@
 
 #include "ds_common.cuh"
 #include "ds_expand.cuh"
+#include "ds_fused.cuh"
 #include "ds_hist.cuh"
 #include "ds_radix.cuh"
 #include "ds_scan.cuh"
@@ -44,11 +45,11 @@ int fail(int code, const std::string& msg) {
 
 enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND,
-  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_COUNT
+  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
                                              "k_scan", "k_expand", "k_radix_hist0", "k_radix_pass",
-                                             "k_range_count", "k_crn_resolve"};
+                                             "k_range_count", "k_crn_resolve", "k_sort_fused"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -91,7 +92,9 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-constexpr size_t kSmemBudget = 227 * 1024 - 2048;  // dynamic smem per CTA (static smem <= 2 KB)
+constexpr size_t kSmemBudget = 227 * 1024 - 4096;  // static smem of the kernels <= 4 KB
+// k_sort_fused workspace: 2 parities of strided tile totals, fallback totals, ready flags
+constexpr uint64_t kFusedTileWords = 2ull * kFusedTileSlots * kTileTotStride + 2 * kFusedTileSlots;
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -131,8 +134,10 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      radix_lb;
+      radix_lb, fused_tiles;
   DevStatus* host_status = nullptr;  // pinned mirror
+  uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
+  unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
   Profiler prof;
   int expand_occ = 4, scan_occ = 2, radix_occ = 1, radix2_occ = 1;
   PhaseTimes* pt = nullptr;  // debug phase timing (DIALSORT_PHASE_TIMING=1)
@@ -155,6 +160,10 @@ int ctx_init(dialsort_ctx c) {
   if ((rc = c->ws_total.ensure(64, true))) return rc;
   if ((rc = c->gridbar.ensure(64, true))) return rc;
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
+  // k_sort_fused: tile totals (2 parities), fallback tile totals, ready flags
+  if ((rc = c->fused_tiles.ensure(4ull * kFusedTileWords, true))) return rc;
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -172,9 +181,7 @@ int ctx_init(dialsort_ctx c) {
   const char* e = getenv("DIALSORT_PHASE_TIMING");
   if (e && e[0] == '1') {
     DS_CUDA(cudaMalloc(&c->pt, sizeof(PhaseTimes)));
-    PhaseTimes init = {};
-    init.start_min = ~0ull;
-    DS_CUDA(cudaMemcpy(c->pt, &init, sizeof(init), cudaMemcpyHostToDevice));
+    DS_CUDA(cudaMemset(c->pt, 0, sizeof(PhaseTimes)));
   }
   return DIALSORT_OK;
 }
@@ -323,6 +330,58 @@ int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, i
   return DIALSORT_OK;
 }
 
+// The whole sort step as one kernel (ds_fused.cuh) for the shared-memory paths.
+// DIALSORT_FUSED=0 selects the two-kernel pipeline (k_hist_fused + k_expand) for A/B.
+bool sort_fused_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("DIALSORT_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
+                       uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a = {};
+  if ((rc = fill_scan_args(c, a, U, true, n, true, nullptr, epoch))) return rc;
+  const bool pack = choose_path(U) == HistPath::Smem16;
+  const uint32_t W = pack ? (U + 1) / 2 : U;
+  const uint32_t ldw = (uint32_t)round_up(W, 8);
+  // histogram | merge scratch + cp.async staging of C packed row segments | mark buffers
+  const size_t smem = std::max<size_t>(std::max<size_t>(4ull * ldw, 4ull * kFusedNSub * kFusedChunk),
+                                       pack ? 4ull * kFusedStageOff + 1024ull * c->nsm : 0);
+  const uint64_t n4 = n / 4 + 1;
+  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);
+  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
+  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
+  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  uint32_t* ft = c->fused_tiles.as<uint32_t>();
+  a.partials = c->partials.as<uint32_t>();
+  a.C = C;
+  a.ldw = ldw;
+  a.pack16 = pack;
+  a.ovfH = c->ovfH.as<uint32_t>();
+  a.H = H;
+  a.tfb = nullptr;
+  a.tsums = nullptr;
+  const uint64_t red_words = (uint64_t)kFusedTileSlots * kTileTotStride;  // per parity
+  a.tile_red = ft + red_words * (c->fused_seq & 1);
+  a.tile_clear = ft + red_words * ((c->fused_seq + 1) & 1);
+  a.tile_red_stride = kTileTotStride;
+  a.tile_alt = ft + 2 * red_words;
+  a.ready = a.tile_alt + kFusedTileSlots;
+  a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
+  a.bar_base = c->bar64_base;
+  if (pack)
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+  else
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+  c->fused_seq++;
+  c->bar64_base += 2ull * C;  // two barriers reserved per launch (one skipped unless overflow)
+  return DIALSORT_OK;
+}
+
 // Host-side enqueue of DialSort-Radix.  Default: 4 reduce-then-scan passes (k_radix_pass2,
 // co-resident grid).  DIALSORT_RADIX=onesweep selects the single-sweep variant (K7 + 4 x K8).
 bool radix_onesweep() {
@@ -457,7 +516,8 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
-                  &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb})
+                  &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb,
+                  &c->fused_tiles})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt) cudaFree(c->pt);
@@ -551,6 +611,8 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     if ((rc = c->Hws.ensure(4ull * U))) return rc;
     H = c->Hws.as<uint32_t>();
   }
+  if (choose_path(U) != HistPath::Global && sort_fused_enabled() && !hist_use_tma())
+    return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);
   if ((rc = enqueue_hist_scan(c, keys, n, U, H, true, n, epoch, s))) return rc;
   return enqueue_expand(c, U, n, 0, out, s);
 }
@@ -616,17 +678,55 @@ const char* dialsort_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? 
 
 // Debug: phase times (ns, relative to the earliest fused-kernel CTA start) of the most recent
 // calls since the last read; zeros unless DIALSORT_PHASE_TIMING=1 at context creation.
-int dialsort_debug_phase_ns(dialsort_ctx c, uint64_t* out8) {
-  if (!c || !out8) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
-  for (int i = 0; i < 8; ++i) out8[i] = 0;
+// Reads and clears the per-CTA stamps; times are ns after the earliest CTA start.
+static int read_phase_stamps(dialsort_ctx c, std::vector<unsigned long long>& st, unsigned long long& t0) {
+  st.assign((size_t)kPhaseMaxCtas * kPhaseSlots, 0ull);
+  t0 = ~0ull;
   if (!c->pt) return DIALSORT_OK;
-  PhaseTimes h;
-  DS_CUDA(cudaMemcpy(&h, c->pt, sizeof(h), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < 8; ++i) out8[i] = h.t[i] > h.start_min ? h.t[i] - h.start_min : 0;
-  PhaseTimes init = {};
-  init.start_min = ~0ull;
-  DS_CUDA(cudaMemcpy(c->pt, &init, sizeof(init), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemcpy(st.data(), c->pt, sizeof(PhaseTimes), cudaMemcpyDeviceToHost));
+  DS_CUDA(cudaMemset(c->pt, 0, sizeof(PhaseTimes)));
+  for (int b = 0; b < kPhaseMaxCtas; ++b)
+    if (st[(size_t)b * kPhaseSlots] && st[(size_t)b * kPhaseSlots] < t0) t0 = st[(size_t)b * kPhaseSlots];
   return DIALSORT_OK;
+}
+
+int dialsort_debug_phase_ns(dialsort_ctx c, uint64_t* out16) {
+  if (!c || !out16) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  std::vector<unsigned long long> st;
+  unsigned long long t0;
+  int rc = read_phase_stamps(c, st, t0);
+  if (rc || t0 == ~0ull) return rc;
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long mx = 0, mn = ~0ull;
+    for (int b = 0; b < kPhaseMaxCtas; ++b) {
+      const unsigned long long v = st[(size_t)b * kPhaseSlots + 1 + i];
+      if (!v) continue;
+      mx = std::max(mx, v);
+      mn = std::min(mn, v);
+    }
+    out16[i] = mx ? mx - t0 : 0;
+    out16[8 + i] = mx ? mn - t0 : 0;
+  }
+  return DIALSORT_OK;
+}
+
+int dialsort_debug_phase_cta(dialsort_ctx c, uint64_t* out, int max_ctas) {
+  if (!c || !out || max_ctas < 0) return -fail(DIALSORT_E_INVALID_ARG, "bad argument");
+  std::vector<unsigned long long> st;
+  unsigned long long t0;
+  int rc = read_phase_stamps(c, st, t0);
+  if (rc) return -rc;
+  int n = 0;
+  for (int b = 0; b < kPhaseMaxCtas && b < max_ctas; ++b) {
+    if (!st[(size_t)b * kPhaseSlots]) break;
+    for (int i = 0; i < kPhaseSlots; ++i) {
+      const unsigned long long v = st[(size_t)b * kPhaseSlots + i];
+      out[(size_t)b * kPhaseSlots + i] = v ? v - t0 : 0;
+    }
+    n = b + 1;
+  }
+  return n;
 }
 
 int dialsort_crn_resolve_async(dialsort_ctx c, const int32_t* lane_keys, const uint32_t* active, uint64_t n_batches,

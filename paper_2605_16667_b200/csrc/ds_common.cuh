@@ -109,10 +109,13 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-// ---- debug phase timing (DIALSORT_PHASE_TIMING=1): max over CTAs of globaltimer per phase --
+// ---- debug phase timing (DIALSORT_PHASE_TIMING=1): per-CTA %globaltimer stamps ------------
+// Plain stores by thread 0 of each CTA (no same-address atomics, which would serialise and
+// distort the timeline); the host reduces them (dialsort_debug_phase_ns / _cta).
+constexpr int kPhaseMaxCtas = 1024;
+constexpr int kPhaseSlots = 9;  // [0] = CTA start, [1 + i] = phase i
 struct PhaseTimes {
-  unsigned long long start_min;  // earliest CTA start
-  unsigned long long t[8];       // latest CTA arrival at phase i
+  unsigned long long stamp[kPhaseMaxCtas][kPhaseSlots];
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -120,11 +123,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void phase_mark(PhaseTimes* pt, int i) {
-  if (pt && threadIdx.x == 0) {
-    const unsigned long long t = gtimer();
-    if (i < 0) atomicMin(&pt->start_min, t);
-    else atomicMax(&pt->t[i], t);
-  }
+  if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) pt->stamp[blockIdx.x][i + 1] = gtimer();
 }
 
 // Fire-and-forget global add (RED.ADD.U32 in SASS).

@@ -255,14 +255,13 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 //          and the expand index tfb (skipped for the histogram-only API).
 // One CTA per SM (1024 threads); the grid (<= #SMs) is co-resident by construction.
 // Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
+// Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
+// writes the row and, per 512-bin tile, the row's tile sum: into tsums[tile][row], or — when
+// a.tile_red is set — added (RED) into the tile total tile_red[tile].
 template <bool PACK16, bool TMA>
-__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
-                                                       uint32_t stages) {
-  extern __shared__ __align__(128) uint32_t sh_hist[];
-  __shared__ uint64_t red64[34];
-  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
-  pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
-  phase_mark(a.pt, -1);
+__device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ keys, uint64_t n, const ScanArgs& a,
+                                                  uint32_t stages, uint32_t* sh_hist, uint64_t* red64,
+                                                  uint64_t* full_bar, uint64_t* empty_bar) {
   const uint32_t U = a.U, ldw = a.ldw;
 
   // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
@@ -383,7 +382,13 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
     }
     v = warp_sum(v);
     fsum += v;
-    if (lane == 0) __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
+    if (lane == 0) {
+      if (a.tile_red) {
+        if (v) red_add_u32(a.tile_red + (uint64_t)t * a.tile_red_stride, v);
+      } else {
+        __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
+      }
+    }
   }
   // (uint4 beyond the last tile are padding zeros and are never read by the merge)
   if (PACK16) {
@@ -395,10 +400,24 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
     if (tot != nvalid) hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
   }
   phase_mark(a.pt, 2);
+}
+
+template <bool PACK16, bool TMA>
+__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
+                                                       uint32_t stages) {
+  extern __shared__ __align__(128) uint32_t sh_hist[];
+  __shared__ uint64_t red64[34];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
+  pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
+  phase_mark(a.pt, -1);
+  hist_ingest_flush<PACK16, TMA>(keys, n, a, stages, sh_hist, red64, full_bar, empty_bar);
+  const uint32_t U = a.U;
+  DevStatus* st = a.st;
   grid_barrier(a.bar);  // every row, tile sum (and any fallback contribution) is in L2
   phase_mark(a.pt, 3);
 
   // Merge + scan this CTA's tile range.
+  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
   const bool use_ovf = ld_acquire_u32(&st->ovf_epoch) == a.epoch;
   uint32_t tb0, tb1;
   my_tiles(ntiles, tb0, tb1);

@@ -70,7 +70,51 @@ struct ScanArgs {
   uint32_t epoch;
   PhaseTimes* pt;            // nullable debug timing
   uint32_t* tsums;           // [C][ntiles] per-row tile sums (fused path), or nullptr
+  // single-kernel sort (k_sort_fused) only:
+  uint32_t* tile_red;        // [ntiles x tile_red_stride] tile totals reduced during the flush (zero on entry)
+  uint32_t* tile_clear;      // the other parity's tile_red, zeroed for the next launch
+  uint32_t tile_red_stride;  // words between consecutive tile totals
+  uint32_t* tile_alt;        // [ntiles] tile totals of the overflow fallback path
+  uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
+  unsigned long long* bar64; // monotonic grid-barrier counter
+  unsigned long long bar_base;  // its value at launch (host-tracked: += 2 * gridDim per launch)
 };
+
+// Monotonic grid barrier (measured 1.25 us vs 2.0 us for counter + generation on B200,
+// profiles/r02_barrier_bench.txt): each CTA arrives with one release atomic on a 64-bit
+// counter that only grows, and waits until it reaches `target` = base + (j + 1) * gridDim
+// for the launch's j-th barrier.  The host advances `base` by the number of barriers a launch
+// reserves; a launch that skips a reserved barrier arrives without waiting (barrier_skip), so
+// the counter always ends a launch at base + reserved * gridDim.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+    while (ld_acquire_u64(cnt) < target) {
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void barrier_skip(unsigned long long* cnt) {
+  if (threadIdx.x == 0) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+}
+
+// Final size / overflow checks and totals, by the CTA owning the last tile.
+__device__ __forceinline__ void scan_finish(const ScanArgs& a, uint64_t total) {
+  a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
+  unsigned flags = 0;
+  if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
+  if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
+  if (flags) atomicOr(&a.st->flags, flags);
+  a.st->last_total = total;
+  if (a.d_total) *a.d_total = total;
+  *a.ws_total = total;
+}
 
 // Tiles [tb0, tb1) of CTA b in a grid of G over ntiles (contiguous ranges).
 __device__ __forceinline__ void my_tiles(uint32_t ntiles, uint32_t& tb0, uint32_t& tb1) {
@@ -156,7 +200,7 @@ __device__ __forceinline__ uint64_t scan_tile(const ScanArgs& a, const uint32_t*
   if (own) {
     const uint64_t pk = offset + ex;
     a.P[bin] = (uint32_t)pk;
-    if (h > 0) {  // output tiles whose first position t*T falls in [pk, pk + h) start in this bin
+    if (a.tfb && h > 0) {  // output tiles whose first position t*T falls in [pk, pk + h) start in this bin
       const uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + h - 1) / a.T;
       for (uint64_t t = t0; t <= t1 && t < a.ntiles_out; ++t) a.tfb[t] = (uint32_t)bin;
     }
@@ -176,46 +220,77 @@ __device__ __forceinline__ void scan_phase_b(const ScanArgs& a, const uint32_t* 
   for (uint32_t j = threadIdx.x; j < blockIdx.x; j += blockDim.x) s += __ldcg(a.range_tot + j);
   uint64_t off = block_sum<uint64_t>(s, red);
   for (uint32_t t = tb0; t < tb1; ++t) off = scan_tile(a, H, t, off, red);
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-    const uint64_t total = off;
-    a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
-    unsigned flags = 0;
-    if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
-    if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
-    if (flags) atomicOr(&a.st->flags, flags);
-    a.st->last_total = total;
-    if (a.d_total) *a.d_total = total;
-    *a.ws_total = total;
-  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) scan_finish(a, off);
 }
 
-// Fused path, after the single grid barrier: this CTA's tile offset is the sum of every
-// row's tile sums over the tiles before its range (tsums, written during the flush); the
-// offset loads are issued before the partial-row loads so both share one L2 round trip,
-// and each tile is merged and scanned straight from registers (no re-read of H).
-__device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0, uint32_t tb1, bool use_ovf,
-                                                 uint32_t* scratch, uint64_t* red) {
-  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
-  // tsums is [tile][row]: the entries of tiles < tb0 are one contiguous block, read as uint4
-  // with all loads of a thread in flight together.
-  uint64_t s = 0;
-  const uint32_t cnt = a.C * tb0;
-  const uint32_t cnt4 = cnt / 4;
-  const uint4* ts4 = reinterpret_cast<const uint4*>(a.tsums);
-  for (uint32_t j0 = threadIdx.x; j0 < cnt4; j0 += 4 * blockDim.x) {
-    uint4 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t j = j0 + u * blockDim.x;
-      x[u] = j < cnt4 ? __ldcg(ts4 + j) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) s += (uint64_t)x[u].x + x[u].y + x[u].z + x[u].w;
-  }
-  for (uint32_t j = 4 * cnt4 + threadIdx.x; j < cnt; j += blockDim.x) s += __ldcg(a.tsums + j);
-  phase_mark(a.pt, 5);  // offset loads issued (debug)
-  uint64_t off = block_sum<uint64_t>(s, red);
+// Merge + scan of tiles [tb0, tb1) whose first bin has exclusive prefix `off`: each tile's
+// rows are summed in registers (all row loads of a thread in flight together), the groups
+// combined through shared memory, and H, P (and tfb when given) written; when a.ready is
+// set, tile t is published (ready[t] = epoch, release) once its P is in memory.  Returns
+// the prefix after tb1.
+// `first_off()` is called once, after the first tile's row loads are issued (so that whatever
+// it reads shares their L2 round trip), and returns the prefix before tb0.
+//
+// STAGE (packed rows, 1024 threads): the C row segments of a tile (1 KB each) are copied into
+// shared memory `stage` with cp.async — all of them in flight at once without holding
+// registers (the register path fits only 8 x 16 B loads per thread under the 64-register cap,
+// i.e. two L2 round trips for 148 rows) — then summed from shared memory by 4 row groups.
+template <bool STAGE = false, typename OffFn>
+__device__ __forceinline__ uint64_t merge_scan_tiles(const ScanArgs& a, uint32_t tb0, uint32_t tb1, OffFn&& first_off,
+                                                     bool use_ovf, uint32_t* scratch, uint64_t* red,
+                                                     uint32_t* stage = nullptr) {
+  uint64_t off = 0;
+  if (tb0 == tb1) return first_off();
   for (uint32_t t = tb0; t < tb1; ++t) {
+    if (STAGE) {
+      // rows r of tile t: partials[r][t*256 .. t*256+256) -> stage[r*256 ..]
+      const uint32_t Wtot4 = ((a.U + 1) / 2 + 3) / 4;  // uint4 groups holding packed words
+      const uint32_t q0 = t * (kTileBins / 8);          // first uint4 of the tile in a row
+      for (uint32_t i = threadIdx.x; i < a.C * 64; i += blockDim.x) {
+        const uint32_t r = i >> 6, l = i & 63;
+        const uint32_t* src = a.partials + (uint64_t)r * a.ldw + 4ull * (q0 + l);
+        const uint32_t dst = smem_addr(stage + r * 256 + 4 * l);
+        const uint32_t bytes = (q0 + l < Wtot4) ? 16u : 0u;  // zero-fill past the last word
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (t == tb0) off = first_off();
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      phase_mark(a.pt, 6);  // partial rows in shared memory (debug)
+      // thread j: packed word column w = j & 255 over rows r = j >> 8 (mod 4)
+      const uint32_t w = threadIdx.x & 255, qg = threadIdx.x >> 8;
+      uint32_t lo = 0, hi = 0;
+      for (uint32_t r = qg; r < a.C; r += 4) {
+        const uint32_t x = stage[r * 256 + w];
+        lo += x & 0xffffu;
+        hi += x >> 16;
+      }
+      scratch[qg * kTileBins + 2 * w] = lo;
+      scratch[qg * kTileBins + 2 * w + 1] = hi;
+      __syncthreads();
+      const uint64_t bin = (uint64_t)t * kTileBins + threadIdx.x;
+      const bool own = threadIdx.x < kTileBins && bin < a.U;
+      uint32_t h = 0;
+      if (own) {
+        h = scratch[threadIdx.x] + scratch[kTileBins + threadIdx.x] + scratch[2 * kTileBins + threadIdx.x] +
+            scratch[3 * kTileBins + threadIdx.x];
+        if (use_ovf) {
+          h += a.ovfH[bin];
+          a.ovfH[bin] = 0;
+        }
+        a.H[bin] = h;
+      }
+      uint64_t tile_total;
+      const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
+      if (own) a.P[bin] = (uint32_t)(off + ex);
+      if (a.ready) {
+        __syncthreads();  // every P of the tile is written
+        if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t), "r"(a.epoch) : "memory");
+      }
+      off += tile_total;
+      continue;
+    }
     // merge: per-group partial sums into scratch[g][bin] (as merge_tile)
     const uint32_t words = a.pack16 ? kTileBins / 2 : kTileBins;
     const uint32_t lanes_per_row = words / 4;
@@ -244,6 +319,7 @@ __device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0
         }
       }
     }
+    if (t == tb0) off = first_off();
     phase_mark(a.pt, 6);  // partial rows summed in registers (debug)
     __syncthreads();
     if (grp < ngroups) {
@@ -269,24 +345,48 @@ __device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0
     if (own) {
       const uint64_t pk = off + ex;
       a.P[bin] = (uint32_t)pk;
-      if (h > 0) {
+      if (a.tfb && h > 0) {
         const uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + h - 1) / a.T;
         for (uint64_t q = t0; q <= t1 && q < a.ntiles_out; ++q) a.tfb[q] = (uint32_t)bin;
       }
     }
+    if (a.ready) {
+      __syncthreads();  // every P of the tile is written
+      if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t), "r"(a.epoch) : "memory");
+    }
     off += tile_total;
   }
-  if (tb1 == ntiles && tb1 > tb0 && threadIdx.x == 0) {
-    const uint64_t total = off;
-    a.P[a.U] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
-    unsigned flags = 0;
-    if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
-    if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
-    if (flags) atomicOr(&a.st->flags, flags);
-    a.st->last_total = total;
-    if (a.d_total) *a.d_total = total;
-    *a.ws_total = total;
+  return off;
+}
+
+// Fused path, after the single grid barrier: this CTA's tile offset is the sum of every
+// row's tile sums over the tiles before its range (tsums, written during the flush); the
+// offset loads are issued before the partial-row loads so both share one L2 round trip,
+// and each tile is merged and scanned straight from registers (no re-read of H).
+__device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0, uint32_t tb1, bool use_ovf,
+                                                 uint32_t* scratch, uint64_t* red) {
+  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
+  // tsums is [tile][row]: the entries of tiles < tb0 are one contiguous block, read as uint4
+  // with all loads of a thread in flight together.
+  uint64_t s = 0;
+  const uint32_t cnt = a.C * tb0;
+  const uint32_t cnt4 = cnt / 4;
+  const uint4* ts4 = reinterpret_cast<const uint4*>(a.tsums);
+  for (uint32_t j0 = threadIdx.x; j0 < cnt4; j0 += 4 * blockDim.x) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = j0 + u * blockDim.x;
+      x[u] = j < cnt4 ? __ldcg(ts4 + j) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += (uint64_t)x[u].x + x[u].y + x[u].z + x[u].w;
   }
+  for (uint32_t j = 4 * cnt4 + threadIdx.x; j < cnt; j += blockDim.x) s += __ldcg(a.tsums + j);
+  phase_mark(a.pt, 5);  // offset loads issued (debug)
+  const uint64_t off0 = block_sum<uint64_t>(s, red);
+  const uint64_t off = merge_scan_tiles(a, tb0, tb1, [&] { return off0; }, use_ovf, scratch, red);
+  if (tb1 == ntiles && tb1 > tb0 && threadIdx.x == 0) scan_finish(a, off);
 }
 
 // Standalone scan of a given H (global path, reconstruct API): persistent co-resident grid.

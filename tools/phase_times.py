@@ -1,25 +1,41 @@
-"""Per-phase timing of the fused DialSort kernels in a back-to-back step loop (debug)."""
+"""Per-phase timing of the fused DialSort kernels (debug): one isolated step at a time,
+per-CTA %globaltimer stamps, printed as min / median / max over CTAs per phase."""
 import os
 import sys
 
 os.environ["DIALSORT_PHASE_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2605_16667_b200 as ds  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
+verbose = len(sys.argv) > 2
 cfg = bench.CONFIGS[cfgname]
 dev = torch.device("cuda:0")
 keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
 outs = [torch.empty_like(k) for k in keys]
-ctx = ds.Context(0, max_n=cfg["n"], max_U=cfg["U"])
-names = ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"]
-for rep in range(3):
-    ctx.debug_phase_ns()
-    for i in range(1):  # one isolated step (previous work drained)
+ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
+fused = os.environ.get("DIALSORT_FUSED") != "0"
+names = (["ingest", "sync", "flush", "barrier1", "merge_scan", "share_ready", "rows_staged", "end"] if fused else
+         ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"])
+for rep in range(4):
+    ctx.debug_phase_cta()
+    if cfg["dist"] == "int32":
+        ctx.sort_int32(keys[rep % 5], out=outs[rep % 5])
+    else:
         ctx.sort(keys[rep % 5], cfg["U"], out=outs[rep % 5])
     torch.cuda.synchronize()
-    t = ctx.debug_phase_ns()
-    print(cfgname, "isolated step phase end times (us):", {n: round(v / 1e3, 2) for n, v in zip(names, t)})
+    st = ctx.debug_phase_cta().astype(np.float64) / 1e3
+    if rep == 0 or len(st) == 0:
+        continue  # first call: warm-up
+    print(f"{cfgname} rep {rep}: {len(st)} CTAs, phase time after the first CTA start (us) min/median/max:")
+    cols = [("start", st[:, 0])] + [(n, st[:, 1 + i]) for i, n in enumerate(names)]
+    print("   " + "  ".join(f"{n}={c[c > 0].min():.2f}/{np.median(c[c > 0]):.2f}/{c.max():.2f}"
+                            for n, c in cols if (c > 0).any()))
+    if verbose and fused:
+        late = np.argsort(-st[:, 6])[:6]
+        for b in late:
+            print("   late share CTA", b, " ".join(f"{n}={st[b, 1 + i]:.2f}" for i, n in enumerate(names)))

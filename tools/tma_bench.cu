@@ -1,0 +1,262 @@
+// LSU vs TMA-bulk for the fused kernel's L2-resident phases (design microbenchmark, not
+// product code).  148 co-resident CTAs x 1024 threads, 128 KB rows (packed 65536-bin
+// sub-histograms).  Each kernel timed by events; "in-kernel" = globaltimer span.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/tma_bench tools/tma_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
+
+constexpr uint32_t ROWB = 128 * 1024;  // bytes per row
+constexpr uint32_t SEGB = 1024;        // bytes per (row, tile) segment
+constexpr uint32_t NT = ROWB / SEGB;   // 128 tiles
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned long long gt() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+__device__ unsigned long long g_t0 = ~0ull, g_t1 = 0;
+__device__ __forceinline__ void mark0() { if (threadIdx.x == 0) atomicMin(&g_t0, gt()); }
+__device__ __forceinline__ void mark1() { __syncthreads(); if (threadIdx.x == 0) atomicMax(&g_t1, gt()); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(c) : "memory"); }
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(sa(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+extern __shared__ __align__(128) uint4 sm[];
+
+__global__ void __launch_bounds__(1024, 1) k_flush_lsu(uint4* rows) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < ROWB / 16; i += 1024) sm[i] = make_uint4(i, 1, 2, 3);
+  __syncthreads();
+  uint4* r = rows + (uint64_t)blockIdx.x * (ROWB / 16);
+  for (uint32_t i = threadIdx.x; i < ROWB / 16; i += 1024) __stcg(r + i, sm[i]);
+  mark1();
+}
+template <uint32_t PIECE>
+__global__ void __launch_bounds__(1024, 1) k_flush_tma(uint4* rows) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < ROWB / 16; i += 1024) sm[i] = make_uint4(i, 1, 2, 3);
+  fence_proxy();
+  __syncthreads();
+  char* r = reinterpret_cast<char*>(rows) + (uint64_t)blockIdx.x * ROWB;
+  constexpr uint32_t NP = ROWB / PIECE;
+  if (threadIdx.x < NP) {
+    bulk_s2g(r + threadIdx.x * PIECE, reinterpret_cast<char*>(sm) + threadIdx.x * PIECE, PIECE);
+    bulk_commit();
+    bulk_wait_all();
+  }
+  mark1();
+}
+// merge: CTA b < NT sums tile b over all G rows
+__global__ void __launch_bounds__(1024, 1) k_merge_lsu(const uint4* rows, uint32_t* out, uint32_t G) {
+  mark0();
+  if (blockIdx.x < NT) {
+    const uint32_t l = threadIdx.x & 63, grp = threadIdx.x >> 6;  // 64 uint4 per segment, 16 groups
+    uint32_t acc = 0;
+    const uint4* base = rows + blockIdx.x * (SEGB / 16) + l;
+    for (uint32_t r0 = grp; r0 < G; r0 += 160) {
+      uint4 x[10];
+#pragma unroll
+      for (int u = 0; u < 10; ++u) { uint32_t r = r0 + u * 16; x[u] = r < G ? __ldcg(base + (uint64_t)r * (ROWB / 16)) : make_uint4(0, 0, 0, 0); }
+#pragma unroll
+      for (int u = 0; u < 10; ++u) acc += x[u].x + x[u].y + x[u].z + x[u].w;
+    }
+    if (acc == 0x12345678u) out[blockIdx.x] = acc;
+  }
+  mark1();
+}
+__global__ void __launch_bounds__(1024, 1) k_merge_tma(const uint4* rows, uint32_t* out, uint32_t G) {
+  __shared__ __align__(8) uint64_t bar;
+  mark0();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  __syncthreads();
+  if (blockIdx.x < NT) {
+    if (threadIdx.x == 0) mbar_expect(&bar, G * SEGB);
+    __syncthreads();
+    if (threadIdx.x < G)
+      bulk_g2s(reinterpret_cast<char*>(sm) + threadIdx.x * SEGB,
+               reinterpret_cast<const char*>(rows) + (uint64_t)threadIdx.x * ROWB + blockIdx.x * SEGB, SEGB, &bar);
+    mbar_wait(&bar, 0);
+    // thread t: word column t % 256, rows t/256 + 4i
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(sm);
+    uint32_t acc = 0;
+    for (uint32_t r = threadIdx.x >> 8; r < G; r += 4) acc += w[r * 256 + (threadIdx.x & 255)];
+    if (acc == 0x12345678u) out[blockIdx.x] = acc;
+  }
+  mark1();
+}
+// output writes: 40 MB in 32 KB chunks from smem, grid-strided chunks
+__global__ void __launch_bounds__(1024, 1) k_write_lsu(uint4* o, uint32_t nchunks) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < 8192; i += 1024) sm[i] = make_uint4(i, i, i, i);
+  __syncthreads();
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    uint4* d = o + (uint64_t)c * 2048;
+    for (uint32_t i = threadIdx.x; i < 2048; i += 1024) __stcs(d + i, sm[(c & 3) * 2048 + i]);
+  }
+  mark1();
+}
+__global__ void __launch_bounds__(1024, 1) k_write_tma(uint4* o, uint32_t nchunks) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < 8192; i += 1024) sm[i] = make_uint4(i, i, i, i);
+  fence_proxy();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t k = 0;
+    for (uint32_t c = blockIdx.x + threadIdx.x * gridDim.x; c < nchunks; c += 32 * gridDim.x, ++k) {
+      bulk_s2g(o + (uint64_t)c * 2048, sm + (c & 3) * 2048, 32768);
+      bulk_commit();
+    }
+    bulk_wait_all();
+  }
+  mark1();
+}
+
+// bulk reduce-add: each CTA adds a 256 KB u32 histogram (from smem, in PIECE-byte pieces,
+// unpacked in STG-byte staging steps) into one shared global accumulator
+__device__ __forceinline__ void bulk_red_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;" ::"l"(dst), "r"(sa(src)), "r"(bytes) : "memory");
+}
+template <uint32_t PIECE, bool ROT>
+__global__ void __launch_bounds__(1024, 1) k_bulk_red(uint32_t* acc) {
+  mark0();
+  // staging: 2 x 32 KB of u32 values (as if unpacked from a packed histogram)
+  uint32_t* st = reinterpret_cast<uint32_t*>(sm);
+  for (uint32_t i = threadIdx.x; i < 16384; i += 1024) st[i] = 1u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  constexpr uint32_t TOT = 65536 * 4;  // bytes of the u32 histogram
+  constexpr uint32_t NP = TOT / PIECE;
+  if (threadIdx.x < 32) {
+    for (uint32_t p = threadIdx.x; p < NP; p += 32) {
+      const uint32_t q = ROT ? (p + blockIdx.x * (NP / gridDim.x + 1)) % NP : p;
+      bulk_red_s2g(reinterpret_cast<char*>(acc) + (uint64_t)q * PIECE, reinterpret_cast<char*>(st) + (q * PIECE) % 65536, PIECE);
+      bulk_commit();
+    }
+    bulk_wait_all();
+  }
+  mark1();
+}
+// thread-level RED of the same data (packed? no: u32 per bin), coalesced, rotated start
+__global__ void __launch_bounds__(1024, 1) k_thread_red(uint32_t* acc) {
+  mark0();
+  const uint32_t off = (blockIdx.x * 443u) & 65535u;
+  for (uint32_t i = threadIdx.x; i < 65536; i += 1024) {
+    const uint32_t j = (i + off) & 65535u;
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(acc + j), "r"(1u) : "memory");
+  }
+  mark1();
+}
+
+// flush + grid barrier + merge in ONE kernel (as in k_sort_fused); times of the merge part
+__device__ unsigned long long g_m0 = ~0ull, g_m1 = 0, g_m1min = ~0ull;
+template <bool DIRTY_L2>
+__global__ void __launch_bounds__(1024, 1) k_flush_merge(uint4* rows, uint32_t* out, unsigned long long* bar,
+                                                        unsigned long long target, uint4* junk) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < ROWB / 16; i += 1024) sm[i] = make_uint4(i, 1, 2, 3);
+  __syncthreads();
+  uint4* r = rows + (uint64_t)blockIdx.x * (ROWB / 16);
+  for (uint32_t i = threadIdx.x; i < ROWB / 16; i += 1024) __stcg(r + i, sm[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned long long v;
+    do { asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory"); } while (v < target);
+    atomicMin(&g_m0, gt());
+  }
+  __syncthreads();
+  const uint32_t G = gridDim.x;
+  if (blockIdx.x < NT) {
+    const uint32_t l = threadIdx.x & 63, grp = threadIdx.x >> 6;
+    uint32_t acc = 0;
+    const uint4* base = rows + blockIdx.x * (SEGB / 16) + l;
+    for (uint32_t r0 = grp; r0 < G; r0 += 160) {
+      uint4 x[10];
+#pragma unroll
+      for (int u = 0; u < 10; ++u) { uint32_t rr = r0 + u * 16; x[u] = rr < G ? __ldcg(base + (uint64_t)rr * (ROWB / 16)) : make_uint4(0, 0, 0, 0); }
+#pragma unroll
+      for (int u = 0; u < 10; ++u) acc += x[u].x + x[u].y + x[u].z + x[u].w;
+    }
+    if (acc == 0x12345678u) out[blockIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) { atomicMax(&g_m1, gt()); atomicMin(&g_m1min, gt()); }
+  }
+  mark1();
+}
+
+int main() {
+  int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  uint4* rows; CK(cudaMalloc(&rows, (size_t)nsm * ROWB));
+  uint32_t* out; CK(cudaMalloc(&out, 4096));
+  const size_t OUTB = 40u << 20;
+  uint4* o; CK(cudaMalloc(&o, OUTB * 4));
+  uint4* flush; CK(cudaMalloc(&flush, 512u << 20));
+  const int SM = 200 * 1024;
+  for (auto f : {(const void*)k_flush_lsu, (const void*)k_flush_tma<4096>, (const void*)k_flush_tma<32768>,
+                 (const void*)k_merge_lsu, (const void*)k_merge_tma, (const void*)k_write_lsu, (const void*)k_write_tma})
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  auto run = [&](const char* nm, auto&& launch, bool flushL2) {
+    float best = 1e9; double bestk = 1e9;
+    for (int r = 0; r < 8; ++r) {
+      if (flushL2) CK(cudaMemsetAsync(flush, r, 512u << 20));
+      unsigned long long z0 = ~0ull, z1 = 0;
+      CK(cudaMemcpyToSymbol(g_t0, &z0, 8)); CK(cudaMemcpyToSymbol(g_t1, &z1, 8));
+      cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+      float t; cudaEventElapsedTime(&t, e0, e1);
+      unsigned long long a, b; CK(cudaMemcpyFromSymbol(&a, g_t0, 8)); CK(cudaMemcpyFromSymbol(&b, g_t1, 8));
+      if (r >= 2) { if (t < best) best = t; if ((b - a) * 1e-3 < bestk) bestk = (b - a) * 1e-3; }
+    }
+    printf("%-36s event %8.2f us   in-kernel %8.2f us\n", nm, best * 1000.f, bestk);
+  };
+  const uint32_t G = nsm;
+  run("flush LSU st.cg 148x128KB", [&] { k_flush_lsu<<<G, 1024, SM>>>(rows); }, false);
+  run("flush TMA bulk 32x4KB", [&] { k_flush_tma<4096><<<G, 1024, SM>>>(rows); }, false);
+  run("flush TMA bulk 4x32KB", [&] { k_flush_tma<32768><<<G, 1024, SM>>>(rows); }, false);
+  run("merge LSU 128 tiles x 148 rows", [&] { k_merge_lsu<<<G, 1024, SM>>>(rows, out, G); }, false);
+  run("merge TMA 128 tiles x 148 rows", [&] { k_merge_tma<<<G, 1024, SM>>>(rows, out, G); }, false);
+  const uint32_t nch = OUTB / 32768;
+  run("write LSU 40MB (32KB chunks)", [&] { k_write_lsu<<<G, 1024, SM>>>(o, nch); }, true);
+  run("write TMA 40MB (32KB chunks)", [&] { k_write_tma<<<G, 1024, SM>>>(o, nch); }, true);
+  run("write LSU 40MB (no L2 flush)", [&] { k_write_lsu<<<G, 1024, SM>>>(o, nch); }, false);
+  run("write TMA 40MB (no L2 flush)", [&] { k_write_tma<<<G, 1024, SM>>>(o, nch); }, false);
+  uint32_t* acc; CK(cudaMalloc(&acc, 1 << 20));
+  for (auto f : {(const void*)k_bulk_red<4096, false>, (const void*)k_bulk_red<4096, true>, (const void*)k_bulk_red<16384, true>,
+                 (const void*)k_bulk_red<1024, true>, (const void*)k_thread_red})
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  {
+    unsigned long long* bar; CK(cudaMalloc(&bar, 64)); CK(cudaMemset(bar, 0, 64));
+    unsigned long long tgt = 0;
+    CK(cudaFuncSetAttribute((const void*)k_flush_merge<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+    for (int rep = 0; rep < 6; ++rep) {
+      unsigned long long z0 = ~0ull, z1 = 0;
+      CK(cudaMemcpyToSymbol(g_m0, &z0, 8)); CK(cudaMemcpyToSymbol(g_m1, &z1, 8)); CK(cudaMemcpyToSymbol(g_m1min, &z0, 8));
+      if (rep & 1) CK(cudaMemsetAsync(flush, rep, 512u << 20));  // odd reps: L2 full of dirty lines
+      tgt += G;
+      k_flush_merge<false><<<G, 1024, SM>>>(rows, out, bar, tgt, flush);
+      CK(cudaDeviceSynchronize());
+      unsigned long long a, b, c; CK(cudaMemcpyFromSymbol(&a, g_m0, 8)); CK(cudaMemcpyFromSymbol(&b, g_m1, 8)); CK(cudaMemcpyFromSymbol(&c, g_m1min, 8));
+      printf("flush+barrier+merge one kernel (%s L2): merge from barrier exit: earliest CTA done %.2f us, latest %.2f us\n",
+             (rep & 1) ? "dirty" : "clean", (c - a) * 1e-3, (b - a) * 1e-3);
+    }
+  }
+  run("bulk reduce.add 148 x 256KB, 4KB pieces", [&] { k_bulk_red<4096, false><<<G, 1024, SM>>>(acc); }, false);
+  run("bulk reduce.add rotated, 4KB pieces", [&] { k_bulk_red<4096, true><<<G, 1024, SM>>>(acc); }, false);
+  run("bulk reduce.add rotated, 16KB pieces", [&] { k_bulk_red<16384, true><<<G, 1024, SM>>>(acc); }, false);
+  run("bulk reduce.add rotated, 1KB pieces", [&] { k_bulk_red<1024, true><<<G, 1024, SM>>>(acc); }, false);
+  run("thread red.add u32 148 x 65536 rotated", [&] { k_thread_red<<<G, 1024, SM>>>(acc); }, false);
+  return 0;
+}
