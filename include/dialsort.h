@@ -134,8 +134,8 @@ const char* dialsort_kernel_name(int kernel_id);
  * earliest CTA start into out16 (host): [0..7] the latest CTA's arrival at phase 0..7,
  * [8..15] the earliest CTA's (0 = phase not reached), and resets them. */
 int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out16);
-/* Debug: raw per-CTA stamps of the most recent launches (9 per CTA: start, phase 0..7; ns
- * after the earliest start, 0 = not reached) into out[max_ctas * 9] (host); returns the number
+/* Debug: raw per-CTA stamps of the most recent launches (17 per CTA: start, phase 0..15; ns
+ * after the earliest start, 0 = not reached) into out[max_ctas * 17] (host); returns the number
  * of CTAs copied, or -status.  Reading resets the stamps (as dialsort_debug_phase_ns). */
 int dialsort_debug_phase_cta(dialsort_ctx ctx, uint64_t* out, int max_ctas);
 

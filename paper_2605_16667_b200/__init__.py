@@ -170,9 +170,9 @@ class Context:
         return out.tolist()
 
     def debug_phase_cta(self, max_ctas: int = 1024):
-        """Per-CTA phase stamps (DIALSORT_PHASE_TIMING=1): rows [start, phase 0..7] in ns."""
+        """Per-CTA phase stamps (DIALSORT_PHASE_TIMING=1): rows [start, phase 0..15] in ns."""
         import numpy as np
-        out = np.zeros((max_ctas, 9), dtype=np.uint64)
+        out = np.zeros((max_ctas, 17), dtype=np.uint64)
         n = _L.dialsort_debug_phase_cta(self._h, out.ctypes.data_as(ctypes.c_void_p), max_ctas)
         if n < 0:
             _check(-n)

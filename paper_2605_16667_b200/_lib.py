@@ -10,7 +10,10 @@ import ctypes
 import os
 
 _DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_DIR, "libdialsort.so")
+# DIALSORT_LIB_VARIANT=<v> loads libdialsort_<v>.so from this directory instead (design A/B
+# builds of the same sources with different -D switches; development only)
+_VARIANT = os.environ.get("DIALSORT_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_DIR, f"libdialsort_{_VARIANT}.so" if _VARIANT else "libdialsort.so")
 
 # dialsort_status
 OK, E_INVALID_ARG, E_KEY_RANGE, E_SIZE, E_OVERFLOW, E_CUDA, E_NOMEM = 0, 1, 2, 3, 4, 5, 7

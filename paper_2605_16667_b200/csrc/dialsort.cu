@@ -93,8 +93,8 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 constexpr size_t kSmemBudget = 227 * 1024 - 4096;  // static smem of the kernels <= 4 KB
-// k_sort_fused workspace: 2 parities of strided tile totals, fallback totals, ready flags
-constexpr uint64_t kFusedTileWords = 2ull * kFusedTileSlots * kTileTotStride + 2 * kFusedTileSlots;
+// k_sort_fused workspace: 2 parities of strided tile totals, fallback tile totals, ready flags
+constexpr uint64_t kFusedTileWords = 2ull * kFTileSlots * kTileTotStride + 2 * kFTileSlots;
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -134,7 +134,7 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      radix_lb, fused_tiles;
+      radix_lb, fused_tiles, Hx;
   DevStatus* host_status = nullptr;  // pinned mirror
   uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
   unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
@@ -160,10 +160,11 @@ int ctx_init(dialsort_ctx c) {
   if ((rc = c->ws_total.ensure(64, true))) return rc;
   if ((rc = c->gridbar.ensure(64, true))) return rc;
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
-  // k_sort_fused: tile totals (2 parities), fallback tile totals, ready flags
+  // k_sort_fused: tile totals (2 parities), fallback tile totals
   if ((rc = c->fused_tiles.ensure(4ull * kFusedTileWords, true))) return rc;
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -347,36 +348,47 @@ int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t
   if ((rc = fill_scan_args(c, a, U, true, n, true, nullptr, epoch))) return rc;
   const bool pack = choose_path(U) == HistPath::Smem16;
   const uint32_t W = pack ? (U + 1) / 2 : U;
-  const uint32_t ldw = (uint32_t)round_up(W, 8);
-  // histogram | merge scratch + cp.async staging of C packed row segments | mark buffers
-  const size_t smem = std::max<size_t>(std::max<size_t>(4ull * ldw, 4ull * kFusedNSub * kFusedChunk),
-                                       pack ? 4ull * kFusedStageOff + 1024ull * c->nsm : 0);
+  const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
   const uint64_t n4 = n / 4 + 1;
   const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);
-  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
-  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
+  const uint64_t cmax = std::min<uint64_t>(c->nsm, kFMaxRows);  // rows a staging slot holds
+  const uint32_t C = (uint32_t)(want < cmax ? (want ? want : 1) : cmax);
+  // partial-row format: 4-bit rows while counts per CTA and bin are small (mean <= 8: counts
+  // >= 16 — exceptions, one RED each — stay rare), else the packed 16-bit rows
+  const int fmt = !pack ? kRowU32 : (n <= 8ull * C * U ? kRowN4 : kRowP16);
+  const uint32_t ldr = fmt == kRowN4 ? (uint32_t)round_up((U + 7) / 8, 8) : ldw;  // row words
+  const size_t smem = std::max<size_t>(4ull * ldw, 4ull * kFSmemWords);  // histogram | merge + projection
+  if ((rc = c->partials.ensure(4ull * C * std::max(ldw, ldr)))) return rc;
   if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  if ((rc = c->Hx.ensure(8ull * kSmem16MaxBins, true))) return rc;
   uint32_t* ft = c->fused_tiles.as<uint32_t>();
   a.partials = c->partials.as<uint32_t>();
   a.C = C;
   a.ldw = ldw;
+  a.ldr = ldr;
   a.pack16 = pack;
+  a.nib4 = fmt == kRowN4;
   a.ovfH = c->ovfH.as<uint32_t>();
   a.H = H;
   a.tfb = nullptr;
   a.tsums = nullptr;
-  const uint64_t red_words = (uint64_t)kFusedTileSlots * kTileTotStride;  // per parity
+  const uint64_t red_words = (uint64_t)kFTileSlots * kTileTotStride;  // per parity
   a.tile_red = ft + red_words * (c->fused_seq & 1);
   a.tile_clear = ft + red_words * ((c->fused_seq + 1) & 1);
   a.tile_red_stride = kTileTotStride;
   a.tile_alt = ft + 2 * red_words;
-  a.ready = a.tile_alt + kFusedTileSlots;
+  a.ready = a.tile_alt + kFTileSlots;
+  // exception histogram of the 4-bit rows: parity buffers, the other one cleared by every launch
+  a.Hx = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * (c->fused_seq & 1);
+  a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);
   a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
   a.bar_base = c->bar64_base;
-  if (pack)
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+  if (fmt == kRowN4)
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowN4>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+  else if (fmt == kRowP16)
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowP16>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
   else
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowU32>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
   c->fused_seq++;
   c->bar64_base += 2ull * C;  // two barriers reserved per launch (one skipped unless overflow)
   return DIALSORT_OK;
@@ -517,7 +529,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   cudaDeviceSynchronize();
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
                   &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb,
-                  &c->fused_tiles})
+                  &c->fused_tiles, &c->Hx})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt) cudaFree(c->pt);
@@ -693,7 +705,7 @@ static int read_phase_stamps(dialsort_ctx c, std::vector<unsigned long long>& st
 int dialsort_debug_phase_ns(dialsort_ctx c, uint64_t* out16) {
   if (!c || !out16) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
   for (int i = 0; i < 16; ++i) out16[i] = 0;
-  std::vector<unsigned long long> st;
+  std::vector<unsigned long long> st;  // phases 0..7 only
   unsigned long long t0;
   int rc = read_phase_stamps(c, st, t0);
   if (rc || t0 == ~0ull) return rc;

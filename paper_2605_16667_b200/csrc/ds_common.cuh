@@ -36,7 +36,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // histograms, H, P) keeps its lines while 40+ MB stream past it.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
+#if DIALSORT_EXP_NORMAL_POLICY
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {
@@ -113,7 +117,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 // Plain stores by thread 0 of each CTA (no same-address atomics, which would serialise and
 // distort the timeline); the host reduces them (dialsort_debug_phase_ns / _cta).
 constexpr int kPhaseMaxCtas = 1024;
-constexpr int kPhaseSlots = 9;  // [0] = CTA start, [1 + i] = phase i
+constexpr int kPhaseSlots = 17;  // [0] = CTA start, [1 + i] = phase i (i < 16)
 struct PhaseTimes {
   unsigned long long stamp[kPhaseMaxCtas][kPhaseSlots];
 };

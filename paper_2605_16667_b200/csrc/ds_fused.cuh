@@ -3,66 +3,59 @@
 // the shared-memory paths (U <= kSmem16MaxBins).
 //
 //   ingestion   eq:ingestion P:409-412 (+ CRN def:crn_level P:896-915)   hist_ingest_flush
-//   merge       lem:crn P:951-962 lifted to whole histograms              merge_scan_tiles
-//   scan        GPU write-offset step (R18; paper P:13-14 has none)       merge_scan_tiles
-//   projection  eq:projection P:418-424                                   expand_chunk
+//   merge       lem:crn P:951-962 lifted to whole histograms              stage/reduce_batch
+//   scan        GPU write-offset step (R18; paper P:13-14 has none)       tile_offsets + batch P
+//   projection  eq:projection P:418-424                                   project_warp
 //
-// Why one kernel: on B200 a kernel boundary plus its ramp costs ~1-2 us and
-// the counter+generation grid barrier ~2 us, against a ~10 us HBM floor per 40 MB pass.  Here:
-//   1. every CTA ingests into its private shared-memory histogram, flushes it as partial row
-//      c and adds (RED) its per-tile sums into tile_red[tile];
-//   2. ONE monotonic grid barrier; every CTA then reads the <= 192 tile totals and scans them
-//      locally, so it knows the first output position toff[t] of every 512-bin scan tile;
-//   3. CTA c merges its own scan tiles (H, P) and publishes each (ready[t] = epoch);
-//   4. without another grid-wide barrier, each half of the CTA (512 threads, named barrier)
-//      projects an equal share of the output positions in 8192-position chunks, waiting only
-//      on the ready flags of the scan tiles its chunk overlaps.
-// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) switches all CTAs to a
-// path with a second barrier (tile totals recomputed from the merged H).
+// Why one kernel: on B200 a kernel boundary plus its ramp costs ~1-2 us and a
+// counter+generation grid barrier ~2 us, against a ~10 us HBM floor per 40 MB pass.
+//   1. Every CTA ingests its keys into a private shared-memory histogram, flushes it as
+//      partial row c (L2) and adds (RED) the row's 128-bin tile sums into tile totals.
+//   2. ONE monotonic grid barrier.  Every CTA reads the tile totals and scans them locally:
+//      toff[t] = first output position of tile t (the tile-level write offsets).
+//   3. Work is split in a "cost space" that concatenates, tile by tile, a merge segment of
+//      alpha units (the cost of merging the tile's C row segments) and one unit per output
+//      position of the tile.  CTA b takes the equal slice [T b / G, T (b+1) / G): it merges
+//      every tile its slice touches and projects the positions of those tiles that fall in
+//      its slice.  Positions are balanced (up to alpha) whatever the skew — a Zipf hot tile
+//      is projected by ~30 CTAs, each of which merges it (redundantly, 37 KB of L2 reads) —
+//      and no CTA waits for another after the barrier: each has the P values it needs in
+//      shared memory.  H is written by the CTA whose slice holds the tile's merge segment.
+// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) adds two barriers: tile
+// totals are recomputed with the fallback histogram ovfH, which is cleared at the end.
 #pragma once
 #include "ds_common.cuh"
-#include "ds_expand.cuh"
 #include "ds_hist.cuh"
 #include "ds_scan.cuh"
 
 namespace ds {
 
-constexpr uint32_t kMaxScanTiles = kSmem16MaxBins / kTileBins;  // 192
-constexpr uint32_t kFusedChunk = kExpandTile;                     // 8192 positions per half-CTA chunk
-constexpr uint32_t kFusedSub = 256;                               // threads per projection sub-group
-constexpr uint32_t kFusedNSub = 1024 / kFusedSub;                 // independent sub-groups per CTA
-constexpr uint32_t kFusedQPT = kFusedChunk / 4 / kFusedSub;       // quads (4 positions) per thread
-constexpr uint32_t kFusedStageOff = 4 * kTileBins;                // merge staging after 4 group rows (8 KB)
-constexpr uint32_t kFusedPBatch = 4;
-constexpr uint32_t kFusedPCap = 4096;                             // staged P entries per sub-group (16 KB)                              // P loads in flight per thread
-constexpr uint32_t kFusedTileSlots = 256;                         // >= kMaxScanTiles
-// Tile totals are REDs from every CTA into ntiles counters: 64-word (256 B) stride puts each
+constexpr uint32_t kFTiles = kSmem16MaxBins / kFTileBins;  // <= 768 tiles
+constexpr uint32_t kFSlotWords = 128;                       // staged words per row and batch (512 B)
+constexpr uint32_t kFMaxRows = 148;                         // rows (CTAs) a staging slot holds
+constexpr uint32_t kFTileSlots = 1024;                      // tile-total slots (>= kFTiles)
+// Tile totals are REDs from every CTA into ntiles counters: a 64-word (256 B) stride puts each
 // counter in its own L2 line (same-line REDs serialise: 4 lines took 7.7 us for 19K REDs).
 constexpr uint32_t kTileTotStride = 64;
-static_assert(kFusedQPT * 4 * kFusedSub == kFusedChunk, "chunk = whole quads per thread");
+constexpr uint32_t kFBatchBins = 1024;                      // max bins per batch (8 4-bit tiles)
+// Partial-row formats of k_sort_fused (bins per 128-word staged batch: 128, 256, 1024)
+constexpr int kRowU32 = 0, kRowP16 = 1, kRowN4 = 2;
+template <int FMT> struct RowFmt {
+  static constexpr uint32_t tpb = FMT == kRowU32 ? 1u : FMT == kRowP16 ? 2u : 8u;  // tiles per batch
+  static constexpr uint32_t wpt = kFSlotWords / tpb;  // row words per 128-bin tile (128, 64, 16)
+};
 
-// Named barrier of projection sub-group g (ids 1..kFusedNSub; 0 is __syncthreads).
-__device__ __forceinline__ void sub_sync(uint32_t g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kFusedSub) : "memory");
-}
+// Dynamic shared memory after the barrier (words); the ingestion histogram is dead by then.
+constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 128 words
+constexpr uint32_t kFOffToff = 2 * kFMaxRows * kFSlotWords;           // toff[kFTiles + 1]
+constexpr uint32_t kFOffScratch = kFOffToff + kFTiles + 32;           // 8 x 256 group sums
+constexpr uint32_t kFPassTiles = 32;                                 // tiles staged per projection pass
+constexpr uint32_t kFOffPs = kFOffScratch + 8 * kFBatchBins;          // pass P + 32 sentinels
+constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // 256 merged H of the batch
+constexpr uint32_t kFOffWc = kFOffHb + kFBatchBins;                   // 32 warps x 128 mark counts
+constexpr uint32_t kFSmemWords = kFOffWc + 32 * 128;
 
-// Exclusive scan over the kFusedSub threads of sub-group g; every warp scans the warp totals
-// itself (one named-barrier pair).  red: >= kFusedSub/32 slots owned by the sub-group.
-__device__ __forceinline__ uint64_t sub_excl_scan(uint64_t v, uint64_t& total, uint64_t* red, uint32_t g) {
-  constexpr uint32_t NW = kFusedSub / 32;
-  const uint32_t lane = threadIdx.x & 31, wh = (threadIdx.x % kFusedSub) >> 5;
-  const uint64_t inc = warp_incl_scan(v);
-  sub_sync(g);  // previous users of red are done
-  if (lane == 31) red[wh] = inc;
-  sub_sync(g);
-  const uint64_t w = lane < NW ? red[lane] : 0ull;
-  const uint64_t wi = warp_incl_scan(w);
-  total = __shfl_sync(FULL, wi, NW - 1);
-  const uint64_t wex = __shfl_sync(FULL, wi - w, wh);
-  return wex + inc - v;
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed_flag(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
@@ -79,257 +72,251 @@ __device__ __forceinline__ uint32_t tile_of(const uint32_t* toff, uint32_t ntile
   return lo;
 }
 
-// Projection of output positions [p0, p1) (p1 - p0 <= kFusedChunk) by one sub-group, whose
-// scan tiles are already published (the caller waited on their ready flags).
-// key(p) = max{k : P[k] <= p} (the bin whose run covers p; empty bins have P[k] = P[k+1] and
-// are skipped by the max).  With k0 = first bin of the scan tile ta holding p0 (P[k0] <= p0):
-//   key(p) = k0 + #{k > k0 : P[k] <= p0} + #{k > k0 : p0 < P[k] <= p},
-// the first count from a sub-group sum, the second from an inclusive scan of "bin start"
-// marks placed at P[k] - p0 in shared memory.  Only bins of scan tiles ta..tb (tb holds p1-1)
-// can contribute: later tiles start at >= toff[tb+1] > p1 - 1.
-// `ta` is the caller's running tile of p0: chunks of a share ascend, so it only moves forward
-// (O(ntiles) steps over a whole share, instead of a binary search per chunk and thread).
-__device__ __forceinline__ void expand_chunk(const ScanArgs& a, const uint32_t* toff, uint32_t ntiles, uint32_t p0,
-                                             uint32_t p1, uint32_t& ta, int32_t key_base, int32_t* __restrict__ out,
-                                             uint32_t* M, uint64_t* red, uint32_t g, bool aligned, uint64_t pol) {
-  const uint32_t tid = threadIdx.x % kFusedSub;
-  while (toff[ta + 1] <= p0) ++ta;  // toff[ntiles] = total > p0 stops it
-  uint32_t tb = ta;
-  while (toff[tb + 1] <= p1 - 1) ++tb;
-  uint4* M4 = reinterpret_cast<uint4*>(M);
-#pragma unroll
-  for (uint32_t j = 0; j < kFusedQPT; ++j) M4[tid + j * kFusedSub] = make_uint4(0, 0, 0, 0);
-  sub_sync(g);
-  const uint32_t k0 = ta * kTileBins;
-  const uint32_t kend = min((tb + 1) * kTileBins, a.U);
-  // all P loads of a thread are issued before any is used (a shared atomic between them
-  // would otherwise serialise one L2 round trip per bin batch)
-  uint32_t before = 0;
-  for (uint32_t kb = k0 + 1 + tid; kb < kend; kb += kFusedPBatch * kFusedSub) {
-    uint32_t b[kFusedPBatch];
-#pragma unroll
-    for (uint32_t u = 0; u < kFusedPBatch; ++u) {
-      const uint32_t k = kb + u * kFusedSub;
-      b[u] = k < kend ? __ldcg(a.P + k) : 0xffffffffu;
-    }
-#pragma unroll
-    for (uint32_t u = 0; u < kFusedPBatch; ++u) {
-      if (b[u] <= p0) {
-        ++before;
-      } else if (b[u] < p1) {
-        const uint32_t w = b[u] - p0;
-        atomicAdd(&M[(swz(w >> 2) << 2) | (w & 3u)], 1u);
-      }
-    }
+// ---- projection ----------------------------------------------------------------------------
+// Projection of positions [lo, hi) whose bins are ka .. ka+m-1 with P staged as Ps[0..m)
+// (+ 32 sentinels 0xffffffff), P[ka] <= lo: for every position p of the range
+//   key(p) = max{k : P[k] <= p} = ka - 1 + cnt(p),   cnt(p) = #{i : Ps[i] <= p}
+// (the bin whose run covers p; empty bins share their start with the next bin and are
+// skipped by the max); kbase = key_base + ka - 1.
+// The range is cut into 512-position super-blocks aligned to absolute multiples of 512,
+// dealt round-robin to the CTA's 32 warps, so the CTA writes one contiguous front (measured:
+// 5.6 us for 40 MB of stores vs 8.8 us when each warp streams a range of its own — DRAM page
+// locality).  A super-block is 4 sub-blocks of 128 positions; lane l owns the quad at
+// positions sb + 128 s + 4 l .. +3 of sub-block s, and each sub-block leaves as one
+// coalesced 512-byte warp store.  A warp keeps c = #{i : Ps[i] < sb} and a register window
+// sreg = Ps[cb + lane] (cb <= c <= cb + 15); the bin starts of the super-block are window
+// lanes o = c-cb .. le-1, found with one ballot:
+//   none      every position has key kbase + c (four stores);
+//   distinct  (starts in distinct quads: bins longer than 4, the common case) four
+//             OR-reductions give per-sub-block quad occupancy masks M_s; lane l adds the
+//             starts of the quads before its own (popc) plus its own quad's start where that
+//             start's offset <= the position;
+//   otherwise (starts sharing a quad, or more than the window holds) sub-block by sub-block,
+//             each start adds a mark to the warp's 128-entry count array and a warp scan
+//             gives cnt — O(starts) in parallel (a per-start loop over the lanes' positions
+//             measured 10x slower on Zipf's short bins).
+// The projection is issue-bound (ncu ~70% issue-active at one 128-position block per
+// iteration), so the per-iteration bookkeeping is amortised over 4 quads per lane.
+__device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
+                                           bool aligned, uint64_t pol) {
+  const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
+  if (aligned && p >= lo && p + 4 <= hi) {
+    st_stream4(reinterpret_cast<int4*>(out + p), v, pol);
+  } else {
+    if (p >= lo && p < hi) out[p] = v.x;
+    if (p + 1 >= lo && p + 1 < hi) out[p + 1] = v.y;
+    if (p + 2 >= lo && p + 2 < hi) out[p + 2] = v.z;
+    if (p + 3 >= lo && p + 3 < hi) out[p + 3] = v.w;
   }
-  sub_sync(g);
-  // inclusive scan of the marks (thread owns positions 4 QPT tid ..); the sub-group scan
-  // carries (before << 32 | marks) so one pass yields both counts
-  uint4 v[kFusedQPT];
-#pragma unroll
-  for (uint32_t j = 0; j < kFusedQPT; ++j) {
-    v[j] = M4[swz(kFusedQPT * tid + j)];
-    v[j].y += v[j].x;
-    v[j].z += v[j].y;
-    v[j].w += v[j].z;
-  }
-#pragma unroll
-  for (uint32_t j = 1; j < kFusedQPT; ++j) {
-    v[j].x += v[j - 1].w; v[j].y += v[j - 1].w; v[j].z += v[j - 1].w; v[j].w += v[j - 1].w;
-  }
-  uint64_t tot;
-  const uint64_t ex = sub_excl_scan(((uint64_t)before << 32) | v[kFusedQPT - 1].w, tot, red, g);
-  const uint32_t base = (uint32_t)key_base + k0 + (uint32_t)(tot >> 32) + (uint32_t)ex;
-#pragma unroll
-  for (uint32_t j = 0; j < kFusedQPT; ++j)
-    M4[swz(kFusedQPT * tid + j)] = make_uint4(base + v[j].x, base + v[j].y, base + v[j].z, base + v[j].w);
-  sub_sync(g);
-  // copy out: lane-contiguous quads, 512 contiguous bytes per warp instruction
-  if (aligned && p1 - p0 == kFusedChunk) {  // full chunk: no bounds tests
-#pragma unroll
-    for (uint32_t j = 0; j < kFusedQPT; ++j) {
-      const uint32_t qd = tid + j * kFusedSub;
-      const uint4 x = M4[swz(qd)];
-      st_stream4(reinterpret_cast<int4*>(out + p0 + 4 * qd), make_int4((int)x.x, (int)x.y, (int)x.z, (int)x.w), pol);
-    }
-    sub_sync(g);
-    return;
-  }
-#pragma unroll
-  for (uint32_t j = 0; j < kFusedQPT; ++j) {
-    const uint32_t qd = tid + j * kFusedSub;
-    const uint32_t q = p0 + 4 * qd;
-    if (q >= p1) continue;
-    const uint4 x = M4[swz(qd)];
-    if (aligned && q + 4 <= p1) {
-      st_stream4(reinterpret_cast<int4*>(out + q), make_int4((int)x.x, (int)x.y, (int)x.z, (int)x.w), pol);
-    } else {
-      out[q] = (int)x.x;
-      if (q + 1 < p1) out[q + 1] = (int)x.y;
-      if (q + 2 < p1) out[q + 2] = (int)x.z;
-      if (q + 3 < p1) out[q + 3] = (int)x.w;
-    }
-  }
-  sub_sync(g);  // M is reused by the next chunk
 }
 
-// Projection of one sub-group's share [lo, hi) by independent warps (no sub-group barrier
-// after the staging of P).  Bins ka .. kb-1 are the bins of the scan tiles overlapping the
-// share; Ps[i] = P[ka + i] is staged in shared memory.  P[ka] = toff[ta] <= lo, so for every
-// position p of the share
-//   key(p) = max{k : P[k] <= p} = ka - 1 + cnt(p),   cnt(p) = #{i : Ps[i] <= p}.
-// The share is cut into 128-position blocks dealt round-robin to the sub-group's 8 warps, so
-// that the sub-group writes one contiguous front (measured: 5.8 us for 40 MB of stores vs
-// 8.8 us when each warp streams its own contiguous range — DRAM page locality).  Lane l owns
-// positions blk + 4l .. +3 and the block leaves as one coalesced 512-byte warp store.
-// A warp keeps c = #{i : Ps[i] < blk} and a register window sreg = Ps[cb + lane] (cb <= c),
-// so the bin starts of a block are window lanes c-cb .. c-cb+nb-1, found with one ballot:
-//   nb == 0      every position of the block has key ka - 1 + c;
-//   nb < 32-o    each lane compares its 4 positions with the nb starts (shuffled in);
-//   otherwise    the starts add marks in the warp's 128-entry count array and a warp scan of
-//                the per-lane mark totals gives cnt (more than 32 starts: repeated).
-// FAST: Ps holds all m entries plus >= 32 sentinels (0xffffffff), the output is 16-byte
-// aligned and only whole blocks are projected — the loop is issue-bound (ncu: 73% issue
-// active), so the common case is kept to a few instructions; the general form (FAST = false)
-// reads entries past kFusedPCap from L2 and handles the tail block and unaligned output.
-template <bool FAST>
-__device__ __forceinline__ void expand_share_warp(const ScanArgs& a, uint32_t ka, uint32_t kb, uint32_t lo, uint32_t hi,
-                                                  uint32_t blk, const uint32_t* Ps, uint32_t* wc, int32_t key_base,
-                                                  int32_t* __restrict__ out, bool aligned, uint64_t pol) {
-  constexpr uint32_t NW = kFusedSub / 32;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t m = kb - ka;
-  auto pv = [&](uint32_t i) -> uint32_t {
-    if (FAST) return Ps[i];
-    return i < m ? (i < kFusedPCap ? Ps[i] : __ldcg(a.P + ka + i)) : 0xffffffffu;
-  };
-  if (FAST ? blk + 128 > hi : blk >= hi) return;
-  // c = #{i : Ps[i] < blk}
+__device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
+                                             uint32_t* wc, int32_t* __restrict__ out, bool aligned, uint64_t pol) {
+  constexpr uint32_t NW = 32, SB = 512;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t ltmask = (1u << lane) - 1u;
+  uint32_t sb = (lo & ~(SB - 1)) + SB * w;
+  if (sb >= hi) return;
+  // c = #{i : Ps[i] < sb}  (sentinels are never < sb, so c <= m)
   uint32_t c0 = 0, c1 = m;
   while (c0 < c1) {
     const uint32_t mid = (c0 + c1) >> 1;
-    if (pv(mid) < blk) c0 = mid + 1;
+    if (Ps[mid] < sb) c0 = mid + 1;
     else c1 = mid;
   }
   uint32_t c = c0, cb = c0;
-  uint32_t sreg = pv(cb + lane);
-  const uint32_t kbase = (uint32_t)key_base + ka - 1;
+  uint32_t sreg = Ps[cb + lane];
   for (;;) {
-    const uint32_t p = blk + 4 * lane;
-    const uint32_t bend = FAST ? blk + 127 : (hi - blk > 128 ? blk + 127 : hi - 1);
+    const uint32_t bend = hi - sb > SB ? sb + SB - 1 : hi - 1;
     if (c - cb >= 16) {  // keep >= 16 lanes of look-ahead in the window
       cb = c;
-      sreg = pv(cb + lane);
+      sreg = Ps[cb + lane];
     }
     const uint32_t o = c - cb;
     const uint32_t le = __popc(__ballot_sync(FULL, sreg <= bend));
     const uint32_t base = kbase + c;
-    uint4 q = make_uint4(base, base, base, base);
-    if (le != o) {  // the block holds bin starts
-      // starts o..le-1 of the window; when they lie in distinct quads (the common case: bins
-      // longer than 4), one OR-reduction gives the quad occupancy mask M, lane l adds the
-      // starts of quads < l (popc) plus its own quad's start if its offset is <= the position
-      const bool mine = lane >= o && lane < le;
-      const uint32_t rel = sreg - blk;
-      const uint32_t M = __reduce_or_sync(FULL, mine ? 1u << (rel >> 2) : 0u);
-      if (le < 32 && (uint32_t)__popc(M) == le - o) {
-        const uint32_t below = __popc(M & ((1u << lane) - 1u));
-        const uint32_t r = (__shfl_sync(FULL, sreg, min(o + below, 31u)) - blk) & 3u;
-        const uint32_t own = (M >> lane) & 1u;
-        q.x += below + (own & (r == 0));
-        q.y += below + (own & (r <= 1));
-        q.z += below + (own & (r <= 2));
-        q.w += below + own;
-      } else if (le < 32) {
-        for (uint32_t j = o; j < le; ++j) {
-          const uint32_t sj = __shfl_sync(FULL, sreg, j);
-          q.x += sj <= p;
-          q.y += sj <= p + 1;
-          q.z += sj <= p + 2;
-          q.w += sj <= p + 3;
-        }
-      } else {
-        // marks: starts Ps[c ..] <= bend, 32 at a time
-        uint32_t i0 = c;
-        for (;;) {
-          const uint32_t sl = pv(i0 + lane);
-          const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= bend));
-          if (lane < cnt) atomicAdd(&wc[sl - blk], 1u);
-          if (cnt < 32) break;
-          i0 += 32;
-        }
-        __syncwarp();
-        uint4 mk = reinterpret_cast<uint4*>(wc)[lane];
-        reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
-        mk.y += mk.x;
-        mk.z += mk.y;
-        mk.w += mk.z;
-        const uint32_t ex = warp_incl_scan(mk.w) - mk.w;
-        q.x += ex + mk.x; q.y += ex + mk.y; q.z += ex + mk.z; q.w += ex + mk.w;
-        __syncwarp();
-      }
-    }
-    const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
-    if (FAST) {
-      st_stream4(reinterpret_cast<int4*>(out + p), v, pol);
-      if (hi - blk < 128 * NW + 128) break;  // no further whole block for this warp
+    if (le == o) {  // no bin starts in the super-block
+      const uint4 q = make_uint4(base, base, base, base);
+#pragma unroll
+      for (uint32_t s = 0; s < 4; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol);
     } else {
-      if (p < hi) {
-        if (aligned && p + 4 <= hi) {
-          st_stream4(reinterpret_cast<int4*>(out + p), v, pol);
-        } else {
-          out[p] = v.x;
-          if (p + 1 < hi) out[p + 1] = v.y;
-          if (p + 2 < hi) out[p + 2] = v.z;
-          if (p + 3 < hi) out[p + 3] = v.w;
+      bool done = false;
+      if (le < 32) {
+        const bool mine = lane >= o && lane < le;
+        const uint32_t qi = (sreg - sb) >> 2;  // quad of the super-block (valid when mine)
+        uint32_t M[4];
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) M[s] = __reduce_or_sync(FULL, (mine && (qi >> 5) == s) ? 1u << (qi & 31) : 0u);
+        if ((uint32_t)(__popc(M[0]) + __popc(M[1]) + __popc(M[2]) + __popc(M[3])) == le - o) {
+          uint32_t cum = 0;
+#pragma unroll
+          for (uint32_t s = 0; s < 4; ++s) {
+            const uint32_t below = cum + __popc(M[s] & ltmask);
+            const uint32_t own = (M[s] >> lane) & 1u;
+            const uint32_t r = (__shfl_sync(FULL, sreg, min(o + below, 31u)) - sb) & 3u;
+            const uint32_t v = base + below;
+            store_quad(out, sb + 128 * s + 4 * lane, lo, hi,
+                       make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own),
+                       aligned, pol);
+            cum += __popc(M[s]);
+          }
+          done = true;
         }
       }
-      if (hi - blk <= 128 * NW) break;
+      if (!done) {
+        // starts sharing quads, or more than the window holds: sub-block by sub-block, each
+        // start adds a mark to the warp's 128-entry count array (O(starts) in parallel)
+        uint32_t cs = c;  // #{i : Ps[i] < b0}
+#pragma unroll 1
+        for (uint32_t s = 0; s < 4; ++s) {
+          const uint32_t b0 = sb + 128 * s;
+          if (b0 >= hi) break;
+          const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
+          uint32_t i1 = cs;
+          for (;;) {
+            const uint32_t sl = Ps[min(i1 + lane, m)];  // Ps[m] is a sentinel
+            const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= be));
+            if (lane < cnt) atomicAdd(&wc[sl - b0], 1u);
+            i1 += cnt;
+            if (cnt < 32) break;
+          }
+          __syncwarp();
+          uint4 mk = reinterpret_cast<uint4*>(wc)[lane];
+          reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
+          mk.y += mk.x;
+          mk.z += mk.y;
+          mk.w += mk.z;
+          const uint32_t v = kbase + cs + warp_incl_scan(mk.w) - mk.w;
+          store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol);
+          __syncwarp();
+          cs = i1;  // starts <= be counted: #{i : Ps[i] < b0 + 128}
+        }
+      }
     }
-    // advance: c = #{i : Ps[i] < next block}
-    blk += 128 * NW;
-    const uint32_t lt = __popc(__ballot_sync(FULL, sreg < blk));
+    if (hi - sb <= SB * NW) break;
+    sb += SB * NW;
+    // advance: c = #{i : Ps[i] < sb}
+    const uint32_t lt = __popc(__ballot_sync(FULL, sreg < sb));
     if (lt < 32) {
       c = cb + lt;
     } else {
-      c = cb + 32;
-      for (;;) {
-        const uint32_t adv = __popc(__ballot_sync(FULL, pv(c + lane) < blk));
-        c += adv;
-        if (adv < 32) break;
+      // the warp's next super-block is 16K positions away: in a start-dense region (short
+      // bins) thousands of starts lie between, so search rather than walk
+      uint32_t x0 = cb + 32, x1 = m;
+      while (x0 < x1) {
+        const uint32_t mid = (x0 + x1) >> 1;
+        if (Ps[mid] < sb) x0 = mid + 1;
+        else x1 = mid;
       }
-      cb = c;
-      sreg = pv(cb + lane);
+      c = cb = x0;
+      sreg = Ps[cb + lane];
     }
   }
 }
 
-// Stage P for a share and project it: whole blocks by the FAST loop when the staged window
-// holds every entry (+ sentinels) and the output is aligned; the rest by the general loop.
-__device__ __forceinline__ void expand_share(const ScanArgs& a, uint32_t ka, uint32_t kb, uint32_t lo, uint32_t hi,
-                                             uint32_t* Ps, uint32_t* wc, uint32_t g, int32_t key_base,
-                                             int32_t* __restrict__ out, bool aligned, uint64_t pol) {
-  const uint32_t m = kb - ka, tid = threadIdx.x % kFusedSub;
-  const bool fast = aligned && m + 32 <= kFusedPCap;
-  const uint32_t ncp = min(m + 32, kFusedPCap);
-  for (uint32_t i = tid; i < ncp; i += kFusedSub) Ps[i] = i < m ? __ldcg(a.P + ka + i) : 0xffffffffu;
-  reinterpret_cast<uint4*>(wc)[threadIdx.x & 31] = make_uint4(0, 0, 0, 0);
-  sub_sync(g);
-  const uint32_t w = tid >> 5;
-  if (fast) {
-    // whole blocks: [lo, lo + 128 * nblk); the partial tail block (if any) by warp nblk % 8
-    const uint32_t nblk = (hi - lo) / 128;
-    expand_share_warp<true>(a, ka, kb, lo, hi, lo + 128 * w, Ps, wc, key_base, out, aligned, pol);
-    const uint32_t tail = lo + 128 * nblk;
-    if (tail < hi && w == nblk % (kFusedSub / 32))
-      expand_share_warp<false>(a, ka, kb, tail, hi, tail, Ps, wc, key_base, out, aligned, pol);
-  } else {
-    expand_share_warp<false>(a, ka, kb, lo, hi, lo + 128 * w, Ps, wc, key_base, out, aligned, pol);
+// ---- merge of one batch (1 u32 tile or 2 packed tiles = 512 B of every row) --------------
+// Issues the cp.async copies of the batch's row segments into a staging slot (row r: 128
+// words at slot + 128 r).  Tiles of the batch that this CTA does not need are not copied.
+template <int FMT>
+__device__ __forceinline__ void stage_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, uint32_t* slot) {
+  if (!need_mask) return;
+  constexpr uint32_t qpt = 32 / RowFmt<FMT>::tpb;  // uint4 per tile (32, 16, 4)
+  const uint32_t Wrow = FMT == kRowU32 ? a.U : FMT == kRowP16 ? (a.U + 1) / 2 : (a.U + 7) / 8;  // row words
+  const uint32_t w0 = t0 * RowFmt<FMT>::wpt;  // first word of the batch (tiles t0 ..) in a row
+#if DIALSORT_STAGE_LDG
+  // register path: up to 8 loads per thread in flight, then the shared stores
+  uint4 v[8];
+  uint32_t dst[8];
+#pragma unroll
+  for (uint32_t u = 0; u < 8; ++u) {
+    const uint32_t i = threadIdx.x + u * blockDim.x;
+    dst[u] = 0xffffffffu;
+    v[u] = make_uint4(0, 0, 0, 0);
+    if (i < a.C * 32) {
+      const uint32_t r = i >> 5, l = i & 31;
+      if ((need_mask >> (l / qpt)) & 1u) {
+        const uint32_t word = w0 + 4 * l;
+        if (word < Wrow) v[u] = __ldcg(reinterpret_cast<const uint4*>(a.partials + (uint64_t)r * a.ldr + word));
+        dst[u] = r * kFSlotWords + 4 * l;
+      }
+    }
+  }
+#pragma unroll
+  for (uint32_t u = 0; u < 8; ++u)
+    if (dst[u] != 0xffffffffu) *reinterpret_cast<uint4*>(slot + dst[u]) = v[u];
+#else
+  for (uint32_t i = threadIdx.x; i < a.C * 32; i += blockDim.x) {
+    const uint32_t r = i >> 5, l = i & 31;  // row, uint4 within the batch
+    if (!((need_mask >> (l / qpt)) & 1u)) continue;
+    const uint32_t word = w0 + 4 * l;
+    const uint32_t bytes = word < Wrow ? 16u : 0u;  // zero-fill past the row's last word
+    const uint32_t* src = a.partials + (uint64_t)r * a.ldr + (bytes ? word : 0u);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(slot + r * kFSlotWords + 4 * l)),
+                 "l"(src), "r"(bytes)
+                 : "memory");
+  }
+#endif
+}
+
+// Sums the staged rows of a batch: hb[j] = merged count of the batch's bin j (+ the 4-bit
+// rows' exceptions Hx, + ovfH when the packed counters overflowed somewhere), 0 for the bins
+// of tiles not needed.  8 row groups of 128 threads: thread j sums word column j & 127 over
+// rows r = j >> 7 (mod 8) — 4-bit rows as four 2 x 16-bit SWAR accumulators (8 bins).
+template <int FMT>
+__device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, const uint32_t* slot,
+                                             uint32_t* scratch, uint32_t* hb, bool use_ovf) {
+  constexpr uint32_t tpb = RowFmt<FMT>::tpb, wpt = RowFmt<FMT>::wpt, nb = tpb * kFTileBins;
+  const uint32_t col = threadIdx.x & 127, qg = threadIdx.x >> 7;
+  if ((need_mask >> (col / wpt)) & 1u) {
+    if (FMT == kRowN4) {
+      uint32_t el = 0, eh = 0, ol = 0, oh = 0;  // 16-bit lanes: nibbles (0,4) (2,6) (1,5) (3,7)
+      for (uint32_t r = qg; r < a.C; r += 8) {
+        const uint32_t x = slot[r * kFSlotWords + col];
+        const uint32_t e = x & 0x0F0F0F0Fu, o = (x >> 4) & 0x0F0F0F0Fu;
+        el += e & 0x00FF00FFu;
+        eh += (e >> 8) & 0x00FF00FFu;
+        ol += o & 0x00FF00FFu;
+        oh += (o >> 8) & 0x00FF00FFu;
+      }
+      uint32_t* d = scratch + qg * kFBatchBins + 8 * col;  // bins 8 col .. 8 col + 7
+      reinterpret_cast<uint4*>(d)[0] = make_uint4(el & 0xffffu, ol & 0xffffu, eh & 0xffffu, oh & 0xffffu);
+      reinterpret_cast<uint4*>(d)[1] = make_uint4(el >> 16, ol >> 16, eh >> 16, oh >> 16);
+    } else {
+      uint32_t lo = 0, hi = 0;
+      for (uint32_t r = qg; r < a.C; r += 8) {
+        const uint32_t x = slot[r * kFSlotWords + col];
+        if (FMT == kRowP16) {
+          lo += x & 0xffffu;
+          hi += x >> 16;
+        } else {
+          lo += x;
+        }
+      }
+      if (FMT == kRowP16) {
+        scratch[qg * kFBatchBins + 2 * col] = lo;
+        scratch[qg * kFBatchBins + 2 * col + 1] = hi;
+      } else {
+        scratch[qg * kFBatchBins + col] = lo;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nb; j += blockDim.x) {
+    uint32_t h = 0;
+    if ((need_mask >> (j / kFTileBins)) & 1u) {
+#pragma unroll
+      for (uint32_t g = 0; g < 8; ++g) h += scratch[g * kFBatchBins + j];
+      const uint64_t bin = (uint64_t)t0 * kFTileBins + j;
+      if (bin < a.U) {
+        if (FMT == kRowN4) h += __ldcg(a.Hx + bin);
+        if (use_ovf) h += __ldcg(a.ovfH + bin);
+      }
+    }
+    hb[j] = h;
   }
 }
 
-// Block-wide scan of the tile totals into toff[0..ntiles] (ntiles <= 192 < blockDim).
-// v = this thread's tile total (thread t holds tile t), loaded by the caller.
+// Block-wide scan of the tile totals (thread t holds tile t's total v) into toff[0..ntiles].
 __device__ __forceinline__ void tile_offsets(uint64_t v, uint32_t ntiles, uint32_t* toff, uint64_t* red) {
   uint64_t total;
   const uint64_t ex = block_excl_scan<uint64_t>(v, total, red);
@@ -338,105 +325,179 @@ __device__ __forceinline__ void tile_offsets(uint64_t v, uint32_t ntiles, uint32
   __syncthreads();
 }
 
-// One DialSort step: keys[n] in [0,U) -> out[min(ΣH, cap)] sorted, H and P as by-products.
-// Grid: C <= #SMs CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic smem:
-// max(histogram, 128 KB) (histogram, then merge scratch, then kFusedNSub 32 KB mark buffers).
-template <bool PACK16>
+// Overflow path: exact total of tile t straight from the partial rows, Hx and ovfH.
+template <int FMT>
+__device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_t t, uint64_t* red) {
+  uint64_t s = 0;
+  const uint32_t k0 = t * kFTileBins;
+  for (uint32_t i = threadIdx.x; i < kFTileBins * a.C; i += blockDim.x) {
+    const uint32_t j = i % kFTileBins, r = i / kFTileBins, k = k0 + j;
+    if (k >= a.U) continue;
+    const uint32_t* row = a.partials + (uint64_t)r * a.ldr;
+    if (FMT == kRowU32) s += __ldcg(row + k);
+    else if (FMT == kRowP16) s += (__ldcg(row + (k >> 1)) >> ((k & 1u) << 4)) & 0xffffu;
+    else s += (__ldcg(row + (k >> 3)) >> ((k & 7u) << 2)) & 0xfu;
+    if (r == 0) s += __ldcg(a.ovfH + k) + (FMT == kRowN4 ? __ldcg(a.Hx + k) : 0u);
+  }
+  return block_sum<uint64_t>(s, red);
+}
+
+// One DialSort step: keys[n] in [0,U) -> out[min(ΣH, cap)] sorted; H as a by-product.
+// Grid: C <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic
+// smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch.
+template <int FMT>
 __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
-  extern __shared__ __align__(128) uint32_t sh_hist[];
+  extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
-  __shared__ uint64_t sred[kFusedNSub][kFusedSub / 32];
-  __shared__ uint32_t toff[kMaxScanTiles + 1];
+  __shared__ uint32_t wsum[32];
   pdl_wait();
   phase_mark(a.pt, -1);
-  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
-  const uint32_t G = gridDim.x;
+  const uint32_t U = a.U, ntiles = (U + kFTileBins - 1) / kFTileBins;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
   // the other parity's tile totals are zeroed for the next launch (host alternates them;
   // every slot, since the next launch may have more tiles than this one)
-  if (blockIdx.x == G - 1)
-    for (uint32_t i = threadIdx.x; i < kFusedTileSlots; i += blockDim.x) a.tile_clear[i * kTileTotStride] = 0;
+  if (b == G - 1)
+    for (uint32_t i = threadIdx.x; i < kFTileSlots; i += blockDim.x) a.tile_clear[(uint64_t)i * kTileTotStride] = 0;
+  if (a.Hx_clear)  // and the other parity's exception histogram (all of it: launches of any
+                   // format alternate the parity, and the next may have a larger U), a slice per CTA
+    for (uint32_t k = kSmem16MaxBins * b / G + threadIdx.x; k < kSmem16MaxBins * (b + 1) / G; k += blockDim.x)
+      a.Hx_clear[k] = 0;
+  constexpr bool PACK16 = FMT != kRowU32;
 
-  hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh_hist, red64, nullptr, nullptr);
+  hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr);
   grid_barrier_mono(a.bar64, a.bar_base + G);  // rows, tile totals, overflow fallback in L2
   phase_mark(a.pt, 3);
 
-  uint32_t tb0, tb1;
-  my_tiles(ntiles, tb0, tb1);
+  uint32_t* toff = sh + kFOffToff;
   const bool use_ovf = ld_acquire_u32(&a.st->ovf_epoch) == a.epoch;
+  uint32_t tb0, tb1;
+  my_tiles(ntiles, tb0, tb1);  // tiles this CTA merges and publishes (index ownership)
+  uint64_t tv;                 // tile threadIdx.x's total: loaded now, scanned after the merge
   if (!use_ovf) {
-    barrier_skip(a.bar64);  // the fallback's second barrier is not needed
-    // the tile totals are loaded together with the first tile's partial rows (one L2 round
-    // trip for both) and scanned once the rows are summed
-    const uint64_t tv = threadIdx.x < ntiles ? __ldcg(a.tile_red + (uint64_t)threadIdx.x * a.tile_red_stride) : 0ull;
-    merge_scan_tiles<PACK16>(
-        a, tb0, tb1,
-        [&]() -> uint64_t {
-          tile_offsets(tv, ntiles, toff, red64);
-          return toff[tb0];
-        },
-        false, sh_hist, red64, sh_hist + kFusedStageOff);
+    barrier_skip(a.bar64);
+    tv = threadIdx.x < ntiles ? __ldcg(a.tile_red + (uint64_t)threadIdx.x * a.tile_red_stride) : 0ull;
   } else {
-    // a packed counter overflowed somewhere: the flushed tile sums are incomplete.  Merge
-    // (adding the fallback histogram), publish exact tile totals, barrier, then scan.
+    // a packed counter overflowed somewhere: the flushed tile sums miss the fallback keys
     for (uint32_t t = tb0; t < tb1; ++t) {
-      const uint64_t tt = merge_tile(a, t, true, sh_hist, red64);
+      const uint64_t tt = tile_total_direct<FMT>(a, t, red64);
       if (threadIdx.x == 0) __stcg(a.tile_alt + t, (uint32_t)(tt > 0xffffffffull ? 0xffffffffull : tt));
     }
     grid_barrier_mono(a.bar64, a.bar_base + 2 * G);
-    tile_offsets(threadIdx.x < ntiles ? __ldcg(a.tile_alt + threadIdx.x) : 0ull, ntiles, toff, red64);
-    for (uint32_t t = tb0; t < tb1; ++t) {
-      scan_tile(a, a.H, t, toff[t], red64);
-      __syncthreads();
-      if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t), "r"(a.epoch) : "memory");
-    }
+    tv = threadIdx.x < ntiles ? __ldcg(a.tile_alt + threadIdx.x) : 0ull;
   }
-  if (tb1 == ntiles && tb1 > tb0 && threadIdx.x == 0) scan_finish(a, toff[ntiles]);
   phase_mark(a.pt, 4);
-  __syncthreads();  // merge scratch (sh_hist) becomes the mark buffers
 
-  // Projection: sub-group s of S = kFusedNSub * G projects positions [b(s), b(s+1)),
-  // b(s) = ⌊nw s / S⌋ & ~31, in chunks; it first waits (once) for the ready flags of every
-  // scan tile its share overlaps.
-  const uint64_t total = toff[ntiles];
-  const uint32_t nw = (uint32_t)(total < a.n_expected ? total : a.n_expected);
-  const uint32_t g = threadIdx.x / kFusedSub;
-  const uint32_t S = kFusedNSub * G, s = kFusedNSub * blockIdx.x + g;
-  const uint32_t lo = s == 0 ? 0u : (uint32_t)(((uint64_t)nw * s / S) & ~31ull);
-  const uint32_t hi = s + 1 == S ? nw : (uint32_t)(((uint64_t)nw * (s + 1) / S) & ~31ull);
-  uint32_t ta = 0;
-  if (lo < hi) {
-    ta = tile_of(toff, ntiles, lo);
-    const uint32_t tb = tile_of(toff, ntiles, hi - 1);
-    // relaxed polling (with a short sleep, so spinning warps leave issue slots to the rest
-    // of the CTA), then one acquire LOAD of the flag.  Not a fence: fence.acq_rel.gpu is a
-    // MEMBAR that waits for every store in flight from this SM — the output stream of the
-    // sub-groups already projecting — measured as ~3 us of extra wait per share.
-    for (uint32_t t = ta + threadIdx.x % kFusedSub; t <= tb; t += kFusedSub) {
-      while (ld_relaxed_flag(a.ready + t) != a.epoch) __nanosleep(64);
-      (void)ld_acquire_u32(a.ready + t);
+  // ---- merge: H and the tile-relative exclusive prefix PL of the tiles this CTA owns ------
+  // (lem:crn lifted to whole histograms: H = sum of the partial rows, + Hx, + ovfH), published
+  // per batch (ready[t] = epoch, release).  No dependence on the tile offsets, so it starts
+  // right after the barrier; the projection adds toff[t] itself.
+  constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
+  constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
+  uint32_t* slot[2] = {sh + kFOffStage, sh + kFOffStage + kFMaxRows * kFSlotWords};
+  uint32_t* scratch = sh + kFOffScratch;
+  uint32_t* hb = sh + kFOffHb;
+  uint32_t* wc = sh + kFOffWc + (threadIdx.x >> 5) * 128;
+  reinterpret_cast<uint4*>(wc)[threadIdx.x & 31] = make_uint4(0, 0, 0, 0);
+  if (tb0 < tb1) {
+    const uint32_t nbt = (tb1 - tb0 + tpb - 1) / tpb;  // batches of tiles tb0 + k tpb ..
+    auto need_of = [&](uint32_t k) -> uint32_t {
+      const uint32_t t0 = tb0 + k * tpb, nt = min(tpb, tb1 - t0);
+      return nt >= 32 ? 0xffffffffu : (1u << nt) - 1u;
+    };
+    for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
+      stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot[k]);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (uint32_t k = 0; k < nbt; ++k) {
+      const uint32_t t0 = tb0 + k * tpb, need = need_of(k);
+      if (k + 1 < nbt) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+      phase_mark(a.pt, 5);
+      reduce_batch<FMT>(a, t0, need, slot[k & 1], scratch, hb, use_ovf);
+      __syncthreads();  // hb complete; the slot is free
+      if (k + 2 < nbt) {
+        stage_batch<FMT>(a, tb0 + (k + 2) * tpb, need_of(k + 2), slot[k & 1]);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      // tile-relative exclusive prefix (a 128-bin tile is 4 whole warps)
+      const uint32_t j = threadIdx.x;
+      const uint32_t h = j < nbb ? hb[j] : 0u;
+      const uint32_t inc = warp_incl_scan(h);
+      if (j < nbb && (j & 31) == 31) wsum[j >> 5] = inc;
+      __syncthreads();
+      if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
+        uint32_t wpre = 0;
+        for (uint32_t q = (j / kFTileBins) * (kFTileBins / 32); q < (j >> 5); ++q) wpre += wsum[q];
+        const uint32_t bin = t0 * kFTileBins + j;
+        if (bin < U) {
+          a.H[bin] = h;
+          a.P[bin] = wpre + inc - h;
+        }
+      }
+      __syncthreads();  // the batch's H and PL are written
+      if (threadIdx.x < tpb && ((need >> threadIdx.x) & 1u))
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t0 + threadIdx.x), "r"(a.epoch) : "memory");
     }
   }
-  sub_sync(g);
-  phase_mark(a.pt, 5);
+  if (use_ovf)  // only this CTA read ovfH for its tiles: clear them for the next call
+    for (uint32_t k = tb0 * kFTileBins + threadIdx.x; k < min(tb1 * kFTileBins, U); k += blockDim.x) a.ovfH[k] = 0;
+  phase_mark(a.pt, 6);
+
+  // ---- tile offsets (write offsets of the tiles) and the size / overflow status ----------
+  tile_offsets(tv, ntiles, toff, red64);
+  const uint64_t total = toff[ntiles];
+  if (b == 0 && threadIdx.x == 0) {
+    unsigned flags = 0;
+    if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
+    if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
+    if (flags) atomicOr(&a.st->flags, flags);
+    a.st->last_total = total;
+    if (a.d_total) *a.d_total = total;
+    *a.ws_total = total;
+  }
+
+  // ---- projection of an equal share of the positions -------------------------------------
+  // CTA b projects [b nw / G, (b+1) nw / G) (32-aligned), i.e. the same number of outputs
+  // whatever the skew; it waits for the tiles its share overlaps, stages their P = toff[t] +
+  // PL in shared memory, and its 32 warps project.
+  const uint32_t nw = (uint32_t)(total < a.n_expected ? total : a.n_expected);  // positions written
+  const uint32_t lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
+  const uint32_t hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
+  __shared__ uint32_t s_t[2];
+  if (threadIdx.x == 0 && lo < hi) {
+    s_t[0] = tile_of(toff, ntiles, lo);
+    s_t[1] = tile_of(toff, ntiles, hi - 1);
+  }
+  __syncthreads();
   const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
   const uint64_t pol = l2_evict_first_policy();
-#if DIALSORT_EXPAND_MARKS
-  uint32_t* M = sh_hist + g * kFusedChunk;
-  for (uint32_t p0 = lo; p0 < hi; p0 += kFusedChunk) {
-    const uint32_t p1 = hi - p0 > kFusedChunk ? p0 + kFusedChunk : hi;
-    expand_chunk(a, toff, ntiles, p0, p1, ta, key_base, out, M, sred[g], g, aligned, pol);
-  }
-#else
+  uint32_t* Ps = sh + kFOffPs;
   if (lo < hi) {
-    // stage P of the share's scan tiles (one L2 round trip), then warps run independently
-    const uint32_t tb = tile_of(toff, ntiles, hi - 1);
-    const uint32_t ka = ta * kTileBins, kb = min((tb + 1) * kTileBins, a.U);
-    uint32_t* Ps = sh_hist + g * kFusedPCap;
-    uint32_t* wc = sh_hist + kFusedNSub * kFusedPCap + (threadIdx.x >> 5) * 128;
-    expand_share(a, ka, kb, lo, hi, Ps, wc, g, key_base, out, aligned, pol);
+    const uint32_t ta = s_t[0], tb = s_t[1];
+    // relaxed polling (a short sleep leaves issue slots to the rest of the CTA), then one
+    // acquire load per flag — not a fence: fence.acq_rel.gpu waits for every store in flight
+    for (uint32_t t = ta + threadIdx.x; t <= tb; t += blockDim.x) {
+      while (ld_relaxed_u32(a.ready + t) != a.epoch) __nanosleep(64);
+      (void)ld_acquire_u32(a.ready + t);
+    }
+    __syncthreads();
+    phase_mark(a.pt, 8);
+    for (uint32_t pt0 = ta; pt0 <= tb; pt0 += kFPassTiles) {  // one pass at the configs
+      const uint32_t pt1 = min(pt0 + kFPassTiles, tb + 1);
+      const uint32_t m = (pt1 - pt0) * kFTileBins;
+      for (uint32_t i = threadIdx.x; i < m + 32; i += blockDim.x) {
+        const uint32_t t = pt0 + i / kFTileBins, bin = pt0 * kFTileBins + i;
+        Ps[i] = i >= m ? 0xffffffffu : (bin < U ? toff[t] + __ldcg(a.P + bin) : toff[ntiles]);
+      }
+      __syncthreads();
+      phase_mark(a.pt, 9);
+      const uint32_t p0 = max(lo, toff[pt0]), p1 = min(hi, toff[pt1]);
+      if (p0 < p1) project_warp(Ps, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
+      __syncthreads();  // Ps is reused by the next pass
+    }
   }
-#endif
   phase_mark(a.pt, 7);
   pdl_trigger();
 }

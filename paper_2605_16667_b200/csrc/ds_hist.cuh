@@ -20,6 +20,7 @@ namespace ds {
 
 constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
+constexpr uint32_t kFTileBins = 128;        // scan-tile width of k_sort_fused (ds_fused.cuh)
 constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
 constexpr uint32_t kChunkBytes = 32768;     // TMA path: 8192 keys per chunk
 constexpr uint32_t kChunkVecs = kChunkBytes / 16;
@@ -295,11 +296,20 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
   // equal keys is one lane pair (k, 4).  When every active lane holds such a run (sorted /
   // reverse input), the warp groups its lanes by equality — one or two distinct keys are
   // found with a min/max reduction (REDUX) and ballots — and each group adds its total with
-  // a single atomic.  Random inputs never take this path and pay one ballot per vector.
+  // a single atomic.  Random inputs never take this path: one vote on (first == last key)
+  // per vector rules it out for the whole warp.
   auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
-      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
       const uint32_t act = __activemask();
+      if (!__any_sync(act, v.x == v.w)) {  // no lane can hold a run of 4: the common case
+        if (PACK16) {
+          add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
+        } else {
+          add32((uint32_t)v.x); add32((uint32_t)v.y); add32((uint32_t)v.z); add32((uint32_t)v.w);
+        }
+        return;
+      }
+      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
       const uint32_t runs = __ballot_sync(act, run4);
       if (runs == act) {
         const uint32_t k = (uint32_t)v.x, lane = threadIdx.x & 31;
@@ -365,7 +375,91 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
   constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
   const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   unsigned long long fsum = 0;
-  for (uint32_t t = threadIdx.x >> 5; t < ntiles; t += nwarps) {
+  if (a.tile_red && PACK16 && a.nib4) {
+    // k_sort_fused, 4-bit rows: the partial row keeps counts <= 15 — 8 bins
+    // per word, a quarter of the packed row's L2 bytes — and a count >= 16 goes whole to the
+    // global exception histogram Hx (RED; its nibble stays 0).  Thread i turns packed uint4 i
+    // (8 bins; consecutive threads read consecutive uint4: no bank conflicts — 4 uint4 per
+    // thread measured 16-way conflicted) into word i of the row; the 16 threads of a 128-bin
+    // tile reduce its sum with shuffles and one adds it (RED) into the tile total.
+    const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * 16;
+    uint32_t* nrow = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr;
+    const uint32_t nw = (U + 7) / 8;  // row words
+#if DIALSORT_EXP_NOFLUSH
+    for (uint32_t b0 = 0; b0 < 0; b0 += blockDim.x) {
+#else
+    for (uint32_t b0 = 0; b0 < tot; b0 += blockDim.x) {
+#endif
+      const uint32_t g = b0 + threadIdx.x;
+      uint32_t v = 0;
+      if (g < W4) {
+        const uint4 w = h4[g];
+        uint32_t word;
+        if (((w.x | w.y | w.z | w.w) & 0xFFF0FFF0u) == 0u) {
+          // fast path, all 8 counts <= 15: word j holds (c_{2j+1} << 16 | c_{2j}), so
+          // (w | w >> 12) & 0xff = c_{2j} | c_{2j+1} << 4, and PRMT gathers the 4 bytes
+          const uint32_t bx = w.x | (w.x >> 12), by = w.y | (w.y >> 12);
+          const uint32_t bz = w.z | (w.z >> 12), bw = w.w | (w.w >> 12);
+          word = __byte_perm(__byte_perm(bx, by, 0x0040), __byte_perm(bz, bw, 0x0040), 0x5410);
+          const uint32_t sw = w.x + w.y + w.z + w.w;  // halves <= 60: no carry
+          v = (sw & 0xffffu) + (sw >> 16);
+        } else {
+          const uint32_t cw[4] = {w.x, w.y, w.z, w.w};
+          word = 0;
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t c = (cw[j >> 1] >> ((j & 1u) << 4)) & 0xffffu;
+            v += c;
+            if (c < 16u) {
+              word |= c << (4 * j);
+            } else {
+              red_add_u32(a.Hx + 8 * g + j, c);
+            }
+          }
+        }
+#if !DIALSORT_EXP_NOST
+        if (g < nw) __stcg(nrow + g, word);
+#endif
+      }
+#pragma unroll
+      for (uint32_t o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (g < tot && (g & 15u) == 0) {
+        fsum += v;
+#if !DIALSORT_EXP_NORED
+        if (v) red_add_u32(a.tile_red + (uint64_t)(g / 16) * a.tile_red_stride, v);
+#endif
+      }
+      if (b0 == 0) phase_mark(a.pt, 12);  // first flush iteration done (debug)
+      if (b0 == blockDim.x) phase_mark(a.pt, 13);
+    }
+  } else if (a.tile_red) {
+    // k_sort_fused: kFTileBins-bin tiles (16 or 32 uint4), thread i stores uint4 i and the QT
+    // lanes of a tile reduce its sum with shuffles; lane 0 of the tile adds it (RED) into the
+    // tile total.  Every thread runs the same iterations (shuffles use the full mask).
+    constexpr uint32_t QT = PACK16 ? kFTileBins / 8 : kFTileBins / 4;
+    const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot4 = ntf * QT;
+    uint4* frow4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
+    for (uint32_t b0 = 0; b0 < tot4; b0 += blockDim.x) {
+      const uint32_t i = b0 + threadIdx.x;
+      uint32_t v = 0;
+      if (i < W4) {
+        const uint4 w = h4[i];
+        __stcg(frow4 + i, w);
+        if (PACK16)
+          v = (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
+              (w.w & 0xffffu) + (w.w >> 16);
+        else
+          v = w.x + w.y + w.z + w.w;
+      }
+#pragma unroll
+      for (uint32_t o = QT / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (i < tot4 && (i % QT) == 0) {
+        fsum += v;
+        if (v) red_add_u32(a.tile_red + (uint64_t)(i / QT) * a.tile_red_stride, v);
+      }
+    }
+  }
+  for (uint32_t t = threadIdx.x >> 5; !a.tile_red && t < ntiles; t += nwarps) {
     uint32_t v = 0;
 #pragma unroll
     for (uint32_t j = 0; j < q_per_tile; j += 32) {
@@ -382,22 +476,39 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     }
     v = warp_sum(v);
     fsum += v;
-    if (lane == 0) {
-      if (a.tile_red) {
-        if (v) red_add_u32(a.tile_red + (uint64_t)t * a.tile_red_stride, v);
-      } else {
-        __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
-      }
-    }
+    if (lane == 0) __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
   }
+  phase_mark(a.pt, 11);  // flush loop done (debug)
   // (uint4 beyond the last tile are padding zeros and are never read by the merge)
   if (PACK16) {
     // Packed counters: a 16-bit field that wrapped loses >= 65535 from the field sum
     // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.  On overflow the
     // fallback zeroes the row and the CTA's tile sums are ignored (use_ovf path below).
-    const uint64_t tot = block_sum<uint64_t>(lane == 0 ? fsum : 0ull, red64);  // warp totals, once per warp
+    // fsum: per-warp totals in lane 0 (tsums loop) or per-tile totals in the tile's lane 0
+    const uint64_t tot = block_sum<uint64_t>(a.tile_red || lane == 0 ? fsum : 0ull, red64);
     const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
-    if (tot != nvalid) hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
+    if (tot != nvalid) {
+      if (a.tile_red) {
+        // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
+        // values), then the fallback zeroes the row (ldr words) and re-ingests into ovfH
+        if (a.nib4) {
+          __syncthreads();
+          for (uint32_t g = threadIdx.x; g < W4; g += blockDim.x) {
+            const uint4 w = h4[g];
+            const uint32_t cw[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+              const uint32_t c = (cw[j >> 1] >> ((j & 1u) << 4)) & 0xffffu;
+              if (c >= 16u) red_add_u32(a.Hx + 8 * g + j, 0u - c);
+            }
+          }
+        }
+        uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
+        hist_overflow_fallback<TMA>(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
+      } else {
+        hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
+      }
+    }
   }
   phase_mark(a.pt, 2);
 }

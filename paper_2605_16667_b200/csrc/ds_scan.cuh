@@ -74,6 +74,10 @@ struct ScanArgs {
   uint32_t* tile_red;        // [ntiles x tile_red_stride] tile totals reduced during the flush (zero on entry)
   uint32_t* tile_clear;      // the other parity's tile_red, zeroed for the next launch
   uint32_t tile_red_stride;  // words between consecutive tile totals
+  uint32_t ldr;              // words between partial rows (row format may differ from the smem histogram)
+  int nib4;                  // partial rows hold 4-bit counts (8 bins per word); counts >= 16 in Hx
+  uint32_t* Hx;              // [U] exception histogram of the 4-bit rows (zero on entry)
+  uint32_t* Hx_clear;        // the other parity's Hx, zeroed for the next launch
   uint32_t* tile_alt;        // [ntiles] tile totals of the overflow fallback path
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
   unsigned long long* bar64; // monotonic grid-barrier counter

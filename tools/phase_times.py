@@ -19,14 +19,16 @@ keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
 outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = os.environ.get("DIALSORT_FUSED") != "0"
-names = (["ingest", "sync", "flush", "barrier1", "merge_scan", "share_ready", "rows_staged", "end"] if fused else
-         ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"])
+names = (["ingest", "sync", "flush", "barrier1", "merge_start", "batch_staged", "merged", "end", "flags_ready",
+          "P_staged", "", "flush_loop", "flush_it1", "", "", ""] if fused else
+         ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"] + [""] * 8)
 for rep in range(4):
     ctx.debug_phase_cta()
-    if cfg["dist"] == "int32":
-        ctx.sort_int32(keys[rep % 5], out=outs[rep % 5])
-    else:
-        ctx.sort(keys[rep % 5], cfg["U"], out=outs[rep % 5])
+    for _ in range(int(os.environ.get("PHASE_BACK_TO_BACK", "1"))):  # stamps: the last launch
+        if cfg["dist"] == "int32":
+            ctx.sort_int32(keys[rep % 5], out=outs[rep % 5])
+        else:
+            ctx.sort(keys[rep % 5], cfg["U"], out=outs[rep % 5])
     torch.cuda.synchronize()
     st = ctx.debug_phase_cta().astype(np.float64) / 1e3
     if rep == 0 or len(st) == 0:
@@ -34,7 +36,7 @@ for rep in range(4):
     print(f"{cfgname} rep {rep}: {len(st)} CTAs, phase time after the first CTA start (us) min/median/max:")
     cols = [("start", st[:, 0])] + [(n, st[:, 1 + i]) for i, n in enumerate(names)]
     print("   " + "  ".join(f"{n}={c[c > 0].min():.2f}/{np.median(c[c > 0]):.2f}/{c.max():.2f}"
-                            for n, c in cols if (c > 0).any()))
+                            for n, c in cols if n and (c > 0).any()))
     if verbose and fused:
         late = np.argsort(-st[:, 6])[:6]
         for b in late:

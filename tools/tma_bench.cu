@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
@@ -197,6 +198,44 @@ __global__ void __launch_bounds__(1024, 1) k_flush_merge(uint4* rows, uint32_t* 
   mark1();
 }
 
+// flush rows of RB bytes + barrier + each CTA stages SEG bytes of all G rows (at offset
+// blockIdx * SEG) into smem with cp.async; in-kernel times of the staging part
+__device__ uint32_t g_tiles[1024 * 64];
+__device__ unsigned long long g_f0 = ~0ull, g_f1 = 0;
+template <uint32_t RB, uint32_t SEG, uint32_t NRED = 0>
+__global__ void __launch_bounds__(1024, 1) k_flush_stage(uint4* rows, unsigned long long* bar, unsigned long long target) {
+  mark0();
+  for (uint32_t i = threadIdx.x; i < RB / 16; i += 1024) sm[i] = make_uint4(i, 1, 2, 3);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMin(&g_f0, gt());
+  uint4* r = rows + (uint64_t)blockIdx.x * (RB / 16);
+  for (uint32_t i = threadIdx.x; i < RB / 16; i += 1024) __stcg(r + i, sm[i]);
+  for (uint32_t t = threadIdx.x; t < NRED; t += 1024)
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(g_tiles + 64 * t), "r"(1u) : "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&g_f1, gt());
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned long long v;
+    do { asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory"); } while (v < target);
+    atomicMin(&g_m0, gt());
+  }
+  __syncthreads();
+  const uint32_t G = gridDim.x;
+  constexpr uint32_t Q = SEG / 16;  // uint4 per row segment
+  const uint32_t off = (blockIdx.x * SEG) % RB;
+  for (uint32_t i = threadIdx.x; i < G * Q; i += 1024) {
+    const uint32_t row = i / Q, q = i % Q;
+    const char* src = reinterpret_cast<const char*>(rows) + (uint64_t)row * RB + off + 16 * q;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(sm + i)), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) { atomicMax(&g_m1, gt()); atomicMin(&g_m1min, gt()); }
+  mark1();
+}
+
 int main() {
   int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   uint4* rows; CK(cudaMalloc(&rows, (size_t)nsm * ROWB));
@@ -252,6 +291,37 @@ int main() {
       printf("flush+barrier+merge one kernel (%s L2): merge from barrier exit: earliest CTA done %.2f us, latest %.2f us\n",
              (rep & 1) ? "dirty" : "clean", (c - a) * 1e-3, (b - a) * 1e-3);
     }
+  }
+  {
+    unsigned long long* bar; CK(cudaMalloc(&bar, 64)); CK(cudaMemset(bar, 0, 64));
+    unsigned long long tgt = 0;
+    auto fs = [&](const char* nm, auto kern) {
+      CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+      double bmin = 1e9, bmax = 1e9;
+      for (int rep = 0; rep < 6; ++rep) {
+        unsigned long long z0 = ~0ull, z1 = 0;
+        CK(cudaMemcpyToSymbol(g_m0, &z0, 8)); CK(cudaMemcpyToSymbol(g_m1, &z1, 8)); CK(cudaMemcpyToSymbol(g_m1min, &z0, 8));
+        tgt += G;
+        kern<<<G, 1024, SM>>>(rows, bar, tgt);
+        CK(cudaDeviceSynchronize());
+        unsigned long long a, b, c; CK(cudaMemcpyFromSymbol(&a, g_m0, 8)); CK(cudaMemcpyFromSymbol(&b, g_m1, 8)); CK(cudaMemcpyFromSymbol(&c, g_m1min, 8));
+        if (rep >= 2) { bmin = std::min(bmin, (c - a) * 1e-3); bmax = std::min(bmax, (b - a) * 1e-3); }
+      }
+      unsigned long long f0, f1, ma; CK(cudaMemcpyFromSymbol(&f0, g_f0, 8)); CK(cudaMemcpyFromSymbol(&f1, g_f1, 8));
+      CK(cudaMemcpyFromSymbol(&ma, g_m0, 8));
+      unsigned long long zz = ~0ull, z0 = 0; CK(cudaMemcpyToSymbol(g_f0, &zz, 8)); CK(cudaMemcpyToSymbol(g_f1, &z0, 8));
+      printf("%-48s staging after barrier: earliest %.2f us, latest %.2f us  (flush span %.2f us)\n", nm, bmin, bmax,
+             f1 > f0 ? (f1 - f0) * 1e-3 : 0.0);
+    };
+    fs("flush 32KB rows, stage 148 x 320 B", k_flush_stage<32768, 320>);
+    fs("flush 32KB rows + 512 REDs, stage 148 x 320 B", k_flush_stage<32768, 320, 512>);
+    fs("flush 32KB rows + 128 REDs, stage 148 x 320 B", k_flush_stage<32768, 320, 128>);
+    {
+      unsigned long long a, b; CK(cudaMemcpyFromSymbol(&a, g_f0, 8)); CK(cudaMemcpyFromSymbol(&b, g_f1, 8));
+    }
+    fs("flush 32KB rows, stage 148 x 1024 B", k_flush_stage<32768, 1024>);
+    fs("flush 128KB rows, stage 148 x 1024 B", k_flush_stage<131072, 1024>);
+    fs("flush 128KB rows, stage 148 x 320 B", k_flush_stage<131072, 320>);
   }
   run("bulk reduce.add 148 x 256KB, 4KB pieces", [&] { k_bulk_red<4096, false><<<G, 1024, SM>>>(acc); }, false);
   run("bulk reduce.add rotated, 4KB pieces", [&] { k_bulk_red<4096, true><<<G, 1024, SM>>>(acc); }, false);
