@@ -22,6 +22,7 @@
 #include "ds_expand.cuh"
 #include "ds_fused.cuh"
 #include "ds_hist.cuh"
+#include "ds_part.cuh"
 #include "ds_radix.cuh"
 #include "ds_scan.cuh"
 
@@ -45,11 +46,13 @@ int fail(int code, const std::string& msg) {
 
 enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND,
-  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_COUNT
+  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN,
+  KID_PART_SCATTER, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
                                              "k_scan", "k_expand", "k_radix_hist0", "k_radix_pass",
-                                             "k_range_count", "k_crn_resolve", "k_sort_fused"};
+                                             "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count",
+                                             "k_part_scan", "k_part_scatter"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -134,7 +137,7 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      radix_lb, fused_tiles, Hx;
+      radix_lb, fused_tiles, Hx, part, htmp;
   DevStatus* host_status = nullptr;  // pinned mirror
   uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
   unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
@@ -341,11 +344,16 @@ bool sort_fused_enabled() {
   return v;
 }
 
+// d_n / d_off (nullable): the key count and the keys/out offset are on the device (a universe
+// block of the hierarchical path); n is then only the size hint for the grid and row format.
 int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
-                       uint32_t epoch, cudaStream_t s) {
+                       uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
+                       const uint64_t* d_off = nullptr) {
   int rc;
   ScanArgs a = {};
   if ((rc = fill_scan_args(c, a, U, true, n, true, nullptr, epoch))) return rc;
+  a.d_n = d_n;
+  a.d_off = d_off;
   const bool pack = choose_path(U) == HistPath::Smem16;
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
@@ -384,13 +392,54 @@ int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t
   a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
   a.bar_base = c->bar64_base;
   if (fmt == kRowN4)
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowN4>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowN4>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
   else if (fmt == kRowP16)
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowP16>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowP16>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
   else
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowU32>, dim3(C), dim3(1024), smem, s, keys, n, a, out, (int32_t)0));
+    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowU32>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
   c->fused_seq++;
   c->bar64_base += 2ull * C;  // two barriers reserved per launch (one skipped unless overflow)
+  return DIALSORT_OK;
+}
+
+// Hierarchical DialSort for 98304 < U <= 2^22 (ds_part.cuh): MSD split into 65536-bin universe
+// blocks, then one k_sort_fused per block (device-resident block sizes / offsets: no host
+// round trip).  DIALSORT_HIER=0 selects the L2 path (one RED per distinct key per warp).
+bool hier_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("DIALSORT_HIER");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+bool hier_applies(uint32_t U) {
+  return U > kSmem16MaxBins && (uint64_t)U <= ((uint64_t)kPartMaxBlocks << kPartShift) && hier_enabled() &&
+         sort_fused_enabled();
+}
+
+int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
+                      cudaStream_t s) {
+  int rc;
+  const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
+  const uint32_t Gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * c->nsm, cdiv(n, kPartTile)));
+  if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
+  if ((rc = c->htmp.ensure(4ull * n + 16))) return rc;
+  PartWs w;
+  w.bsz = c->part.as<uint64_t>();
+  w.boff = w.bsz + B;
+  w.cnt = reinterpret_cast<uint32_t*>(w.boff + B);
+  w.st = c->status.as<DevStatus>();
+  int32_t* tmp = c->htmp.as<int32_t>();
+  DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
+  DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
+  DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
+  for (uint32_t b = 0; b < B; ++b) {
+    const uint32_t Ub = (uint32_t)std::min<uint64_t>(1ull << kPartShift, (uint64_t)U - ((uint64_t)b << kPartShift));
+    const uint32_t epoch = next_epoch(c, s);  // each block launch has its own ready-flag epoch
+    if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, H + ((uint64_t)b << kPartShift), out, epoch, s,
+                                 (int32_t)(b << kPartShift), w.bsz + b, w.boff + b)))
+      return rc;
+  }
   return DIALSORT_OK;
 }
 
@@ -529,7 +578,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   cudaDeviceSynchronize();
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
                   &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb,
-                  &c->fused_tiles, &c->Hx})
+                  &c->fused_tiles, &c->Hx, &c->part, &c->htmp})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt) cudaFree(c->pt);
@@ -625,6 +674,7 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
   }
   if (choose_path(U) != HistPath::Global && sort_fused_enabled() && !hist_use_tma())
     return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);
+  if (hier_applies(U)) return enqueue_sort_hier(c, keys, n, U, H, out, s);
   if ((rc = enqueue_hist_scan(c, keys, n, U, H, true, n, epoch, s))) return rc;
   return enqueue_expand(c, U, n, 0, out, s);
 }

@@ -348,11 +348,20 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
 template <int FMT>
 __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
+  // (keys, out, n are adjusted below for hierarchical blocks)
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
   __shared__ uint32_t wsum[32];
   pdl_wait();
   phase_mark(a.pt, -1);
+  uint64_t n_exp = a.n_expected;
+  if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
+    const uint64_t off = *a.d_off;
+    n = *a.d_n;
+    keys += off;
+    out += off;
+    n_exp = n;
+  }
   const uint32_t U = a.U, ntiles = (U + kFTileBins - 1) / kFTileBins;
   const uint32_t G = gridDim.x, b = blockIdx.x;
   // the other parity's tile totals are zeroed for the next launch (host alternates them;
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   if (b == 0 && threadIdx.x == 0) {
     unsigned flags = 0;
     if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
-    if (a.exact ? (total != a.n_expected) : (total > a.n_expected)) flags |= FLAG_SIZE;
+    if (a.exact ? (total != n_exp) : (total > n_exp)) flags |= FLAG_SIZE;
     if (flags) atomicOr(&a.st->flags, flags);
     a.st->last_total = total;
     if (a.d_total) *a.d_total = total;
@@ -462,7 +471,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // CTA b projects [b nw / G, (b+1) nw / G) (32-aligned), i.e. the same number of outputs
   // whatever the skew; it waits for the tiles its share overlaps, stages their P = toff[t] +
   // PL in shared memory, and its 32 warps project.
-  const uint32_t nw = (uint32_t)(total < a.n_expected ? total : a.n_expected);  // positions written
+  const uint32_t nw = (uint32_t)(total < n_exp ? total : n_exp);  // positions written
   const uint32_t lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
   const uint32_t hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
   __shared__ uint32_t s_t[2];

@@ -1,0 +1,198 @@
+// ds_part.cuh — hierarchical DialSort for universes larger than one SM's shared-memory
+// histogram (the paper's "hierarchical partitioning is required" for large U, P:2780-2782,
+// future work P:2847).
+//
+// U > kSmem16MaxBins: the keys are first partitioned by their high bits into B = ceil(U/2^16)
+// universe blocks of 65536 bins (an MSD split on key >> 16 — order inside a block is
+// irrelevant: the histogram is order-free, eq:ingestion P:409-412), each block's keys stored
+// as their low 16 bits; then each block is sorted by k_sort_fused with U_b <= 65536 and
+// key_base = b << 16, writing its output at the block's offset and its H slice at b << 16.
+// This replaces one L2 RED per key (the global path, bound by the L2 atomic rate) with
+// 12 bytes per key of streaming traffic (count read, scatter read + write) plus the
+// shared-memory path of each block.
+//
+//   k_part_count    per-CTA chunk: block counts (per-warp shared counters)      [G][B]
+//   k_part_scan     exclusive offsets off[c][b] (block-major), block sizes and starts
+//   k_part_scatter  per-CTA chunk again, 4096-key sub-tiles staged in shared memory by
+//                   block and written as contiguous runs at the CTA's offsets
+#pragma once
+#include "ds_common.cuh"
+
+namespace ds {
+
+constexpr uint32_t kPartShift = 16;         // 65536-bin universe blocks
+constexpr uint32_t kPartMaxBlocks = 64;     // U <= 2^22 take this path (larger: the L2 path)
+constexpr uint32_t kPartThreads = 512;
+constexpr uint32_t kPartKPT = 8;            // keys per thread per scatter sub-tile
+constexpr uint32_t kPartTile = kPartThreads * kPartKPT;  // 4096
+
+struct PartWs {
+  uint32_t* cnt;   // [G][B] block counts of each CTA chunk, then offsets (in place)
+  uint64_t* bsz;   // [B] block sizes
+  uint64_t* boff;  // [B] block starts
+  DevStatus* st;
+};
+
+// Chunk [lo, hi) of CTA c in a grid of G over n keys.
+__device__ __forceinline__ void part_chunk(uint64_t n, uint64_t& lo, uint64_t& hi) {
+  lo = n * blockIdx.x / gridDim.x;
+  hi = n * (blockIdx.x + 1) / gridDim.x;
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
+                                                             uint32_t B, PartWs w) {
+  __shared__ uint32_t wcnt[kPartThreads / 32][kPartMaxBlocks];
+  pdl_wait();
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < (kPartThreads / 32) * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  uint64_t lo, hi;
+  part_chunk(n, lo, hi);
+  uint32_t* wc = wcnt[warp];
+  auto one = [&](uint32_t k, uint64_t idx) {
+    if (k < U) atomicAdd(&wc[k >> kPartShift], 1u);
+    else record_bad(w.st, idx, k);
+  };
+  // 16-byte aligned interior as int4, scalar head / tail
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(keys + lo) >> 2) & 3u;
+  const uint64_t a4 = min(hi, lo + ((4u - mis) & 3u));
+  const uint64_t b4 = a4 + ((hi - a4) & ~3ull);
+  for (uint64_t i = lo + threadIdx.x; i < a4; i += blockDim.x) one((uint32_t)keys[i], i);
+  for (uint64_t i = b4 + threadIdx.x; i < hi; i += blockDim.x) one((uint32_t)keys[i], i);
+  const int4* body = reinterpret_cast<const int4*>(keys + a4);
+  const uint64_t nv = (b4 - a4) / 4;
+  const uint64_t pol = l2_evict_first_policy();
+  uint64_t v = threadIdx.x;
+  for (; v + 3 * blockDim.x < nv; v += 4 * blockDim.x) {
+    int4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = ld_stream4(body + v + u * blockDim.x, pol);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i0 = a4 + 4 * (v + u * blockDim.x);
+      if (umax4(x[u]) < U) {
+        atomicAdd(&wc[(uint32_t)x[u].x >> kPartShift], 1u);
+        atomicAdd(&wc[(uint32_t)x[u].y >> kPartShift], 1u);
+        atomicAdd(&wc[(uint32_t)x[u].z >> kPartShift], 1u);
+        atomicAdd(&wc[(uint32_t)x[u].w >> kPartShift], 1u);
+      } else {
+        one((uint32_t)x[u].x, i0); one((uint32_t)x[u].y, i0 + 1); one((uint32_t)x[u].z, i0 + 2); one((uint32_t)x[u].w, i0 + 3);
+      }
+    }
+  }
+  for (; v < nv; v += blockDim.x) {
+    const int4 x = ld_stream4(body + v, pol);
+    const uint64_t i0 = a4 + 4 * v;
+    one((uint32_t)x.x, i0); one((uint32_t)x.y, i0 + 1); one((uint32_t)x.z, i0 + 2); one((uint32_t)x.w, i0 + 3);
+  }
+  __syncthreads();
+  if (threadIdx.x < B) {
+    uint32_t s = 0;
+#pragma unroll 4
+    for (uint32_t q = 0; q < kPartThreads / 32; ++q) s += wcnt[q][threadIdx.x];
+    w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x] = s;
+  }
+  pdl_trigger();
+}
+
+// One CTA: off[c][b] = start(b) + Σ_{c' < c} cnt[c'][b], start(b) = Σ_{b' < b} size(b').
+__global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, PartWs w) {
+  __shared__ uint64_t sz[kPartMaxBlocks];
+  pdl_wait();
+  // thread b sums its column (B <= 64 columns, G <= a few hundred rows)
+  if (threadIdx.x < B) {
+    uint64_t s = 0;
+    for (uint32_t c = 0; c < G; ++c) s += w.cnt[(uint64_t)c * B + threadIdx.x];
+    sz[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < B) {
+    uint64_t start = 0;
+    for (uint32_t b = 0; b < threadIdx.x; ++b) start += sz[b];
+    w.bsz[threadIdx.x] = sz[threadIdx.x];
+    w.boff[threadIdx.x] = start;
+    uint64_t run = start;
+    for (uint32_t c = 0; c < G; ++c) {
+      const uint64_t x = w.cnt[(uint64_t)c * B + threadIdx.x];
+      w.cnt[(uint64_t)c * B + threadIdx.x] = (uint32_t)run;  // positions < n < 2^32
+      run += x;
+    }
+  }
+  pdl_trigger();
+}
+
+// Re-reads the CTA's chunk and writes every valid key's low 16 bits into its universe block,
+// sub-tile by sub-tile (4096 keys, 8 per thread as two 16-byte loads; the next sub-tile's
+// loads are in flight while the current one is placed): per-warp block counters, a scan over
+// (block, warp) gives every warp its slot range in the staged sub-tile, a per-warp cursor
+// atomic gives each key its slot (order inside a block is free), and the staged sub-tile
+// leaves as contiguous runs (~256 keys per block) at the CTA's running block offsets.
+// The chunk interior must be 16-byte aligned for the vector loads; other chunks take the
+// scalar path (keys of an unaligned base).
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
+                                                               uint32_t B, PartWs w, int32_t* __restrict__ tmp) {
+  constexpr uint32_t NW = kPartThreads / 32;
+  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];  // counts, then cursors
+  __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks];
+  __shared__ uint32_t stage[kPartTile];
+  pdl_wait();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t lo, hi;
+  part_chunk(n, lo, hi);
+  if (threadIdx.x < B) gpos[threadIdx.x] = w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x];
+  const bool vec = ((reinterpret_cast<uintptr_t>(keys + lo)) & 15u) == 0;
+  // thread t holds sub-tile keys 8t .. 8t+7 (blocked: two int4)
+  auto load = [&](uint64_t t0, uint32_t (&k)[kPartKPT]) {
+    const uint64_t i0 = t0 + (uint64_t)kPartKPT * threadIdx.x;
+    if (vec && i0 + kPartKPT <= hi) {
+      const int4 x0 = __ldcs(reinterpret_cast<const int4*>(keys + i0));
+      const int4 x1 = __ldcs(reinterpret_cast<const int4*>(keys + i0) + 1);
+      k[0] = x0.x; k[1] = x0.y; k[2] = x0.z; k[3] = x0.w; k[4] = x1.x; k[5] = x1.y; k[6] = x1.z; k[7] = x1.w;
+    } else {
+#pragma unroll
+      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : 0xffffffffu;
+    }
+  };
+  uint32_t k[kPartKPT], kn[kPartKPT];
+  if (lo < hi) load(lo, k);
+  for (uint64_t t0 = lo; t0 < hi; t0 += kPartTile) {
+    if (t0 + kPartTile < hi) load(t0 + kPartTile, kn);  // next sub-tile in flight
+    for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t i = 0; i < kPartKPT; ++i)
+      if (k[i] < U) atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u);
+    __syncthreads();
+    // scan over (block, warp): thread q < B*NW handles block q / NW, warp q % NW
+    {
+      const uint32_t q = threadIdx.x, bq = q / NW, wq = q % NW;
+      const uint32_t v = q < B * NW ? wcnt[wq][bq] : 0u;
+      __shared__ uint32_t red[34];
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t>(v, tot, red);
+      if (q < B * NW) {
+        wcnt[wq][bq] = ex;  // cursor of warp wq in block bq
+        if (wq == 0) bofs[bq] = ex;
+      }
+      if (q == 0) bofs[B] = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t i = 0; i < kPartKPT; ++i)
+      if (k[i] < U) stage[atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u)] = k[i];
+    __syncthreads();
+    const uint32_t nvld = bofs[B];  // valid keys of the sub-tile (bad keys were dropped)
+    for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
+      const uint32_t key = stage[j], bb = key >> kPartShift;
+      __stcs(tmp + gpos[bb] + (j - bofs[bb]), (int32_t)(key & 0xffffu));
+    }
+    __syncthreads();
+    if (threadIdx.x < B) gpos[threadIdx.x] += bofs[threadIdx.x + 1] - bofs[threadIdx.x];
+#pragma unroll
+    for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = kn[i];
+  }
+  (void)lane;
+  pdl_trigger();
+}
+
+}  // namespace ds

@@ -78,6 +78,8 @@ struct ScanArgs {
   int nib4;                  // partial rows hold 4-bit counts (8 bins per word); counts >= 16 in Hx
   uint32_t* Hx;              // [U] exception histogram of the 4-bit rows (zero on entry)
   uint32_t* Hx_clear;        // the other parity's Hx, zeroed for the next launch
+  const uint64_t* d_n;       // nullable: key count on the device (hierarchical blocks); then
+  const uint64_t* d_off;     //   keys and out start at *d_off and n_expected = *d_n
   uint32_t* tile_alt;        // [ntiles] tile totals of the overflow fallback path
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
   unsigned long long* bar64; // monotonic grid-barrier counter
