@@ -142,7 +142,7 @@ struct dialsort_ctx_s {
   uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
   unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
   Profiler prof;
-  int expand_occ = 4, scan_occ = 2, radix_occ = 1, radix2_occ = 1;
+  int expand_occ = 4, scan_occ = 2, radix_occ = 1, radix2_occ = 1, radix3_occ = 1, radix4_occ = 1;
   PhaseTimes* pt = nullptr;  // debug phase timing (DIALSORT_PHASE_TIMING=1)
 };
 
@@ -178,6 +178,10 @@ int ctx_init(dialsort_ctx c) {
   c->radix_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass2, kRadixThreads, sizeof(RadixSmem)));
   c->radix2_occ = occ > 0 ? occ : 1;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass3, kRadixThreads, sizeof(Radix3Smem)));
+  c->radix3_occ = occ > 0 ? occ : 1;
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass4, kRadixThreads, sizeof(Radix4Smem)));
+  c->radix4_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kExpandThreads, 0));
   c->expand_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan, kTileBins, 0));
@@ -443,15 +447,17 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   return DIALSORT_OK;
 }
 
-// Host-side enqueue of DialSort-Radix.  Default: 4 reduce-then-scan passes (k_radix_pass2,
-// co-resident grid).  DIALSORT_RADIX=onesweep selects the single-sweep variant (K7 + 4 x K8).
-bool radix_onesweep() {
-  static const bool v = [] {
+// Host-side enqueue of DialSort-Radix.  Default: 4 reduce-then-scan passes with 8192-key
+// sub-tiles, TMA-staged when the buffers are 16-byte aligned (k_radix_pass4, else pass3;
+// co-resident grid).  DIALSORT_RADIX=pass3 / pass2 / onesweep select the other variants (A/B).
+const char* radix_variant() {
+  static const char* v = [] {
     const char* e = getenv("DIALSORT_RADIX");
-    return e && strcmp(e, "onesweep") == 0;
+    return e ? e : "pass4";
   }();
   return v;
 }
+bool radix_onesweep() { return strcmp(radix_variant(), "onesweep") == 0; }
 
 int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, cudaStream_t s) {
   if (n >= (1ull << 30)) return fail(DIALSORT_E_INVALID_ARG, "radix path supports n < 2^30 per call");
@@ -459,7 +465,13 @@ int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out,
   const uint32_t* src = reinterpret_cast<const uint32_t*>(keys);
   uint32_t* bufs[2] = {reinterpret_cast<uint32_t*>(tmp), reinterpret_cast<uint32_t*>(out)};
   if (!radix_onesweep()) {
-    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(n, kRadixTile), (uint64_t)c->nsm * c->radix2_occ));
+    const bool p3 = strcmp(radix_variant(), "pass2") != 0;
+    // pass4 (TMA-staged) needs 16-byte aligned buffers: keys, tmp and out of every pass
+    const bool p4 = p3 && strcmp(radix_variant(), "pass3") != 0 && ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && ((reinterpret_cast<uintptr_t>(tmp) & 15u) == 0);
+    const uint32_t G = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>(cdiv(n, p3 ? kR3Tile : kRadixTile),
+                              (uint64_t)c->nsm * (p4 ? c->radix4_occ : p3 ? c->radix3_occ : c->radix2_occ)));
     if ((rc = c->radix_hist.ensure(8ull * 256 * G + 4 * 256 + 64))) return rc;
     Radix2Ws w;
     w.cnt = c->radix_hist.as<uint32_t>();
@@ -469,8 +481,15 @@ int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out,
     w.pt = c->pt;
     for (int p = 0; p < 4; ++p) {
       uint32_t* dst = bufs[p & 1];
-      DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass2, dim3(G), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
-                       (uint32_t)n, p, w));
+      if (p4)
+        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass4, dim3(G), dim3(kRadixThreads), sizeof(Radix4Smem), s, src, dst,
+                         (uint32_t)n, p, w));
+      else if (p3)
+        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass3, dim3(G), dim3(kRadixThreads), sizeof(Radix3Smem), s, src, dst,
+                         (uint32_t)n, p, w));
+      else
+        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass2, dim3(G), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
+                         (uint32_t)n, p, w));
       src = dst;
     }
     return DIALSORT_OK;

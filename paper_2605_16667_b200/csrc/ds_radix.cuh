@@ -478,9 +478,399 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass2(const uint32_t
   pdl_trigger();
 }
 
+// ---- K8'' reduce-then-scan pass with 8192-key sub-tiles (default) ---------------------------
+// Phases 1-2 as k_radix_pass2 (chunk digit counts, column scans, two grid barriers).  Phase 3
+// scatters the chunk in 8192-key sub-tiles, the next sub-tile's keys in flight (registers)
+// while the current one is placed:
+//   a. per-(warp, digit) counts of the sub-tile (warp w owns sub-tile keys [512w, 512w+512),
+//      16 steps of 32 consecutive keys), one block scan over (digit, warp) gives every warp its
+//      first slot per digit and the sub-tile's digit starts;
+//   b. stable in-warp ranks, step by step: the lanes of a step are grouped by equal digit
+//      through a shared lane-mask word (atomicOr, the CRN's equality merge), the group's
+//      leader advances the warp's digit cursor; the key goes to its slot of the digit-sorted
+//      sub-tile;
+//   c. the sorted sub-tile leaves as digit runs at the CTA's running global offsets.
+// 12n bytes per pass (the chunk is read twice: counts, then scatter).
+constexpr int kR3KPT = 16;
+constexpr int kR3Tile = kRadixThreads * kR3KPT;  // 8192 keys
+struct Radix3Smem {
+  uint32_t wcur[kRadixWarps][256];      // per-warp digit counts -> cursors (16 KB)
+  uint32_t wmask[2][kRadixWarps][256];  // equality-grouping lane masks, 2 buffers (32 KB)
+  uint32_t sorted[kR3Tile];             // sub-tile sorted by digit (32 KB)
+  uint32_t dstart[257];                 // digit starts in the sorted sub-tile
+  uint32_t grun[256];                   // running global position of digit d for this chunk
+  uint32_t hnext[256];
+  uint32_t red[34];
+};
+
+__global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass3(const uint32_t* __restrict__ src,
+                                                                   uint32_t* __restrict__ dst, uint32_t n, int p,
+                                                                   Radix2Ws w) {
+  extern __shared__ __align__(16) unsigned char radix_smem_raw[];
+  Radix3Smem& S = *reinterpret_cast<Radix3Smem*>(radix_smem_raw);
+  pdl_wait();
+  phase_mark(w.pt, -1);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
+  const uint32_t dsel = 0x4440u | (uint32_t)p;
+  const uint32_t flip_in = p == 0 ? kSignFlip : 0u, flip_out = p == 3 ? kSignFlip : 0u;
+  const uint32_t lo = (uint32_t)((uint64_t)n * c / G), hi = (uint32_t)((uint64_t)n * (c + 1) / G);
+  for (int i = threadIdx.x; i < 2 * kRadixWarps * 256; i += blockDim.x) (&S.wmask[0][0][0])[i] = 0;
+  // ---- phase 1: digit counts of the chunk
+  if (threadIdx.x < 256) S.hnext[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    const uint64_t pol = l2_evict_first_policy();
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(src) >> 2) & 3u);
+    const uint32_t a4 = min(hi, lo + ((4u - ((lo + mis) & 3u)) & 3u));
+    const uint32_t b4 = a4 + ((hi - a4) & ~3u);
+    for (uint32_t i = lo + threadIdx.x; i < min(a4, hi); i += blockDim.x)
+      atomicAdd(&S.hnext[__byte_perm(__ldcs(src + i) ^ flip_in, 0, dsel)], 1u);
+    if (a4 < b4) {
+      const int4* body = reinterpret_cast<const int4*>(src + a4);
+      const uint32_t nv = (b4 - a4) / 4;
+      uint32_t v = threadIdx.x;
+      for (; v + 3 * blockDim.x < nv; v += 4 * blockDim.x) {
+        int4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = ld_stream4(body + v + u * blockDim.x, pol);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].x ^ flip_in, 0, dsel)], 1u);
+          atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].y ^ flip_in, 0, dsel)], 1u);
+          atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].z ^ flip_in, 0, dsel)], 1u);
+          atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].w ^ flip_in, 0, dsel)], 1u);
+        }
+      }
+      for (; v < nv; v += blockDim.x) {
+        const int4 x = ld_stream4(body + v, pol);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x.x ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x.y ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x.z ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x.w ^ flip_in, 0, dsel)], 1u);
+      }
+    }
+    for (uint32_t i = b4 + threadIdx.x; i < hi; i += blockDim.x)
+      atomicAdd(&S.hnext[__byte_perm(__ldcs(src + i) ^ flip_in, 0, dsel)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) __stcg(w.cnt + (size_t)c * 256 + threadIdx.x, S.hnext[threadIdx.x]);
+  phase_mark(w.pt, 0);
+  grid_barrier_r(w.bar);
+  phase_mark(w.pt, 1);
+  // ---- phase 2: column scans (CTA d scans digit d over the G chunks)
+  for (uint32_t d = c; d < 256; d += G) {
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < G; c0 += blockDim.x) {
+      const uint32_t cc = c0 + threadIdx.x;
+      const uint32_t v = cc < G ? __ldcg(w.cnt + (size_t)cc * 256 + d) : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t>(v, tot, S.red);
+      if (cc < G) __stcg(w.pre + (size_t)cc * 256 + d, carry + ex);
+      carry += tot;
+    }
+    if (threadIdx.x == 0) __stcg(w.total + d, carry);
+  }
+  phase_mark(w.pt, 2);
+  grid_barrier_r(w.bar);
+  phase_mark(w.pt, 3);
+  // ---- phase 3
+  {
+    uint32_t gtot;
+    const uint32_t gs = block_excl_scan<uint32_t>(threadIdx.x < 256 ? __ldcg(w.total + threadIdx.x) : 0u, gtot, S.red);
+    if (threadIdx.x < 256) S.grun[threadIdx.x] = gs + __ldcg(w.pre + (size_t)c * 256 + threadIdx.x);
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t k[kR3KPT], kn[kR3KPT];
+  auto load = [&](uint32_t t0, uint32_t (&kk)[kR3KPT]) {
+#pragma unroll
+    for (int i = 0; i < kR3KPT; ++i) {
+      const uint32_t idx = t0 + warp * 32 * kR3KPT + i * 32 + lane;
+      kk[i] = idx < hi ? (__ldcs(src + idx) ^ flip_in) : 0u;
+    }
+  };
+  load(lo, k);
+  for (uint32_t t0 = lo; t0 < hi; t0 += kR3Tile) {
+    const uint32_t tn = min((uint32_t)kR3Tile, hi - t0);
+    if (t0 + kR3Tile < hi) load(t0 + kR3Tile, kn);
+    for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&S.wcur[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t wseg = warp * 32 * kR3KPT;  // warp's first key in the sub-tile
+#pragma unroll
+    for (int i = 0; i < kR3KPT; ++i)
+      if (wseg + i * 32 + lane < tn) atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u);
+    __syncthreads();
+    {  // exclusive scan over (digit, warp): thread t has digit t >> 1, warps (t & 1) * 8 .. + 7
+      const uint32_t d = threadIdx.x >> 1, w0 = (threadIdx.x & 1u) * (kRadixWarps / 2);
+      uint32_t v[kRadixWarps / 2], s = 0;
+#pragma unroll
+      for (int j = 0; j < kRadixWarps / 2; ++j) {
+        v[j] = S.wcur[w0 + j][d];
+        s += v[j];
+      }
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(s, tot, S.red);
+      if ((threadIdx.x & 1u) == 0) S.dstart[d] = ex;
+      if (threadIdx.x == 0) S.dstart[256] = tot;
+#pragma unroll
+      for (int j = 0; j < kRadixWarps / 2; ++j) {
+        S.wcur[w0 + j][d] = ex;
+        ex += v[j];
+      }
+    }
+    __syncthreads();
+    if (wseg + 32 * kR3KPT <= tn) {
+#pragma unroll
+      for (int i = 0; i < kR3KPT; ++i) {
+        const uint32_t d = __byte_perm(k[i], 0, dsel);
+        uint32_t* wm = &S.wmask[i & 1][warp][d];
+        atomicOr(wm, 1u << lane);
+        __syncwarp();
+        const uint32_t g = *wm;
+        const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
+        __syncwarp();
+        if (lane == (uint32_t)(__ffs(g) - 1)) {
+          S.wcur[warp][d] = pos + __popc(g);  // the leader has no lower lane in its group
+          *wm = 0u;
+        }
+        S.sorted[pos] = k[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kR3KPT; ++i) {
+        const uint32_t idx0 = wseg + i * 32;
+        const uint32_t vmask = idx0 >= tn ? 0u : (tn - idx0 >= 32 ? FULL : ((1u << (tn - idx0)) - 1u));
+        if ((vmask >> lane) & 1u) {
+          const uint32_t d = __byte_perm(k[i], 0, dsel);
+          const uint32_t g = digit_group(d, vmask);
+          const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
+          __syncwarp(vmask);
+          if (lane == (uint32_t)(__ffs(g) - 1)) S.wcur[warp][d] = pos + __popc(g);
+          S.sorted[pos] = k[i];
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+      const uint32_t u = S.sorted[j];
+      const uint32_t d = __byte_perm(u, 0, dsel);
+      __stcs(dst + S.grun[d] + (j - S.dstart[d]), u ^ flip_out);
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) S.grun[threadIdx.x] += S.dstart[threadIdx.x + 1] - S.dstart[threadIdx.x];
+#pragma unroll
+    for (int i = 0; i < kR3KPT; ++i) k[i] = kn[i];
+  }
+  phase_mark(w.pt, 4);
+  pdl_trigger();
+}
+
+// ---- K8 variant with TMA-staged sub-tiles (default for 16-byte aligned src) ----------------
+// As k_radix_pass3, but the scatter phase streams each 8192-key sub-tile into shared memory
+// with one bulk copy (cp.async.bulk, completion on an mbarrier) instead of 16 scalar loads
+// per thread (ncu: those loads were the top stall, LSU queue full).  The copy of sub-tile
+// k+1 is issued as soon as sub-tile k's keys are in registers (after its counting), so it
+// overlaps the ranking and the write-out; one stage buffer and one lane-mask buffer keep the
+// footprint at ~98 KB (2 CTAs per SM).  Requires src 16-byte aligned.
+struct Radix4Smem {
+  uint32_t wcur[kRadixWarps][256];   // per-warp digit counts -> cursors (16 KB)
+  uint32_t wmask[kRadixWarps][256];  // equality-grouping lane masks (16 KB)
+  uint32_t sorted[kR3Tile];          // sub-tile sorted by digit (32 KB)
+  uint32_t stage[kR3Tile + 4];       // staged sub-tile (+ alignment shift) (32 KB)
+  uint32_t dstart[257];
+  uint32_t grun[256];
+  uint32_t hnext[256];
+  uint32_t red[34];
+  uint64_t bar;
+};
+
+__global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t* __restrict__ src,
+                                                                   uint32_t* __restrict__ dst, uint32_t n, int p,
+                                                                   Radix2Ws w) {
+  extern __shared__ __align__(16) unsigned char radix_smem_raw[];
+  Radix4Smem& S = *reinterpret_cast<Radix4Smem*>(radix_smem_raw);
+  pdl_wait();
+  phase_mark(w.pt, -1);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
+  const uint32_t dsel = 0x4440u | (uint32_t)p;
+  const uint32_t flip_in = p == 0 ? kSignFlip : 0u, flip_out = p == 3 ? kSignFlip : 0u;
+  const uint32_t lo = (uint32_t)((uint64_t)n * c / G), hi = (uint32_t)((uint64_t)n * (c + 1) / G);
+  for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&S.wmask[0][0])[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar, 1);
+    mbar_fence_init();
+  }
+  // ---- phase 1: digit counts of the chunk (16-byte vectors; src is aligned)
+  if (threadIdx.x < 256) S.hnext[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    const uint64_t pol = l2_evict_first_policy();
+    const uint32_t a4 = min(hi, (lo + 3u) & ~3u), b4 = max(a4, hi & ~3u);
+    for (uint32_t i = lo + threadIdx.x; i < a4; i += blockDim.x)
+      atomicAdd(&S.hnext[__byte_perm(__ldcs(src + i) ^ flip_in, 0, dsel)], 1u);
+    const int4* body = reinterpret_cast<const int4*>(src + a4);
+    const uint32_t nv = (b4 - a4) / 4;
+    uint32_t v = threadIdx.x;
+    for (; v + 3 * blockDim.x < nv; v += 4 * blockDim.x) {
+      int4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = ld_stream4(body + v + u * blockDim.x, pol);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].x ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].y ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].z ^ flip_in, 0, dsel)], 1u);
+        atomicAdd(&S.hnext[__byte_perm((uint32_t)x[u].w ^ flip_in, 0, dsel)], 1u);
+      }
+    }
+    for (; v < nv; v += blockDim.x) {
+      const int4 x = ld_stream4(body + v, pol);
+      atomicAdd(&S.hnext[__byte_perm((uint32_t)x.x ^ flip_in, 0, dsel)], 1u);
+      atomicAdd(&S.hnext[__byte_perm((uint32_t)x.y ^ flip_in, 0, dsel)], 1u);
+      atomicAdd(&S.hnext[__byte_perm((uint32_t)x.z ^ flip_in, 0, dsel)], 1u);
+      atomicAdd(&S.hnext[__byte_perm((uint32_t)x.w ^ flip_in, 0, dsel)], 1u);
+    }
+    for (uint32_t i = b4 + threadIdx.x; i < hi; i += blockDim.x)
+      atomicAdd(&S.hnext[__byte_perm(__ldcs(src + i) ^ flip_in, 0, dsel)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) __stcg(w.cnt + (size_t)c * 256 + threadIdx.x, S.hnext[threadIdx.x]);
+  phase_mark(w.pt, 0);
+  grid_barrier_r(w.bar);
+  phase_mark(w.pt, 1);
+  // ---- phase 2: column scans (CTA d scans digit d over the G chunks)
+  for (uint32_t d = c; d < 256; d += G) {
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < G; c0 += blockDim.x) {
+      const uint32_t cc = c0 + threadIdx.x;
+      const uint32_t v = cc < G ? __ldcg(w.cnt + (size_t)cc * 256 + d) : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t>(v, tot, S.red);
+      if (cc < G) __stcg(w.pre + (size_t)cc * 256 + d, carry + ex);
+      carry += tot;
+    }
+    if (threadIdx.x == 0) __stcg(w.total + d, carry);
+  }
+  phase_mark(w.pt, 2);
+  grid_barrier_r(w.bar);
+  phase_mark(w.pt, 3);
+  // ---- phase 3
+  {
+    uint32_t gtot;
+    const uint32_t gs = block_excl_scan<uint32_t>(threadIdx.x < 256 ? __ldcg(w.total + threadIdx.x) : 0u, gtot, S.red);
+    if (threadIdx.x < 256) S.grun[threadIdx.x] = gs + __ldcg(w.pre + (size_t)c * 256 + threadIdx.x);
+  }
+  const uint64_t pol = l2_evict_first_policy();
+  // sub-tile [t0, t0 + tn): key t0 + j sits at stage[sft + j], sft = t0 & 3, so that the
+  // 16-byte aligned body [ab, ae) arrives by one bulk copy at the 16-byte aligned
+  // stage + (ab - (t0 & ~3)); the at most 3 keys before ab and after ae are loaded by threads
+  auto bounds = [&](uint32_t t0, uint32_t& tn, uint32_t& ab, uint32_t& ae) {
+    tn = min((uint32_t)kR3Tile, hi - t0);
+    ab = min(t0 + tn, (t0 + 3u) & ~3u);
+    ae = max(ab, (t0 + tn) & ~3u);
+  };
+  auto issue = [&](uint32_t t0) {
+    uint32_t tn, ab, ae;
+    bounds(t0, tn, ab, ae);
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = 4u * (ae - ab);
+      mbar_arrive_expect_tx(&S.bar, bytes);
+      if (bytes) tma_load_1d(S.stage + (ab - (t0 & ~3u)), src + ab, bytes, &S.bar, pol);
+    }
+  };
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t phase = 0;
+  __syncthreads();
+  if (lo < hi) issue(lo);
+  for (uint32_t t0 = lo; t0 < hi; t0 += kR3Tile) {
+    uint32_t tn, ab, ae;
+    bounds(t0, tn, ab, ae);
+    for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&S.wcur[0][0])[i] = 0;
+    const uint32_t sft = t0 & 3u;
+    if (threadIdx.x < ab - t0) S.stage[sft + threadIdx.x] = __ldcs(src + t0 + threadIdx.x);
+    if (threadIdx.x >= 8 && threadIdx.x - 8 < t0 + tn - ae)
+      S.stage[sft + (ae - t0) + threadIdx.x - 8] = __ldcs(src + ae + threadIdx.x - 8);
+    mbar_wait_sleep(&S.bar, phase);
+    phase ^= 1u;
+    __syncthreads();  // staged keys (bulk + edges) visible; wcur cleared
+    const uint32_t wseg = warp * 32 * kR3KPT;
+    uint32_t k[kR3KPT];
+#pragma unroll
+    for (int i = 0; i < kR3KPT; ++i) {
+      const uint32_t j = wseg + i * 32 + lane;
+      k[i] = j < tn ? (S.stage[sft + j] ^ flip_in) : 0u;
+      if (j < tn) atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u);
+    }
+    __syncthreads();  // counts complete; the stage buffer is free
+    if (t0 + kR3Tile < hi) issue(t0 + kR3Tile);
+    {  // exclusive scan over (digit, warp): thread t has digit t >> 1, warps (t & 1) * 8 .. + 7
+      const uint32_t d = threadIdx.x >> 1, w0 = (threadIdx.x & 1u) * (kRadixWarps / 2);
+      uint32_t v[kRadixWarps / 2], s = 0;
+#pragma unroll
+      for (int j = 0; j < kRadixWarps / 2; ++j) {
+        v[j] = S.wcur[w0 + j][d];
+        s += v[j];
+      }
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(s, tot, S.red);
+      if ((threadIdx.x & 1u) == 0) S.dstart[d] = ex;
+      if (threadIdx.x == 0) S.dstart[256] = tot;
+#pragma unroll
+      for (int j = 0; j < kRadixWarps / 2; ++j) {
+        S.wcur[w0 + j][d] = ex;
+        ex += v[j];
+      }
+    }
+    __syncthreads();
+    if (wseg + 32 * kR3KPT <= tn) {
+#pragma unroll
+      for (int i = 0; i < kR3KPT; ++i) {
+        const uint32_t d = __byte_perm(k[i], 0, dsel);
+        uint32_t* wm = &S.wmask[warp][d];
+        atomicOr(wm, 1u << lane);
+        __syncwarp();
+        const uint32_t g = *wm;
+        const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
+        __syncwarp();
+        if (lane == (uint32_t)(__ffs(g) - 1)) {
+          S.wcur[warp][d] = pos + __popc(g);
+          *wm = 0u;
+        }
+        S.sorted[pos] = k[i];
+        __syncwarp();  // the mask word is clear before the next step's atomicOr
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kR3KPT; ++i) {
+        const uint32_t idx0 = wseg + i * 32;
+        const uint32_t vmask = idx0 >= tn ? 0u : (tn - idx0 >= 32 ? FULL : ((1u << (tn - idx0)) - 1u));
+        if ((vmask >> lane) & 1u) {
+          const uint32_t d = __byte_perm(k[i], 0, dsel);
+          const uint32_t g = digit_group(d, vmask);
+          const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
+          __syncwarp(vmask);
+          if (lane == (uint32_t)(__ffs(g) - 1)) S.wcur[warp][d] = pos + __popc(g);
+          S.sorted[pos] = k[i];
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+      const uint32_t u = S.sorted[j];
+      const uint32_t d = __byte_perm(u, 0, dsel);
+      __stcs(dst + S.grun[d] + (j - S.dstart[d]), u ^ flip_out);
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) S.grun[threadIdx.x] += S.dstart[threadIdx.x + 1] - S.dstart[threadIdx.x];
+  }
+  phase_mark(w.pt, 4);
+  pdl_trigger();
+}
+
 inline void radix_configure() {
   cudaFuncSetAttribute(k_radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RadixSmem));
   cudaFuncSetAttribute(k_radix_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RadixSmem));
+  cudaFuncSetAttribute(k_radix_pass3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Radix3Smem));
+  cudaFuncSetAttribute(k_radix_pass4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Radix4Smem));
 }
 
 }  // namespace ds
