@@ -1,8 +1,15 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+# Full GPU check: smoke, pytest -m gpu, all bench configs (short), default bench line
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pytest_gpu.log
+rm -f gpurun_out/bench_all.jsonl
 for c in c2 c1 c3-zipf c3-sorted c3-reverse c3-hot1 c5 c4; do
-  timeout 300 python bench.py --config $c --steps 200 --warmup 10 --no-cpu-baseline --no-e2e >> gpurun_out/bench_all.jsonl 2>> gpurun_out/bench_err.log
+  timeout 300 python bench.py --config $c --steps 100 --warmup 5 --no-cpu-baseline --no-e2e >> gpurun_out/bench_all.jsonl 2>> gpurun_out/bench_err.log
 done
 timeout 300 python bench.py > gpurun_out/bench_default.jsonl 2>gpurun_out/bench_default.err; echo bench=$?
+python - <<'PY'
+import json
+for l in open('gpurun_out/bench_all.jsonl'):
+    d=json.loads(l); r=d['roofline']; st=d['step_roofline']
+    print(d['config']['workload'][:42].ljust(42), '%.3e keys/s'%d['value'], '%.4f ms'%d['ms_per_step'], 'dom', r['kernel'], 'frac %.3f'%r['frac'], 'step %.3f'%st['frac_of_measured'], 'launches/step %.1f'%(d['gpu_launches']/d['steps']))
+PY
