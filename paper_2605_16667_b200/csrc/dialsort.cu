@@ -97,7 +97,9 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 constexpr size_t kSmemBudget = 227 * 1024 - 4096;  // static smem of the kernels <= 4 KB
 // k_sort_fused workspace: 2 parities of strided tile totals, fallback tile totals, ready flags
-constexpr uint64_t kFusedTileWords = 2ull * kFTileSlots * kTileTotStride + 2 * kFTileSlots;
+// and 2 parities of strided owner totals + the fallback owner totals
+constexpr uint64_t kFusedTileWords =
+    2ull * kFTileSlots * kTileTotStride + 2 * kFTileSlots + 2ull * kFOwnSlots * kTileTotStride + kFOwnSlots;
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -390,6 +392,11 @@ int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t
   a.tile_red_stride = kTileTotStride;
   a.tile_alt = ft + 2 * red_words;
   a.ready = a.tile_alt + kFTileSlots;
+  uint32_t* ownb = a.ready + kFTileSlots;
+  const uint64_t own_words = (uint64_t)kFOwnSlots * kTileTotStride;  // per parity
+  a.own_red = ownb + own_words * (c->fused_seq & 1);
+  a.own_clear = ownb + own_words * ((c->fused_seq + 1) & 1);
+  a.own_alt = ownb + 2 * own_words;
   // exception histogram of the 4-bit rows: parity buffers, the other one cleared by every launch
   a.Hx = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * (c->fused_seq & 1);
   a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);

@@ -129,6 +129,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void phase_mark(PhaseTimes* pt, int i) {
   if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) pt->stamp[blockIdx.x][i + 1] = gtimer();
 }
+// The same, stamped only once `dep` has arrived (thread 0's register).
+__device__ __forceinline__ void phase_mark_dep(PhaseTimes* pt, int i, uint32_t dep) {
+  if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) {
+    uint32_t z;
+    asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(dep));
+    pt->stamp[blockIdx.x][i + 1] = gtimer() + z;
+  }
+}
 
 // Fire-and-forget global add (RED.ADD.U32 in SASS).
 __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {

@@ -10,18 +10,18 @@
 // Why one kernel: on B200 a kernel boundary plus its ramp costs ~1-2 us and a
 // counter+generation grid barrier ~2 us, against a ~10 us HBM floor per 40 MB pass.
 //   1. Every CTA ingests its keys into a private shared-memory histogram, flushes it as
-//      partial row c (L2) and adds (RED) the row's 128-bin tile sums into tile totals.
-//   2. ONE monotonic grid barrier.  Every CTA reads the tile totals and scans them locally:
-//      toff[t] = first output position of tile t (the tile-level write offsets).
-//   3. Work is split in a "cost space" that concatenates, tile by tile, a merge segment of
-//      alpha units (the cost of merging the tile's C row segments) and one unit per output
-//      position of the tile.  CTA b takes the equal slice [T b / G, T (b+1) / G): it merges
-//      every tile its slice touches and projects the positions of those tiles that fall in
-//      its slice.  Positions are balanced (up to alpha) whatever the skew — a Zipf hot tile
-//      is projected by ~30 CTAs, each of which merges it (redundantly, 37 KB of L2 reads) —
-//      and no CTA waits for another after the barrier: each has the P values it needs in
-//      shared memory.  H is written by the CTA whose slice holds the tile's merge segment.
-// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) adds two barriers: tile
+//      partial row c (L2; 4-bit, 16-bit or 32-bit counters) and adds (RED) the row's 64-bin
+//      tile sums into tile totals.
+//   2. ONE monotonic grid barrier.  Every CTA requests its first row segments, reads the
+//      tile totals and scans them locally: toff[t] = first output position of tile t.
+//   3. CTA b merges the tiles [ntiles b / G, ntiles (b+1) / G) (index ownership): H and the
+//      exclusive prefix P of its bins.
+//   4. Projection.  Near-uniform histograms (every CTA's own tiles hold ~nw / G positions):
+//      each CTA projects its own tiles from P in shared memory — no cross-CTA dependence
+//      after the barrier.  Skewed ones: P goes through L2 with per-tile release flags and
+//      CTA b projects the equal position share [b nw / G, (b+1) nw / G) — a Zipf hot tile
+//      is projected by many CTAs.
+// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) adds one barrier: tile
 // totals are recomputed with the fallback histogram ovfH, which is cleared at the end.
 #pragma once
 #include "ds_common.cuh"
@@ -30,19 +30,23 @@
 
 namespace ds {
 
-constexpr uint32_t kFTiles = kSmem16MaxBins / kFTileBins;  // <= 768 tiles
+constexpr uint32_t kFTiles = kSmem16MaxBins / kFTileBins;  // <= 1536 tiles (2 per thread)
 constexpr uint32_t kFSlotWords = 128;                       // staged words per row and batch (512 B)
 constexpr uint32_t kFMaxRows = 148;                         // rows (CTAs) a staging slot holds
-constexpr uint32_t kFTileSlots = 1024;                      // tile-total slots (>= kFTiles)
+constexpr uint32_t kFTileSlots = 2048;                      // tile-total slots (>= kFTiles)
+constexpr uint32_t kFOwnSlots = 256;                        // owner-total slots (>= kFMaxRows)
 // Tile totals are REDs from every CTA into ntiles counters: a 64-word (256 B) stride puts each
 // counter in its own L2 line (same-line REDs serialise: 4 lines took 7.7 us for 19K REDs).
-constexpr uint32_t kTileTotStride = 64;
+#ifndef DIALSORT_TILE_STRIDE
+#define DIALSORT_TILE_STRIDE 64
+#endif
+constexpr uint32_t kTileTotStride = DIALSORT_TILE_STRIDE;
 constexpr uint32_t kFBatchBins = 1024;                      // max bins per batch (8 4-bit tiles)
 // Partial-row formats of k_sort_fused (bins per 128-word staged batch: 128, 256, 1024)
 constexpr int kRowU32 = 0, kRowP16 = 1, kRowN4 = 2;
 template <int FMT> struct RowFmt {
-  static constexpr uint32_t tpb = FMT == kRowU32 ? 1u : FMT == kRowP16 ? 2u : 8u;  // tiles per batch
-  static constexpr uint32_t wpt = kFSlotWords / tpb;  // row words per 128-bin tile (128, 64, 16)
+  static constexpr uint32_t tpb = FMT == kRowU32 ? 2u : FMT == kRowP16 ? 4u : 16u;  // tiles per batch
+  static constexpr uint32_t wpt = kFSlotWords / tpb;  // row words per 64-bin tile (64, 32, 8)
 };
 
 // Dynamic shared memory after the barrier (words); the ingestion histogram is dead by then.
@@ -53,7 +57,9 @@ constexpr uint32_t kFPassTiles = 32;                                 // tiles st
 constexpr uint32_t kFOffPs = kFOffScratch + 8 * kFBatchBins;          // pass P + 32 sentinels
 constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // 256 merged H of the batch
 constexpr uint32_t kFOffWc = kFOffHb + kFBatchBins;                   // 32 warps x 128 mark counts
-constexpr uint32_t kFSmemWords = kFOffWc + 32 * 128;
+constexpr uint32_t kFOffOwn = kFOffWc + 32 * 128;                    // oo[G + 1] owner offsets
+constexpr uint32_t kFOffTsh = kFOffOwn + kFMaxRows + 32;              // share window offsets
+constexpr uint32_t kFSmemWords = kFOffTsh + kFTiles + 32;
 
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
@@ -264,19 +270,28 @@ __device__ __forceinline__ void stage_batch(const ScanArgs& a, uint32_t t0, uint
 // rows r = j >> 7 (mod 8) — 4-bit rows as four 2 x 16-bit SWAR accumulators (8 bins).
 template <int FMT>
 __device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, const uint32_t* slot,
-                                             uint32_t* scratch, uint32_t* hb, bool use_ovf) {
+                                             uint32_t* scratch, uint32_t* hb, bool use_ovf, uint32_t hx) {
   constexpr uint32_t tpb = RowFmt<FMT>::tpb, wpt = RowFmt<FMT>::wpt, nb = tpb * kFTileBins;
+  static_assert(nb <= 1024, "one bin of the batch per thread");
   const uint32_t col = threadIdx.x & 127, qg = threadIdx.x >> 7;
   if ((need_mask >> (col / wpt)) & 1u) {
     if (FMT == kRowN4) {
-      uint32_t el = 0, eh = 0, ol = 0, oh = 0;  // 16-bit lanes: nibbles (0,4) (2,6) (1,5) (3,7)
-      for (uint32_t r = qg; r < a.C; r += 8) {
-        const uint32_t x = slot[r * kFSlotWords + col];
-        const uint32_t e = x & 0x0F0F0F0Fu, o = (x >> 4) & 0x0F0F0F0Fu;
-        el += e & 0x00FF00FFu;
-        eh += (e >> 8) & 0x00FF00FFu;
-        ol += o & 0x00FF00FFu;
-        oh += (o >> 8) & 0x00FF00FFu;
+      // nibbles summed in byte lanes for up to 17 rows (17 x 15 = 255), then widened into
+      // four 2 x 16-bit accumulators: nibbles (0,4) (2,6) (1,5) (3,7)
+      uint32_t el = 0, eh = 0, ol = 0, oh = 0;
+      for (uint32_t r0 = qg; r0 < a.C; r0 += 8 * 16) {
+        uint32_t be = 0, bo = 0;
+        const uint32_t r1 = min(a.C, r0 + 8 * 16);
+#pragma unroll 4
+        for (uint32_t r = r0; r < r1; r += 8) {
+          const uint32_t x = slot[r * kFSlotWords + col];
+          be += x & 0x0F0F0F0Fu;
+          bo += (x >> 4) & 0x0F0F0F0Fu;
+        }
+        el += be & 0x00FF00FFu;
+        eh += (be >> 8) & 0x00FF00FFu;
+        ol += bo & 0x00FF00FFu;
+        oh += (bo >> 8) & 0x00FF00FFu;
       }
       uint32_t* d = scratch + qg * kFBatchBins + 8 * col;  // bins 8 col .. 8 col + 7
       reinterpret_cast<uint4*>(d)[0] = make_uint4(el & 0xffffu, ol & 0xffffu, eh & 0xffffu, oh & 0xffffu);
@@ -301,28 +316,18 @@ __device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uin
     }
   }
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < nb; j += blockDim.x) {
+  const uint32_t j = threadIdx.x;
+  if (j < nb) {
     uint32_t h = 0;
     if ((need_mask >> (j / kFTileBins)) & 1u) {
 #pragma unroll
       for (uint32_t g = 0; g < 8; ++g) h += scratch[g * kFBatchBins + j];
       const uint64_t bin = (uint64_t)t0 * kFTileBins + j;
-      if (bin < a.U) {
-        if (FMT == kRowN4) h += __ldcg(a.Hx + bin);
-        if (use_ovf) h += __ldcg(a.ovfH + bin);
-      }
+      h += hx;  // Hx[bin] of 4-bit rows (0 otherwise), prefetched by the caller
+      if (use_ovf && bin < a.U) h += __ldcg(a.ovfH + bin);
     }
     hb[j] = h;
   }
-}
-
-// Block-wide scan of the tile totals (thread t holds tile t's total v) into toff[0..ntiles].
-__device__ __forceinline__ void tile_offsets(uint64_t v, uint32_t ntiles, uint32_t* toff, uint64_t* red) {
-  uint64_t total;
-  const uint64_t ex = block_excl_scan<uint64_t>(v, total, red);
-  if (threadIdx.x < ntiles) toff[threadIdx.x] = (uint32_t)ex;
-  if (threadIdx.x == 0) toff[ntiles] = (uint32_t)(total > 0xffffffffull ? 0xffffffffull : total);
-  __syncthreads();
 }
 
 // Overflow path: exact total of tile t straight from the partial rows, Hx and ovfH.
@@ -366,86 +371,173 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   const uint32_t G = gridDim.x, b = blockIdx.x;
   // the other parity's tile totals are zeroed for the next launch (host alternates them;
   // every slot, since the next launch may have more tiles than this one)
-  if (b == G - 1)
+  if (b == G - 1) {
     for (uint32_t i = threadIdx.x; i < kFTileSlots; i += blockDim.x) a.tile_clear[(uint64_t)i * kTileTotStride] = 0;
+    for (uint32_t i = threadIdx.x; i < kFOwnSlots; i += blockDim.x) a.own_clear[(uint64_t)i * kTileTotStride] = 0;
+  }
   if (a.Hx_clear)  // and the other parity's exception histogram (all of it: launches of any
                    // format alternate the parity, and the next may have a larger U), a slice per CTA
     for (uint32_t k = kSmem16MaxBins * b / G + threadIdx.x; k < kSmem16MaxBins * (b + 1) / G; k += blockDim.x)
       a.Hx_clear[k] = 0;
   constexpr bool PACK16 = FMT != kRowU32;
 
-  hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr);
-  grid_barrier_mono(a.bar64, a.bar_base + G);  // rows, tile totals, overflow fallback in L2
+  // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram
+  static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
+  hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
+  grid_barrier_mono(a.bar64, a.bar_base + G);  // rows, tile / owner totals, overflow fallback in L2
   phase_mark(a.pt, 3);
 
-  uint32_t* toff = sh + kFOffToff;
-  const bool use_ovf = ld_acquire_u32(&a.st->ovf_epoch) == a.epoch;
   uint32_t tb0, tb1;
-  my_tiles(ntiles, tb0, tb1);  // tiles this CTA merges and publishes (index ownership)
-  uint64_t tv;                 // tile threadIdx.x's total: loaded now, scanned after the merge
-  if (!use_ovf) {
-    barrier_skip(a.bar64);
-    tv = threadIdx.x < ntiles ? __ldcg(a.tile_red + (uint64_t)threadIdx.x * a.tile_red_stride) : 0ull;
-  } else {
-    // a packed counter overflowed somewhere: the flushed tile sums miss the fallback keys
-    for (uint32_t t = tb0; t < tb1; ++t) {
-      const uint64_t tt = tile_total_direct<FMT>(a, t, red64);
-      if (threadIdx.x == 0) __stcg(a.tile_alt + t, (uint32_t)(tt > 0xffffffffull ? 0xffffffffull : tt));
-    }
-    grid_barrier_mono(a.bar64, a.bar_base + 2 * G);
-    tv = threadIdx.x < ntiles ? __ldcg(a.tile_alt + threadIdx.x) : 0ull;
-  }
-  phase_mark(a.pt, 4);
-
-  // ---- merge: H and the tile-relative exclusive prefix PL of the tiles this CTA owns ------
-  // (lem:crn lifted to whole histograms: H = sum of the partial rows, + Hx, + ovfH), published
-  // per batch (ready[t] = epoch, release).  No dependence on the tile offsets, so it starts
-  // right after the barrier; the projection adds toff[t] itself.
+  my_tiles(ntiles, tb0, tb1);  // tiles this CTA merges (index ownership)
+  const uint32_t nown = tb1 - tb0;
   constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
   constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
-  uint32_t* slot[2] = {sh + kFOffStage, sh + kFOffStage + kFMaxRows * kFSlotWords};
+  const uint32_t S = a.tile_red_stride;
+  auto slot = [&](uint32_t k) { return sh + kFOffStage + (k & 1u) * (kFMaxRows * kFSlotWords); };  // 2 slots
   uint32_t* scratch = sh + kFOffScratch;
   uint32_t* hb = sh + kFOffHb;
+  uint32_t* Ps = sh + kFOffPs;
+  uint32_t* oo = sh + kFOffOwn;   // oo[c] = first output position of owner c's tiles, oo[G] = total
+  uint32_t* tw = sh + kFOffToff;  // tw[i] = first position of own tile tb0 + i, relative to oo[b]
   uint32_t* wc = sh + kFOffWc + (threadIdx.x >> 5) * 128;
   reinterpret_cast<uint4*>(wc)[threadIdx.x & 31] = make_uint4(0, 0, 0, 0);
-  if (tb0 < tb1) {
-    const uint32_t nbt = (tb1 - tb0 + tpb - 1) / tpb;  // batches of tiles tb0 + k tpb ..
-    auto need_of = [&](uint32_t k) -> uint32_t {
-      const uint32_t t0 = tb0 + k * tpb, nt = min(tpb, tb1 - t0);
-      return nt >= 32 ? 0xffffffffu : (1u << nt) - 1u;
-    };
-    for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
-      stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot[k]);
+  const uint32_t nbt = nown ? (nown + tpb - 1) / tpb : 0u;  // batches tb0 + k tpb ..
+  auto need_of = [&](uint32_t k) -> uint32_t {
+    const uint32_t t0 = tb0 + k * tpb, nt = min(tpb, tb1 - t0);
+    return nt >= 32 ? 0xffffffffu : (1u << nt) - 1u;
+  };
+  // The owner totals, the own tiles' totals, the overflow state and the first two batches' row
+  // segments (and their exception counts) are requested together, totals first: none depends
+  // on another, and the barrier ordered every CTA's flush before them.  Each CTA reads G + its
+  // own ~ntiles / G counters (reading all ntiles strided counters from every CTA measured
+  // ~2.5 us: 148-way fan-in on the same L2 lines).
+  const uint32_t t2 = 2 * threadIdx.x;
+  uint32_t ov = threadIdx.x < G ? __ldcg(a.own_red + (uint64_t)threadIdx.x * S) : 0u;
+  uint32_t w0 = t2 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2) * S) : 0u;
+  uint32_t w1 = t2 + 1 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2 + 1) * S) : 0u;
+  const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
+#if DIALSORT_EXP_LATPROBE
+  phase_mark(a.pt, 13);  // before the staging
+#endif
+  for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
+    stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot(k));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // Hx of bin t0 kFTileBins + threadIdx.x of batch k (4-bit rows), loaded a batch ahead
+  auto hx_of = [&](uint32_t k) -> uint32_t {
+    if (FMT != kRowN4 || k >= nbt || threadIdx.x >= nbb || !((need_of(k) >> (threadIdx.x / kFTileBins)) & 1u)) return 0u;
+    const uint32_t bin = (tb0 + k * tpb) * kFTileBins + threadIdx.x;
+    return bin < U ? __ldcg(a.Hx + bin) : 0u;
+  };
+  uint32_t hx = hx_of(0);
+#if DIALSORT_EXP_LATPROBE
+  phase_mark(a.pt, 10);                 // staging issued
+  phase_mark_dep(a.pt, 11, ov | w0 | w1);  // thread 0's totals arrived
+  phase_mark_dep(a.pt, 12, (uint32_t)__syncthreads_or(use_ovf));  // every thread's overflow state
+#endif
+  if (!use_ovf) {
+    barrier_skip(a.bar64);
+  } else {
+    // a packed counter overflowed somewhere: the flushed sums miss the fallback keys
+    uint64_t osd = 0;
+    for (uint32_t t = tb0; t < tb1; ++t) {
+      const uint64_t tt = tile_total_direct<FMT>(a, t, red64);
+      osd += tt;
+      if (threadIdx.x == 0) __stcg(a.tile_alt + t, (uint32_t)tt);
+    }
+    if (threadIdx.x == 0) __stcg(a.own_alt + b, (uint32_t)osd);
+    grid_barrier_mono(a.bar64, a.bar_base + 2 * G);
+    ov = threadIdx.x < G ? __ldcg(a.own_alt + threadIdx.x) : 0u;
+    w0 = t2 < nown ? __ldcg(a.tile_alt + tb0 + t2) : 0u;
+    w1 = t2 + 1 < nown ? __ldcg(a.tile_alt + tb0 + t2 + 1) : 0u;
+  }
+  const uint32_t* tsrc = use_ovf ? a.tile_alt : a.tile_red;  // tile totals, stride:
+  const uint32_t tstr = use_ovf ? 1u : S;
+
+  // ---- owner offsets and the own tiles' offsets: one scan, two halves --------------------
+  // (every count sum here is <= n < 2^32, R4: the low half never carries into the high one)
+  {
+    uint64_t tot2;
+    const uint64_t ex = block_excl_scan<uint64_t>(((uint64_t)ov << 32) | (uint64_t)(w0 + w1), tot2, red64);
+    if (threadIdx.x < G) oo[threadIdx.x] = (uint32_t)(ex >> 32);
+    if (threadIdx.x == 0) {
+      oo[G] = (uint32_t)(tot2 >> 32);
+      tw[nown] = (uint32_t)tot2;
+    }
+    if (t2 < nown) tw[t2] = (uint32_t)ex;
+    if (t2 + 1 < nown) tw[t2 + 1] = (uint32_t)ex + w0;
+    __syncthreads();
+  }
+  phase_mark(a.pt, 4);
+  const uint64_t total = oo[G];
+  const uint32_t obase = oo[b];  // first output position of this CTA's tiles
+  if (b == 0 && threadIdx.x == 0) {
+    unsigned flags = 0;
+    if (a.exact ? (total != n_exp) : (total > n_exp)) flags |= FLAG_SIZE;
+    if (flags) atomicOr(&a.st->flags, flags);
+    a.st->last_total = total;
+    if (a.d_total) *a.d_total = total;
+    *a.ws_total = total;
+  }
+  const uint32_t nw = (uint32_t)(total < n_exp ? total : n_exp);  // positions written
+  // Own-tile mode: when every CTA's own tiles hold about nw / G positions (near-uniform
+  // histograms), each CTA projects exactly the tiles it merged, from P in its shared memory —
+  // no cross-CTA flags, no P round trip through L2.  Otherwise (skew) equal position shares.
+  bool own = (ntiles + G - 1) / G <= kFPassTiles;
+  if (own) {
+    const uint32_t lim = nw / G + nw / (16 * G) + 1024;
+    own = !__syncthreads_or(threadIdx.x < G && ov > lim);
+  }
+  // equal share [lo, hi) (share mode): the totals of the tiles of the owners it overlaps are
+  // requested now and scanned after the merge
+  const uint32_t lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
+  const uint32_t hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
+  const bool share = !own && lo < hi;
+  uint32_t oa = 0, ob = 0, x0 = 0, x1 = 0, s0 = 0, s1 = 0;
+  if (share) {
+    oa = tile_of(oo, G, lo);
+    ob = tile_of(oo, G, hi - 1);
+    x0 = (uint32_t)((uint64_t)ntiles * oa / G);
+    x1 = (uint32_t)((uint64_t)ntiles * (ob + 1) / G);
+    s0 = x0 + t2 < x1 ? __ldcg(tsrc + (uint64_t)(x0 + t2) * tstr) : 0u;
+    s1 = x0 + t2 + 1 < x1 ? __ldcg(tsrc + (uint64_t)(x0 + t2 + 1) * tstr) : 0u;
+  }
+
+  // ---- merge: H and the exclusive prefix P of the tiles this CTA owns --------------------
+  // (lem:crn lifted to whole histograms: H = sum of the partial rows, + Hx, + ovfH).  Own-tile
+  // mode keeps P in shared memory; otherwise P goes to L2 and each batch is published
+  // (ready[t] = epoch, release) for the CTAs whose shares overlap it.
+  for (uint32_t k = 0; k < nbt; ++k) {
+    const uint32_t t0 = tb0 + k * tpb, need = need_of(k);
+    if (k + 1 < nbt) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    phase_mark(a.pt, 5);
+    reduce_batch<FMT>(a, t0, need, slot(k), scratch, hb, use_ovf, hx);
+    __syncthreads();  // hb complete; the slot is free
+    if (k + 2 < nbt) {
+      stage_batch<FMT>(a, tb0 + (k + 2) * tpb, need_of(k + 2), slot(k));
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (uint32_t k = 0; k < nbt; ++k) {
-      const uint32_t t0 = tb0 + k * tpb, need = need_of(k);
-      if (k + 1 < nbt) asm volatile("cp.async.wait_group 1;" ::: "memory");
-      else asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncthreads();
-      phase_mark(a.pt, 5);
-      reduce_batch<FMT>(a, t0, need, slot[k & 1], scratch, hb, use_ovf);
-      __syncthreads();  // hb complete; the slot is free
-      if (k + 2 < nbt) {
-        stage_batch<FMT>(a, tb0 + (k + 2) * tpb, need_of(k + 2), slot[k & 1]);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
-      // tile-relative exclusive prefix (a 128-bin tile is 4 whole warps)
-      const uint32_t j = threadIdx.x;
-      const uint32_t h = j < nbb ? hb[j] : 0u;
-      const uint32_t inc = warp_incl_scan(h);
-      if (j < nbb && (j & 31) == 31) wsum[j >> 5] = inc;
-      __syncthreads();
-      if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
-        uint32_t wpre = 0;
-        for (uint32_t q = (j / kFTileBins) * (kFTileBins / 32); q < (j >> 5); ++q) wpre += wsum[q];
-        const uint32_t bin = t0 * kFTileBins + j;
-        if (bin < U) {
-          a.H[bin] = h;
-          a.P[bin] = wpre + inc - h;
-        }
-      }
-      __syncthreads();  // the batch's H and PL are written
+    hx = hx_of(k + 1);
+    // exclusive prefix within the tile (a tile is kFTileBins / 32 whole warps) + its offset
+    const uint32_t j = threadIdx.x;
+    const uint32_t h = j < nbb ? hb[j] : 0u;
+    const uint32_t inc = warp_incl_scan(h);
+    if (j < nbb && (j & 31) == 31) wsum[j >> 5] = inc;
+    __syncthreads();
+    if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
+      const uint32_t t = t0 + j / kFTileBins;
+      uint32_t wpre = obase + tw[t - tb0];
+      for (uint32_t q = (j / kFTileBins) * (kFTileBins / 32); q < (j >> 5); ++q) wpre += wsum[q];
+      const uint32_t bin = t0 * kFTileBins + j;
+      const uint32_t p = bin < U ? wpre + inc - h : (uint32_t)total;
+      if (bin < U) a.H[bin] = h;
+      if (own) Ps[(t0 - tb0) * kFTileBins + j] = p;
+      else if (bin < U) a.P[bin] = p;
+    }
+    if (!own) {
+      __syncthreads();  // the batch's H and P are written
       if (threadIdx.x < tpb && ((need >> threadIdx.x) & 1u))
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t0 + threadIdx.x), "r"(a.epoch) : "memory");
     }
@@ -454,37 +546,35 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     for (uint32_t k = tb0 * kFTileBins + threadIdx.x; k < min(tb1 * kFTileBins, U); k += blockDim.x) a.ovfH[k] = 0;
   phase_mark(a.pt, 6);
 
-  // ---- tile offsets (write offsets of the tiles) and the size / overflow status ----------
-  tile_offsets(tv, ntiles, toff, red64);
-  const uint64_t total = toff[ntiles];
-  if (b == 0 && threadIdx.x == 0) {
-    unsigned flags = 0;
-    if (total > 0xffffffffull) flags |= FLAG_OVERFLOW;
-    if (a.exact ? (total != n_exp) : (total > n_exp)) flags |= FLAG_SIZE;
-    if (flags) atomicOr(&a.st->flags, flags);
-    a.st->last_total = total;
-    if (a.d_total) *a.d_total = total;
-    *a.ws_total = total;
+  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  const uint64_t pol = l2_evict_first_policy();
+  if (own) {
+    // ---- projection of the own tiles' positions [oo[b], oo[b+1]) ∩ [0, nw) -----------------
+    const uint32_t m = nown * kFTileBins;
+    if (threadIdx.x < 32) Ps[m + threadIdx.x] = 0xffffffffu;
+    __syncthreads();
+    phase_mark(a.pt, 9);
+    const uint32_t p0 = obase, p1 = min(obase + tw[nown], nw);
+    if (nown && p0 < p1) project_warp(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
+    phase_mark(a.pt, 7);
+    pdl_trigger();
+    return;
   }
 
   // ---- projection of an equal share of the positions -------------------------------------
-  // CTA b projects [b nw / G, (b+1) nw / G) (32-aligned), i.e. the same number of outputs
-  // whatever the skew; it waits for the tiles its share overlaps, stages their P = toff[t] +
-  // PL in shared memory, and its 32 warps project.
-  const uint32_t nw = (uint32_t)(total < n_exp ? total : n_exp);  // positions written
-  const uint32_t lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
-  const uint32_t hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
-  __shared__ uint32_t s_t[2];
-  if (threadIdx.x == 0 && lo < hi) {
-    s_t[0] = tile_of(toff, ntiles, lo);
-    s_t[1] = tile_of(toff, ntiles, hi - 1);
-  }
-  __syncthreads();
-  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-  const uint64_t pol = l2_evict_first_policy();
-  uint32_t* Ps = sh + kFOffPs;
-  if (lo < hi) {
-    const uint32_t ta = s_t[0], tb = s_t[1];
+  // CTA b projects [lo, hi) = [b nw / G, (b+1) nw / G) (32-aligned), the same number of
+  // outputs whatever the skew: offsets of the window tiles [x0, x1) (the tiles of owners
+  // oa..ob), then it waits for the tiles the share overlaps, stages their P in shared memory,
+  // and its 32 warps project.
+  if (share) {
+    uint32_t* ts = sh + kFOffTsh;  // ts[i] = first position of tile x0 + i
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<uint32_t>(s0 + s1, tot, reinterpret_cast<uint32_t*>(red64));
+    if (x0 + t2 < x1) ts[t2] = oo[oa] + ex;
+    if (x0 + t2 + 1 < x1) ts[t2 + 1] = oo[oa] + ex + s0;
+    if (threadIdx.x == 0) ts[x1 - x0] = oo[ob + 1];
+    __syncthreads();
+    const uint32_t ta = x0 + tile_of(ts, x1 - x0, lo), tb = x0 + tile_of(ts, x1 - x0, hi - 1);
     // relaxed polling (a short sleep leaves issue slots to the rest of the CTA), then one
     // acquire load per flag — not a fence: fence.acq_rel.gpu waits for every store in flight
     for (uint32_t t = ta + threadIdx.x; t <= tb; t += blockDim.x) {
@@ -497,12 +587,12 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
       const uint32_t pt1 = min(pt0 + kFPassTiles, tb + 1);
       const uint32_t m = (pt1 - pt0) * kFTileBins;
       for (uint32_t i = threadIdx.x; i < m + 32; i += blockDim.x) {
-        const uint32_t t = pt0 + i / kFTileBins, bin = pt0 * kFTileBins + i;
-        Ps[i] = i >= m ? 0xffffffffu : (bin < U ? toff[t] + __ldcg(a.P + bin) : toff[ntiles]);
+        const uint32_t bin = pt0 * kFTileBins + i;
+        Ps[i] = i >= m ? 0xffffffffu : (bin < U ? __ldcg(a.P + bin) : (uint32_t)total);
       }
       __syncthreads();
       phase_mark(a.pt, 9);
-      const uint32_t p0 = max(lo, toff[pt0]), p1 = min(hi, toff[pt1]);
+      const uint32_t p0 = max(lo, ts[pt0 - x0]), p1 = min(hi, ts[pt1 - x0]);
       if (p0 < p1) project_warp(Ps, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
       __syncthreads();  // Ps is reused by the next pass
     }

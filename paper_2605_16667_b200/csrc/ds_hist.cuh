@@ -20,7 +20,7 @@ namespace ds {
 
 constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
-constexpr uint32_t kFTileBins = 128;        // scan-tile width of k_sort_fused (ds_fused.cuh)
+constexpr uint32_t kFTileBins = 64;         // scan-tile width of k_sort_fused (ds_fused.cuh)
 constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
 constexpr uint32_t kChunkBytes = 32768;     // TMA path: 8192 keys per chunk
 constexpr uint32_t kChunkVecs = kChunkBytes / 16;
@@ -259,10 +259,23 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
 // writes the row and, per 512-bin tile, the row's tile sum: into tsums[tile][row], or — when
 // a.tile_red is set — added (RED) into the tile total tile_red[tile].
+// k_sort_fused: thread b < G adds the row's sums of CTA b's tiles (tsum_sh, per 64-bin tile,
+// written by the flush loop) into the owner total own_red[b].
+__device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U) {
+  const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x;
+  for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) {
+    const uint32_t t0 = (uint32_t)((uint64_t)ntf * b / G), t1 = (uint32_t)((uint64_t)ntf * (b + 1) / G);
+    uint32_t s = 0;
+    for (uint32_t t = t0; t < t1; ++t) s += tsum_sh[t];
+    if (s) red_add_u32(a.own_red + (uint64_t)b * a.tile_red_stride, s);
+  }
+}
+
 template <bool PACK16, bool TMA>
 __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ keys, uint64_t n, const ScanArgs& a,
                                                   uint32_t stages, uint32_t* sh_hist, uint64_t* red64,
-                                                  uint64_t* full_bar, uint64_t* empty_bar) {
+                                                  uint64_t* full_bar, uint64_t* empty_bar,
+                                                  uint32_t* tsum_sh = nullptr) {
   const uint32_t U = a.U, ldw = a.ldw;
 
   // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
@@ -380,9 +393,10 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     // per word, a quarter of the packed row's L2 bytes — and a count >= 16 goes whole to the
     // global exception histogram Hx (RED; its nibble stays 0).  Thread i turns packed uint4 i
     // (8 bins; consecutive threads read consecutive uint4: no bank conflicts — 4 uint4 per
-    // thread measured 16-way conflicted) into word i of the row; the 16 threads of a 128-bin
+    // thread measured 16-way conflicted) into word i of the row; the 8 threads of a 64-bin
     // tile reduce its sum with shuffles and one adds it (RED) into the tile total.
-    const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * 16;
+    constexpr uint32_t QT = kFTileBins / 8;  // threads (packed uint4) per tile
+    const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * QT;
     uint32_t* nrow = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr;
     const uint32_t nw = (U + 7) / 8;  // row words
 #if DIALSORT_EXP_NOFLUSH
@@ -422,12 +436,13 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
 #endif
       }
 #pragma unroll
-      for (uint32_t o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (g < tot && (g & 15u) == 0) {
+      for (uint32_t o = QT / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (g < tot && (g % QT) == 0) {
         fsum += v;
 #if !DIALSORT_EXP_NORED
-        if (v) red_add_u32(a.tile_red + (uint64_t)(g / 16) * a.tile_red_stride, v);
+        if (v) red_add_u32(a.tile_red + (uint64_t)(g / QT) * a.tile_red_stride, v);
 #endif
+        if (tsum_sh) tsum_sh[g / QT] = v;
       }
       if (b0 == 0) phase_mark(a.pt, 12);  // first flush iteration done (debug)
       if (b0 == blockDim.x) phase_mark(a.pt, 13);
@@ -456,6 +471,7 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
       if (i < tot4 && (i % QT) == 0) {
         fsum += v;
         if (v) red_add_u32(a.tile_red + (uint64_t)(i / QT) * a.tile_red_stride, v);
+        if (tsum_sh) tsum_sh[i / QT] = v;
       }
     }
   }
@@ -487,6 +503,9 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     // fsum: per-warp totals in lane 0 (tsums loop) or per-tile totals in the tile's lane 0
     const uint64_t tot = block_sum<uint64_t>(a.tile_red || lane == 0 ? fsum : 0ull, red64);
     const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
+    // k_sort_fused: the row's owner totals (its tile sums summed per owning CTA) — only for
+    // an exact row (an overflowed one is recounted after the barrier)
+    if (tsum_sh && tot == nvalid) flush_owner_totals(a, tsum_sh, U);
     if (tot != nvalid) {
       if (a.tile_red) {
         // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
@@ -509,6 +528,9 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
         hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
       }
     }
+  } else if (tsum_sh) {  // 32-bit rows cannot overflow
+    __syncthreads();
+    flush_owner_totals(a, tsum_sh, U);
   }
   phase_mark(a.pt, 2);
 }

@@ -80,6 +80,9 @@ struct ScanArgs {
   uint32_t* Hx_clear;        // the other parity's Hx, zeroed for the next launch
   const uint64_t* d_n;       // nullable: key count on the device (hierarchical blocks); then
   const uint64_t* d_off;     //   keys and out start at *d_off and n_expected = *d_n
+  uint32_t* own_red;         // [G x tile_red_stride] per-owner totals (tiles of CTA b) reduced during the flush
+  uint32_t* own_clear;       // the other parity's own_red, zeroed for the next launch
+  uint32_t* own_alt;         // [G] owner totals of the overflow fallback path
   uint32_t* tile_alt;        // [ntiles] tile totals of the overflow fallback path
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
   unsigned long long* bar64; // monotonic grid-barrier counter
@@ -127,6 +130,13 @@ __device__ __forceinline__ void my_tiles(uint32_t ntiles, uint32_t& tb0, uint32_
   const uint32_t G = gridDim.x, b = blockIdx.x;
   tb0 = (uint32_t)((uint64_t)ntiles * b / G);
   tb1 = (uint32_t)((uint64_t)ntiles * (b + 1) / G);
+}
+
+// The CTA whose my_tiles range holds tile t.
+__device__ __forceinline__ uint32_t owner_of(uint32_t t, uint32_t ntiles, uint32_t G) {
+  uint32_t b = (uint32_t)((uint64_t)t * G / ntiles);  // ntiles b / G <= t
+  while (b + 1 < G && (uint32_t)((uint64_t)ntiles * (b + 1) / G) <= t) ++b;
+  return b;
 }
 
 // Phase A for one tile: H[tile] = Σ_rows partial[row][tile] (+ ovfH), written to a.H.

@@ -19,8 +19,8 @@ keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
 outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = os.environ.get("DIALSORT_FUSED") != "0"
-names = (["ingest", "sync", "flush", "barrier1", "merge_start", "batch_staged", "merged", "end", "flags_ready",
-          "P_staged", "", "flush_loop", "flush_it1", "", "", ""] if fused else
+names = (["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
+          "proj_start", "p_staged_issued", "p_tot_thr0", "p_ovf_all", "p_before_stage", "", ""] if fused else
          ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"] + [""] * 8)
 for rep in range(4):
     ctx.debug_phase_cta()
