@@ -220,48 +220,22 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
   }
 }
 
-// ---- merge of one batch (1 u32 tile or 2 packed tiles = 512 B of every row) --------------
+// ---- merge of one batch (128 words = 512 B of every row: 2, 4 or 16 tiles) ----------------
 // Issues the cp.async copies of the batch's row segments into a staging slot (row r: 128
 // words at slot + 128 r).  Tiles of the batch that this CTA does not need are not copied.
 template <int FMT>
 __device__ __forceinline__ void stage_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, uint32_t* slot) {
-  if (!need_mask) return;
-  constexpr uint32_t qpt = 32 / RowFmt<FMT>::tpb;  // uint4 per tile (32, 16, 4)
+  constexpr uint32_t qpt = 32 / RowFmt<FMT>::tpb;  // uint4 per tile (16, 8, 2)
+  const uint32_t l = threadIdx.x & 31, r0 = threadIdx.x >> 5;  // uint4 l of rows r0, r0 + 32, ..
+  if (!((need_mask >> (l / qpt)) & 1u)) return;
   const uint32_t Wrow = FMT == kRowU32 ? a.U : FMT == kRowP16 ? (a.U + 1) / 2 : (a.U + 7) / 8;  // row words
-  const uint32_t w0 = t0 * RowFmt<FMT>::wpt;  // first word of the batch (tiles t0 ..) in a row
-#if DIALSORT_STAGE_LDG
-  // register path: up to 8 loads per thread in flight, then the shared stores
-  uint4 v[8];
-  uint32_t dst[8];
-#pragma unroll
-  for (uint32_t u = 0; u < 8; ++u) {
-    const uint32_t i = threadIdx.x + u * blockDim.x;
-    dst[u] = 0xffffffffu;
-    v[u] = make_uint4(0, 0, 0, 0);
-    if (i < a.C * 32) {
-      const uint32_t r = i >> 5, l = i & 31;
-      if ((need_mask >> (l / qpt)) & 1u) {
-        const uint32_t word = w0 + 4 * l;
-        if (word < Wrow) v[u] = __ldcg(reinterpret_cast<const uint4*>(a.partials + (uint64_t)r * a.ldr + word));
-        dst[u] = r * kFSlotWords + 4 * l;
-      }
-    }
-  }
-#pragma unroll
-  for (uint32_t u = 0; u < 8; ++u)
-    if (dst[u] != 0xffffffffu) *reinterpret_cast<uint4*>(slot + dst[u]) = v[u];
-#else
-  for (uint32_t i = threadIdx.x; i < a.C * 32; i += blockDim.x) {
-    const uint32_t r = i >> 5, l = i & 31;  // row, uint4 within the batch
-    if (!((need_mask >> (l / qpt)) & 1u)) continue;
-    const uint32_t word = w0 + 4 * l;
-    const uint32_t bytes = word < Wrow ? 16u : 0u;  // zero-fill past the row's last word
-    const uint32_t* src = a.partials + (uint64_t)r * a.ldr + (bytes ? word : 0u);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(slot + r * kFSlotWords + 4 * l)),
-                 "l"(src), "r"(bytes)
-                 : "memory");
-  }
-#endif
+  const uint32_t word = t0 * RowFmt<FMT>::wpt + 4 * l;
+  const uint32_t bytes = word < Wrow ? 16u : 0u;  // zero-fill past the row's last word
+  const uint32_t* src = a.partials + (uint64_t)r0 * a.ldr + (bytes ? word : 0u);
+  uint32_t dst = smem_addr(slot + r0 * kFSlotWords + 4 * l);
+  const uint64_t sstep = 32ull * a.ldr;  // (blockDim = 1024: 32 warps)
+  for (uint32_t r = r0; r < a.C; r += 32, src += sstep, dst += 32 * kFSlotWords * 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
 // Sums the staged rows of a batch: hb[j] = merged count of the batch's bin j (+ the 4-bit
@@ -384,11 +358,13 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
   hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
-  grid_barrier_mono(a.bar64, a.bar_base + G);  // rows, tile / owner totals, overflow fallback in L2
+  __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
+  grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
+    my_tiles(ntiles, s_own[0], s_own[1]);
+  });
   phase_mark(a.pt, 3);
 
-  uint32_t tb0, tb1;
-  my_tiles(ntiles, tb0, tb1);  // tiles this CTA merges (index ownership)
+  const uint32_t tb0 = s_own[0], tb1 = s_own[1];  // tiles this CTA merges
   const uint32_t nown = tb1 - tb0;
   constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
   constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
@@ -424,10 +400,10 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // Hx of bin t0 kFTileBins + threadIdx.x of batch k (4-bit rows), loaded a batch ahead
+  const uint32_t binend = min(tb1 * kFTileBins, U);  // bins of the own tiles end here
   auto hx_of = [&](uint32_t k) -> uint32_t {
-    if (FMT != kRowN4 || k >= nbt || threadIdx.x >= nbb || !((need_of(k) >> (threadIdx.x / kFTileBins)) & 1u)) return 0u;
     const uint32_t bin = (tb0 + k * tpb) * kFTileBins + threadIdx.x;
-    return bin < U ? __ldcg(a.Hx + bin) : 0u;
+    return FMT == kRowN4 && threadIdx.x < nbb && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
 #if DIALSORT_EXP_LATPROBE
@@ -483,15 +459,16 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // Own-tile mode: when every CTA's own tiles hold about nw / G positions (near-uniform
   // histograms), each CTA projects exactly the tiles it merged, from P in its shared memory —
   // no cross-CTA flags, no P round trip through L2.  Otherwise (skew) equal position shares.
-  bool own = (ntiles + G - 1) / G <= kFPassTiles;
-  if (own) {
-    const uint32_t lim = nw / G + nw / (16 * G) + 1024;
-    own = !__syncthreads_or(threadIdx.x < G && ov > lim);
-  }
+  bool own = ntiles <= kFPassTiles * G;  // every CTA's tiles fit one projection pass
+  if (own)  // max owner total <= (17/16) nw / G + 1024
+    own = !__syncthreads_or(threadIdx.x < G && 16ull * G * ov > 17ull * nw + 16384ull * G);
   // equal share [lo, hi) (share mode): the totals of the tiles of the owners it overlaps are
   // requested now and scanned after the merge
-  const uint32_t lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
-  const uint32_t hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
+  uint32_t lo = 0, hi = 0;
+  if (!own) {
+    lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
+    hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
+  }
   const bool share = !own && lo < hi;
   uint32_t oa = 0, ob = 0, x0 = 0, x1 = 0, s0 = 0, s1 = 0;
   if (share) {
@@ -528,8 +505,8 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     __syncthreads();
     if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
       const uint32_t t = t0 + j / kFTileBins;
-      uint32_t wpre = obase + tw[t - tb0];
-      for (uint32_t q = (j / kFTileBins) * (kFTileBins / 32); q < (j >> 5); ++q) wpre += wsum[q];
+      static_assert(kFTileBins == 64, "a tile is two warps");
+      const uint32_t wpre = obase + tw[t - tb0] + ((j & 32u) ? wsum[(j >> 5) - 1] : 0u);
       const uint32_t bin = t0 * kFTileBins + j;
       const uint32_t p = bin < U ? wpre + inc - h : (uint32_t)total;
       if (bin < U) a.H[bin] = h;

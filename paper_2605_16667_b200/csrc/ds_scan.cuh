@@ -109,6 +109,21 @@ __device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt, unsig
   }
   __syncthreads();
 }
+// The same, with `side()` run by thread 32 while thread 0 waits (uniform set-up work for the
+// next phase that would otherwise be repeated by all 32 warps; its smem results are visible
+// after the barrier's closing __syncthreads).
+template <class F>
+__device__ __forceinline__ void grid_barrier_mono_side(unsigned long long* cnt, unsigned long long target, F side) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+    while (ld_acquire_u64(cnt) < target) {
+    }
+  } else if (threadIdx.x == 32) {
+    side();
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void barrier_skip(unsigned long long* cnt) {
   if (threadIdx.x == 0) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
 }
