@@ -129,8 +129,9 @@ int dialsort_profile_enable(dialsort_ctx ctx, int enable);
  * the last read into the host arrays; returns the record count (or -status on error). */
 int dialsort_profile_read(dialsort_ctx ctx, int max, int* kernel_ids, float* ms);
 const char* dialsort_kernel_name(int kernel_id);
-/* Debug: with DIALSORT_PHASE_TIMING=1 in the environment at context creation, the fused
- * kernels record %globaltimer phase stamps; this copies 16 values in ns relative to the
+/* Debug: with DIALSORT_PHASE_TIMING=1 in the environment at context creation, a library
+ * built with -DDIALSORT_PHASE_MARKS=1 (tools/build_variant.sh phase; the product build has no
+ * stamps and returns zeros) records %globaltimer phase stamps in the fused kernels; this copies 16 values in ns relative to the
  * earliest CTA start into out16 (host): [0..7] the latest CTA's arrival at phase 0..7,
  * [8..15] the earliest CTA's (0 = phase not reached), and resets them. */
 int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out16);

@@ -126,15 +126,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Stamps are compiled in only with -DDIALSORT_PHASE_MARKS=1 (the tools' libdialsort_phase.so):
+// even a disabled mark costs every warp its test, ~4% of the fused kernel's instructions.
+#ifndef DIALSORT_PHASE_MARKS
+#define DIALSORT_PHASE_MARKS 0
+#endif
 __device__ __forceinline__ void phase_mark(PhaseTimes* pt, int i) {
-  if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) pt->stamp[blockIdx.x][i + 1] = gtimer();
-}
-// The same, stamped only once `dep` has arrived (thread 0's register).
-__device__ __forceinline__ void phase_mark_dep(PhaseTimes* pt, int i, uint32_t dep) {
-  if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) {
-    uint32_t z;
-    asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(dep));
-    pt->stamp[blockIdx.x][i + 1] = gtimer() + z;
+  if constexpr (DIALSORT_PHASE_MARKS) {
+    if (pt && threadIdx.x == 0 && blockIdx.x < kPhaseMaxCtas) pt->stamp[blockIdx.x][i + 1] = gtimer();
   }
 }
 

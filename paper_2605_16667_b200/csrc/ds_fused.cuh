@@ -103,10 +103,26 @@ __device__ __forceinline__ uint32_t tile_of(const uint32_t* toff, uint32_t ntile
 //             measured 10x slower on Zipf's short bins).
 // The projection is issue-bound (ncu ~70% issue-active at one 128-position block per
 // iteration), so the per-iteration bookkeeping is amortised over 4 quads per lane.
+// #{i : Ps[i] < x} for a warp, given that it lies in [x0, m] (Ps[m ..] are sentinels): rounds of
+// 32 lane probes narrow the range 32-fold each (two rounds for m <= 1024), a last round of
+// consecutive probes gives the count.
+__device__ __forceinline__ uint32_t count_below(const uint32_t* Ps, uint32_t m, uint32_t x0, uint32_t x) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t len = m - x0;  // the count is in [x0, x0 + len]
+  while (len > 32) {
+    const uint32_t step = (len + 31) >> 5;
+    const uint32_t q = x0 + step * (lane + 1) - 1;
+    const uint32_t k = __popc(__ballot_sync(FULL, q < m && Ps[q] < x));
+    x0 += step * k;
+    len = min(step - 1, m - x0);
+  }
+  return x0 + __popc(__ballot_sync(FULL, Ps[x0 + lane] < x));  // x0 + lane < m + 32: sentinels
+}
+
 __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
-                                           bool aligned, uint64_t pol) {
+                                           bool aligned, uint64_t pol, bool full = false) {
   const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
-  if (aligned && p >= lo && p + 4 <= hi) {
+  if (full || (aligned && p >= lo && p + 4 <= hi)) {
     st_stream4(reinterpret_cast<int4*>(out + p), v, pol);
   } else {
     if (p >= lo && p < hi) out[p] = v.x;
@@ -124,16 +140,11 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
   uint32_t sb = (lo & ~(SB - 1)) + SB * w;
   if (sb >= hi) return;
   // c = #{i : Ps[i] < sb}  (sentinels are never < sb, so c <= m)
-  uint32_t c0 = 0, c1 = m;
-  while (c0 < c1) {
-    const uint32_t mid = (c0 + c1) >> 1;
-    if (Ps[mid] < sb) c0 = mid + 1;
-    else c1 = mid;
-  }
-  uint32_t c = c0, cb = c0;
+  uint32_t c = count_below(Ps, m, 0, sb), cb = c;
   uint32_t sreg = Ps[cb + lane];
   for (;;) {
     const uint32_t bend = hi - sb > SB ? sb + SB - 1 : hi - 1;
+    const bool full = aligned && sb >= lo && hi - sb >= SB;  // every quad in [lo, hi)
     if (c - cb >= 16) {  // keep >= 16 lanes of look-ahead in the window
       cb = c;
       sreg = Ps[cb + lane];
@@ -144,7 +155,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
     if (le == o) {  // no bin starts in the super-block
       const uint4 q = make_uint4(base, base, base, base);
 #pragma unroll
-      for (uint32_t s = 0; s < 4; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol);
+      for (uint32_t s = 0; s < 4; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol, full);
     } else {
       bool done = false;
       if (le < 32) {
@@ -163,7 +174,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
             const uint32_t v = base + below;
             store_quad(out, sb + 128 * s + 4 * lane, lo, hi,
                        make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own),
-                       aligned, pol);
+                       aligned, pol, full);
             cum += __popc(M[s]);
           }
           done = true;
@@ -208,13 +219,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
     } else {
       // the warp's next super-block is 16K positions away: in a start-dense region (short
       // bins) thousands of starts lie between, so search rather than walk
-      uint32_t x0 = cb + 32, x1 = m;
-      while (x0 < x1) {
-        const uint32_t mid = (x0 + x1) >> 1;
-        if (Ps[mid] < sb) x0 = mid + 1;
-        else x1 = mid;
-      }
-      c = cb = x0;
+      c = cb = count_below(Ps, m, cb + 32, sb);
       sreg = Ps[cb + lane];
     }
   }
@@ -392,9 +397,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   uint32_t w0 = t2 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2) * S) : 0u;
   uint32_t w1 = t2 + 1 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2 + 1) * S) : 0u;
   const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
-#if DIALSORT_EXP_LATPROBE
-  phase_mark(a.pt, 13);  // before the staging
-#endif
   for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
     stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot(k));
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -406,11 +408,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     return FMT == kRowN4 && threadIdx.x < nbb && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
-#if DIALSORT_EXP_LATPROBE
-  phase_mark(a.pt, 10);                 // staging issued
-  phase_mark_dep(a.pt, 11, ov | w0 | w1);  // thread 0's totals arrived
-  phase_mark_dep(a.pt, 12, (uint32_t)__syncthreads_or(use_ovf));  // every thread's overflow state
-#endif
   if (!use_ovf) {
     barrier_skip(a.bar64);
   } else {

@@ -387,7 +387,7 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
   const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
   constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
   const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  unsigned long long fsum = 0;
+  uint32_t fsum = 0;  // <= the CTA's keys < 2^32
   if (a.tile_red && PACK16 && a.nib4) {
     // k_sort_fused, 4-bit rows: the partial row keeps counts <= 15 — 8 bins
     // per word, a quarter of the packed row's L2 bytes — and a count >= 16 goes whole to the
@@ -397,16 +397,16 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     // tile reduce its sum with shuffles and one adds it (RED) into the tile total.
     constexpr uint32_t QT = kFTileBins / 8;  // threads (packed uint4) per tile
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * QT;
-    uint32_t* nrow = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr;
-    const uint32_t nw = (U + 7) / 8;  // row words
-#if DIALSORT_EXP_NOFLUSH
-    for (uint32_t b0 = 0; b0 < 0; b0 += blockDim.x) {
-#else
-    for (uint32_t b0 = 0; b0 < tot; b0 += blockDim.x) {
-#endif
-      const uint32_t g = b0 + threadIdx.x;
+    const uint32_t lim = min(W4, (U + 7) / 8);  // uint4 g < lim: in the histogram and a row word
+    // per-thread pointers advance by one block (1024 uint4 = 128 tiles) per iteration
+    uint32_t* wp = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr + threadIdx.x;
+    uint32_t* rp = a.tile_red + (uint64_t)(threadIdx.x / QT) * a.tile_red_stride;
+    uint32_t* tp = tsum_sh + threadIdx.x / QT;
+    const uint64_t rstep = (uint64_t)(1024 / QT) * a.tile_red_stride;
+    const bool leader = threadIdx.x % QT == 0;
+    for (uint32_t g = threadIdx.x; g - threadIdx.x < tot; g += 1024, wp += 1024, rp += rstep, tp += 1024 / QT) {
       uint32_t v = 0;
-      if (g < W4) {
+      if (g < lim) {
         const uint4 w = h4[g];
         uint32_t word;
         if (((w.x | w.y | w.z | w.w) & 0xFFF0FFF0u) == 0u) {
@@ -431,21 +431,17 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
             }
           }
         }
-#if !DIALSORT_EXP_NOST
-        if (g < nw) __stcg(nrow + g, word);
-#endif
-      }
+        __stcg(wp, word);
+      }  // (uint4 lim .. tot hold bins >= U: zero)
 #pragma unroll
       for (uint32_t o = QT / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (g < tot && (g % QT) == 0) {
+      if (leader && g < tot) {
         fsum += v;
-#if !DIALSORT_EXP_NORED
-        if (v) red_add_u32(a.tile_red + (uint64_t)(g / QT) * a.tile_red_stride, v);
-#endif
-        if (tsum_sh) tsum_sh[g / QT] = v;
+        if (v) red_add_u32(rp, v);
+        *tp = v;
       }
-      if (b0 == 0) phase_mark(a.pt, 12);  // first flush iteration done (debug)
-      if (b0 == blockDim.x) phase_mark(a.pt, 13);
+      if (g == threadIdx.x) phase_mark(a.pt, 12);  // first flush iteration done (debug)
+      if (g == threadIdx.x + 1024) phase_mark(a.pt, 13);
     }
   } else if (a.tile_red) {
     // k_sort_fused: kFTileBins-bin tiles (16 or 32 uint4), thread i stores uint4 i and the QT
@@ -501,12 +497,15 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     // (DESIGN.md §5.2), so Σ fields == #valid keys  <=>  no field overflowed.  On overflow the
     // fallback zeroes the row and the CTA's tile sums are ignored (use_ovf path below).
     // fsum: per-warp totals in lane 0 (tsums loop) or per-tile totals in the tile's lane 0
-    const uint64_t tot = block_sum<uint64_t>(a.tile_red || lane == 0 ? fsum : 0ull, red64);
-    const uint64_t nvalid = block_sum<uint64_t>((uint64_t)(seen - bad), red64);
+    // One block sum of (field sums - valid keys), mod 2^32: the shortfall of a wrapped row is in
+    // (0, keys of the CTA] and the CTA holds < 2^32 keys, so the sum is 0 iff nothing wrapped.
+    const uint32_t dsum = block_sum<uint32_t>((a.tile_red || lane == 0 ? fsum : 0u) - (uint32_t)(seen - bad),
+                                              reinterpret_cast<uint32_t*>(red64));
+    const bool exact = dsum == 0u;
     // k_sort_fused: the row's owner totals (its tile sums summed per owning CTA) — only for
     // an exact row (an overflowed one is recounted after the barrier)
-    if (tsum_sh && tot == nvalid) flush_owner_totals(a, tsum_sh, U);
-    if (tot != nvalid) {
+    if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U);
+    if (!exact) {
       if (a.tile_red) {
         // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
         // values), then the fallback zeroes the row (ldr words) and re-ingests into ovfH

@@ -4,6 +4,8 @@ import os
 import sys
 
 os.environ["DIALSORT_PHASE_TIMING"] = "1"
+# the stamps exist only in the -DDIALSORT_PHASE_MARKS=1 build (tools/build_variant.sh phase)
+os.environ.setdefault("DIALSORT_LIB_VARIANT", "phase")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -20,7 +22,7 @@ outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = os.environ.get("DIALSORT_FUSED") != "0"
 names = (["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
-          "proj_start", "p_staged_issued", "p_tot_thr0", "p_ovf_all", "p_before_stage", "", ""] if fused else
+          "proj_start", "", "flush_loop", "flush_it1", "flush_it2", "", ""] if fused else
          ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"] + [""] * 8)
 for rep in range(4):
     ctx.debug_phase_cta()
