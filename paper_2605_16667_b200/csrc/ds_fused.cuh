@@ -255,30 +255,42 @@ __device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uin
   const uint32_t col = threadIdx.x & 127, qg = threadIdx.x >> 7;
   if ((need_mask >> (col / wpt)) & 1u) {
     if (FMT == kRowN4) {
-      // nibbles summed in byte lanes for up to 17 rows (17 x 15 = 255), then widened into
-      // four 2 x 16-bit accumulators: nibbles (0,4) (2,6) (1,5) (3,7)
+      // nibbles summed in byte lanes (<= 17 rows per byte: 17 x 15 = 255), then widened into
+      // four 2 x 16-bit accumulators: nibbles (0,4) (2,6) (1,5) (3,7).  Fully unrolled over the
+      // <= 19 rows of the group (predicated): a rolled loop measured 2.3K cycles at 1024
+      // threads, shared-load latency under load (tools/lds_bench.cu).
       uint32_t el = 0, eh = 0, ol = 0, oh = 0;
-      for (uint32_t r0 = qg; r0 < a.C; r0 += 8 * 16) {
+      constexpr uint32_t RPG = (kFMaxRows + 7) / 8;  // rows per group
+      static_assert(RPG <= 2 * 17, "two byte-lane chunks");
+      uint32_t x[RPG];
+#pragma unroll
+      for (uint32_t i = 0; i < RPG; ++i) {
+        const uint32_t r = qg + 8 * i;
+        x[i] = r < a.C ? slot[r * kFSlotWords + col] : 0u;
+      }
+#pragma unroll
+      for (uint32_t c0 = 0; c0 < RPG; c0 += 16) {
         uint32_t be = 0, bo = 0;
-        const uint32_t r1 = min(a.C, r0 + 8 * 16);
-#pragma unroll 4
-        for (uint32_t r = r0; r < r1; r += 8) {
-          const uint32_t x = slot[r * kFSlotWords + col];
-          be += x & 0x0F0F0F0Fu;
-          bo += (x >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (uint32_t i = c0; i < RPG && i < c0 + 16; ++i) {
+          be += x[i] & 0x0F0F0F0Fu;
+          bo += (x[i] >> 4) & 0x0F0F0F0Fu;
         }
         el += be & 0x00FF00FFu;
         eh += (be >> 8) & 0x00FF00FFu;
         ol += bo & 0x00FF00FFu;
         oh += (bo >> 8) & 0x00FF00FFu;
       }
+      phase_mark(a.pt, 12);
       uint32_t* d = scratch + qg * kFBatchBins + 8 * col;  // bins 8 col .. 8 col + 7
       reinterpret_cast<uint4*>(d)[0] = make_uint4(el & 0xffffu, ol & 0xffffu, eh & 0xffffu, oh & 0xffffu);
       reinterpret_cast<uint4*>(d)[1] = make_uint4(el >> 16, ol >> 16, eh >> 16, oh >> 16);
     } else {
       uint32_t lo = 0, hi = 0;
-      for (uint32_t r = qg; r < a.C; r += 8) {
-        const uint32_t x = slot[r * kFSlotWords + col];
+#pragma unroll
+      for (uint32_t i = 0; i < (kFMaxRows + 7) / 8; ++i) {
+        const uint32_t r = qg + 8 * i;
+        const uint32_t x = r < a.C ? slot[r * kFSlotWords + col] : 0u;
         if (FMT == kRowP16) {
           lo += x & 0xffffu;
           hi += x >> 16;
@@ -295,6 +307,7 @@ __device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uin
     }
   }
   __syncthreads();
+  phase_mark(a.pt, 13);
   const uint32_t j = threadIdx.x;
   if (j < nb) {
     uint32_t h = 0;
@@ -360,8 +373,10 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
       a.Hx_clear[k] = 0;
   constexpr bool PACK16 = FMT != kRowU32;
 
-  // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram
+  // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram; zeroed here
+  // (the ingestion's first __syncthreads orders this before the flush)
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
+  for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
   hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
   __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
@@ -489,6 +504,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     phase_mark(a.pt, 5);
     reduce_batch<FMT>(a, t0, need, slot(k), scratch, hb, use_ovf, hx);
     __syncthreads();  // hb complete; the slot is free
+    phase_mark(a.pt, 10);
     if (k + 2 < nbt) {
       stage_batch<FMT>(a, tb0 + (k + 2) * tpb, need_of(k + 2), slot(k));
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -500,6 +516,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     const uint32_t inc = warp_incl_scan(h);
     if (j < nbb && (j & 31) == 31) wsum[j >> 5] = inc;
     __syncthreads();
+    phase_mark(a.pt, 14);
     if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
       const uint32_t t = t0 + j / kFTileBins;
       static_assert(kFTileBins == 64, "a tile is two warps");
@@ -510,6 +527,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
       if (own) Ps[(t0 - tb0) * kFTileBins + j] = p;
       else if (bin < U) a.P[bin] = p;
     }
+    phase_mark(a.pt, 15);
     if (!own) {
       __syncthreads();  // the batch's H and P are written
       if (threadIdx.x < tpb && ((need >> threadIdx.x) & 1u))

@@ -393,22 +393,27 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     // per word, a quarter of the packed row's L2 bytes — and a count >= 16 goes whole to the
     // global exception histogram Hx (RED; its nibble stays 0).  Thread i turns packed uint4 i
     // (8 bins; consecutive threads read consecutive uint4: no bank conflicts — 4 uint4 per
-    // thread measured 16-way conflicted) into word i of the row; the 8 threads of a 64-bin
-    // tile reduce its sum with shuffles and one adds it (RED) into the tile total.
-    constexpr uint32_t QT = kFTileBins / 8;  // threads (packed uint4) per tile
+    // thread measured 16-way conflicted) into word i of the row and adds its 8-bin sum to the
+    // tile sum tsum_sh[i / 8] (shared atomic: the unit merges a warp's 4 equal addresses;
+    // 3 shuffles per iteration cost more in the shared-memory pipe).
+    constexpr uint32_t QT = kFTileBins / 8;  // packed uint4 per tile
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * QT;
     const uint32_t lim = min(W4, (U + 7) / 8);  // uint4 g < lim: in the histogram and a row word
-    // per-thread pointers advance by one block (1024 uint4 = 128 tiles) per iteration
     uint32_t* wp = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr + threadIdx.x;
-    uint32_t* rp = a.tile_red + (uint64_t)(threadIdx.x / QT) * a.tile_red_stride;
     uint32_t* tp = tsum_sh + threadIdx.x / QT;
-    const uint64_t rstep = (uint64_t)(1024 / QT) * a.tile_red_stride;
-    const bool leader = threadIdx.x % QT == 0;
-    for (uint32_t g = threadIdx.x; g - threadIdx.x < tot; g += 1024, wp += 1024, rp += rstep, tp += 1024 / QT) {
-      uint32_t v = 0;
-      if (g < lim) {
-        const uint4 w = h4[g];
-        uint32_t word;
+    // 4 iterations' loads first: the shared atomics order the loop (smem may alias), so an
+    // unbatched loop waits a full load latency per iteration
+    constexpr uint32_t B = 4;
+    for (uint32_t g0 = threadIdx.x; g0 - threadIdx.x < tot; g0 += B * 1024, wp += B * 1024, tp += B * 1024 / QT) {
+      uint4 wv[B];
+#pragma unroll
+      for (uint32_t u = 0; u < B; ++u) wv[u] = g0 + u * 1024 < lim ? h4[g0 + u * 1024] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (uint32_t u = 0; u < B; ++u) {
+        const uint32_t g = g0 + u * 1024;
+        if (g >= lim) break;  // (uint4 lim .. tot hold bins >= U: zero)
+        const uint4 w = wv[u];
+        uint32_t word, v = 0;
         if (((w.x | w.y | w.z | w.w) & 0xFFF0FFF0u) == 0u) {
           // fast path, all 8 counts <= 15: word j holds (c_{2j+1} << 16 | c_{2j}), so
           // (w | w >> 12) & 0xff = c_{2j} | c_{2j+1} << 4, and PRMT gathers the 4 bytes
@@ -431,44 +436,38 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
             }
           }
         }
-        __stcg(wp, word);
-      }  // (uint4 lim .. tot hold bins >= U: zero)
-#pragma unroll
-      for (uint32_t o = QT / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (leader && g < tot) {
-        fsum += v;
-        if (v) red_add_u32(rp, v);
-        *tp = v;
+        __stcg(wp + u * 1024, word);
+        if (v) atomicAdd(tp + u * (1024 / QT), v);
       }
-      if (g == threadIdx.x) phase_mark(a.pt, 12);  // first flush iteration done (debug)
-      if (g == threadIdx.x + 1024) phase_mark(a.pt, 13);
     }
   } else if (a.tile_red) {
-    // k_sort_fused: kFTileBins-bin tiles (16 or 32 uint4), thread i stores uint4 i and the QT
-    // lanes of a tile reduce its sum with shuffles; lane 0 of the tile adds it (RED) into the
-    // tile total.  Every thread runs the same iterations (shuffles use the full mask).
+    // k_sort_fused, 16- or 32-bit rows: thread i stores uint4 i of the row and adds its sum to
+    // the tile sum tsum_sh[i / QT] (shared atomic).
     constexpr uint32_t QT = PACK16 ? kFTileBins / 8 : kFTileBins / 4;
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot4 = ntf * QT;
     uint4* frow4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
-    for (uint32_t b0 = 0; b0 < tot4; b0 += blockDim.x) {
-      const uint32_t i = b0 + threadIdx.x;
-      uint32_t v = 0;
+    for (uint32_t i = threadIdx.x; i < tot4; i += blockDim.x) {
       if (i < W4) {
         const uint4 w = h4[i];
         __stcg(frow4 + i, w);
+        uint32_t v;
         if (PACK16)
           v = (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
               (w.w & 0xffffu) + (w.w >> 16);
         else
           v = w.x + w.y + w.z + w.w;
+        if (v) atomicAdd(tsum_sh + i / QT, v);
       }
-#pragma unroll
-      for (uint32_t o = QT / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (i < tot4 && (i % QT) == 0) {
-        fsum += v;
-        if (v) red_add_u32(a.tile_red + (uint64_t)(i / QT) * a.tile_red_stride, v);
-        if (tsum_sh) tsum_sh[i / QT] = v;
-      }
+    }
+  }
+  if (a.tile_red) {
+    // the row's tile sums into the tile totals (one RED per nonzero tile; fsum: the checksum)
+    __syncthreads();
+    const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins;
+    for (uint32_t t = threadIdx.x; t < ntf; t += blockDim.x) {
+      const uint32_t v = tsum_sh[t];
+      fsum += v;
+      if (v) red_add_u32(a.tile_red + (uint64_t)t * a.tile_red_stride, v);
     }
   }
   for (uint32_t t = threadIdx.x >> 5; !a.tile_red && t < ntiles; t += nwarps) {
