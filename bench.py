@@ -185,7 +185,7 @@ def cpu_baseline(cfg, seed, budget_s=10.0):
         fn()
         reps += 1
         el = time.perf_counter() - t0
-        if el > budget_s or reps >= 200:
+        if el > budget_s or reps >= 2000:
             break
     return {"value": m * reps / el, "unit": "keys/s", "cores": 1, "kind": "oracle",
             "sample": f"{reps} x oracle sort of the first {m} keys of the {cfg['desc']} input ({el:.1f} s, 1 thread)"}
@@ -330,8 +330,8 @@ def main():
         import glob
         tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
         with open(tfiles[-1]) as f:
-            tk = json.load(f)["kernels"].get(dom or "", None)
-        if tk and args.config == "c2" and G == 1:
+            tk = json.load(f)["configs"].get(args.config, {}).get(dom or "", None)
+        if tk and G == 1:  # (the capture is of the single-GPU launch configuration)
             traffic = tk["dram_read_bytes"] + tk["dram_write_bytes"]
     except Exception:
         traffic = None
