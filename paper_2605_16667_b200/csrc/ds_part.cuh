@@ -163,18 +163,30 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const int32_t* __
     for (uint32_t i = 0; i < kPartKPT; ++i)
       if (k[i] < U) atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u);
     __syncthreads();
-    // scan over (block, warp): thread q < B*NW handles block q / NW, warp q % NW
+    // scan over (block, warp) pairs q = block * NW + warp: thread t handles the QP consecutive
+    // pairs QP t .. QP t + QP - 1 (B * NW <= 64 * 16 = 2 * kPartThreads)
     {
-      const uint32_t q = threadIdx.x, bq = q / NW, wq = q % NW;
-      const uint32_t v = q < B * NW ? wcnt[wq][bq] : 0u;
+      constexpr uint32_t QP = (kPartMaxBlocks * NW + kPartThreads - 1) / kPartThreads;
+      uint32_t v[QP], sum = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < QP; ++j) {
+        const uint32_t q = QP * threadIdx.x + j;
+        v[j] = q < B * NW ? wcnt[q % NW][q / NW] : 0u;
+        sum += v[j];
+      }
       __shared__ uint32_t red[34];
       uint32_t tot;
-      const uint32_t ex = block_excl_scan<uint32_t>(v, tot, red);
-      if (q < B * NW) {
-        wcnt[wq][bq] = ex;  // cursor of warp wq in block bq
-        if (wq == 0) bofs[bq] = ex;
+      uint32_t ex = block_excl_scan<uint32_t>(sum, tot, red);
+#pragma unroll
+      for (uint32_t j = 0; j < QP; ++j) {
+        const uint32_t q = QP * threadIdx.x + j, bq = q / NW, wq = q % NW;
+        if (q < B * NW) {
+          wcnt[wq][bq] = ex;  // cursor of warp wq in block bq
+          if (wq == 0) bofs[bq] = ex;
+        }
+        ex += v[j];
       }
-      if (q == 0) bofs[B] = tot;
+      if (threadIdx.x == 0) bofs[B] = tot;
     }
     __syncthreads();
 #pragma unroll

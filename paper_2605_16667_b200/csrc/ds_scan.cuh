@@ -90,7 +90,7 @@ struct ScanArgs {
 };
 
 // Monotonic grid barrier (measured 1.25 us vs 2.0 us for counter + generation on B200,
-// profiles/r02_barrier_bench.txt): each CTA arrives with one release atomic on a 64-bit
+// profiles/r01_barrier_bench.txt): each CTA arrives with one release atomic on a 64-bit
 // counter that only grows, and waits until it reaches `target` = base + (j + 1) * gridDim
 // for the launch's j-th barrier.  The host advances `base` by the number of barriers a launch
 // reserves; a launch that skips a reserved barrier arrives without waiting (barrier_skip), so
