@@ -53,7 +53,8 @@ template <int FMT> struct RowFmt {
 constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 128 words
 constexpr uint32_t kFOffToff = 2 * kFMaxRows * kFSlotWords;           // toff[kFTiles + 1]
 constexpr uint32_t kFOffScratch = kFOffToff + kFTiles + 32;           // 8 x 256 group sums
-constexpr uint32_t kFPassTiles = 32;                                 // tiles staged per projection pass
+constexpr uint32_t kFPassTiles = 32;                                 // own tiles per CTA (own-tile mode)
+constexpr uint32_t kFSharePassTiles = (kFMaxRows * kFSlotWords - 32) / kFTileBins;  // share mode: 295
 constexpr uint32_t kFOffPs = kFOffScratch + 8 * kFBatchBins;          // pass P + 32 sentinels
 constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // 256 merged H of the batch
 constexpr uint32_t kFOffWc = kFOffHb + kFBatchBins;                   // 32 warps x 128 mark counts
@@ -132,9 +133,20 @@ __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p
   }
 }
 
+#if DIALSORT_EXP_PATHCNT
+__shared__ uint32_t s_pathcnt[4];  // debug: super-blocks per projection path
+#define DS_PATHCNT(i) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_pathcnt[i], 1u)
+#else
+#define DS_PATHCNT(i)
+#endif
 __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
                                              uint32_t* wc, int32_t* __restrict__ out, bool aligned, uint64_t pol) {
-  constexpr uint32_t NW = 32, SB = 512;
+#ifndef DIALSORT_QPL
+#define DIALSORT_QPL 4
+#endif
+  constexpr uint32_t QPL = DIALSORT_QPL;  // quads per lane and super-block
+  constexpr uint32_t NW = 32, SB = 128 * QPL;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t ltmask = (1u << lane) - 1u;
   uint32_t sb = (lo & ~(SB - 1)) + SB * w;
@@ -153,21 +165,25 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
     const uint32_t le = __popc(__ballot_sync(FULL, sreg <= bend));
     const uint32_t base = kbase + c;
     if (le == o) {  // no bin starts in the super-block
+      DS_PATHCNT(0);
       const uint4 q = make_uint4(base, base, base, base);
 #pragma unroll
-      for (uint32_t s = 0; s < 4; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol, full);
+      for (uint32_t s = 0; s < QPL; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol, full);
     } else {
       bool done = false;
       if (le < 32) {
         const bool mine = lane >= o && lane < le;
         const uint32_t qi = (sreg - sb) >> 2;  // quad of the super-block (valid when mine)
-        uint32_t M[4];
+        uint32_t M[QPL], pc = 0;
 #pragma unroll
-        for (uint32_t s = 0; s < 4; ++s) M[s] = __reduce_or_sync(FULL, (mine && (qi >> 5) == s) ? 1u << (qi & 31) : 0u);
-        if ((uint32_t)(__popc(M[0]) + __popc(M[1]) + __popc(M[2]) + __popc(M[3])) == le - o) {
+        for (uint32_t s = 0; s < QPL; ++s) {
+          M[s] = __reduce_or_sync(FULL, (mine && (qi >> 5) == s) ? 1u << (qi & 31) : 0u);
+          pc += __popc(M[s]);
+        }
+        if (pc == le - o) {
           uint32_t cum = 0;
 #pragma unroll
-          for (uint32_t s = 0; s < 4; ++s) {
+          for (uint32_t s = 0; s < QPL; ++s) {
             const uint32_t below = cum + __popc(M[s] & ltmask);
             const uint32_t own = (M[s] >> lane) & 1u;
             const uint32_t r = (__shfl_sync(FULL, sreg, min(o + below, 31u)) - sb) & 3u;
@@ -178,14 +194,16 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
             cum += __popc(M[s]);
           }
           done = true;
+          DS_PATHCNT(1);
         }
       }
       if (!done) {
+        DS_PATHCNT(2);
         // starts sharing quads, or more than the window holds: sub-block by sub-block, each
         // start adds a mark to the warp's 128-entry count array (O(starts) in parallel)
         uint32_t cs = c;  // #{i : Ps[i] < b0}
 #pragma unroll 1
-        for (uint32_t s = 0; s < 4; ++s) {
+        for (uint32_t s = 0; s < QPL; ++s) {
           const uint32_t b0 = sb + 128 * s;
           if (b0 >= hi) break;
           const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
@@ -222,6 +240,99 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
       c = cb = count_below(Ps, m, cb + 32, sb);
       sreg = Ps[cb + lane];
     }
+  }
+}
+
+// ---- table-driven projection (block-level) ----------------------------------------------
+// The positions [lo, hi) are cut into 128-position sub-blocks j (absolute: [128 j, 128 j + 128)),
+// processed in windows of up to kFTblCap sub-blocks.  Per window, one pass over the bins
+// whose start falls in it builds a table entry per sub-block (shared atomics, one bin per
+// thread): T.x = #starts (then, after a block scan, c0 = #{i : Ps[i] < 128 j}) | bit 31 when
+// two starts share a quad, T.y = the quad occupancy mask, T.z / T.w = each start's offset in
+// its quad (2 bits per quad).  Warp w then writes sub-blocks w, w + 32, .. (the CTA writes one
+// contiguous front): lane l's quad holds keys kbase + c0 + popc(M & lanes below l), + 1 from
+// its start's offset on — about 25 instructions per quad, a third of the ballot / REDUX /
+// shuffle path of project_warp.  A sub-block whose quads hold several starts (bins shorter
+// than 4 positions, empty bins) takes the count-mark path.
+constexpr uint32_t kFTblCap = kFMaxRows * kFSlotWords / 4;  // 4736 sub-blocks per window
+__device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
+                                            uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out,
+                                            bool aligned, uint64_t pol) {
+  __shared__ uint32_t s_ib[2];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t ltmask = (1u << lane) - 1u;
+  const uint32_t jl = lo >> 7, jh = (hi + 127) >> 7;
+  for (uint32_t jw = jl; jw < jh; jw += kFTblCap) {
+    const uint32_t nsb = min(kFTblCap, jh - jw);
+    for (uint32_t j = threadIdx.x; j < nsb; j += blockDim.x) T[j] = make_uint4(0, 0, 0, 0);
+    if (w == 0) {  // bins [ia, ib) start in the window
+      const uint32_t ia = count_below(Ps, m, 0, jw << 7);
+      const uint32_t ib = count_below(Ps, m, ia, (jw + nsb) << 7);
+      if (lane == 0) s_ib[0] = ia, s_ib[1] = ib;
+    }
+    __syncthreads();
+    const uint32_t ia = s_ib[0], ib = s_ib[1];
+    for (uint32_t i = ia + threadIdx.x; i < ib; i += blockDim.x) {
+      const uint32_t p = Ps[i], j = (p >> 7) - jw, q = (p >> 2) & 31u;
+      uint32_t* t = reinterpret_cast<uint32_t*>(T + j);
+      const uint32_t old = atomicOr(t + 1, 1u << q);
+      atomicAdd(t, 1u);
+      if ((old >> q) & 1u) atomicOr(t, 0x80000000u);  // a second start in the quad
+      atomicOr(t + 2 + (q >> 4), (p & 3u) << (2 * (q & 15u)));
+    }
+    __syncthreads();
+    {  // c0[j] = ia + Σ_{j' < j} #starts(j'): up to 5 consecutive entries per thread
+      constexpr uint32_t K = (kFTblCap + 1023) / 1024;
+      const uint32_t j0 = K * threadIdx.x;
+      uint32_t v[K], sum = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < K; ++k) {
+        v[k] = j0 + k < nsb ? T[j0 + k].x : 0u;
+        sum += v[k] & 0x7fffffffu;
+      }
+      uint32_t tot;
+      uint32_t ex = ia + block_excl_scan<uint32_t>(sum, tot, red);
+#pragma unroll
+      for (uint32_t k = 0; k < K; ++k) {
+        if (j0 + k < nsb) T[j0 + k].x = ex | (v[k] & 0x80000000u);
+        ex += v[k] & 0x7fffffffu;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = w; j < nsb; j += 32) {
+      const uint32_t b0 = (jw + j) << 7;
+      const uint4 e = T[j];
+      const uint32_t c0 = e.x & 0x7fffffffu;
+      if (!(e.x >> 31)) {
+        const bool full = aligned && b0 >= lo && hi - b0 >= 128;
+        const uint32_t below = __popc(e.y & ltmask), own = (e.y >> lane) & 1u;
+        const uint32_t r = ((lane < 16 ? e.z : e.w) >> (2 * (lane & 15u))) & 3u;
+        const uint32_t v = kbase + c0 + below;
+        store_quad(out, b0 + 4 * lane, lo, hi,
+                   make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own), aligned,
+                   pol, full);
+      } else {  // count marks of the sub-block's starts, then a warp scan
+        const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
+        uint32_t i1 = c0;
+        for (;;) {
+          const uint32_t sl = Ps[min(i1 + lane, m)];  // Ps[m] is a sentinel
+          const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= be));
+          if (lane < cnt) atomicAdd(&wc[sl - b0], 1u);
+          i1 += cnt;
+          if (cnt < 32) break;
+        }
+        __syncwarp();
+        uint4 mk = reinterpret_cast<uint4*>(wc)[lane];
+        reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
+        mk.y += mk.x;
+        mk.z += mk.y;
+        mk.w += mk.z;
+        const uint32_t v = kbase + c0 + warp_incl_scan(mk.w) - mk.w;
+        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol);
+        __syncwarp();
+      }
+    }
+    __syncthreads();  // T is reused by the next window
   }
 }
 
@@ -351,6 +462,9 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   __shared__ uint32_t wsum[32];
   pdl_wait();
   phase_mark(a.pt, -1);
+#if DIALSORT_EXP_PATHCNT
+  if (threadIdx.x < 4) s_pathcnt[threadIdx.x] = 0;
+#endif
   uint64_t n_exp = a.n_expected;
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
     const uint64_t off = *a.d_off;
@@ -483,9 +597,18 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   }
   const bool share = !own && lo < hi;
   uint32_t oa = 0, ob = 0, x0 = 0, x1 = 0, s0 = 0, s1 = 0;
+  __shared__ uint32_t s_find[2];
+  if (!own) {  // the owners holding positions lo and hi - 1: one test per owner, not a search
+    if (lo < hi)
+      for (uint32_t c = threadIdx.x; c < G; c += blockDim.x) {
+        if (oo[c] <= lo && lo < oo[c + 1]) s_find[0] = c;
+        if (oo[c] <= hi - 1 && hi - 1 < oo[c + 1]) s_find[1] = c;
+      }
+    __syncthreads();
+  }
   if (share) {
-    oa = tile_of(oo, G, lo);
-    ob = tile_of(oo, G, hi - 1);
+    oa = s_find[0];
+    ob = s_find[1];
     x0 = (uint32_t)((uint64_t)ntiles * oa / G);
     x1 = (uint32_t)((uint64_t)ntiles * (ob + 1) / G);
     s0 = x0 + t2 < x1 ? __ldcg(tsrc + (uint64_t)(x0 + t2) * tstr) : 0u;
@@ -547,7 +670,21 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     __syncthreads();
     phase_mark(a.pt, 9);
     const uint32_t p0 = obase, p1 = min(obase + tw[nown], nw);
+#if DIALSORT_PROJ_WARP
     if (nown && p0 < p1) project_warp(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
+#else
+    if (nown && p0 < p1)  // (uniform per CTA) table in the second staging slot, dead after the merge
+      project_tbl(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1,
+                  reinterpret_cast<uint4*>(sh + kFOffStage + kFMaxRows * kFSlotWords), wc,
+                  reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
+#endif
+#if DIALSORT_EXP_PATHCNT
+    __syncthreads();
+    if (a.pt && threadIdx.x == 0) {  // slot 12..14: t + count, slot 15: t (stamps are read relative)
+      const unsigned long long t = gtimer();
+      for (int i = 0; i < 4; ++i) a.pt->stamp[blockIdx.x][12 + i] = t + (i < 3 ? s_pathcnt[i] : 0u);
+    }
+#endif
     phase_mark(a.pt, 7);
     pdl_trigger();
     return;
@@ -566,7 +703,12 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     if (x0 + t2 + 1 < x1) ts[t2 + 1] = oo[oa] + ex + s0;
     if (threadIdx.x == 0) ts[x1 - x0] = oo[ob + 1];
     __syncthreads();
-    const uint32_t ta = x0 + tile_of(ts, x1 - x0, lo), tb = x0 + tile_of(ts, x1 - x0, hi - 1);
+    for (uint32_t i = threadIdx.x; i < x1 - x0; i += blockDim.x) {  // the tiles holding lo, hi - 1
+      if (ts[i] <= lo && lo < ts[i + 1]) s_find[0] = i;
+      if (ts[i] <= hi - 1 && hi - 1 < ts[i + 1]) s_find[1] = i;
+    }
+    __syncthreads();
+    const uint32_t ta = x0 + s_find[0], tb = x0 + s_find[1];
     // relaxed polling (a short sleep leaves issue slots to the rest of the CTA), then one
     // acquire load per flag — not a fence: fence.acq_rel.gpu waits for every store in flight
     for (uint32_t t = ta + threadIdx.x; t <= tb; t += blockDim.x) {
@@ -575,20 +717,46 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     }
     __syncthreads();
     phase_mark(a.pt, 8);
-    for (uint32_t pt0 = ta; pt0 <= tb; pt0 += kFPassTiles) {  // one pass at the configs
-      const uint32_t pt1 = min(pt0 + kFPassTiles, tb + 1);
-      const uint32_t m = (pt1 - pt0) * kFTileBins;
-      for (uint32_t i = threadIdx.x; i < m + 32; i += blockDim.x) {
-        const uint32_t bin = pt0 * kFTileBins + i;
-        Ps[i] = i >= m ? 0xffffffffu : (bin < U ? __ldcg(a.P + bin) : (uint32_t)total);
+    // P of the share's tiles staged in the (now dead) first row-staging slot: up to 295 tiles
+    // per pass (a Zipf share in the cold tail spans ~200 tiles; 32-tile passes left most warps
+    // idle); the projection table takes the second slot
+    uint32_t* Pw = sh + kFOffStage;
+    for (uint32_t pt0 = ta; pt0 <= tb; pt0 += kFSharePassTiles) {
+      const uint32_t pt1 = min(pt0 + kFSharePassTiles, tb + 1);
+      const uint32_t m = (pt1 - pt0) * kFTileBins, b0 = pt0 * kFTileBins;
+      for (uint32_t i = 4 * threadIdx.x; i < m; i += 4 * blockDim.x) {  // 16 B per copy, zero-fill past U
+        const uint32_t bytes = b0 + i + 4 <= U ? 16u : (b0 + i < U ? 4u * (U - b0 - i) : 0u);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(Pw + i)),
+                     "l"(a.P + (bytes ? b0 + i : 0u)), "r"(bytes) : "memory");
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (threadIdx.x < 32) Pw[m + threadIdx.x] = 0xffffffffu;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
+      if (b0 + m > U) {  // bins >= U of a last partial tile
+        for (uint32_t i = U - b0 + threadIdx.x; i < m; i += blockDim.x) Pw[i] = (uint32_t)total;
+        __syncthreads();
+      }
       phase_mark(a.pt, 9);
       const uint32_t p0 = max(lo, ts[pt0 - x0]), p1 = min(hi, ts[pt1 - x0]);
-      if (p0 < p1) project_warp(Ps, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
-      __syncthreads();  // Ps is reused by the next pass
+#if DIALSORT_PROJ_WARP
+      if (p0 < p1) project_warp(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
+#else
+      if (p0 < p1)
+        project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
+                    reinterpret_cast<uint4*>(sh + kFOffStage + kFMaxRows * kFSlotWords), wc,
+                    reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
+#endif
+      __syncthreads();  // Pw is reused by the next pass
     }
   }
+#if DIALSORT_EXP_PATHCNT
+  __syncthreads();
+    if (a.pt && threadIdx.x == 0) {  // slot 12..14: t + count, slot 15: t (stamps are read relative)
+      const unsigned long long t = gtimer();
+      for (int i = 0; i < 4; ++i) a.pt->stamp[blockIdx.x][12 + i] = t + (i < 3 ? s_pathcnt[i] : 0u);
+    }
+#endif
   phase_mark(a.pt, 7);
   pdl_trigger();
 }

@@ -22,7 +22,7 @@ outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = os.environ.get("DIALSORT_FUSED") != "0"
 names = (["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
-          "proj_start", "", "flush_loop", "flush_it1", "flush_it2", "", ""] if fused else
+          "proj_start", "m_reduced", "flush_loop", "r_rows", "r_synced", "m_scanned", "m_Pwritten"] if fused else
          ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"] + [""] * 8)
 for rep in range(4):
     ctx.debug_phase_cta()
@@ -40,6 +40,9 @@ for rep in range(4):
     print("   " + "  ".join(f"{n}={c[c > 0].min():.2f}/{np.median(c[c > 0]):.2f}/{c.max():.2f}"
                             for n, c in cols if n and (c > 0).any()))
     if verbose and fused:
-        late = np.argsort(-st[:, 6])[:6]
+        late = np.argsort(-st[:, 8])[:8]  # by end (phase 7)
         for b in late:
-            print("   late share CTA", b, " ".join(f"{n}={st[b, 1 + i]:.2f}" for i, n in enumerate(names)))
+            print(f"   late CTA {b}: projection {st[b, 8] - st[b, 10]:.2f} us;",
+                  " ".join(f"{n}={st[b, 1 + i]:.2f}" for i, n in enumerate(names) if n))
+        pj = st[:, 8] - st[:, 10]
+        print("   projection duration min/median/max %.2f/%.2f/%.2f us" % (pj.min(), np.median(pj), pj.max()))
