@@ -32,6 +32,9 @@ namespace ds {
 
 constexpr uint32_t kFTiles = kSmem16MaxBins / kFTileBins;  // <= 1536 tiles (2 per thread)
 constexpr uint32_t kFSlotWords = 128;                       // staged words per row and batch (512 B)
+// Staged rows are 132 words apart: the 32 lanes of a warp read one uint4 column from 32 rows,
+// and a 4-word pad puts rows r .. r+7 in distinct 16-byte bank groups (conflict-free LDS.128).
+constexpr uint32_t kFRowStride = kFSlotWords + 4;
 constexpr uint32_t kFMaxRows = 148;                         // rows (CTAs) a staging slot holds
 constexpr uint32_t kFTileSlots = 2048;                      // tile-total slots (>= kFTiles)
 constexpr uint32_t kFOwnSlots = 256;                        // owner-total slots (>= kFMaxRows)
@@ -50,16 +53,18 @@ template <int FMT> struct RowFmt {
 };
 
 // Dynamic shared memory after the barrier (words); the ingestion histogram is dead by then.
-constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 128 words
-constexpr uint32_t kFOffToff = 2 * kFMaxRows * kFSlotWords;           // toff[kFTiles + 1]
-constexpr uint32_t kFOffScratch = kFOffToff + kFTiles + 32;           // 8 x 256 group sums
+constexpr uint32_t kFSlot = kFMaxRows * kFRowStride;                 // one staging slot (19536 words)
+constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 132 words
+constexpr uint32_t kFOffToff = 2 * kFSlot;                           // own tiles' offsets [kFTiles + 1]
 constexpr uint32_t kFPassTiles = 32;                                 // own tiles per CTA (own-tile mode)
-constexpr uint32_t kFSharePassTiles = (kFMaxRows * kFSlotWords - 32) / kFTileBins;  // share mode: 295
-constexpr uint32_t kFOffPs = kFOffScratch + 8 * kFBatchBins;          // pass P + 32 sentinels
-constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // 256 merged H of the batch
+constexpr uint32_t kFSharePassTiles = (kFSlot - 32) / kFTileBins;    // share mode: 304 tiles per pass
+constexpr uint32_t kFOffPs = kFOffToff + kFTiles + 32;                // own-mode P + 32 sentinels
+constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // merged H of the batch (<= 1024)
 constexpr uint32_t kFOffWc = kFOffHb + kFBatchBins;                   // 32 warps x 128 mark counts
 constexpr uint32_t kFOffOwn = kFOffWc + 32 * 128;                    // oo[G + 1] owner offsets
-constexpr uint32_t kFOffTsh = kFOffOwn + kFMaxRows + 32;              // share window offsets
+// the flush's tile sums (and later the share window offsets) sit past the largest histogram
+constexpr uint32_t kFOffTsh = kFOffOwn + kFMaxRows + 32 > kSmem16MaxBins / 2 ? kFOffOwn + kFMaxRows + 32
+                                                                             : kSmem16MaxBins / 2;
 constexpr uint32_t kFSmemWords = kFOffTsh + kFTiles + 32;
 
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
@@ -254,7 +259,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
 // its start's offset on — about 25 instructions per quad, a third of the ballot / REDUX /
 // shuffle path of project_warp.  A sub-block whose quads hold several starts (bins shorter
 // than 4 positions, empty bins) takes the count-mark path.
-constexpr uint32_t kFTblCap = kFMaxRows * kFSlotWords / 4;  // 4736 sub-blocks per window
+constexpr uint32_t kFTblCap = kFSlot / 4;  // 4884 sub-blocks per window (one staging slot)
 __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
                                             uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out,
                                             bool aligned, uint64_t pol) {
@@ -348,85 +353,123 @@ __device__ __forceinline__ void stage_batch(const ScanArgs& a, uint32_t t0, uint
   const uint32_t word = t0 * RowFmt<FMT>::wpt + 4 * l;
   const uint32_t bytes = word < Wrow ? 16u : 0u;  // zero-fill past the row's last word
   const uint32_t* src = a.partials + (uint64_t)r0 * a.ldr + (bytes ? word : 0u);
-  uint32_t dst = smem_addr(slot + r0 * kFSlotWords + 4 * l);
+  uint32_t dst = smem_addr(slot + r0 * kFRowStride + 4 * l);
   const uint64_t sstep = 32ull * a.ldr;  // (blockDim = 1024: 32 warps)
-  for (uint32_t r = r0; r < a.C; r += 32, src += sstep, dst += 32 * kFSlotWords * 4)
+  for (uint32_t r = r0; r < a.C; r += 32, src += sstep, dst += 32 * kFRowStride * 4)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
-// Sums the staged rows of a batch: hb[j] = merged count of the batch's bin j (+ the 4-bit
-// rows' exceptions Hx, + ovfH when the packed counters overflowed somewhere), 0 for the bins
-// of tiles not needed.  8 row groups of 128 threads: thread j sums word column j & 127 over
-// rows r = j >> 7 (mod 8) — 4-bit rows as four 2 x 16-bit SWAR accumulators (8 bins).
-template <int FMT>
-__device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, const uint32_t* slot,
-                                             uint32_t* scratch, uint32_t* hb, bool use_ovf, uint32_t hx) {
-  constexpr uint32_t tpb = RowFmt<FMT>::tpb, wpt = RowFmt<FMT>::wpt, nb = tpb * kFTileBins;
-  static_assert(nb <= 1024, "one bin of the batch per thread");
-  const uint32_t col = threadIdx.x & 127, qg = threadIdx.x >> 7;
-  if ((need_mask >> (col / wpt)) & 1u) {
-    if (FMT == kRowN4) {
-      // nibbles summed in byte lanes (<= 17 rows per byte: 17 x 15 = 255), then widened into
-      // four 2 x 16-bit accumulators: nibbles (0,4) (2,6) (1,5) (3,7).  Fully unrolled over the
-      // <= 19 rows of the group (predicated): a rolled loop measured 2.3K cycles at 1024
-      // threads, shared-load latency under load (tools/lds_bench.cu).
-      uint32_t el = 0, eh = 0, ol = 0, oh = 0;
-      constexpr uint32_t RPG = (kFMaxRows + 7) / 8;  // rows per group
-      static_assert(RPG <= 2 * 17, "two byte-lane chunks");
-      uint32_t x[RPG];
+// Reduce-scatter of a warp's N partial sums (registers v[0..N)) across its 32 lanes: at each
+// halving step a lane keeps one half (by its lane bit) and adds the partner's copy of it;
+// finally lane l holds the warp total of index (l >> (5 - log2 N)) in v[0] (N <= 16).
+template <uint32_t N, uint32_t O>
+__device__ __forceinline__ void reduce_scatter_step(uint32_t (&v)[16], uint32_t lane) {
+  if constexpr (O != 0) {
+    if constexpr (N > 1) {
+      const bool up = (lane & O) != 0;
 #pragma unroll
-      for (uint32_t i = 0; i < RPG; ++i) {
-        const uint32_t r = qg + 8 * i;
-        x[i] = r < a.C ? slot[r * kFSlotWords + col] : 0u;
+      for (uint32_t i = 0; i < N / 2; ++i) {
+        const uint32_t send = up ? v[i] : v[i + N / 2];
+        const uint32_t keep = up ? v[i + N / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(FULL, send, O);
       }
-#pragma unroll
-      for (uint32_t c0 = 0; c0 < RPG; c0 += 16) {
-        uint32_t be = 0, bo = 0;
-#pragma unroll
-        for (uint32_t i = c0; i < RPG && i < c0 + 16; ++i) {
-          be += x[i] & 0x0F0F0F0Fu;
-          bo += (x[i] >> 4) & 0x0F0F0F0Fu;
-        }
-        el += be & 0x00FF00FFu;
-        eh += (be >> 8) & 0x00FF00FFu;
-        ol += bo & 0x00FF00FFu;
-        oh += (bo >> 8) & 0x00FF00FFu;
-      }
-      phase_mark(a.pt, 12);
-      uint32_t* d = scratch + qg * kFBatchBins + 8 * col;  // bins 8 col .. 8 col + 7
-      reinterpret_cast<uint4*>(d)[0] = make_uint4(el & 0xffffu, ol & 0xffffu, eh & 0xffffu, oh & 0xffffu);
-      reinterpret_cast<uint4*>(d)[1] = make_uint4(el >> 16, ol >> 16, eh >> 16, oh >> 16);
+      reduce_scatter_step<N / 2, O / 2>(v, lane);
     } else {
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (uint32_t i = 0; i < (kFMaxRows + 7) / 8; ++i) {
-        const uint32_t r = qg + 8 * i;
-        const uint32_t x = r < a.C ? slot[r * kFSlotWords + col] : 0u;
-        if (FMT == kRowP16) {
-          lo += x & 0xffffu;
-          hi += x >> 16;
-        } else {
-          lo += x;
-        }
-      }
-      if (FMT == kRowP16) {
-        scratch[qg * kFBatchBins + 2 * col] = lo;
-        scratch[qg * kFBatchBins + 2 * col + 1] = hi;
-      } else {
-        scratch[qg * kFBatchBins + col] = lo;
-      }
+      v[0] += __shfl_xor_sync(FULL, v[0], O);
+      reduce_scatter_step<1, O / 2>(v, lane);
     }
   }
-  __syncthreads();
-  phase_mark(a.pt, 13);
-  const uint32_t j = threadIdx.x;
-  if (j < nb) {
-    uint32_t h = 0;
-    if ((need_mask >> (j / kFTileBins)) & 1u) {
+}
+
+// Bin of the batch that lane `lane` of warp `w` produces in reduce_batch (N4: every lane;
+// P16 / U32: the lanes with (lane & 3) == 0 / (lane & 7) == 0).
+template <int FMT>
+__device__ __forceinline__ uint32_t batch_bin(uint32_t w, uint32_t lane) {
+  if (FMT == kRowN4) {  // register 4k + a holds nibbles nlo(a), nlo(a) + 4 of word k
+    const uint32_t i = lane >> 1, k = i >> 2, a = i & 3u;
+    return 32 * w + 8 * k + (((a & 1u) << 1) | (a >> 1)) + 4 * (lane & 1u);
+  } else if (FMT == kRowP16) {
+    return 8 * w + (lane >> 2);
+  } else {
+    return 4 * w + (lane >> 3);
+  }
+}
+
+// Sums the staged rows of a batch into hb[j] = merged count of the batch's bin j (+ the 4-bit
+// rows' exceptions Hx, + ovfH when the packed counters overflowed somewhere); bins of tiles
+// not needed get 0.  Warp w takes uint4 column w of the 128-word batch and lane l the rows
+// l, l + 32, .. (five 16-byte shared loads); the 32 lanes' partial sums — 4-bit rows in byte
+// then 16-bit SWAR lanes — meet in a warp reduce-scatter (16 / 9 / 6 shuffles).  The caller
+// synchronises before hb is read.
+template <int FMT>
+__device__ __forceinline__ void reduce_batch(const ScanArgs& a, uint32_t t0, uint32_t need_mask, const uint32_t* slot,
+                                             uint32_t* hb, bool use_ovf, uint32_t hx) {
+  constexpr uint32_t wpt = RowFmt<FMT>::wpt;
+  constexpr uint32_t RPL = (kFMaxRows + 31) / 32;  // rows per lane (5)
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool need = (need_mask >> (4 * w / wpt)) & 1u;
+  uint32_t v[16];
+  if (need) {
+    uint4 x[RPL];
 #pragma unroll
-      for (uint32_t g = 0; g < 8; ++g) h += scratch[g * kFBatchBins + j];
-      const uint64_t bin = (uint64_t)t0 * kFTileBins + j;
+    for (uint32_t i = 0; i < RPL; ++i) {
+      const uint32_t r = lane + 32 * i;
+      x[i] = r < a.C ? *reinterpret_cast<const uint4*>(slot + r * kFRowStride + 4 * w) : make_uint4(0, 0, 0, 0);
+    }
+    if (FMT == kRowN4) {
+      uint32_t be[4] = {0, 0, 0, 0}, bo[4] = {0, 0, 0, 0};  // <= 5 rows of 15 per byte lane
+#pragma unroll
+      for (uint32_t i = 0; i < RPL; ++i) {
+        const uint32_t xw[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          be[k] += xw[k] & 0x0F0F0F0Fu;
+          bo[k] += (xw[k] >> 4) & 0x0F0F0F0Fu;
+        }
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) {  // 16-bit lanes: nibbles (0,4) (2,6) (1,5) (3,7)
+        v[4 * k + 0] = be[k] & 0x00FF00FFu;
+        v[4 * k + 1] = (be[k] >> 8) & 0x00FF00FFu;
+        v[4 * k + 2] = bo[k] & 0x00FF00FFu;
+        v[4 * k + 3] = (bo[k] >> 8) & 0x00FF00FFu;
+      }
+      reduce_scatter_step<16, 16>(v, lane);  // <= 32 x 75 per 16-bit lane
+    } else if (FMT == kRowP16) {
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) v[k] = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < RPL; ++i) {
+        const uint32_t xw[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          v[2 * k] += xw[k] & 0xffffu;
+          v[2 * k + 1] += xw[k] >> 16;
+        }
+      }
+      reduce_scatter_step<8, 16>(v, lane);
+    } else {
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) v[k] = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < RPL; ++i) {
+        v[0] += x[i].x;
+        v[1] += x[i].y;
+        v[2] += x[i].z;
+        v[3] += x[i].w;
+      }
+      reduce_scatter_step<4, 16>(v, lane);
+    }
+  }
+  phase_mark(a.pt, 12);
+  const bool writer = FMT == kRowN4 ? true : FMT == kRowP16 ? (lane & 3u) == 0 : (lane & 7u) == 0;
+  if (writer) {
+    const uint32_t j = batch_bin<FMT>(w, lane);
+    uint32_t h = 0;
+    if (need) {
+      h = FMT == kRowN4 ? ((lane & 1u) ? v[0] >> 16 : v[0] & 0xffffu) : v[0];
       h += hx;  // Hx[bin] of 4-bit rows (0 otherwise), prefetched by the caller
+      const uint64_t bin = (uint64_t)t0 * kFTileBins + j;
       if (use_ovf && bin < a.U) h += __ldcg(a.ovfH + bin);
     }
     hb[j] = h;
@@ -503,8 +546,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
   constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
   const uint32_t S = a.tile_red_stride;
-  auto slot = [&](uint32_t k) { return sh + kFOffStage + (k & 1u) * (kFMaxRows * kFSlotWords); };  // 2 slots
-  uint32_t* scratch = sh + kFOffScratch;
+  auto slot = [&](uint32_t k) { return sh + kFOffStage + (k & 1u) * kFSlot; };  // 2 slots
   uint32_t* hb = sh + kFOffHb;
   uint32_t* Ps = sh + kFOffPs;
   uint32_t* oo = sh + kFOffOwn;   // oo[c] = first output position of owner c's tiles, oo[G] = total
@@ -532,9 +574,9 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   }
   // Hx of bin t0 kFTileBins + threadIdx.x of batch k (4-bit rows), loaded a batch ahead
   const uint32_t binend = min(tb1 * kFTileBins, U);  // bins of the own tiles end here
-  auto hx_of = [&](uint32_t k) -> uint32_t {
-    const uint32_t bin = (tb0 + k * tpb) * kFTileBins + threadIdx.x;
-    return FMT == kRowN4 && threadIdx.x < nbb && bin < binend ? __ldcg(a.Hx + bin) : 0u;
+  auto hx_of = [&](uint32_t k) -> uint32_t {  // (the bin this thread produces in reduce_batch)
+    const uint32_t bin = (tb0 + k * tpb) * kFTileBins + batch_bin<FMT>(threadIdx.x >> 5, threadIdx.x & 31);
+    return FMT == kRowN4 && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
   if (!use_ovf) {
@@ -625,7 +667,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     phase_mark(a.pt, 5);
-    reduce_batch<FMT>(a, t0, need, slot(k), scratch, hb, use_ovf, hx);
+    reduce_batch<FMT>(a, t0, need, slot(k), hb, use_ovf, hx);
     __syncthreads();  // hb complete; the slot is free
     phase_mark(a.pt, 10);
     if (k + 2 < nbt) {
@@ -675,7 +717,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
 #else
     if (nown && p0 < p1)  // (uniform per CTA) table in the second staging slot, dead after the merge
       project_tbl(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1,
-                  reinterpret_cast<uint4*>(sh + kFOffStage + kFMaxRows * kFSlotWords), wc,
+                  reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
                   reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
 #endif
 #if DIALSORT_EXP_PATHCNT
@@ -744,7 +786,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
 #else
       if (p0 < p1)
         project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
-                    reinterpret_cast<uint4*>(sh + kFOffStage + kFMaxRows * kFSlotWords), wc,
+                    reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
                     reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
 #endif
       __syncthreads();  // Pw is reused by the next pass
