@@ -55,10 +55,9 @@ template <int FMT> struct RowFmt {
 // Dynamic shared memory after the barrier (words); the ingestion histogram is dead by then.
 constexpr uint32_t kFSlot = kFMaxRows * kFRowStride;                 // one staging slot (19536 words)
 constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 132 words
-constexpr uint32_t kFOffToff = 2 * kFSlot;                           // own tiles' offsets [kFTiles + 1]
 constexpr uint32_t kFPassTiles = 32;                                 // own tiles per CTA (own-tile mode)
 constexpr uint32_t kFSharePassTiles = (kFSlot - 32) / kFTileBins;    // share mode: 304 tiles per pass
-constexpr uint32_t kFOffPs = kFOffToff + kFTiles + 32;                // own-mode P + 32 sentinels
+constexpr uint32_t kFOffPs = 2 * kFSlot;                             // own-mode P + 32 sentinels
 constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // merged H of the batch (<= 1024)
 constexpr uint32_t kFOffWc = kFOffHb + kFBatchBins;                   // 32 warps x 128 mark counts
 constexpr uint32_t kFOffOwn = kFOffWc + 32 * 128;                    // oo[G + 1] owner offsets
@@ -521,7 +520,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // the other parity's tile totals are zeroed for the next launch (host alternates them;
   // every slot, since the next launch may have more tiles than this one)
   if (b == G - 1) {
-    for (uint32_t i = threadIdx.x; i < kFTileSlots; i += blockDim.x) a.tile_clear[(uint64_t)i * kTileTotStride] = 0;
     for (uint32_t i = threadIdx.x; i < kFOwnSlots; i += blockDim.x) a.own_clear[(uint64_t)i * kTileTotStride] = 0;
   }
   if (a.Hx_clear)  // and the other parity's exception histogram (all of it: launches of any
@@ -545,12 +543,11 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   const uint32_t nown = tb1 - tb0;
   constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
   constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
-  const uint32_t S = a.tile_red_stride;
+  const uint32_t S = a.tile_red_stride;  // (counter stride)
   auto slot = [&](uint32_t k) { return sh + kFOffStage + (k & 1u) * kFSlot; };  // 2 slots
   uint32_t* hb = sh + kFOffHb;
   uint32_t* Ps = sh + kFOffPs;
   uint32_t* oo = sh + kFOffOwn;   // oo[c] = first output position of owner c's tiles, oo[G] = total
-  uint32_t* tw = sh + kFOffToff;  // tw[i] = first position of own tile tb0 + i, relative to oo[b]
   uint32_t* wc = sh + kFOffWc + (threadIdx.x >> 5) * 128;
   reinterpret_cast<uint4*>(wc)[threadIdx.x & 31] = make_uint4(0, 0, 0, 0);
   const uint32_t nbt = nown ? (nown + tpb - 1) / tpb : 0u;  // batches tb0 + k tpb ..
@@ -558,23 +555,20 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     const uint32_t t0 = tb0 + k * tpb, nt = min(tpb, tb1 - t0);
     return nt >= 32 ? 0xffffffffu : (1u << nt) - 1u;
   };
-  // The owner totals, the own tiles' totals, the overflow state and the first two batches' row
-  // segments (and their exception counts) are requested together, totals first: none depends
-  // on another, and the barrier ordered every CTA's flush before them.  Each CTA reads G + its
-  // own ~ntiles / G counters (reading all ntiles strided counters from every CTA measured
-  // ~2.5 us: 148-way fan-in on the same L2 lines).
-  const uint32_t t2 = 2 * threadIdx.x;
+  // The owner totals, the overflow state and the first two batches' row segments (and their
+  // exception counts) are requested together, totals first: none depends on another, and the
+  // barrier ordered every CTA's flush before them.  Each CTA reads the G owner totals only
+  // (reading all ntiles strided tile counters from every CTA measured ~2.5 us: a 148-way
+  // fan-in on the same L2 lines); its own tiles' offsets come out of its merge.
   uint32_t ov = threadIdx.x < G ? __ldcg(a.own_red + (uint64_t)threadIdx.x * S) : 0u;
-  uint32_t w0 = t2 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2) * S) : 0u;
-  uint32_t w1 = t2 + 1 < nown ? __ldcg(a.tile_red + (uint64_t)(tb0 + t2 + 1) * S) : 0u;
   const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
   for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
     stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot(k));
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // Hx of bin t0 kFTileBins + threadIdx.x of batch k (4-bit rows), loaded a batch ahead
+  // Hx of the bin this thread produces in reduce_batch (4-bit rows), loaded a batch ahead
   const uint32_t binend = min(tb1 * kFTileBins, U);  // bins of the own tiles end here
-  auto hx_of = [&](uint32_t k) -> uint32_t {  // (the bin this thread produces in reduce_batch)
+  auto hx_of = [&](uint32_t k) -> uint32_t {
     const uint32_t bin = (tb0 + k * tpb) * kFTileBins + batch_bin<FMT>(threadIdx.x >> 5, threadIdx.x & 31);
     return FMT == kRowN4 && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
@@ -582,34 +576,20 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   if (!use_ovf) {
     barrier_skip(a.bar64);
   } else {
-    // a packed counter overflowed somewhere: the flushed sums miss the fallback keys
+    // a packed counter overflowed somewhere: the flushed owner sums miss the fallback keys
     uint64_t osd = 0;
-    for (uint32_t t = tb0; t < tb1; ++t) {
-      const uint64_t tt = tile_total_direct<FMT>(a, t, red64);
-      osd += tt;
-      if (threadIdx.x == 0) __stcg(a.tile_alt + t, (uint32_t)tt);
-    }
+    for (uint32_t t = tb0; t < tb1; ++t) osd += tile_total_direct<FMT>(a, t, red64);
     if (threadIdx.x == 0) __stcg(a.own_alt + b, (uint32_t)osd);
     grid_barrier_mono(a.bar64, a.bar_base + 2 * G);
     ov = threadIdx.x < G ? __ldcg(a.own_alt + threadIdx.x) : 0u;
-    w0 = t2 < nown ? __ldcg(a.tile_alt + tb0 + t2) : 0u;
-    w1 = t2 + 1 < nown ? __ldcg(a.tile_alt + tb0 + t2 + 1) : 0u;
   }
-  const uint32_t* tsrc = use_ovf ? a.tile_alt : a.tile_red;  // tile totals, stride:
-  const uint32_t tstr = use_ovf ? 1u : S;
 
-  // ---- owner offsets and the own tiles' offsets: one scan, two halves --------------------
-  // (every count sum here is <= n < 2^32, R4: the low half never carries into the high one)
+  // ---- owner offsets: oo[c] = first output position of owner c's tiles ----------------------
   {
-    uint64_t tot2;
-    const uint64_t ex = block_excl_scan<uint64_t>(((uint64_t)ov << 32) | (uint64_t)(w0 + w1), tot2, red64);
-    if (threadIdx.x < G) oo[threadIdx.x] = (uint32_t)(ex >> 32);
-    if (threadIdx.x == 0) {
-      oo[G] = (uint32_t)(tot2 >> 32);
-      tw[nown] = (uint32_t)tot2;
-    }
-    if (t2 < nown) tw[t2] = (uint32_t)ex;
-    if (t2 + 1 < nown) tw[t2 + 1] = (uint32_t)ex + w0;
+    uint32_t tot;  // (every count sum here is <= n < 2^32, R4)
+    const uint32_t ex = block_excl_scan<uint32_t>(ov, tot, reinterpret_cast<uint32_t*>(red64));
+    if (threadIdx.x < G) oo[threadIdx.x] = ex;
+    if (threadIdx.x == 0) oo[G] = tot;
     __syncthreads();
   }
   phase_mark(a.pt, 4);
@@ -630,15 +610,14 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   bool own = ntiles <= kFPassTiles * G;  // every CTA's tiles fit one projection pass
   if (own)  // max owner total <= (17/16) nw / G + 1024
     own = !__syncthreads_or(threadIdx.x < G && 16ull * G * ov > 17ull * nw + 16384ull * G);
-  // equal share [lo, hi) (share mode): the totals of the tiles of the owners it overlaps are
-  // requested now and scanned after the merge
+  // equal share [lo, hi) (share mode) and the owners oa..ob (tiles [x0, x1)) it overlaps
   uint32_t lo = 0, hi = 0;
   if (!own) {
     lo = b == 0 ? 0u : (uint32_t)(((uint64_t)nw * b / G) & ~31ull);
     hi = b + 1 == G ? nw : (uint32_t)(((uint64_t)nw * (b + 1) / G) & ~31ull);
   }
   const bool share = !own && lo < hi;
-  uint32_t oa = 0, ob = 0, x0 = 0, x1 = 0, s0 = 0, s1 = 0;
+  uint32_t oa = 0, ob = 0, x0 = 0, x1 = 0;
   __shared__ uint32_t s_find[2];
   if (!own) {  // the owners holding positions lo and hi - 1: one test per owner, not a search
     if (lo < hi)
@@ -653,14 +632,14 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     ob = s_find[1];
     x0 = (uint32_t)((uint64_t)ntiles * oa / G);
     x1 = (uint32_t)((uint64_t)ntiles * (ob + 1) / G);
-    s0 = x0 + t2 < x1 ? __ldcg(tsrc + (uint64_t)(x0 + t2) * tstr) : 0u;
-    s1 = x0 + t2 + 1 < x1 ? __ldcg(tsrc + (uint64_t)(x0 + t2 + 1) * tstr) : 0u;
   }
 
   // ---- merge: H and the exclusive prefix P of the tiles this CTA owns --------------------
   // (lem:crn lifted to whole histograms: H = sum of the partial rows, + Hx, + ovfH).  Own-tile
   // mode keeps P in shared memory; otherwise P goes to L2 and each batch is published
   // (ready[t] = epoch, release) for the CTAs whose shares overlap it.
+  __shared__ uint32_t wex[32], s_btot;
+  uint32_t carry = 0;  // positions of the own tiles of earlier batches
   for (uint32_t k = 0; k < nbt; ++k) {
     const uint32_t t0 = tb0 + k * tpb, need = need_of(k);
     if (k + 1 < nbt) asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -675,23 +654,29 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     hx = hx_of(k + 1);
-    // exclusive prefix within the tile (a tile is kFTileBins / 32 whole warps) + its offset
+    // exclusive prefix over the batch's bins (the own tiles are consecutive; bins of tiles not
+    // needed hold 0): warp scans, then warp 0 scans the warp totals; + the earlier batches
     const uint32_t j = threadIdx.x;
     const uint32_t h = j < nbb ? hb[j] : 0u;
     const uint32_t inc = warp_incl_scan(h);
-    if (j < nbb && (j & 31) == 31) wsum[j >> 5] = inc;
+    if ((j & 31) == 31) wsum[j >> 5] = inc;
+    __syncthreads();
+    if (j < 32) {
+      const uint32_t x = wsum[j], xi = warp_incl_scan(x);
+      wex[j] = xi - x;
+      if (j == 31) s_btot = xi;
+    }
     __syncthreads();
     phase_mark(a.pt, 14);
     if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
-      const uint32_t t = t0 + j / kFTileBins;
-      static_assert(kFTileBins == 64, "a tile is two warps");
-      const uint32_t wpre = obase + tw[t - tb0] + ((j & 32u) ? wsum[(j >> 5) - 1] : 0u);
+      const uint32_t wpre = obase + carry + wex[j >> 5];
       const uint32_t bin = t0 * kFTileBins + j;
       const uint32_t p = bin < U ? wpre + inc - h : (uint32_t)total;
       if (bin < U) a.H[bin] = h;
       if (own) Ps[(t0 - tb0) * kFTileBins + j] = p;
       else if (bin < U) a.P[bin] = p;
     }
+    carry += s_btot;  // (read before the next batch's scan rewrites it: two barriers apart)
     phase_mark(a.pt, 15);
     if (!own) {
       __syncthreads();  // the batch's H and P are written
@@ -711,7 +696,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     if (threadIdx.x < 32) Ps[m + threadIdx.x] = 0xffffffffu;
     __syncthreads();
     phase_mark(a.pt, 9);
-    const uint32_t p0 = obase, p1 = min(obase + tw[nown], nw);
+    const uint32_t p0 = obase, p1 = min(oo[b + 1], nw);
 #if DIALSORT_PROJ_WARP
     if (nown && p0 < p1) project_warp(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
 #else
@@ -738,27 +723,24 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // oa..ob), then it waits for the tiles the share overlaps, stages their P in shared memory,
   // and its 32 warps project.
   if (share) {
+    // wait for the tiles of owners oa..ob (relaxed polling — a short sleep leaves issue slots to
+    // the rest of the CTA — then one acquire load per flag; not a fence: fence.acq_rel.gpu
+    // waits for every store in flight); their first bins' P are the window's tile offsets
     uint32_t* ts = sh + kFOffTsh;  // ts[i] = first position of tile x0 + i
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan<uint32_t>(s0 + s1, tot, reinterpret_cast<uint32_t*>(red64));
-    if (x0 + t2 < x1) ts[t2] = oo[oa] + ex;
-    if (x0 + t2 + 1 < x1) ts[t2 + 1] = oo[oa] + ex + s0;
+    for (uint32_t t = x0 + threadIdx.x; t < x1; t += blockDim.x) {
+      while (ld_relaxed_u32(a.ready + t) != a.epoch) __nanosleep(64);
+      (void)ld_acquire_u32(a.ready + t);
+      ts[t - x0] = __ldcg(a.P + (uint64_t)t * kFTileBins);
+    }
     if (threadIdx.x == 0) ts[x1 - x0] = oo[ob + 1];
     __syncthreads();
+    phase_mark(a.pt, 8);
     for (uint32_t i = threadIdx.x; i < x1 - x0; i += blockDim.x) {  // the tiles holding lo, hi - 1
       if (ts[i] <= lo && lo < ts[i + 1]) s_find[0] = i;
       if (ts[i] <= hi - 1 && hi - 1 < ts[i + 1]) s_find[1] = i;
     }
     __syncthreads();
     const uint32_t ta = x0 + s_find[0], tb = x0 + s_find[1];
-    // relaxed polling (a short sleep leaves issue slots to the rest of the CTA), then one
-    // acquire load per flag — not a fence: fence.acq_rel.gpu waits for every store in flight
-    for (uint32_t t = ta + threadIdx.x; t <= tb; t += blockDim.x) {
-      while (ld_relaxed_u32(a.ready + t) != a.epoch) __nanosleep(64);
-      (void)ld_acquire_u32(a.ready + t);
-    }
-    __syncthreads();
-    phase_mark(a.pt, 8);
     // P of the share's tiles staged in the (now dead) first row-staging slot: up to 295 tiles
     // per pass (a Zipf share in the cold tail spans ~200 tiles; 32-tile passes left most warps
     // idle); the projection table takes the second slot

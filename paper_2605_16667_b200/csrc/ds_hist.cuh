@@ -257,10 +257,9 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // One CTA per SM (1024 threads); the grid (<= #SMs) is co-resident by construction.
 // Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
 // Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
-// writes the row and, per 512-bin tile, the row's tile sum: into tsums[tile][row], or — when
-// a.tile_red is set — added (RED) into the tile total tile_red[tile].
-// k_sort_fused: thread b < G adds the row's sums of CTA b's tiles (tsum_sh, per 64-bin tile,
-// written by the flush loop) into the owner total own_red[b].
+// writes the row and, per 512-bin tile, the row's tile sum into tsums[tile][row] — or, for
+// k_sort_fused (a.tile_red set), the row's 64-bin tile sums into shared memory (tsum_sh), from
+// which thread b < G adds the row's sum over CTA b's tiles into the owner total own_red[b].
 __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U) {
   const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x;
   for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) {
@@ -460,15 +459,10 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
       }
     }
   }
-  if (a.tile_red) {
-    // the row's tile sums into the tile totals (one RED per nonzero tile; fsum: the checksum)
+  if (a.tile_red) {  // fsum (the checksum) from the row's tile sums
     __syncthreads();
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins;
-    for (uint32_t t = threadIdx.x; t < ntf; t += blockDim.x) {
-      const uint32_t v = tsum_sh[t];
-      fsum += v;
-      if (v) red_add_u32(a.tile_red + (uint64_t)t * a.tile_red_stride, v);
-    }
+    for (uint32_t t = threadIdx.x; t < ntf; t += blockDim.x) fsum += tsum_sh[t];
   }
   for (uint32_t t = threadIdx.x >> 5; !a.tile_red && t < ntiles; t += nwarps) {
     uint32_t v = 0;

@@ -71,7 +71,7 @@ struct ScanArgs {
   PhaseTimes* pt;            // nullable debug timing
   uint32_t* tsums;           // [C][ntiles] per-row tile sums (fused path), or nullptr
   // single-kernel sort (k_sort_fused) only:
-  uint32_t* tile_red;        // [ntiles x tile_red_stride] tile totals reduced during the flush (zero on entry)
+  uint32_t* tile_red;        // non-null: k_sort_fused flush (row formats, owner totals; no tile counters)
   uint32_t* tile_clear;      // the other parity's tile_red, zeroed for the next launch
   uint32_t tile_red_stride;  // words between consecutive tile totals
   uint32_t ldr;              // words between partial rows (row format may differ from the smem histogram)
