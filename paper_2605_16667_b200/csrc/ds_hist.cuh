@@ -313,7 +313,11 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
   auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
       const uint32_t act = __activemask();
-      if (!__any_sync(act, v.x == v.w)) {  // no lane can hold a run of 4: the common case
+      // (the full run test, not the cheaper x == w filter: under Zipf a quarter of the vectors
+      // pass x == w, and 86% of the warps would take the slow path for nothing)
+      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
+      const uint32_t runs = __ballot_sync(act, run4);
+      if (runs == 0u) {  // no lane holds a run of 4: the common case
         if (PACK16) {
           add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
         } else {
@@ -321,8 +325,6 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
         }
         return;
       }
-      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
-      const uint32_t runs = __ballot_sync(act, run4);
       if (runs == act) {
         const uint32_t k = (uint32_t)v.x, lane = threadIdx.x & 31;
         const uint32_t kmin = __reduce_min_sync(act, k), kmax = __reduce_max_sync(act, k);
@@ -422,18 +424,28 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
           const uint32_t sw = w.x + w.y + w.z + w.w;  // halves <= 60: no carry
           v = (sw & 0xffffu) + (sw >> 16);
         } else {
-          const uint32_t cw[4] = {w.x, w.y, w.z, w.w};
-          word = 0;
+          // some count >= 16: it goes whole to Hx (RED) and its nibble stays 0; the other
+          // counts pack as in the fast path
+          uint32_t cw[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (uint32_t j = 0; j < 8; ++j) {
-            const uint32_t c = (cw[j >> 1] >> ((j & 1u) << 4)) & 0xffffu;
-            v += c;
-            if (c < 16u) {
-              word |= c << (4 * j);
-            } else {
-              red_add_u32(a.Hx + 8 * g + j, c);
+          for (uint32_t k = 0; k < 4; ++k) {
+            v += (cw[k] & 0xffffu) + (cw[k] >> 16);
+            if (cw[k] & 0x0000FFF0u) {
+#if !DIALSORT_EXP_NOHXRED
+              red_add_u32(a.Hx + 8 * g + 2 * k, cw[k] & 0xffffu);
+#endif
+              cw[k] &= 0xFFFF0000u;
+            }
+            if (cw[k] & 0xFFF00000u) {
+#if !DIALSORT_EXP_NOHXRED
+              red_add_u32(a.Hx + 8 * g + 2 * k + 1, cw[k] >> 16);
+#endif
+              cw[k] &= 0x0000FFFFu;
             }
           }
+          const uint32_t bx = cw[0] | (cw[0] >> 12), by = cw[1] | (cw[1] >> 12);
+          const uint32_t bz = cw[2] | (cw[2] >> 12), bw = cw[3] | (cw[3] >> 12);
+          word = __byte_perm(__byte_perm(bx, by, 0x0040), __byte_perm(bz, bw, 0x0040), 0x5410);
         }
         __stcg(wp + u * 1024, word);
         if (v) atomicAdd(tp + u * (1024 / QT), v);
