@@ -524,8 +524,12 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   }
   if (a.Hx_clear)  // and the other parity's exception histogram (all of it: launches of any
                    // format alternate the parity, and the next may have a larger U), a slice per CTA
-    for (uint32_t k = kSmem16MaxBins * b / G + threadIdx.x; k < kSmem16MaxBins * (b + 1) / G; k += blockDim.x)
-      a.Hx_clear[k] = 0;
+  {  // 16-byte stores, bounds computed once (Hx buffers are 16-byte aligned, kSmem16MaxBins % 4 == 0)
+    const uint32_t q0 = (kSmem16MaxBins / 4) * b / G, q1 = (kSmem16MaxBins / 4) * (b + 1) / G;
+    if (q0 + threadIdx.x < q1) reinterpret_cast<uint4*>(a.Hx_clear)[q0 + threadIdx.x] = make_uint4(0, 0, 0, 0);
+    for (uint32_t q = q0 + threadIdx.x + blockDim.x; q < q1; q += blockDim.x)
+      reinterpret_cast<uint4*>(a.Hx_clear)[q] = make_uint4(0, 0, 0, 0);
+  }
   constexpr bool PACK16 = FMT != kRowU32;
 
   // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram; zeroed here
