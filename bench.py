@@ -351,24 +351,37 @@ def main():
     # ---- e2e: host buffers through the C ABI ----------------------------------------------
     e2e = None
     if not args.no_e2e and G == 1:
+        # a pipeline of host batches: two contexts on two streams, so batch i+1's host->device
+        # copy runs while batch i sorts and copies back (PCIe is full duplex); every step still
+        # copies its whole input in and its whole sorted output out
         xh = torch.empty(n, dtype=torch.int32, pin_memory=True)
         xh.copy_(ins[0][:n].cpu())
-        oh = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        for _ in range(3):
-            ctx.sort_host(xh, U, oh)
-        k2 = max(3, min(args.steps, 50))
+        ohs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        ctxs = [ctx, dsl.Context(local, max_n=n, max_U=max(U, 256))]
+        sts = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        for c in range(2):  # warm-up (and the staging buffers)
+            with torch.cuda.stream(sts[c]):
+                ctxs[c].sort_host(xh, U, ohs[c])
+        k2 = max(4, min(args.steps, 50))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(k2):
-            ctx.sort_host(xh, U, oh)
-        b.record(stream)
-        torch.cuda.synchronize()
+        for i in range(k2):
+            with torch.cuda.stream(sts[i % 2]):
+                ctxs[i % 2].sort_host(xh, U, ohs[i % 2], wait=False)
+        for c in range(2):
+            with torch.cuda.stream(sts[c]):
+                ctxs[c].sync()
         wall = (time.perf_counter() - t0) / k2
-        dev_ms = a.elapsed_time(b) / k2
-        e2e = {"value": n / max(wall, dev_ms * 1e-3), "unit": "keys/s", "h2d_bytes_per_step": 4 * n,
-               "d2h_bytes_per_step": 4 * n, "ms_per_step": max(wall * 1e3, dev_ms), "api": "dialsort_sort_host"}
+        e2e = {"value": n / wall, "unit": "keys/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+               "ms_per_step": wall * 1e3, "api": "dialsort_sort_host_async",
+               "pipeline": "2 contexts x 2 streams: batch i+1's H2D overlaps batch i's sort + D2H (wall clock)"}
+        ref = torch.empty_like(ins[0][:n])  # the e2e output against the device path's own
+        if U:
+            ctx.sort(ins[0][:n], U, out=ref)
+        else:
+            ctx.sort_int32(ins[0][:n], out=ref)
+        ctx.sync()
+        e2e["verified"] = bool(torch.equal(ohs[(k2 - 1) % 2], ref.cpu()))
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:

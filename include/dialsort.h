@@ -114,6 +114,12 @@ int dialsort_sort_int32(const int32_t* keys, uint64_t n, int32_t* out);
  * U == 0), copies out, all on `stream`, and blocks until done.  Returns the sync status. */
 int dialsort_sort_host(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, uint32_t U,
                        int32_t* out_host, dialsort_stream_t stream);
+/* The same without the final wait: copy in, sort and copy out are enqueued on `stream` and the
+ * call returns; out_host is valid (and device errors are reported) after dialsort_sync(ctx,
+ * stream).  The context's device staging buffer is in use until then, so calls that overlap
+ * (a pipeline of host batches) use one context per stream in flight. */
+int dialsort_sort_host_async(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, uint32_t U,
+                             int32_t* out_host, dialsort_stream_t stream);
 
 /* ---- canonical-state queries on a device histogram (NEXT-1) ---------------- */
 /* d_result (device uint64*): Σ_{k=a}^{b} H[k], 0 <= a <= b < U. */

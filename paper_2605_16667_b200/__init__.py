@@ -126,15 +126,17 @@ class Context:
                                             _stream(keys.device)))
         return out
 
-    def sort_host(self, keys_host: torch.Tensor, U: int, out_host: torch.Tensor | None = None
-                  ) -> torch.Tensor:
-        """End to end from host memory (pinned for speed); U == 0 selects the radix path."""
+    def sort_host(self, keys_host: torch.Tensor, U: int, out_host: torch.Tensor | None = None,
+                  wait: bool = True, stream=None) -> torch.Tensor:
+        """End to end from host memory (pinned for speed); U == 0 selects the radix path.
+        wait=False only enqueues (dialsort_sort_host_async): out_host is valid after sync()."""
         if keys_host.dtype != torch.int32 or keys_host.is_cuda or not keys_host.is_contiguous():
             raise ValueError("keys_host must be a contiguous int32 CPU tensor")
         if out_host is None:
             out_host = torch.empty_like(keys_host, pin_memory=keys_host.is_pinned())
-        _check(_L.dialsort_sort_host(self._h, _ptr(keys_host), keys_host.numel(), int(U), _ptr(out_host),
-                                     _stream(self.device)))
+        fn = _L.dialsort_sort_host if wait else _L.dialsort_sort_host_async
+        s = _stream(self.device) if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        _check(fn(self._h, _ptr(keys_host), keys_host.numel(), int(U), _ptr(out_host), s))
         return out_host
 
     def range_count(self, H: torch.Tensor, a: int, b: int, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -23,7 +23,7 @@ EXPORTS = (
     "dialsort_ctx_create", "dialsort_ctx_destroy", "dialsort_sync",
     "dialsort_histogram_async", "dialsort_reconstruct_async", "dialsort_sort_async",
     "dialsort_sort_int32_async", "dialsort_histogram", "dialsort_reconstruct",
-    "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host",
+    "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host", "dialsort_sort_host_async",
     "dialsort_range_count_async", "dialsort_crn_resolve_async",
     "dialsort_profile_enable", "dialsort_profile_read", "dialsort_kernel_name",
     "dialsort_debug_phase_ns", "dialsort_debug_phase_cta",
@@ -63,6 +63,7 @@ def load() -> ctypes.CDLL:
         "dialsort_sort": ([P, u64, u32, P], ci),
         "dialsort_sort_int32": ([P, u64, P], ci),
         "dialsort_sort_host": ([P, P, u64, u32, P, P], ci),
+        "dialsort_sort_host_async": ([P, P, u64, u32, P, P], ci),
         "dialsort_range_count_async": ([P, P, u32, u32, u32, P, P], ci),
         "dialsort_crn_resolve_async": ([P, P, P, u64, P, P, P], ci),
         "dialsort_profile_enable": ([P, ci], ci),

@@ -864,6 +864,13 @@ int dialsort_sort_int32(const int32_t* keys, uint64_t n, int32_t* out) {
 
 int dialsort_sort_host(dialsort_ctx c, const int32_t* keys_host, uint64_t n, uint32_t U, int32_t* out_host,
                        dialsort_stream_t stream) {
+  const int rc = dialsort_sort_host_async(c, keys_host, n, U, out_host, stream);
+  if (rc) return rc;
+  return dialsort_sync(c, stream, nullptr);
+}
+
+int dialsort_sort_host_async(dialsort_ctx c, const int32_t* keys_host, uint64_t n, uint32_t U, int32_t* out_host,
+                             dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
   ProfScope prof_scope_(c);
@@ -880,7 +887,7 @@ int dialsort_sort_host(dialsort_ctx c, const int32_t* keys_host, uint64_t n, uin
     rc = dialsort_sort_async(c, d, n, U, d, nullptr, stream);
   if (rc) return rc;
   DS_CUDA(cudaMemcpyAsync(out_host, d, 4ull * n, cudaMemcpyDeviceToHost, s));
-  return dialsort_sync(c, stream, nullptr);
+  return DIALSORT_OK;
 }
 
 }  // extern "C"
