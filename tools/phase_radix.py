@@ -1,6 +1,7 @@
 """Phase timing of one radix pass kernel sequence (debug)."""
 import os, sys
 os.environ["DIALSORT_PHASE_TIMING"] = "1"
+os.environ.setdefault("DIALSORT_LIB_VARIANT", "phase")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth
