@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--seed", type=int, default=20260321)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: histogram exchange over peer memory (default) or NCCL reduce-scatter")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.warmup < 3:
@@ -222,7 +224,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2605_16667_b200 as dsl
-    from paper_2605_16667_b200.sharded import sharded_sort
+    from paper_2605_16667_b200.sharded import PeerExchange, sharded_sort, sharded_sort_p2p
 
     n, U = cfg["n"], cfg["U"]
     radix = cfg["dist"] == "int32"
@@ -245,12 +247,20 @@ def main():
     outs = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(R)]
     torch.cuda.synchronize()
 
+    # N > 1: the exchange over peer memory (histogram kernel storing into the owners' slots over
+    # NVLink / NVSwitch); --exchange nccl selects the NCCL reduce-scatter baseline
+    ex = None
+    if G > 1 and args.exchange == "p2p":
+        ex = PeerExchange(U, dev, ctx=ctx)
+
     def step(i):
         j = i % R
         if radix:
             ctx.sort_int32(ins[j], out=outs[j])
         elif G == 1:
             ctx.sort(ins[j], U, out=outs[j])
+        elif ex is not None:
+            sharded_sort_p2p(ins[j], ex, capacity=cap, out=outs[j])
         else:
             sharded_sort(ins[j], U, capacity=cap, ctx=ctx, out=outs[j])
 
@@ -393,7 +403,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "U": U, "dist": cfg["dist"], "seed": args.seed,
-                       "parallelism": f"dp{G}: keys sharded, H reduce-scatter (NCCL), per-slice projection"
+                       "parallelism": (f"dp{G}: keys sharded, H slices stored into the owners' slots over "
+                                       "peer memory by the histogram kernel, per-slice projection"
+                                       if ex is not None else
+                                       f"dp{G}: keys sharded, H reduce-scatter (NCCL), per-slice projection")
                        if G > 1 else "single GPU",
                        "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -121,6 +121,32 @@ int dialsort_sort_host(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, u
 int dialsort_sort_host_async(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, uint32_t U,
                              int32_t* out_host, dialsort_stream_t stream);
 
+/* ---- multi-GPU exchange over peer memory (lem:crn P:951-962) -- */
+/* One rank of G (one process per GPU).  U % G == 0; universe slice s = [s L, (s+1) L), L = U/G,
+ * is owned by rank s.  peer_recv: DEVICE array of G device pointers; peer_recv[s] is rank s's
+ * receive buffer (uint32[G * L], mapped into this process with dialsort_ipc_open, or this
+ * rank's own buffer for s == rank).  Computes the local histogram of keys[n] (device) and
+ * stores its slice s into peer_recv[s][rank * L .. rank * L + L) for every s — on the
+ * shared-memory paths (U <= 98304) the histogram kernel's merge stores each finished bin
+ * straight into the owner's slot (P2P stores over NVLink / NVSwitch, overlapping the rest of
+ * the merge); for larger U the local histogram is pushed by one copy kernel.  The writes are
+ * complete when the stream's work completes; the owner reads its buffer only after every
+ * rank's call completed (e.g. stream sync + a process-group barrier).  Errors as
+ * dialsort_histogram_async (E_KEY_RANGE deferred), E_INVALID_ARG for bad G / rank. */
+int dialsort_histogram_scatter_async(dialsort_ctx ctx, const int32_t* keys, uint64_t n, uint32_t U,
+                                     uint32_t G, uint32_t rank, uint32_t* const* peer_recv,
+                                     dialsort_stream_t stream);
+/* The owner's step: H_slice[j] = sum over src < G of recv[src * L + j] (device buffers). */
+int dialsort_slice_sum_async(dialsort_ctx ctx, const uint32_t* recv, uint32_t G, uint32_t L,
+                             uint32_t* H_slice, dialsort_stream_t stream);
+/* CUDA IPC of a device allocation (cudaIpcGetMemHandle / cudaIpcOpenMemHandle with lazy peer
+ * access / cudaIpcCloseMemHandle) on the context's device; handles are
+ * DIALSORT_IPC_HANDLE_BYTES opaque bytes (host memory) exchanged by the caller. */
+#define DIALSORT_IPC_HANDLE_BYTES 64
+int dialsort_ipc_handle(dialsort_ctx ctx, const void* dev_ptr, void* handle_out);
+int dialsort_ipc_open(dialsort_ctx ctx, const void* handle, void** dev_ptr_out);
+int dialsort_ipc_close(dialsort_ctx ctx, void* dev_ptr);
+
 /* ---- canonical-state queries on a device histogram (NEXT-1) ---------------- */
 /* d_result (device uint64*): Σ_{k=a}^{b} H[k], 0 <= a <= b < U. */
 int dialsort_range_count_async(dialsort_ctx ctx, const uint32_t* H, uint32_t U, uint32_t a,

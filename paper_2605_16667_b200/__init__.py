@@ -139,6 +139,36 @@ class Context:
         _check(fn(self._h, _ptr(keys_host), keys_host.numel(), int(U), _ptr(out_host), s))
         return out_host
 
+    # -- multi-GPU exchange over peer memory (sharded.py drives these) ----------------------------
+    def histogram_scatter(self, keys: torch.Tensor, U: int, G: int, rank: int, peers: torch.Tensor) -> None:
+        """Local histogram, universe slice s stored into peers[s] (device int64 array of G device
+        pointers to the owners' receive buffers) at slot `rank` (dialsort_histogram_scatter_async)."""
+        keys = _keys(keys)
+        if peers.dtype != torch.int64 or not peers.is_cuda or peers.numel() != G:
+            raise ValueError("peers must be a device int64 tensor of G pointers")
+        _check(_L.dialsort_histogram_scatter_async(self._h, _ptr(keys), keys.numel(), int(U), int(G), int(rank),
+                                                   _ptr(peers), _stream(self.device)))
+
+    def slice_sum(self, recv: torch.Tensor, G: int, L: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """out[j] = Σ_src recv[src * L + j] (uint32 counts carried in int32 tensors)."""
+        if out is None:
+            out = torch.empty(L, dtype=torch.int32, device=recv.device)
+        _check(_L.dialsort_slice_sum_async(self._h, _ptr(recv), int(G), int(L), _ptr(out), _stream(self.device)))
+        return out
+
+    def ipc_handle(self, t: torch.Tensor) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(_L.dialsort_ipc_handle(self._h, ctypes.c_void_p(t.data_ptr()), buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        _check(_L.dialsort_ipc_open(self._h, ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, ptr: int) -> None:
+        _check(_L.dialsort_ipc_close(self._h, ctypes.c_void_p(ptr)))
+
     def range_count(self, H: torch.Tensor, a: int, b: int, out: torch.Tensor | None = None) -> torch.Tensor:
         """range-count(a, b) = Σ_{k=a}^{b} H[k] on the canonical state."""
         if out is None:

@@ -25,6 +25,8 @@ EXPORTS = (
     "dialsort_sort_int32_async", "dialsort_histogram", "dialsort_reconstruct",
     "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host", "dialsort_sort_host_async",
     "dialsort_range_count_async", "dialsort_crn_resolve_async",
+    "dialsort_histogram_scatter_async", "dialsort_slice_sum_async",
+    "dialsort_ipc_handle", "dialsort_ipc_open", "dialsort_ipc_close",
     "dialsort_profile_enable", "dialsort_profile_read", "dialsort_kernel_name",
     "dialsort_debug_phase_ns", "dialsort_debug_phase_cta",
 )
@@ -66,6 +68,11 @@ def load() -> ctypes.CDLL:
         "dialsort_sort_host_async": ([P, P, u64, u32, P, P], ci),
         "dialsort_range_count_async": ([P, P, u32, u32, u32, P, P], ci),
         "dialsort_crn_resolve_async": ([P, P, P, u64, P, P, P], ci),
+        "dialsort_histogram_scatter_async": ([P, P, u64, u32, u32, u32, P, P], ci),
+        "dialsort_slice_sum_async": ([P, P, u32, u32, P, P], ci),
+        "dialsort_ipc_handle": ([P, P, P], ci),
+        "dialsort_ipc_open": ([P, P, ctypes.POINTER(P)], ci),
+        "dialsort_ipc_close": ([P, P], ci),
         "dialsort_profile_enable": ([P, ci], ci),
         "dialsort_profile_read": ([P, ci, P, P], ci),
         "dialsort_kernel_name": ([ci], ctypes.c_char_p),

@@ -23,6 +23,7 @@
 #include "ds_fused.cuh"
 #include "ds_hist.cuh"
 #include "ds_part.cuh"
+#include "ds_peer.cuh"
 #include "ds_radix.cuh"
 #include "ds_scan.cuh"
 
@@ -47,12 +48,12 @@ int fail(int code, const std::string& msg) {
 enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND,
   KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN,
-  KID_PART_SCATTER, KID_COUNT
+  KID_PART_SCATTER, KID_PUSH_SLICES, KID_SLICE_SUM, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
                                              "k_scan", "k_expand", "k_radix_hist0", "k_radix_pass",
                                              "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count",
-                                             "k_part_scan", "k_part_scatter"};
+                                             "k_part_scan", "k_part_scatter", "k_push_slices", "k_slice_sum"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -262,10 +263,14 @@ int fill_scan_args(dialsort_ctx c, ScanArgs& a, uint32_t U, bool do_scan, uint64
 // Histogram of keys into H; when do_scan, also P / tfb for a projection of `cap` outputs.
 // Smem paths: one fused co-resident kernel.  Global path: zero + L2 ingest + k_scan.
 int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, bool do_scan,
-                      uint64_t cap, uint32_t epoch, cudaStream_t s) {
+                      uint64_t cap, uint32_t epoch, cudaStream_t s, uint32_t* const* Hpeer = nullptr,
+                      uint32_t peerL = 0, uint32_t peerRank = 0) {
   int rc;
   ScanArgs a = {};
   if ((rc = fill_scan_args(c, a, U, do_scan, cap, true, nullptr, epoch))) return rc;
+  a.Hpeer = Hpeer;  // (smem paths only: the merge stores into the owners' slots)
+  a.peerL = peerL;
+  a.peerRank = peerRank;
   const HistPath path = choose_path(U);
   if (path == HistPath::Global) {
     DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, H, (uint64_t)U));
@@ -660,6 +665,70 @@ int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, ui
     return DIALSORT_OK;
   }
   return enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s);
+}
+
+int dialsort_histogram_scatter_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t G,
+                                     uint32_t rank, uint32_t* const* peer_recv, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
+  if (G == 0 || U % G != 0 || rank >= G) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and rank < G");
+  if (!peer_recv) return fail(DIALSORT_E_INVALID_ARG, "peer_recv is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c, s);
+  const uint32_t L = U / G;
+  if (n > 0 && choose_path(U) != HistPath::Global)  // one kernel: histogram, merge, P2P stores
+    return enqueue_hist_scan(c, keys, n, U, nullptr, false, 0, epoch, s, peer_recv, L, rank);
+  // L2 path (or no keys): the local histogram, then one push kernel
+  if ((rc = c->Hws.ensure(4ull * U + 16))) return rc;
+  uint32_t* H = c->Hws.as<uint32_t>();
+  if (n == 0)
+    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
+  else if ((rc = enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s)))
+    return rc;
+  DS_CUDA(launch_k(KID_PUSH_SLICES, k_push_slices, dim3(2 * c->nsm), dim3(256), 0, s, (const uint32_t*)H, U, L, rank,
+                   peer_recv));
+  return DIALSORT_OK;
+}
+
+int dialsort_slice_sum_async(dialsort_ctx c, const uint32_t* recv, uint32_t G, uint32_t L, uint32_t* H_slice,
+                             dialsort_stream_t stream) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if (!recv || !H_slice || G == 0 || L == 0) return fail(DIALSORT_E_INVALID_ARG, "bad slice-sum arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(2ull * c->nsm, cdiv(L, 256));
+  DS_CUDA(launch_k(KID_SLICE_SUM, k_slice_sum, dim3(grid), dim3(256), 0, s, recv, G, L, H_slice));
+  return DIALSORT_OK;
+}
+
+int dialsort_ipc_handle(dialsort_ctx c, const void* dev_ptr, void* handle_out) {
+  if (!c || !dev_ptr || !handle_out) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_handle arguments");
+  DS_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  DS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == DIALSORT_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  return DIALSORT_OK;
+}
+
+int dialsort_ipc_open(dialsort_ctx c, const void* handle, void** dev_ptr_out) {
+  if (!c || !handle || !dev_ptr_out) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_open arguments");
+  DS_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  DS_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return DIALSORT_OK;
+}
+
+int dialsort_ipc_close(dialsort_ctx c, void* dev_ptr) {
+  if (!c || !dev_ptr) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_close arguments");
+  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return DIALSORT_OK;
 }
 
 int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int32_t key_base, int32_t* out,

@@ -56,6 +56,11 @@ struct ScanArgs {
   uint32_t* ovfH;            // packed-overflow side histogram (added and cleared if flagged)
   uint32_t U;
   uint32_t* H;               // C > 0: merged H written here (user H or workspace)
+  // Multi-GPU (dialsort_histogram_scatter_async): instead of H, bin k of universe slice
+  // s = k / peerL goes straight to peer rank s's receive buffer, slot peerRank:
+  // Hpeer[s][peerRank * peerL + k - s * peerL] (P2P stores over NVLink / NVSwitch)
+  uint32_t* const* Hpeer;    // device array of G device pointers, or null
+  uint32_t peerL, peerRank;
   int do_scan;
   uint32_t* P;               // [U+1] exclusive prefix
   uint64_t* range_tot;       // [gridDim] per-CTA range totals
@@ -88,6 +93,17 @@ struct ScanArgs {
   unsigned long long* bar64; // monotonic grid-barrier counter
   unsigned long long bar_base;  // its value at launch (host-tracked: += 2 * gridDim per launch)
 };
+
+// H[bin] = h, or — multi-GPU histogram — the owner rank's slot of this rank (see Hpeer).
+__device__ __forceinline__ void store_H(const ScanArgs& a, uint32_t bin, uint32_t h) {
+  if (a.Hpeer) {
+    const uint32_t sl = bin / a.peerL;
+    a.Hpeer[sl][(uint64_t)a.peerRank * a.peerL + (bin - sl * a.peerL)] = h;
+  } else {
+    a.H[bin] = h;
+  }
+}
+
 
 // Monotonic grid barrier (measured 1.25 us vs 2.0 us for counter + generation on B200,
 // profiles/r01_barrier_bench.txt): each CTA arrives with one release atomic on a 64-bit
@@ -203,7 +219,7 @@ __device__ __forceinline__ uint64_t merge_tile(const ScanArgs& a, uint32_t tile,
       h += a.ovfH[bin];
       a.ovfH[bin] = 0;  // consumed: ovfH is zero again for the next call
     }
-    a.H[bin] = h;
+    store_H(a, bin, h);
     tile_sum += h;
   }
   return block_sum<uint64_t>(tile_sum, red);
@@ -310,7 +326,7 @@ __device__ __forceinline__ uint64_t merge_scan_tiles(const ScanArgs& a, uint32_t
           h += a.ovfH[bin];
           a.ovfH[bin] = 0;
         }
-        a.H[bin] = h;
+        store_H(a, bin, h);
       }
       uint64_t tile_total;
       const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
@@ -369,7 +385,7 @@ __device__ __forceinline__ uint64_t merge_scan_tiles(const ScanArgs& a, uint32_t
         h += a.ovfH[bin];
         a.ovfH[bin] = 0;
       }
-      a.H[bin] = h;
+      store_H(a, bin, h);
     }
     uint64_t tile_total;
     const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
