@@ -437,7 +437,11 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
                       cudaStream_t s) {
   int rc;
   const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
-  const uint32_t Gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * c->nsm, cdiv(n, kPartTile)));
+#ifndef DIALSORT_PART_CTAS_PER_SM
+#define DIALSORT_PART_CTAS_PER_SM 4
+#endif
+  const uint32_t Gp = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t)DIALSORT_PART_CTAS_PER_SM * c->nsm, cdiv(n, kPartTile)));
   if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
   if ((rc = c->htmp.ensure(4ull * n + 16))) return rc;
   PartWs w;
