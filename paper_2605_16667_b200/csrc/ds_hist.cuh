@@ -310,14 +310,14 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
   // found with a min/max reduction (REDUX) and ballots — and each group adds its total with
   // a single atomic.  Random inputs never take this path: one vote on (first == last key)
   // per vector rules it out for the whole warp.
+  constexpr uint32_t kRunMiss = 8;
+  uint32_t run_state = 0;  // vectors since the last run; >= kRunMiss: detection off
   auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
-      const uint32_t act = __activemask();
-      // (the full run test, not the cheaper x == w filter: under Zipf a quarter of the vectors
-      // pass x == w, and 86% of the warps would take the slow path for nothing)
-      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
-      const uint32_t runs = __ballot_sync(act, run4);
-      if (runs == 0u) {  // no lane holds a run of 4: the common case
+      // Run detection adapts per warp: after kRunMiss vectors in a row without a run of 4 in
+      // any lane it is switched off for the rest of the launch (it costs ~0.5 us at c2, where
+      // runs never occur, and is what makes sorted inputs fast; a warp's first vectors decide)
+      if (run_state >= kRunMiss) {
         if (PACK16) {
           add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
         } else {
@@ -325,6 +325,21 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
         }
         return;
       }
+      const uint32_t act = __activemask();
+      // (the full run test, not the cheaper x == w filter: under Zipf a quarter of the vectors
+      // pass x == w, and 86% of the warps would take the slow path for nothing)
+      const bool run4 = (v.x == v.y) & (v.y == v.z) & (v.z == v.w);
+      const uint32_t runs = __ballot_sync(act, run4);
+      if (runs == 0u) {  // no lane holds a run of 4: the common case
+        ++run_state;
+        if (PACK16) {
+          add16((uint32_t)v.x); add16((uint32_t)v.y); add16((uint32_t)v.z); add16((uint32_t)v.w);
+        } else {
+          add32((uint32_t)v.x); add32((uint32_t)v.y); add32((uint32_t)v.z); add32((uint32_t)v.w);
+        }
+        return;
+      }
+      run_state = 0;
       if (runs == act) {
         const uint32_t k = (uint32_t)v.x, lane = threadIdx.x & 31;
         const uint32_t kmin = __reduce_min_sync(act, k), kmax = __reduce_max_sync(act, k);
