@@ -36,11 +36,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // histograms, H, P) keeps its lines while 40+ MB stream past it.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
-#if DIALSORT_EXP_NORMAL_POLICY
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#endif
   return pol;
 }
 __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {

@@ -40,10 +40,7 @@ constexpr uint32_t kFTileSlots = 2048;                      // tile-total slots 
 constexpr uint32_t kFOwnSlots = 256;                        // owner-total slots (>= kFMaxRows)
 // Tile totals are REDs from every CTA into ntiles counters: a 64-word (256 B) stride puts each
 // counter in its own L2 line (same-line REDs serialise: 4 lines took 7.7 us for 19K REDs).
-#ifndef DIALSORT_TILE_STRIDE
-#define DIALSORT_TILE_STRIDE 64
-#endif
-constexpr uint32_t kTileTotStride = DIALSORT_TILE_STRIDE;
+constexpr uint32_t kTileTotStride = 64;
 constexpr uint32_t kFBatchBins = 1024;                      // max bins per batch (8 4-bit tiles)
 // Partial-row formats of k_sort_fused (bins per 128-word staged batch: 128, 256, 1024)
 constexpr int kRowU32 = 0, kRowP16 = 1, kRowN4 = 2;
@@ -146,10 +143,7 @@ __shared__ uint32_t s_pathcnt[4];  // debug: super-blocks per projection path
 #endif
 __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
                                              uint32_t* wc, int32_t* __restrict__ out, bool aligned, uint64_t pol) {
-#ifndef DIALSORT_QPL
-#define DIALSORT_QPL 4
-#endif
-  constexpr uint32_t QPL = DIALSORT_QPL;  // quads per lane and super-block
+  constexpr uint32_t QPL = 4;  // quads per lane and super-block (1 and 2 measured slower)
   constexpr uint32_t NW = 32, SB = 128 * QPL;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t ltmask = (1u << lane) - 1u;

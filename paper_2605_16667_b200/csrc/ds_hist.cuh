@@ -446,15 +446,11 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
           for (uint32_t k = 0; k < 4; ++k) {
             v += (cw[k] & 0xffffu) + (cw[k] >> 16);
             if (cw[k] & 0x0000FFF0u) {
-#if !DIALSORT_EXP_NOHXRED
               red_add_u32(a.Hx + 8 * g + 2 * k, cw[k] & 0xffffu);
-#endif
               cw[k] &= 0xFFFF0000u;
             }
             if (cw[k] & 0xFFF00000u) {
-#if !DIALSORT_EXP_NOHXRED
               red_add_u32(a.Hx + 8 * g + 2 * k + 1, cw[k] >> 16);
-#endif
               cw[k] &= 0x0000FFFFu;
             }
           }
