@@ -678,6 +678,7 @@ struct Radix4Smem {
   uint32_t stage[kR3Tile + 4];       // staged sub-tile (+ alignment shift) (32 KB)
   uint32_t dstart[257];
   uint32_t grun[256];
+  int32_t gdel[256];                 // grun[d] - dstart[d]: output index of sorted slot j is gdel[d] + j
   uint32_t hnext[256];
   uint32_t red[34];
   uint64_t bar;
@@ -821,6 +822,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
       }
     }
     __syncthreads();
+    if (threadIdx.x < 256) S.gdel[threadIdx.x] = (int32_t)(S.grun[threadIdx.x] - S.dstart[threadIdx.x]);
     if (wseg + 32 * kR3KPT <= tn) {
 #pragma unroll
       for (int i = 0; i < kR3KPT; ++i) {
@@ -856,8 +858,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
       const uint32_t u = S.sorted[j];
-      const uint32_t d = __byte_perm(u, 0, dsel);
-      __stcs(dst + S.grun[d] + (j - S.dstart[d]), u ^ flip_out);
+      __stcs(dst + (int64_t)S.gdel[__byte_perm(u, 0, dsel)] + j, u ^ flip_out);
     }
     __syncthreads();
     if (threadIdx.x < 256) S.grun[threadIdx.x] += S.dstart[threadIdx.x + 1] - S.dstart[threadIdx.x];
