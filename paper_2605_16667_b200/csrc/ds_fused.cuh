@@ -4,24 +4,24 @@
 //
 //   ingestion   eq:ingestion P:409-412 (+ CRN def:crn_level P:896-915)   hist_ingest_flush
 //   merge       lem:crn P:951-962 lifted to whole histograms              stage/reduce_batch
-//   scan        GPU write-offset step (R18; paper P:13-14 has none)       tile_offsets + batch P
-//   projection  eq:projection P:418-424                                   project_warp
+//   scan        GPU write-offset step (R18; paper P:13-14 has none)       owner offsets + batch scan
+//   projection  eq:projection P:418-424                                   project_tbl
 //
 // Why one kernel: on B200 a kernel boundary plus its ramp costs ~1-2 us and a
 // counter+generation grid barrier ~2 us, against a ~10 us HBM floor per 40 MB pass.
-//   1. Every CTA ingests its keys into a private shared-memory histogram, flushes it as
-//      partial row c (L2; 4-bit, 16-bit or 32-bit counters) and adds (RED) the row's 64-bin
-//      tile sums into tile totals.
-//   2. ONE monotonic grid barrier.  Every CTA requests its first row segments, reads the
-//      tile totals and scans them locally: toff[t] = first output position of tile t.
+//   1. Every CTA ingests its keys into a private shared-memory histogram and flushes it as
+//      partial row c (L2; 4-bit, 16-bit or 32-bit counters); its sums over each owning CTA's
+//      tiles are added (RED) into G owner totals.
+//   2. ONE monotonic grid barrier.  Every CTA requests its first row segments, reads the G
+//      owner totals and scans them: oo[c] = first output position of owner c's tiles.
 //   3. CTA b merges the tiles [ntiles b / G, ntiles (b+1) / G) (index ownership): H and the
-//      exclusive prefix P of its bins.
-//   4. Projection.  Near-uniform histograms (every CTA's own tiles hold ~nw / G positions):
-//      each CTA projects its own tiles from P in shared memory — no cross-CTA dependence
-//      after the barrier.  Skewed ones: P goes through L2 with per-tile release flags and
-//      CTA b projects the equal position share [b nw / G, (b+1) nw / G) — a Zipf hot tile
-//      is projected by many CTAs.
-// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) adds one barrier: tile
+//      exclusive prefix P of its bins (its tiles' offsets come out of the merge's own scan).
+//   4. Projection (project_tbl).  Near-uniform histograms (every CTA's own tiles hold ~nw / G
+//      positions): each CTA projects its own tiles from P in shared memory — no cross-CTA
+//      dependence after the barrier.  Skewed ones: P goes through L2 with per-tile release
+//      flags and CTA b projects the equal position share [b nw / G, (b+1) nw / G) — a Zipf
+//      hot tile is projected by many CTAs.
+// A packed-counter overflow anywhere (exact detection, ds_hist.cuh) adds one barrier: owner
 // totals are recomputed with the fallback histogram ovfH, which is cleared at the end.
 #pragma once
 #include "ds_common.cuh"
@@ -69,16 +69,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
-// Last t in [0, ntiles) with toff[t] <= x (toff[0] = 0 <= x < toff[ntiles] = total).
-__device__ __forceinline__ uint32_t tile_of(const uint32_t* toff, uint32_t ntiles, uint32_t x) {
-  uint32_t lo = 0, hi = ntiles;  // toff[lo] <= x < toff[hi]
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (toff[mid] <= x) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
 
 // ---- projection ----------------------------------------------------------------------------
 // Projection of positions [lo, hi) whose bins are ka .. ka+m-1 with P staged as Ps[0..m)
@@ -86,7 +76,8 @@ __device__ __forceinline__ uint32_t tile_of(const uint32_t* toff, uint32_t ntile
 //   key(p) = max{k : P[k] <= p} = ka - 1 + cnt(p),   cnt(p) = #{i : Ps[i] <= p}
 // (the bin whose run covers p; empty bins share their start with the next bin and are
 // skipped by the max); kbase = key_base + ka - 1.
-// The range is cut into 512-position super-blocks aligned to absolute multiples of 512,
+// project_warp (warp-level; the A/B reference of project_tbl below, DIALSORT_PROJ_WARP=1):
+// the range is cut into 512-position super-blocks aligned to absolute multiples of 512,
 // dealt round-robin to the CTA's 32 warps, so the CTA writes one contiguous front (measured:
 // 5.6 us for 40 MB of stores vs 8.8 us when each warp streams a range of its own — DRAM page
 // locality).  A super-block is 4 sub-blocks of 128 positions; lane l owns the quad at
@@ -488,7 +479,8 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
 
 // One DialSort step: keys[n] in [0,U) -> out[min(ΣH, cap)] sorted; H as a by-product.
 // Grid: C <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic
-// smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch.
+// smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch (the
+// second one is only waited for after a packed-counter overflow).
 template <int FMT>
 __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
@@ -511,8 +503,8 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   }
   const uint32_t U = a.U, ntiles = (U + kFTileBins - 1) / kFTileBins;
   const uint32_t G = gridDim.x, b = blockIdx.x;
-  // the other parity's tile totals are zeroed for the next launch (host alternates them;
-  // every slot, since the next launch may have more tiles than this one)
+  // the other parity's owner totals are zeroed for the next launch (host alternates them;
+  // every slot, since the next launch may have more CTAs than this one)
   if (b == G - 1) {
     for (uint32_t i = threadIdx.x; i < kFOwnSlots; i += blockDim.x) a.own_clear[(uint64_t)i * kTileTotStride] = 0;
   }
