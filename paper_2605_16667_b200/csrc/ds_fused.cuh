@@ -550,7 +550,14 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // barrier ordered every CTA's flush before them.  Each CTA reads the G owner totals only
   // (reading all ntiles strided tile counters from every CTA measured ~2.5 us: a 148-way
   // fan-in on the same L2 lines); its own tiles' offsets come out of its merge.
-  uint32_t ov = threadIdx.x < G ? __ldcg(a.own_red + (uint64_t)threadIdx.x * S) : 0u;
+  // (warp 0, lane l: owners kOPL l .. kOPL l + kOPL - 1, scanned by that warp alone)
+  constexpr uint32_t kOPL = (kFMaxRows + 31) / 32;
+  uint32_t ov[kOPL];
+#pragma unroll
+  for (uint32_t j = 0; j < kOPL; ++j) {
+    const uint32_t c = kOPL * threadIdx.x + j;
+    ov[j] = threadIdx.x < 32 && c < G ? __ldcg(a.own_red + (uint64_t)c * S) : 0u;
+  }
   const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
   for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
     stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot(k));
@@ -571,17 +578,29 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
     for (uint32_t t = tb0; t < tb1; ++t) osd += tile_total_direct<FMT>(a, t, red64);
     if (threadIdx.x == 0) __stcg(a.own_alt + b, (uint32_t)osd);
     grid_barrier_mono(a.bar64, a.bar_base + 2 * G);
-    ov = threadIdx.x < G ? __ldcg(a.own_alt + threadIdx.x) : 0u;
+#pragma unroll
+    for (uint32_t j = 0; j < kOPL; ++j) {
+      const uint32_t c = kOPL * threadIdx.x + j;
+      ov[j] = threadIdx.x < 32 && c < G ? __ldcg(a.own_alt + c) : 0u;
+    }
   }
 
-  // ---- owner offsets: oo[c] = first output position of owner c's tiles ----------------------
-  {
-    uint32_t tot;  // (every count sum here is <= n < 2^32, R4)
-    const uint32_t ex = block_excl_scan<uint32_t>(ov, tot, reinterpret_cast<uint32_t*>(red64));
-    if (threadIdx.x < G) oo[threadIdx.x] = ex;
-    if (threadIdx.x == 0) oo[G] = tot;
-    __syncthreads();
+  // ---- owner offsets: oo[c] = first output position of owner c's tiles (one warp) ------------
+  if (threadIdx.x < 32) {  // (every count sum here is <= n < 2^32, R4)
+    uint32_t sum = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kOPL; ++j) sum += ov[j];
+    const uint32_t inc = warp_incl_scan(sum);
+    uint32_t ex = inc - sum;
+#pragma unroll
+    for (uint32_t j = 0; j < kOPL; ++j) {
+      const uint32_t c = kOPL * threadIdx.x + j;
+      if (c < G) oo[c] = ex;
+      ex += ov[j];
+    }
+    if (threadIdx.x == 31) oo[G] = inc;
   }
+  __syncthreads();
   phase_mark(a.pt, 4);
   const uint64_t total = oo[G];
   const uint32_t obase = oo[b];  // first output position of this CTA's tiles
@@ -599,7 +618,8 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // no cross-CTA flags, no P round trip through L2.  Otherwise (skew) equal position shares.
   bool own = ntiles <= kFPassTiles * G;  // every CTA's tiles fit one projection pass
   if (own)  // max owner total <= (17/16) nw / G + 1024
-    own = !__syncthreads_or(threadIdx.x < G && 16ull * G * ov > 17ull * nw + 16384ull * G);
+    own = !__syncthreads_or(threadIdx.x < G &&
+                            16ull * G * (oo[threadIdx.x + 1] - oo[threadIdx.x]) > 17ull * nw + 16384ull * G);
   // equal share [lo, hi) (share mode) and the owners oa..ob (tiles [x0, x1)) it overlaps
   uint32_t lo = 0, hi = 0;
   if (!own) {
