@@ -327,8 +327,10 @@ def main():
     nblk = max(1, -(-U // 65536))
     kb = {  # k_sort_fused = the whole step (keys read, out written, H and P written + read);
         # hierarchical path: one launch per 65536-bin block, plus the partition kernels
-        "k_sort_fused": (8 * n_loc // nblk + 8 * 65536) if hier else 8 * n_loc + 8 * U,
-        "k_part_count": 4 * n_loc, "k_part_scatter": 8 * n_loc, "k_part_scan": 0,
+        # hierarchical: blocks hold uint16 keys (2 B read + 4 B written a key); the scatter reads
+        # 4 B and writes 2 B a key
+        "k_sort_fused": (6 * n_loc // nblk + 8 * 65536) if hier else 8 * n_loc + 8 * U,
+        "k_part_count": 4 * n_loc, "k_part_scatter": 6 * n_loc, "k_part_scan": 0,
         # two-kernel pipeline: fused ingest+merge+scan (keys read + H and P written), expand
         "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
         "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),

@@ -168,9 +168,12 @@ int ctx_init(dialsort_ctx c) {
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
   // k_sort_fused: tile totals (2 parities), fallback tile totals
   if ((rc = c->fused_tiles.ensure(4ull * kFusedTileWords, true))) return rc;
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -357,9 +360,10 @@ bool sort_fused_enabled() {
 
 // d_n / d_off (nullable): the key count and the keys/out offset are on the device (a universe
 // block of the hierarchical path); n is then only the size hint for the grid and row format.
-int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
+// k16: keys are uint16 (the hierarchical path's universe blocks), else int32.
+int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
                        uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
-                       const uint64_t* d_off = nullptr) {
+                       const uint64_t* d_off = nullptr, bool k16 = false) {
   int rc;
   ScanArgs a = {};
   if ((rc = fill_scan_args(c, a, U, true, n, true, nullptr, epoch))) return rc;
@@ -407,12 +411,16 @@ int enqueue_sort_fused(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t
   a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);
   a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
   a.bar_base = c->bar64_base;
-  if (fmt == kRowN4)
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowN4>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
-  else if (fmt == kRowP16)
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowP16>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
-  else
-    DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<kRowU32>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base));
+#define DS_LAUNCH_FUSED(F, K)                                                                                 \
+  DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
+  if (fmt == kRowN4) {
+    if (k16) DS_LAUNCH_FUSED(kRowN4, true); else DS_LAUNCH_FUSED(kRowN4, false);
+  } else if (fmt == kRowP16) {
+    if (k16) DS_LAUNCH_FUSED(kRowP16, true); else DS_LAUNCH_FUSED(kRowP16, false);
+  } else {
+    if (k16) DS_LAUNCH_FUSED(kRowU32, true); else DS_LAUNCH_FUSED(kRowU32, false);
+  }
+#undef DS_LAUNCH_FUSED
   c->fused_seq++;
   c->bar64_base += 2ull * C;  // two barriers reserved per launch (one skipped unless overflow)
   return DIALSORT_OK;
@@ -443,13 +451,13 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   const uint32_t Gp = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t)DIALSORT_PART_CTAS_PER_SM * c->nsm, cdiv(n, kPartTile)));
   if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
-  if ((rc = c->htmp.ensure(4ull * n + 16))) return rc;
+  if ((rc = c->htmp.ensure(2ull * n + 16))) return rc;  // uint16 block keys
   PartWs w;
   w.bsz = c->part.as<uint64_t>();
   w.boff = w.bsz + B;
   w.cnt = reinterpret_cast<uint32_t*>(w.boff + B);
   w.st = c->status.as<DevStatus>();
-  int32_t* tmp = c->htmp.as<int32_t>();
+  uint16_t* tmp = c->htmp.as<uint16_t>();
   DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
   DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
   DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
@@ -457,7 +465,7 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
     const uint32_t Ub = (uint32_t)std::min<uint64_t>(1ull << kPartShift, (uint64_t)U - ((uint64_t)b << kPartShift));
     const uint32_t epoch = next_epoch(c, s);  // each block launch has its own ready-flag epoch
     if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, H + ((uint64_t)b << kPartShift), out, epoch, s,
-                                 (int32_t)(b << kPartShift), w.bsz + b, w.boff + b)))
+                                 (int32_t)(b << kPartShift), w.bsz + b, w.boff + b, true)))
       return rc;
   }
   return DIALSORT_OK;

@@ -481,9 +481,10 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
 // Grid: C <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic
 // smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch (the
 // second one is only waited for after a packed-counter overflow).
-template <int FMT>
-__global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
+template <int FMT, bool K16 = false>
+__global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
+  // (K16: uint16 keys, the hierarchical path's universe blocks; otherwise int32)
   // (keys, out, n are adjusted below for hierarchical blocks)
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
     const uint64_t off = *a.d_off;
     n = *a.d_n;
-    keys += off;
+    keys = static_cast<const char*>(keys) + off * (K16 ? 2 : 4);
     out += off;
     n_exp = n;
   }
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const int32_t* __restric
   // (the ingestion's first __syncthreads orders this before the flush)
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
   for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
-  hist_ingest_flush<PACK16, false>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
+  hist_ingest_flush<PACK16, false, K16>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
   __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
     my_tiles(ntiles, s_own[0], s_own[1]);

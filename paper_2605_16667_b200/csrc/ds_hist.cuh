@@ -270,8 +270,98 @@ __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint
   }
 }
 
-template <bool PACK16, bool TMA>
-__device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ keys, uint64_t n, const ScanArgs& a,
+// ---- 16-bit keys (the hierarchical path's universe blocks, ds_part.cuh) -------------------
+// A block's keys are stored as their low 16 bits (2 bytes a key: half the bytes of the block
+// sorts' ingestion).  Keys [head, head + 8 n8) are 16-byte vectors of 8 keys, visited grid-
+// strided like for_each_key4 (vector v by thread v mod (G T) of CTA (v / T) mod G); the
+// unaligned head (CTA 0) and tail (last CTA) go through f1.  Returns this thread's vectors.
+struct KeySpan16 {
+  const uint16_t* keys;
+  uint64_t n, head, n8, tail;
+};
+__device__ __forceinline__ KeySpan16 make_span16(const uint16_t* keys, uint64_t n) {
+  KeySpan16 s;
+  s.keys = keys;
+  s.n = n;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(keys) >> 1) & 7u;
+  s.head = mis ? 8 - mis : 0;
+  if (s.head > n) s.head = n;
+  s.n8 = (n - s.head) / 8;
+  s.tail = n - s.head - 8 * s.n8;
+  return s;
+}
+template <typename F4, typename F1>
+__device__ __forceinline__ uint32_t for_each_key8_u16(const KeySpan16& s, F4&& f4, F1&& f1) {
+  const uint32_t T = blockDim.x, G = gridDim.x;
+  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
+  if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
+    const uint64_t i = s.head + 8 * s.n8 + threadIdx.x;
+    f1((uint32_t)s.keys[i], i);
+  }
+  const uint64_t pol = l2_evict_first_policy();
+  const int4* __restrict__ body = reinterpret_cast<const int4*>(s.keys + s.head);
+  const uint32_t n8 = (uint32_t)s.n8, stride = G * T;
+  auto expand = [&](const int4& x, uint32_t v) {  // 8 keys -> two vectors of 4
+    f4(make_int4((int)((uint32_t)x.x & 0xffffu), (int)((uint32_t)x.x >> 16), (int)((uint32_t)x.y & 0xffffu),
+                 (int)((uint32_t)x.y >> 16)), 2 * v);
+    f4(make_int4((int)((uint32_t)x.z & 0xffffu), (int)((uint32_t)x.z >> 16), (int)((uint32_t)x.w & 0xffffu),
+                 (int)((uint32_t)x.w >> 16)), 2 * v + 1);
+  };
+  uint32_t cnt = 0;
+  uint32_t i = blockIdx.x * T + threadIdx.x;
+  int4 a[kHistUnroll / 2];
+#pragma unroll
+  for (int u = 0; u < kHistUnroll / 2; ++u)
+    a[u] = (i + u * stride < n8) ? ld_stream4(body + i + u * stride, pol) : make_int4(0, 0, 0, 0);
+  while (i < n8) {
+    const uint32_t in = i + (kHistUnroll / 2) * stride;
+    int4 b[kHistUnroll / 2];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll / 2; ++u)
+      b[u] = (in + u * stride < n8) ? ld_stream4(body + in + u * stride, pol) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < kHistUnroll / 2; ++u)
+      if (i + u * stride < n8) {
+        expand(a[u], i + u * stride);
+        ++cnt;
+      }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll / 2; ++u) a[u] = b[u];
+    i = in;
+  }
+  return cnt;
+}
+// Overflow fallback of a 16-bit-key CTA: zero the row, re-ingest this CTA's keys (the same
+// head / tail / grid-strided vectors) into ovfH through the warp CRN.
+__device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
+                                                      uint32_t U, DevStatus* st, uint32_t epoch) {
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
+  const uint32_t T = blockDim.x, G = gridDim.x;
+  if (threadIdx.x < 32) {
+    bool v = blockIdx.x == 0 && threadIdx.x < s.head;
+    crn_red(ovfH, v ? (uint32_t)s.keys[threadIdx.x] : 0u, v && s.keys[threadIdx.x] < U);
+    v = blockIdx.x == G - 1 && threadIdx.x < s.tail;
+    const uint64_t ti = s.head + 8 * s.n8 + threadIdx.x;
+    crn_red(ovfH, v ? (uint32_t)s.keys[ti] : 0u, v && s.keys[ti] < U);
+  }
+  const int4* body = reinterpret_cast<const int4*>(s.keys + s.head);
+  for (uint64_t w = (uint64_t)blockIdx.x * T + (threadIdx.x & ~31u); w < s.n8; w += (uint64_t)G * T) {
+    const uint64_t i = w + (threadIdx.x & 31);
+    const bool ok = i < s.n8;
+    const int4 x = ok ? ld_stream4(body + i) : make_int4(0, 0, 0, 0);
+    const uint32_t h[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t k = (h[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+      crn_red(ovfH, k, ok && k < U);
+    }
+  }
+}
+
+template <bool PACK16, bool TMA, bool K16 = false>
+__device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_v, uint64_t n, const ScanArgs& a,
                                                   uint32_t stages, uint32_t* sh_hist, uint64_t* red64,
                                                   uint64_t* full_bar, uint64_t* empty_bar,
                                                   uint32_t* tsum_sh = nullptr) {
@@ -286,7 +376,8 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
 
   // Ingestion (eq:ingestion): one shared atomic per key; equal addresses inside one warp
   // instruction are merged by the shared-memory atomic unit (the CRN's equality merge).
-  const KeySpan s = make_span(keys, n);
+  const KeySpan s = make_span(K16 ? nullptr : static_cast<const int32_t*>(keys_v), K16 ? 0 : n);
+  const KeySpan16 s16 = make_span16(K16 ? static_cast<const uint16_t*>(keys_v) : nullptr, K16 ? n : 0);
   DevStatus* st = a.st;
   uint32_t seen = 0, bad = 0, deferred = 0;
   // packed word of key k: k >> 1 at byte offset (2k) & ~3; increment 1 or 65536
@@ -371,7 +462,9 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
       ++bad;
     }
   };
-  if (TMA) {
+  if (K16) {
+    seen += 8 * for_each_key8_u16(s16, f4, f1);  // (16-bit keys are < U by construction)
+  } else if (TMA) {
     if (threadIdx.x == 0) {
       for (uint32_t q = 0; q < stages; ++q) {
         mbar_init(&full_bar[q], 1);
@@ -390,7 +483,7 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
     const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
     seen += 4 * cnt;
   }
-  if (deferred) bad += ingest_deferred<PACK16, TMA>(sh_hist, s, U, st);
+  if (!K16 && deferred) bad += ingest_deferred<PACK16, TMA>(sh_hist, s, U, st);
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
@@ -538,7 +631,8 @@ __device__ __forceinline__ void hist_ingest_flush(const int32_t* __restrict__ ke
           }
         }
         uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
-        hist_overflow_fallback<TMA>(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
+        if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
+        else hist_overflow_fallback<TMA>(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
       } else {
         hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
       }

@@ -8,8 +8,8 @@
 // as their low 16 bits; then each block is sorted by k_sort_fused with U_b <= 65536 and
 // key_base = b << 16, writing its output at the block's offset and its H slice at b << 16.
 // This replaces one L2 RED per key (the global path, bound by the L2 atomic rate) with
-// 12 bytes per key of streaming traffic (count read, scatter read + write) plus the
-// shared-memory path of each block.
+// 10 bytes per key of streaming traffic (count read 4, scatter read 4 + write 2: the blocks
+// hold their keys' low 16 bits as uint16) plus the shared-memory path of each block.
 //
 //   k_part_count    per-CTA chunk: block counts (per-warp shared counters)      [G][B]
 //   k_part_scan     exclusive offsets off[c][b] (block-major), block sizes and starts
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
 #define DIALSORT_PART_MINB 4  // 4 CTAs per SM (32 registers): more loads in flight (c4 6.44 -> 6.19 ms)
 #endif
 __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatter(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
-                                                               uint32_t B, PartWs w, int32_t* __restrict__ tmp) {
+                                                               uint32_t B, PartWs w, uint16_t* __restrict__ tmp) {
   constexpr uint32_t NW = kPartThreads / 32;
   __shared__ uint32_t wcnt[NW][kPartMaxBlocks];  // counts, then cursors
   __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
     const uint32_t nvld = bofs[B];  // valid keys of the sub-tile (bad keys were dropped)
     for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
       const uint32_t key = stage[j], bb = key >> kPartShift;
-      __stcs(tmp + gpos[bb] + (j - bofs[bb]), (int32_t)(key & 0xffffu));
+      __stcs(reinterpret_cast<unsigned short*>(tmp) + gpos[bb] + (j - bofs[bb]), (unsigned short)(key & 0xffffu));
     }
     __syncthreads();
     if (threadIdx.x < B) gpos[threadIdx.x] += bofs[threadIdx.x + 1] - bofs[threadIdx.x];
