@@ -399,9 +399,13 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.tile_red = ft + red_words * (c->fused_seq & 1);
   a.tile_clear = ft + red_words * ((c->fused_seq + 1) & 1);
   a.tile_red_stride = kTileTotStride;
-  a.tile_alt = ft + 2 * red_words;
-  a.ready = a.tile_alt + kFTileSlots;
-  uint32_t* ownb = a.ready + kFTileSlots;
+  // per-tile ready flags (share mode), two parities: each launch clears the other one, so a
+  // flag never holds a value from an earlier launch (the epoch wraps after 2^24 launches)
+  uint32_t* rdy = ft + 2 * red_words;
+  a.ready = rdy + kFTileSlots * (c->fused_seq & 1);
+  a.ready_clear = rdy + kFTileSlots * ((c->fused_seq + 1) & 1);
+  a.tile_alt = nullptr;
+  uint32_t* ownb = rdy + 2 * kFTileSlots;
   const uint64_t own_words = (uint64_t)kFOwnSlots * kTileTotStride;  // per parity
   a.own_red = ownb + own_words * (c->fused_seq & 1);
   a.own_clear = ownb + own_words * ((c->fused_seq + 1) & 1);

@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   // every slot, since the next launch may have more CTAs than this one)
   if (b == G - 1) {
     for (uint32_t i = threadIdx.x; i < kFOwnSlots; i += blockDim.x) a.own_clear[(uint64_t)i * kTileTotStride] = 0;
+    for (uint32_t i = threadIdx.x; i < kFTileSlots; i += blockDim.x) a.ready_clear[i] = 0;
   }
   if (a.Hx_clear)  // and the other parity's exception histogram (all of it: launches of any
                    // format alternate the parity, and the next may have a larger U), a slice per CTA

@@ -88,7 +88,8 @@ struct ScanArgs {
   uint32_t* own_red;         // [G x tile_red_stride] per-owner totals (tiles of CTA b) reduced during the flush
   uint32_t* own_clear;       // the other parity's own_red, zeroed for the next launch
   uint32_t* own_alt;         // [G] owner totals of the overflow fallback path
-  uint32_t* tile_alt;        // [ntiles] tile totals of the overflow fallback path
+  uint32_t* tile_alt;        // (unused by k_sort_fused)
+  uint32_t* ready_clear;     // k_sort_fused: the other parity's ready flags, zeroed for the next launch
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
   unsigned long long* bar64; // monotonic grid-barrier counter
   unsigned long long bar_base;  // its value at launch (host-tracked: += 2 * gridDim per launch)
