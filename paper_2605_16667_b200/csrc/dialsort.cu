@@ -97,10 +97,9 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 constexpr size_t kSmemBudget = 227 * 1024 - 4096;  // static smem of the kernels <= 4 KB
-// k_sort_fused workspace: 2 parities of strided tile totals, fallback tile totals, ready flags
-// and 2 parities of strided owner totals + the fallback owner totals
-constexpr uint64_t kFusedTileWords =
-    2ull * kFTileSlots * kTileTotStride + 2 * kFTileSlots + 2ull * kFOwnSlots * kTileTotStride + kFOwnSlots;
+// k_sort_fused workspace: 2 parities of per-tile ready flags, 2 parities of strided owner
+// totals, the fallback owner totals
+constexpr uint64_t kFusedTileWords = 2ull * kFTileSlots + 2ull * kFOwnSlots * kTileTotStride + kFOwnSlots;
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t round_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -395,16 +394,13 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.H = H;
   a.tfb = nullptr;
   a.tsums = nullptr;
-  const uint64_t red_words = (uint64_t)kFTileSlots * kTileTotStride;  // per parity
-  a.tile_red = ft + red_words * (c->fused_seq & 1);
-  a.tile_clear = ft + red_words * ((c->fused_seq + 1) & 1);
-  a.tile_red_stride = kTileTotStride;
+  a.fused = 1;
+  a.ctr_stride = kTileTotStride;
   // per-tile ready flags (share mode), two parities: each launch clears the other one, so a
   // flag never holds a value from an earlier launch (the epoch wraps after 2^24 launches)
-  uint32_t* rdy = ft + 2 * red_words;
+  uint32_t* rdy = ft;
   a.ready = rdy + kFTileSlots * (c->fused_seq & 1);
   a.ready_clear = rdy + kFTileSlots * ((c->fused_seq + 1) & 1);
-  a.tile_alt = nullptr;
   uint32_t* ownb = rdy + 2 * kFTileSlots;
   const uint64_t own_words = (uint64_t)kFOwnSlots * kTileTotStride;  // per parity
   a.own_red = ownb + own_words * (c->fused_seq & 1);

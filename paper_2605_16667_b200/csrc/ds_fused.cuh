@@ -36,9 +36,9 @@ constexpr uint32_t kFSlotWords = 128;                       // staged words per 
 // and a 4-word pad puts rows r .. r+7 in distinct 16-byte bank groups (conflict-free LDS.128).
 constexpr uint32_t kFRowStride = kFSlotWords + 4;
 constexpr uint32_t kFMaxRows = 148;                         // rows (CTAs) a staging slot holds
-constexpr uint32_t kFTileSlots = 2048;                      // tile-total slots (>= kFTiles)
+constexpr uint32_t kFTileSlots = 2048;                      // ready-flag slots per parity (>= kFTiles)
 constexpr uint32_t kFOwnSlots = 256;                        // owner-total slots (>= kFMaxRows)
-// Tile totals are REDs from every CTA into ntiles counters: a 64-word (256 B) stride puts each
+// Owner totals are REDs from every CTA into G counters: a 64-word (256 B) stride puts each
 // counter in its own L2 line (same-line REDs serialise: 4 lines took 7.7 us for 19K REDs).
 constexpr uint32_t kTileTotStride = 64;
 constexpr uint32_t kFBatchBins = 1024;                      // max bins per batch (8 4-bit tiles)
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   const uint32_t nown = tb1 - tb0;
   constexpr uint32_t tpb = RowFmt<FMT>::tpb;  // tiles per batch
   constexpr uint32_t nbb = tpb * kFTileBins;  // bins per batch
-  const uint32_t S = a.tile_red_stride;  // (counter stride)
+  const uint32_t S = a.ctr_stride;  // (counter stride)
   auto slot = [&](uint32_t k) { return sh + kFOffStage + (k & 1u) * kFSlot; };  // 2 slots
   uint32_t* hb = sh + kFOffHb;
   uint32_t* Ps = sh + kFOffPs;

@@ -258,7 +258,7 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
 // Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
 // writes the row and, per 512-bin tile, the row's tile sum into tsums[tile][row] — or, for
-// k_sort_fused (a.tile_red set), the row's 64-bin tile sums into shared memory (tsum_sh), from
+// k_sort_fused (a.fused), the row's 64-bin tile sums into shared memory (tsum_sh), from
 // which thread b < G adds the row's sum over CTA b's tiles into the owner total own_red[b].
 __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U) {
   const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x;
@@ -266,7 +266,7 @@ __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint
     const uint32_t t0 = (uint32_t)((uint64_t)ntf * b / G), t1 = (uint32_t)((uint64_t)ntf * (b + 1) / G);
     uint32_t s = 0;
     for (uint32_t t = t0; t < t1; ++t) s += tsum_sh[t];
-    if (s) red_add_u32(a.own_red + (uint64_t)b * a.tile_red_stride, s);
+    if (s) red_add_u32(a.own_red + (uint64_t)b * a.ctr_stride, s);
   }
 }
 
@@ -497,7 +497,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
   const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   uint32_t fsum = 0;  // <= the CTA's keys < 2^32
-  if (a.tile_red && PACK16 && a.nib4) {
+  if (a.fused && PACK16 && a.nib4) {
     // k_sort_fused, 4-bit rows: the partial row keeps counts <= 15 — 8 bins
     // per word, a quarter of the packed row's L2 bytes — and a count >= 16 goes whole to the
     // global exception histogram Hx (RED; its nibble stays 0).  Thread i turns packed uint4 i
@@ -555,7 +555,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
         if (v) atomicAdd(tp + u * (1024 / QT), v);
       }
     }
-  } else if (a.tile_red) {
+  } else if (a.fused) {
     // k_sort_fused, 16- or 32-bit rows: thread i stores uint4 i of the row and adds its sum to
     // the tile sum tsum_sh[i / QT] (shared atomic).
     constexpr uint32_t QT = PACK16 ? kFTileBins / 8 : kFTileBins / 4;
@@ -575,12 +575,12 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
       }
     }
   }
-  if (a.tile_red) {  // fsum (the checksum) from the row's tile sums
+  if (a.fused) {  // fsum (the checksum) from the row's tile sums
     __syncthreads();
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins;
     for (uint32_t t = threadIdx.x; t < ntf; t += blockDim.x) fsum += tsum_sh[t];
   }
-  for (uint32_t t = threadIdx.x >> 5; !a.tile_red && t < ntiles; t += nwarps) {
+  for (uint32_t t = threadIdx.x >> 5; !a.fused && t < ntiles; t += nwarps) {
     uint32_t v = 0;
 #pragma unroll
     for (uint32_t j = 0; j < q_per_tile; j += 32) {
@@ -608,14 +608,14 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     // fsum: per-warp totals in lane 0 (tsums loop) or per-tile totals in the tile's lane 0
     // One block sum of (field sums - valid keys), mod 2^32: the shortfall of a wrapped row is in
     // (0, keys of the CTA] and the CTA holds < 2^32 keys, so the sum is 0 iff nothing wrapped.
-    const uint32_t dsum = block_sum<uint32_t>((a.tile_red || lane == 0 ? fsum : 0u) - (uint32_t)(seen - bad),
+    const uint32_t dsum = block_sum<uint32_t>((a.fused || lane == 0 ? fsum : 0u) - (uint32_t)(seen - bad),
                                               reinterpret_cast<uint32_t*>(red64));
     const bool exact = dsum == 0u;
     // k_sort_fused: the row's owner totals (its tile sums summed per owning CTA) — only for
     // an exact row (an overflowed one is recounted after the barrier)
     if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U);
     if (!exact) {
-      if (a.tile_red) {
+      if (a.fused) {
         // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
         // values), then the fallback zeroes the row (ldr words) and re-ingests into ovfH
         if (a.nib4) {

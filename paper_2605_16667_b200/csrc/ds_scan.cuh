@@ -76,19 +76,17 @@ struct ScanArgs {
   PhaseTimes* pt;            // nullable debug timing
   uint32_t* tsums;           // [C][ntiles] per-row tile sums (fused path), or nullptr
   // single-kernel sort (k_sort_fused) only:
-  uint32_t* tile_red;        // non-null: k_sort_fused flush (row formats, owner totals; no tile counters)
-  uint32_t* tile_clear;      // the other parity's tile_red, zeroed for the next launch
-  uint32_t tile_red_stride;  // words between consecutive tile totals
+  int fused;                 // k_sort_fused flush (row formats, tile sums in shared memory, owner totals)
+  uint32_t ctr_stride;       // words between consecutive L2 counters / flags (one line each)
   uint32_t ldr;              // words between partial rows (row format may differ from the smem histogram)
   int nib4;                  // partial rows hold 4-bit counts (8 bins per word); counts >= 16 in Hx
   uint32_t* Hx;              // [U] exception histogram of the 4-bit rows (zero on entry)
   uint32_t* Hx_clear;        // the other parity's Hx, zeroed for the next launch
   const uint64_t* d_n;       // nullable: key count on the device (hierarchical blocks); then
   const uint64_t* d_off;     //   keys and out start at *d_off and n_expected = *d_n
-  uint32_t* own_red;         // [G x tile_red_stride] per-owner totals (tiles of CTA b) reduced during the flush
+  uint32_t* own_red;         // [G x ctr_stride] per-owner totals (tiles of CTA b) reduced during the flush
   uint32_t* own_clear;       // the other parity's own_red, zeroed for the next launch
   uint32_t* own_alt;         // [G] owner totals of the overflow fallback path
-  uint32_t* tile_alt;        // (unused by k_sort_fused)
   uint32_t* ready_clear;     // k_sort_fused: the other parity's ready flags, zeroed for the next launch
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
   unsigned long long* bar64; // monotonic grid-barrier counter
