@@ -33,10 +33,22 @@ struct PartWs {
   DevStatus* st;
 };
 
-// Chunk [lo, hi) of CTA c in a grid of G over n keys.
-__device__ __forceinline__ void part_chunk(uint64_t n, uint64_t& lo, uint64_t& hi) {
-  lo = n * blockIdx.x / gridDim.x;
-  hi = n * (blockIdx.x + 1) / gridDim.x;
+// Chunk [lo, hi) of CTA c in a grid of G over n keys.  Interior cuts sit on 256-byte
+// boundaries of the key array (64 keys past its first 16-byte aligned element), so every
+// chunk but the first starts aligned for the 16-byte vector loads (an unaligned start sends
+// the scatter's sub-tiles to the scalar load path: 3 of 4 CTAs before this, c4 scatter
+// 3.0 ms).  Both kernels of the count / scatter pair take the same cuts.
+__device__ __forceinline__ void part_chunk(const int32_t* keys, uint64_t n, uint64_t& lo, uint64_t& hi) {
+  const uint64_t a0 = ((16u - (reinterpret_cast<uintptr_t>(keys) & 15u)) & 15u) >> 2;
+  auto cut = [&](uint32_t c) -> uint64_t {
+    if (c == 0) return 0;
+    if (c >= gridDim.x) return n;
+    const uint64_t x = n * c / gridDim.x;
+    const uint64_t y = a0 + ((x > a0 ? x - a0 : 0) & ~63ull);
+    return y < n ? y : n;
+  };
+  lo = cut(blockIdx.x);
+  hi = cut(blockIdx.x + 1);
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
@@ -47,7 +59,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __re
   for (uint32_t i = threadIdx.x; i < (kPartThreads / 32) * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   uint64_t lo, hi;
-  part_chunk(n, lo, hi);
+  part_chunk(keys, n, lo, hi);
   uint32_t* wc = wcnt[warp];
   auto one = [&](uint32_t k, uint64_t idx) {
     if (k < U) atomicAdd(&wc[k >> kPartShift], 1u);
@@ -123,10 +135,13 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
 
 // Re-reads the CTA's chunk and writes every valid key's low 16 bits into its universe block,
 // sub-tile by sub-tile (4096 keys, 8 per thread as two 16-byte loads; the next sub-tile's
-// loads are in flight while the current one is placed): per-warp block counters, a scan over
-// (block, warp) gives every warp its slot range in the staged sub-tile, a per-warp cursor
-// atomic gives each key its slot (order inside a block is free), and the staged sub-tile
-// leaves as contiguous runs (~256 keys per block) at the CTA's running block offsets.
+// loads are in flight while the current one is placed).  One shared atomic per key: the
+// returned value of the per-warp block counter is the key's rank among the warp's keys of
+// that block in this sub-tile (< 256), kept in the key's register next to the key itself
+// (key < U <= 2^22 fills 22 bits, rank bits 22..29, bit 31 marks a dropped bad key).  A scan
+// over (block, warp) turns the counters into slot bases, every key lands at base + rank in
+// the staged sub-tile (order inside a block is free), and the sub-tile leaves as contiguous
+// runs (~4096 / B keys per block) at the CTA's running block offsets.
 // The chunk interior must be 16-byte aligned for the vector loads; other chunks take the
 // scalar path (keys of an unaligned base).
 #ifndef DIALSORT_PART_MINB
@@ -135,13 +150,14 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
 __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatter(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
                                                                uint32_t B, PartWs w, uint16_t* __restrict__ tmp) {
   constexpr uint32_t NW = kPartThreads / 32;
-  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];  // counts, then cursors
-  __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks];
+  constexpr uint32_t kBad = 0xffffffffu;
+  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];  // counts, then slot bases
+  __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks], delta[kPartMaxBlocks];
   __shared__ uint32_t stage[kPartTile];
   pdl_wait();
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
   uint64_t lo, hi;
-  part_chunk(n, lo, hi);
+  part_chunk(keys, n, lo, hi);
   if (threadIdx.x < B) gpos[threadIdx.x] = w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x];
   const bool vec = ((reinterpret_cast<uintptr_t>(keys + lo)) & 15u) == 0;
   // thread t holds sub-tile keys 8t .. 8t+7 (blocked: two int4)
@@ -153,18 +169,27 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
       k[0] = x0.x; k[1] = x0.y; k[2] = x0.z; k[3] = x0.w; k[4] = x1.x; k[5] = x1.y; k[6] = x1.z; k[7] = x1.w;
     } else {
 #pragma unroll
-      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : 0xffffffffu;
+      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : kBad;
     }
   };
+  unsigned short* const out = reinterpret_cast<unsigned short*>(tmp);
   uint32_t k[kPartKPT], kn[kPartKPT];
   if (lo < hi) load(lo, k);
   for (uint64_t t0 = lo; t0 < hi; t0 += kPartTile) {
     if (t0 + kPartTile < hi) load(t0 + kPartTile, kn);  // next sub-tile in flight
     for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
     __syncthreads();
+    uint32_t kmax = 0;
 #pragma unroll
-    for (uint32_t i = 0; i < kPartKPT; ++i)
-      if (k[i] < U) atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u);
+    for (uint32_t i = 0; i < kPartKPT; ++i) kmax = max(kmax, k[i]);
+    if (kmax < U) {  // every key valid: no per-key test
+#pragma unroll
+      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] |= atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22;
+    } else {
+#pragma unroll
+      for (uint32_t i = 0; i < kPartKPT; ++i)
+        k[i] = k[i] < U ? k[i] | (atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22) : kBad;
+    }
     __syncthreads();
     // scan over (block, warp) pairs q = block * NW + warp: thread t handles the QP consecutive
     // pairs QP t .. QP t + QP - 1 (B * NW <= 64 * 16 = 2 * kPartThreads)
@@ -184,7 +209,7 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
       for (uint32_t j = 0; j < QP; ++j) {
         const uint32_t q = QP * threadIdx.x + j, bq = q / NW, wq = q % NW;
         if (q < B * NW) {
-          wcnt[wq][bq] = ex;  // cursor of warp wq in block bq
+          wcnt[wq][bq] = ex;  // slot base of warp wq in block bq
           if (wq == 0) bofs[bq] = ex;
         }
         ex += v[j];
@@ -192,21 +217,44 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
       if (threadIdx.x == 0) bofs[B] = tot;
     }
     __syncthreads();
+    // staged slot j of block b goes to position delta[b] + j (positions < n < 2^32)
+    if (threadIdx.x < B) {
+      const uint32_t b = threadIdx.x;
+      delta[b] = gpos[b] - bofs[b];
+      gpos[b] += bofs[b + 1] - bofs[b];
+    }
+    if (kmax < U) {
 #pragma unroll
-    for (uint32_t i = 0; i < kPartKPT; ++i)
-      if (k[i] < U) stage[atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u)] = k[i];
-    __syncthreads();
-    const uint32_t nvld = bofs[B];  // valid keys of the sub-tile (bad keys were dropped)
-    for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
-      const uint32_t key = stage[j], bb = key >> kPartShift;
-      __stcs(reinterpret_cast<unsigned short*>(tmp) + gpos[bb] + (j - bofs[bb]), (unsigned short)(key & 0xffffu));
+      for (uint32_t i = 0; i < kPartKPT; ++i) {
+        const uint32_t key = k[i] & 0x3fffffu;
+        stage[wcnt[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+      }
+    } else {
+#pragma unroll
+      for (uint32_t i = 0; i < kPartKPT; ++i)
+        if (k[i] != kBad) {
+          const uint32_t key = k[i] & 0x3fffffu;
+          stage[wcnt[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+        }
     }
     __syncthreads();
-    if (threadIdx.x < B) gpos[threadIdx.x] += bofs[threadIdx.x + 1] - bofs[threadIdx.x];
+    const uint32_t nvld = bofs[B];  // valid keys of the sub-tile (bad keys were dropped)
+    if (nvld == kPartTile) {
+#pragma unroll
+      for (uint32_t r = 0; r < kPartKPT; ++r) {
+        const uint32_t j = r * kPartThreads + threadIdx.x, key = stage[j];
+        __stcs(out + (delta[key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
+        const uint32_t key = stage[j];
+        __stcs(out + (delta[key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
+      }
+    }
+    // the next sub-tile's first barrier orders these stage / delta reads before their rewrite
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = kn[i];
   }
-  (void)lane;
   pdl_trigger();
 }
 
