@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
                                                                uint32_t B, PartWs w, uint16_t* __restrict__ tmp) {
   constexpr uint32_t NW = kPartThreads / 32;
   constexpr uint32_t kBad = 0xffffffffu;
-  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];  // counts, then slot bases
+  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];   // per-warp block counts of the sub-tile
+  __shared__ uint32_t wbase[NW][kPartMaxBlocks];  // their slot bases in the staged sub-tile
   __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks], delta[kPartMaxBlocks];
   __shared__ uint32_t stage[kPartTile];
   pdl_wait();
@@ -173,12 +174,15 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
     }
   };
   unsigned short* const out = reinterpret_cast<unsigned short*>(tmp);
+  for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
   uint32_t k[kPartKPT], kn[kPartKPT];
   if (lo < hi) load(lo, k);
+  // Three barriers per sub-tile: count | scan (warp 0) | stage | write-out + next count.
+  // wcnt is zeroed by the scan warp once read, so the next sub-tile's counting (which
+  // touches only wcnt) follows the write-out without a barrier between them.
   for (uint64_t t0 = lo; t0 < hi; t0 += kPartTile) {
     if (t0 + kPartTile < hi) load(t0 + kPartTile, kn);  // next sub-tile in flight
-    for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
     uint32_t kmax = 0;
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) kmax = max(kmax, k[i]);
@@ -191,50 +195,53 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
         k[i] = k[i] < U ? k[i] | (atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22) : kBad;
     }
     __syncthreads();
-    // scan over (block, warp) pairs q = block * NW + warp: thread t handles the QP consecutive
-    // pairs QP t .. QP t + QP - 1 (B * NW <= 64 * 16 = 2 * kPartThreads)
-    {
-      constexpr uint32_t QP = (kPartMaxBlocks * NW + kPartThreads - 1) / kPartThreads;
-      uint32_t v[QP], sum = 0;
+    if (warp == 0) {
+      // lane l owns blocks l and l + 32: block totals over the NW warps, one warp scan of
+      // the totals (block order), then the per-warp slot bases of each owned block.
+      const uint32_t lane = threadIdx.x & 31;
+      uint32_t t[2] = {0u, 0u};
+      const uint32_t nh = B > 32 ? 2u : 1u;
+      for (uint32_t h = 0; h < nh; ++h) {
+        const uint32_t b = lane + 32 * h;
+        if (b < B) {
 #pragma unroll
-      for (uint32_t j = 0; j < QP; ++j) {
-        const uint32_t q = QP * threadIdx.x + j;
-        v[j] = q < B * NW ? wcnt[q % NW][q / NW] : 0u;
-        sum += v[j];
-      }
-      __shared__ uint32_t red[34];
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t>(sum, tot, red);
-#pragma unroll
-      for (uint32_t j = 0; j < QP; ++j) {
-        const uint32_t q = QP * threadIdx.x + j, bq = q / NW, wq = q % NW;
-        if (q < B * NW) {
-          wcnt[wq][bq] = ex;  // slot base of warp wq in block bq
-          if (wq == 0) bofs[bq] = ex;
+          for (uint32_t q = 0; q < NW; ++q) t[h] += wcnt[q][b];
         }
-        ex += v[j];
       }
-      if (threadIdx.x == 0) bofs[B] = tot;
+      const uint32_t i0 = warp_incl_scan(t[0]), i1 = nh > 1 ? warp_incl_scan(t[1]) : 0u;
+      const uint32_t s0 = __shfl_sync(0xffffffffu, i0, 31);
+      const uint32_t ex[2] = {i0 - t[0], s0 + i1 - t[1]};
+      for (uint32_t h = 0; h < nh; ++h) {
+        const uint32_t b = lane + 32 * h;
+        if (b < B) {
+          uint32_t base = ex[h];
+          bofs[b] = base;
+          delta[b] = gpos[b] - base;  // staged slot j of block b goes to position delta[b] + j
+          gpos[b] += t[h];
+#pragma unroll
+          for (uint32_t q = 0; q < NW; ++q) {
+            const uint32_t x = wcnt[q][b];
+            wbase[q][b] = base;
+            wcnt[q][b] = 0;
+            base += x;
+          }
+        }
+      }
+      if (lane == 31) bofs[B] = s0 + (nh > 1 ? i1 : 0u);  // lane 31 holds both totals
     }
     __syncthreads();
-    // staged slot j of block b goes to position delta[b] + j (positions < n < 2^32)
-    if (threadIdx.x < B) {
-      const uint32_t b = threadIdx.x;
-      delta[b] = gpos[b] - bofs[b];
-      gpos[b] += bofs[b + 1] - bofs[b];
-    }
     if (kmax < U) {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i) {
         const uint32_t key = k[i] & 0x3fffffu;
-        stage[wcnt[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+        stage[wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
       }
     } else {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i)
         if (k[i] != kBad) {
           const uint32_t key = k[i] & 0x3fffffu;
-          stage[wcnt[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+          stage[wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
         }
     }
     __syncthreads();
@@ -251,7 +258,8 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
         __stcs(out + (delta[key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
       }
     }
-    // the next sub-tile's first barrier orders these stage / delta reads before their rewrite
+    // the next sub-tile's count barrier orders these stage / delta / bofs reads before the
+    // scan warp and the staging rewrite them
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = kn[i];
   }
