@@ -446,7 +446,7 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   int rc;
   const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
 #ifndef DIALSORT_PART_CTAS_PER_SM
-#define DIALSORT_PART_CTAS_PER_SM 4
+#define DIALSORT_PART_CTAS_PER_SM (2048 / DIALSORT_PART_THREADS)
 #endif
   const uint32_t Gp = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t)DIALSORT_PART_CTAS_PER_SM * c->nsm, cdiv(n, kPartTile)));

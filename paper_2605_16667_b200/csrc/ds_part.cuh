@@ -22,7 +22,10 @@ namespace ds {
 
 constexpr uint32_t kPartShift = 16;         // 65536-bin universe blocks
 constexpr uint32_t kPartMaxBlocks = 64;     // U <= 2^22 take this path (larger: the L2 path)
-constexpr uint32_t kPartThreads = 512;
+#ifndef DIALSORT_PART_THREADS
+#define DIALSORT_PART_THREADS 512
+#endif
+constexpr uint32_t kPartThreads = DIALSORT_PART_THREADS;
 constexpr uint32_t kPartKPT = 8;            // keys per thread per scatter sub-tile
 constexpr uint32_t kPartTile = kPartThreads * kPartKPT;  // 4096
 
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
 // The chunk interior must be 16-byte aligned for the vector loads; other chunks take the
 // scalar path (keys of an unaligned base).
 #ifndef DIALSORT_PART_MINB
-#define DIALSORT_PART_MINB 4  // 4 CTAs per SM (32 registers): more loads in flight (c4 6.44 -> 6.19 ms)
+#define DIALSORT_PART_MINB (2048 / DIALSORT_PART_THREADS)  // 4 CTAs per SM (32 registers): more loads in flight (c4 6.44 -> 6.19 ms)
 #endif
 __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatter(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
                                                                uint32_t B, PartWs w, uint16_t* __restrict__ tmp) {

@@ -669,11 +669,11 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass3(const uint32_t
 // with one bulk copy (cp.async.bulk, completion on an mbarrier) instead of 16 scalar loads
 // per thread (ncu: those loads were the top stall, LSU queue full).  The copy of sub-tile
 // k+1 is issued as soon as sub-tile k's keys are in registers (after its counting), so it
-// overlaps the ranking and the write-out; one stage buffer and one lane-mask buffer keep the
-// footprint at ~98 KB (2 CTAs per SM).  Requires src 16-byte aligned.
+// overlaps the ranking and the write-out.  Ranking is the counting atomic itself: its
+// returned value is the key's rank among its warp's keys of the digit (no lane-mask
+// grouping pass).  One stage buffer, ~82 KB (2 CTAs per SM).  Requires src 16-byte aligned.
 struct Radix4Smem {
-  uint32_t wcur[kRadixWarps][256];   // per-warp digit counts -> cursors (16 KB)
-  uint32_t wmask[kRadixWarps][256];  // equality-grouping lane masks (16 KB)
+  uint32_t wcur[kRadixWarps][256];   // per-warp digit counts -> slot bases (16 KB)
   uint32_t sorted[kR3Tile];          // sub-tile sorted by digit (32 KB)
   uint32_t stage[kR3Tile + 4];       // staged sub-tile (+ alignment shift) (32 KB)
   uint32_t dstart[257];
@@ -695,7 +695,6 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
   const uint32_t dsel = 0x4440u | (uint32_t)p;
   const uint32_t flip_in = p == 0 ? kSignFlip : 0u, flip_out = p == 3 ? kSignFlip : 0u;
   const uint32_t lo = (uint32_t)((uint64_t)n * c / G), hi = (uint32_t)((uint64_t)n * (c + 1) / G);
-  for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&S.wmask[0][0])[i] = 0;
   if (threadIdx.x == 0) {
     mbar_init(&S.bar, 1);
     mbar_fence_init();
@@ -794,12 +793,16 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
     phase ^= 1u;
     __syncthreads();  // staged keys (bulk + edges) visible; wcur cleared
     const uint32_t wseg = warp * 32 * kR3KPT;
-    uint32_t k[kR3KPT];
+    // the returned counter value is the key's rank among its warp's keys of that digit
+    // (< 32 kR3KPT), two ranks per register; slot = the warp's digit base + rank
+    uint32_t k[kR3KPT], rk[kR3KPT / 2];
 #pragma unroll
     for (int i = 0; i < kR3KPT; ++i) {
       const uint32_t j = wseg + i * 32 + lane;
       k[i] = j < tn ? (S.stage[sft + j] ^ flip_in) : 0u;
-      if (j < tn) atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u);
+      const uint32_t r = j < tn ? atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u) : 0u;
+      if (i & 1) rk[i >> 1] |= r << 16;
+      else rk[i >> 1] = r;
     }
     __syncthreads();  // counts complete; the stage buffer is free
     if (t0 + kR3Tile < hi) issue(t0 + kR3Tile);
@@ -825,35 +828,13 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
     if (threadIdx.x < 256) S.gdel[threadIdx.x] = (int32_t)(S.grun[threadIdx.x] - S.dstart[threadIdx.x]);
     if (wseg + 32 * kR3KPT <= tn) {
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i) {
-        const uint32_t d = __byte_perm(k[i], 0, dsel);
-        uint32_t* wm = &S.wmask[warp][d];
-        atomicOr(wm, 1u << lane);
-        __syncwarp();
-        const uint32_t g = *wm;
-        const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
-        __syncwarp();
-        if (lane == (uint32_t)(__ffs(g) - 1)) {
-          S.wcur[warp][d] = pos + __popc(g);
-          *wm = 0u;
-        }
-        S.sorted[pos] = k[i];
-        __syncwarp();  // the mask word is clear before the next step's atomicOr
-      }
+      for (int i = 0; i < kR3KPT; ++i)
+        S.sorted[S.wcur[warp][__byte_perm(k[i], 0, dsel)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     } else {
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i) {
-        const uint32_t idx0 = wseg + i * 32;
-        const uint32_t vmask = idx0 >= tn ? 0u : (tn - idx0 >= 32 ? FULL : ((1u << (tn - idx0)) - 1u));
-        if ((vmask >> lane) & 1u) {
-          const uint32_t d = __byte_perm(k[i], 0, dsel);
-          const uint32_t g = digit_group(d, vmask);
-          const uint32_t pos = S.wcur[warp][d] + __popc(g & lt);
-          __syncwarp(vmask);
-          if (lane == (uint32_t)(__ffs(g) - 1)) S.wcur[warp][d] = pos + __popc(g);
-          S.sorted[pos] = k[i];
-        }
-      }
+      for (int i = 0; i < kR3KPT; ++i)
+        if (wseg + i * 32 + lane < tn)
+          S.sorted[S.wcur[warp][__byte_perm(k[i], 0, dsel)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
