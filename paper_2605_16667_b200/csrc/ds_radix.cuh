@@ -796,13 +796,24 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
     // the returned counter value is the key's rank among its warp's keys of that digit
     // (< 32 kR3KPT), two ranks per register; slot = the warp's digit base + rank
     uint32_t k[kR3KPT], rk[kR3KPT / 2];
+    if (wseg + 32 * kR3KPT <= tn) {
+      const uint32_t* sk = S.stage + sft + wseg + lane;
 #pragma unroll
-    for (int i = 0; i < kR3KPT; ++i) {
-      const uint32_t j = wseg + i * 32 + lane;
-      k[i] = j < tn ? (S.stage[sft + j] ^ flip_in) : 0u;
-      const uint32_t r = j < tn ? atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u) : 0u;
-      if (i & 1) rk[i >> 1] |= r << 16;
-      else rk[i >> 1] = r;
+      for (int i = 0; i < kR3KPT; ++i) {
+        k[i] = sk[i * 32] ^ flip_in;
+        const uint32_t r = atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u);
+        if (i & 1) rk[i >> 1] |= r << 16;
+        else rk[i >> 1] = r;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kR3KPT; ++i) {
+        const uint32_t j = wseg + i * 32 + lane;
+        k[i] = j < tn ? (S.stage[sft + j] ^ flip_in) : 0u;
+        const uint32_t r = j < tn ? atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u) : 0u;
+        if (i & 1) rk[i >> 1] |= r << 16;
+        else rk[i >> 1] = r;
+      }
     }
     __syncthreads();  // counts complete; the stage buffer is free
     if (t0 + kR3Tile < hi) issue(t0 + kR3Tile);
@@ -837,9 +848,17 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
           S.sorted[S.wcur[warp][__byte_perm(k[i], 0, dsel)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
-      const uint32_t u = S.sorted[j];
-      __stcs(dst + (int64_t)S.gdel[__byte_perm(u, 0, dsel)] + j, u ^ flip_out);
+    if (tn == (uint32_t)kR3Tile) {  // full sub-tile: unrolled, 32-bit output index (n < 2^32)
+#pragma unroll
+      for (int r = 0; r < kR3KPT; ++r) {
+        const uint32_t j = r * kRadixThreads + threadIdx.x, u = S.sorted[j];
+        __stcs(dst + (uint32_t)(S.gdel[__byte_perm(u, 0, dsel)] + (int32_t)j), u ^ flip_out);
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+        const uint32_t u = S.sorted[j];
+        __stcs(dst + (int64_t)S.gdel[__byte_perm(u, 0, dsel)] + j, u ^ flip_out);
+      }
     }
     __syncthreads();
     if (threadIdx.x < 256) S.grun[threadIdx.x] += S.dstart[threadIdx.x + 1] - S.dstart[threadIdx.x];
