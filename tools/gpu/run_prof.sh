@@ -13,5 +13,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_so
   python tools/prof_step.py --config c2 > gpurun_out/ncu_full_c2.log 2>&1; echo full_c2=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_part_scatter -s 1 -c 1 -f -o gpurun_out/full_c4 \
   python tools/prof_step.py --config c4 > gpurun_out/ncu_full_c4.log 2>&1; echo full_c4=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sort_fused -s 17 -c 1 -f -o gpurun_out/full_c4f \
+  python tools/prof_step.py --config c4 > gpurun_out/ncu_full_c4f.log 2>&1; echo full_c4f=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_radix_pass -s 4 -c 1 -f -o gpurun_out/full_c5 \
   python tools/prof_step.py --config c5 > gpurun_out/ncu_full_c5.log 2>&1; echo full_c5=$?

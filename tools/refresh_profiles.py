@@ -21,10 +21,11 @@ with open(P + f"{tag}_ncu_launches_bench_summary.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none of: python bench.py --steps 2 --warmup 3 "
             "(default c2 workload)\n")
     f.write(run(sys.executable, "tools/launch_summary.py", G + "launches_bench.csv"))
-for c in ("c2", "c4", "c5"):
+for c in ("c2", "c4", "c4f", "c5"):
     with open(P + f"{tag}_ncu_full_{c}_summary.txt", "w") as f:
-        f.write(f"# ncu --set full --clock-control none --import-source on, one launch of the dominant kernel of "
-                f"tools/prof_step.py --config {c} (same kernels and launch configuration as bench.py {c})\n")
+        what = "one hierarchical block launch of k_sort_fused" if c == "c4f" else "one launch of the dominant kernel"
+        f.write(f"# ncu --set full --clock-control none --import-source on, {what} of "
+                f"tools/prof_step.py --config {c[:2]} (same kernels and launch configuration as bench.py {c[:2]})\n")
         f.write(run(sys.executable, "tools/ncu_summary.py", G + f"full_{c}.ncu-rep"))
 with open(P + f"{tag}_phase_times.txt", "w") as f:
     f.write("# tools/phase_times.py <config> (libdialsort_phase.so: -DDIALSORT_PHASE_MARKS=1), one isolated step, "
@@ -47,9 +48,10 @@ def metrics(rep):
 
 
 tr = json.load(open(P + f"{tag}_ncu_traffic.json"))
-for c, k in (("c2", "k_sort_fused"), ("c4", "k_part_scatter"), ("c5", "k_radix_pass")):
-    rd, wr, t = metrics(G + f"full_{c}.ncu-rep")
-    e = tr["configs"][c][k]
+for c, k, rep in (("c2", "k_sort_fused", "c2"), ("c4", "k_part_scatter", "c4"), ("c4", "k_sort_fused", "c4f"),
+                  ("c5", "k_radix_pass", "c5")):
+    rd, wr, t = metrics(G + f"full_{rep}.ncu-rep")
+    e = tr["configs"][c].setdefault(k, {})
     e["dram_read_bytes"], e["dram_write_bytes"], e["ncu_duration_us"] = int(rd), int(wr), round(t, 3)
 json.dump(tr, open(P + f"{tag}_ncu_traffic.json", "w"), indent=1)
 print("profiles refreshed")
