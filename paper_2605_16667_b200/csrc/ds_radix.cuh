@@ -777,7 +777,6 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
       if (bytes) tma_load_1d(S.stage + (ab - (t0 & ~3u)), src + ab, bytes, &S.bar, pol);
     }
   };
-  const uint32_t lt = (1u << lane) - 1u;
   uint32_t phase = 0;
   __syncthreads();
   if (lo < hi) issue(lo);
