@@ -121,6 +121,31 @@ __device__ __forceinline__ uint32_t count_below(const uint32_t* Ps, uint32_t m, 
 __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
                                            bool aligned, uint64_t pol, bool full = false) {
   const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
+  if (full && !aligned) {
+    // Warp-cooperative (all 32 lanes, p = p_0 + 4 lane, the 128 positions inside [lo, hi)):
+    // out is 4-byte but not 16-byte aligned (a hierarchical block's output starts at the
+    // block's offset), shifted by sh elements.  Lane L stores the aligned quad at
+    // p + 4 - sh: its own last sh values and lane L+1's first 4 - sh; lane 0 stores the
+    // head p .. p + 3 - sh and lane 31 the tail p + 4 - sh .. p + 3 as scalars.
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) >> 2) & 3u, lane = threadIdx.x & 31u;
+    const int nx = __shfl_down_sync(0xffffffffu, v.x, 1), ny = __shfl_down_sync(0xffffffffu, v.y, 1),
+              nz = __shfl_down_sync(0xffffffffu, v.z, 1);
+    if (lane < 31) {
+      const int4 w = sh == 1 ? make_int4(v.w, nx, ny, nz) : sh == 2 ? make_int4(v.z, v.w, nx, ny)
+                                                              : make_int4(v.y, v.z, v.w, nx);
+      st_stream4(reinterpret_cast<int4*>(out + p + 4 - sh), w);
+    } else {
+      if (sh == 3) out[p + 1] = v.y;
+      if (sh >= 2) out[p + 2] = v.z;
+      out[p + 3] = v.w;
+    }
+    if (lane == 0) {
+      out[p] = v.x;
+      if (sh <= 2) out[p + 1] = v.y;
+      if (sh == 1) out[p + 2] = v.z;
+    }
+    return;
+  }
   if (full || (aligned && p >= lo && p + 4 <= hi)) {
 #if DIALSORT_PROJ_STORE == 1
     st_stream4(reinterpret_cast<int4*>(out + p), v);  // no L2 hint
@@ -157,7 +182,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
   uint32_t sreg = Ps[cb + lane];
   for (;;) {
     const uint32_t bend = hi - sb > SB ? sb + SB - 1 : hi - 1;
-    const bool full = aligned && sb >= lo && hi - sb >= SB;  // every quad in [lo, hi)
+    const bool full = sb >= lo && hi - sb >= SB;  // every quad in [lo, hi) (any alignment)
     if (c - cb >= 16) {  // keep >= 16 lanes of look-ahead in the window
       cb = c;
       sreg = Ps[cb + lane];
@@ -305,7 +330,7 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
       const uint4 e = T[j];
       const uint32_t c0 = e.x & 0x7fffffffu;
       if (!(e.x >> 31)) {
-        const bool full = aligned && b0 >= lo && hi - b0 >= 128;
+        const bool full = b0 >= lo && hi - b0 >= 128;  // (any alignment: store_quad realigns)
         const uint32_t below = __popc(e.y & ltmask), own = (e.y >> lane) & 1u;
         const uint32_t r = ((lane < 16 ? e.z : e.w) >> (2 * (lane & 15u))) & 3u;
         const uint32_t v = kbase + c0 + below;
