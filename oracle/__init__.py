@@ -61,6 +61,7 @@ def _L():
         lib.oracle_radix_pass.argtypes = [P, u64, ci, P]
         lib.oracle_radix_pass.restype = None
         lib.oracle_radix_sort_i32.argtypes = [P, u64, P, P]
+        lib.oracle_sharded_radix_rank.argtypes = [P, u64, ci, ci, P, u64, P, P, P]
         lib.oracle_range_count.argtypes = [P, u64, u64]
         lib.oracle_range_count.restype = u64
         lib.oracle_support_set.argtypes = [P, u64, P]
@@ -191,6 +192,21 @@ def radix_sort_i32(keys, return_passes: bool = False):
     if return_passes:
         return out[: k.size], passes[:, : k.size]
     return out[: k.size]
+
+
+def sharded_radix_rank(keys, G: int, g: int):
+    """O4' reading R19: (out int32, count, global offset, D[0..G]) of rank g of G."""
+    k = _keys(keys)
+    out = np.empty(max(k.size, 1), dtype=np.int32)
+    cnt = np.zeros(1, dtype=np.uint64)
+    off = np.zeros(1, dtype=np.uint64)
+    D = np.zeros(9, dtype=np.uint32)
+    rc = _L().oracle_sharded_radix_rank(_ptr(k), k.size, int(G), int(g), _ptr(out), k.size, _ptr(cnt), _ptr(off),
+                                        _ptr(D))
+    if rc != OK:
+        raise OracleError(rc, f"oracle_sharded_radix_rank rc={rc}")
+    c = int(cnt[0])
+    return out[:c], c, int(off[0]), D[: int(G) + 1].astype(np.int64)
 
 
 def range_count(H, a: int, b: int) -> int:

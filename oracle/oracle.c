@@ -216,6 +216,59 @@ int oracle_radix_sort_i32(const int32_t *in, uint64_t n, int32_t *out, uint32_t 
   return ORACLE_OK;
 }
 
+/* O4' — DialSort-Radix sharded over G ranks (reading R19 of DESIGN.md; the paper is single-host:
+ * its lanes take disjoint key shards, thm:par proof P:678-680, and DialSort-Radix is "LSD, base
+ * 256, 4 passes").  Rank r holds the contiguous shard [r n/G, (r+1) n/G).  Step by step:
+ *   1. C[d] = number of keys whose biased top byte (u >> 24, u = x XOR 0x80000000) is d
+ *      (eq:ingestion with U = 256 over all shards);
+ *   2. rank r owns the contiguous top-byte range [D[r], D[r+1]): D[0] = 0, D[G] = 256, and for
+ *      0 < r < G, D[r] = the smallest d whose exclusive prefix Σ_{j<d} C[j] reaches floor(r n / G)
+ *      (256 when no d does);
+ *   3. rank g's output = DialSort-Radix (A8) of the keys whose top byte lies in its range; its
+ *      count and its global offset = Σ_{d < D[g]} C[d].
+ * The rank-order concatenation of the outputs is the sorted array. */
+int oracle_sharded_radix_rank(const int32_t *keys, uint64_t n, int G, int g, int32_t *out,
+                              uint64_t out_cap, uint64_t *out_count, uint64_t *out_offset,
+                              uint32_t *D_out) {
+  uint64_t C[256], D[9], i, d, run, cnt = 0, off = 0;
+  int r, rc;
+  if (G <= 0 || G > 8 || g < 0 || g >= G) return ORACLE_E_INVALID_ARG;
+  for (d = 0; d < 256; d++) C[d] = 0;
+  for (i = 0; i < n; i++) {
+    d = oracle_radix_bias(keys[i]) >> 24;
+    C[d] = C[d] + 1;
+  }
+  D[0] = 0;
+  D[G] = 256;
+  for (r = 1; r < G; r++) {
+    uint64_t target = (uint64_t)r * n / (uint64_t)G;
+    D[r] = 256;
+    run = 0;
+    for (d = 0; d < 256; d++) {
+      if (run >= target) { D[r] = d; break; }
+      run = run + C[d];
+    }
+  }
+  for (r = 0; r <= G; r++) if (D_out) D_out[r] = (uint32_t)D[r];
+  for (d = 0; d < D[g]; d++) off += C[d];
+  for (d = D[g]; d < D[g + 1]; d++) cnt += C[d];
+  *out_count = cnt;
+  *out_offset = off;
+  if (cnt > out_cap) return ORACLE_E_SIZE;
+  {
+    int32_t *sel = (int32_t *)malloc((cnt ? cnt : 1) * sizeof(int32_t));
+    uint64_t m = 0;
+    if (!sel) return ORACLE_E_INVALID_ARG;
+    for (i = 0; i < n; i++) {
+      d = oracle_radix_bias(keys[i]) >> 24;
+      if (d >= D[g] && d < D[g + 1]) { sel[m] = keys[i]; m = m + 1; }
+    }
+    rc = oracle_radix_sort_i32(sel, m, out, NULL);
+    free(sel);
+    return rc;
+  }
+}
+
 /* NEXT-1 canonical-state queries on H: frequency(k) = H[k], presence(k) =
  * H[k] > 0, range-count(a,b) = Σ_{k=a}^{b} H[k] (O(b-a)), support set D = {k : H(k) > 0}
  * (P:326-329).  Returns |D| and writes D ascending into D_out (capacity U). */

@@ -219,3 +219,56 @@ def test_sharded_concatenation_is_the_sort(G):
         off_expect += cnt
         pieces.append(out)
     assert np.concatenate(pieces).tolist() == sorted(keys.tolist())
+
+
+# ---- O4' sharded DialSort-Radix (reading R19) -------------------------------------------------
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_sharded_radix_concatenation_is_the_sort(G):
+    """Against Python's sorted (independent of the oracle's own radix): the rank-order
+    concatenation is the sort, offsets are running counts, every rank's keys lie in its own
+    contiguous top-byte range, and the ranges tile [0, 256)."""
+    rng = np.random.default_rng(70 + G)
+    for trial in range(12):
+        n = int(rng.choice([0, 1, 5, 257, 4000, 30001]))
+        kind = trial % 4
+        if kind == 0:
+            x = rng.integers(-2 ** 31, 2 ** 31, size=n, dtype=np.int64).astype(np.int32)
+        elif kind == 1:
+            x = rng.integers(-3, 3, size=n).astype(np.int32)          # two top bytes only
+        elif kind == 2:
+            x = np.full(n, 2 ** 31 - 1, dtype=np.int32)                # one top byte
+        else:
+            x = (rng.integers(0, 4, size=n) * 0x40000000 - 2 ** 31).astype(np.int32)  # 4 hot top bytes
+        pieces, off = [], 0
+        prevD = None
+        for g in range(G):
+            out, cnt, o, D = oracle.sharded_radix_rank(x, G, g)
+            assert D[0] == 0 and D[G] == 256 and all(D[i] <= D[i + 1] for i in range(G))
+            assert prevD is None or list(D) == prevD
+            prevD = list(D)
+            assert o == off and cnt == out.size
+            tb = (out.view(np.uint32) ^ np.uint32(0x80000000)) >> 24
+            assert ((tb >= D[g]) & (tb < D[g + 1])).all()
+            off += cnt
+            pieces.append(out)
+        assert off == n
+        got = np.concatenate(pieces) if pieces else np.empty(0, np.int32)
+        assert got.tolist() == sorted(x.tolist())
+
+
+def test_sharded_radix_balance():
+    """Closed forms of step 2: with every top byte equally frequent the ranges are exact
+    256/G-byte blocks, and on uniform keys no rank is off n/G by more than one digit's count."""
+    G = 4
+    x = (np.repeat(np.arange(256, dtype=np.int64), 10) << 24) ^ 0x80000000
+    x = (x & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    for g in range(G):
+        _, cnt, o, D = oracle.sharded_radix_rank(x, G, g)
+        assert list(D) == [0, 64, 128, 192, 256] and cnt == 640 and o == 640 * g
+    x = synth.full_int32(100_000, seed=3)
+    C = np.bincount((x.view(np.uint32) ^ np.uint32(0x80000000)) >> 24, minlength=256)
+    for G in (2, 8):
+        for g in range(G):
+            _, cnt, _, _ = oracle.sharded_radix_rank(x, G, g)
+            assert abs(cnt - 100_000 / G) <= C.max() + 1
