@@ -224,13 +224,13 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2605_16667_b200 as dsl
-    from paper_2605_16667_b200.sharded import PeerExchange, sharded_sort, sharded_sort_p2p
+    from paper_2605_16667_b200.sharded import PeerComm, sharded_sort, sharded_sort_int32, sharded_sort_p2p
 
     n, U = cfg["n"], cfg["U"]
     radix = cfg["dist"] == "int32"
     G = world
-    if G > 1 and (radix or U % G):
-        raise SystemExit("multi-GPU bench supports the bounded-universe configs with U % G == 0")
+    if G > 1 and not radix and U % G:
+        raise SystemExit("multi-GPU bench needs U % G == 0 on the bounded-universe configs")
     lo, hi = rank * n // G, (rank + 1) * n // G
     n_loc = hi - lo
     ctx = dsl.Context(local, max_n=n_loc, max_U=max(U, 256))
@@ -243,24 +243,26 @@ def main():
         R = 2
     base = make_device_input(cfg, args.seed, dev, lo=lo, count=n_loc)
     ins = [base] + [base.clone() for _ in range(R - 1)]
-    cap = n_loc if G == 1 else min(n, 2 * n_loc + (1 << 20))
+    cap = n_loc if G == 1 else min(n, 2 * n_loc + (1 << 20))  # room for this rank's slice / range
     outs = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(R)]
     torch.cuda.synchronize()
 
     # N > 1: the exchange over peer memory (histogram kernel storing into the owners' slots over
     # NVLink / NVSwitch); --exchange nccl selects the NCCL reduce-scatter baseline
     ex = None
-    if G > 1 and args.exchange == "p2p":
-        ex = PeerExchange(U, dev, ctx=ctx)
+    if G > 1 and (args.exchange == "p2p" or radix):
+        ex = PeerComm(max(U, 1), dev, ctx=ctx, max_recv_keys=cap if radix else 0)
 
     def step(i):
         j = i % R
-        if radix:
+        if radix and G == 1:
             ctx.sort_int32(ins[j], out=outs[j])
+        elif radix:
+            sharded_sort_int32(ins[j], ex, capacity=cap, out=outs[j])
         elif G == 1:
             ctx.sort(ins[j], U, out=outs[j])
         elif ex is not None:
-            sharded_sort_p2p(ins[j], ex, capacity=cap, out=outs[j])
+            sharded_sort_p2p(ins[j], ex, U, capacity=cap, out=outs[j])
         else:
             sharded_sort(ins[j], U, capacity=cap, ctx=ctx, out=outs[j])
 

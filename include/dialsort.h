@@ -41,6 +41,7 @@ typedef enum {
   DIALSORT_E_SIZE = 3,        /* reconstruct: ΣH != n (exact) or ΣH > capacity          */
   DIALSORT_E_OVERFLOW = 4,    /* ΣH >= 2^32 in reconstruct                              */
   DIALSORT_E_CUDA = 5,        /* a CUDA runtime error (message: dialsort_last_error)     */
+  DIALSORT_E_COMM = 6,        /* multi-GPU: a peer did not reach the exchange in time     */
   DIALSORT_E_NOMEM = 7        /* workspace allocation failed                             */
 } dialsort_status;
 
@@ -48,7 +49,7 @@ typedef struct {
   uint64_t bad_count;       /* number of keys outside [0,U) seen since the last sync      */
   uint64_t first_bad_index; /* minimum offending index (UINT64_MAX if none)              */
   int32_t first_bad_key;    /* the key at first_bad_index                                */
-  uint32_t flags;           /* bit0 size error, bit1 overflow                            */
+  uint32_t flags;           /* bit0 size error, bit1 overflow, bit2 exchange timeout     */
   uint64_t last_total;      /* ΣH computed by the most recent reconstruct / sort         */
 } dialsort_error_info;
 
@@ -69,6 +70,30 @@ int dialsort_ctx_destroy(dialsort_ctx ctx);
 /* Block until `stream` drains, then report (and clear) the deferred device errors of all
  * work enqueued through `ctx`.  info may be NULL.  Returns the first error kind seen. */
 int dialsort_sync(dialsort_ctx ctx, dialsort_stream_t stream, dialsort_error_info* info);
+
+/* Context options.
+ *   DIALSORT_OPT_RADIX_VARIANT (read / write): 0 = automatic (default), 3 = k_radix_pass3
+ *     (in-warp ranks by explicit equality grouping: stable by construction), 4 = k_radix_pass4
+ *     (ranks from the counting shared atomic; needs 16-byte aligned buffers, else pass3).
+ *     Automatic uses pass4 only on a device whose lane-order probe (run once per device at
+ *     the first dialsort_ctx_create) found no violation, else pass3.
+ *   DIALSORT_OPT_RADIX_PROBE_VIOLATIONS (read): lanes of the probe whose atomic return value
+ *     broke lane order on this device (0 = pass4 is stable here).
+ *   DIALSORT_OPT_RADIX_ACTIVE (read): the variant an aligned radix call uses now (3 or 4).
+ *   DIALSORT_OPT_NUM_SMS (read): streaming multiprocessors of the context's device.
+ *   DIALSORT_OPT_COOPERATIVE (read / write): the kernels that synchronise their whole grid need it
+ *     co-resident.  0 (default): the library orders its co-resident launches of all contexts of a
+ *     device in one FIFO (a launch on another stream than the previous one waits for that stream's
+ *     enqueued work), so two of them never overlap; 1: cudaLaunchAttributeCooperative, which also
+ *     rejects a grid another tenant keeps from being co-resident (DIALSORT_E_CUDA) at ~2 us per
+ *     launch. */
+#define DIALSORT_OPT_RADIX_VARIANT 1
+#define DIALSORT_OPT_RADIX_PROBE_VIOLATIONS 2
+#define DIALSORT_OPT_RADIX_ACTIVE 3
+#define DIALSORT_OPT_NUM_SMS 4
+#define DIALSORT_OPT_COOPERATIVE 5
+int dialsort_ctx_set_option(dialsort_ctx ctx, int option, int64_t value);
+int dialsort_ctx_get_option(dialsort_ctx ctx, int option, int64_t* value);
 
 /* ---- the hot path (async: enqueue on `stream`, return after enqueue) ----------------- */
 
@@ -121,36 +146,109 @@ int dialsort_sort_host(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, u
 int dialsort_sort_host_async(dialsort_ctx ctx, const int32_t* keys_host, uint64_t n, uint32_t U,
                              int32_t* out_host, dialsort_stream_t stream);
 
-/* ---- multi-GPU exchange over peer memory (lem:crn P:951-962) -- */
-/* One rank of G (one process per GPU).  U % G == 0; universe slice s = [s L, (s+1) L), L = U/G,
- * is owned by rank s.  peer_recv: DEVICE array of G device pointers; peer_recv[s] is rank s's
- * receive buffer (uint32[G * L], mapped into this process with dialsort_ipc_open, or this
- * rank's own buffer for s == rank).  Computes the local histogram of keys[n] (device) and
- * stores its slice s into peer_recv[s][rank * L .. rank * L + L) for every s — on the
- * shared-memory paths (U <= 98304) the histogram kernel's merge stores each finished bin
- * straight into the owner's slot (P2P stores over NVLink / NVSwitch, overlapping the rest of
- * the merge); for larger U the local histogram is pushed by one copy kernel.  The writes are
- * complete when the stream's work completes; the owner reads its buffer only after every
- * rank's call completed (e.g. stream sync + a process-group barrier).  Errors as
- * dialsort_histogram_async (E_KEY_RANGE deferred), E_INVALID_ARG for bad G / rank. */
-int dialsort_histogram_scatter_async(dialsort_ctx ctx, const int32_t* keys, uint64_t n, uint32_t U,
-                                     uint32_t G, uint32_t rank, uint32_t* const* peer_recv,
-                                     dialsort_stream_t stream);
-/* The owner's step: H_slice[j] = sum over src < G of recv[src * L + j] (device buffers). */
-int dialsort_slice_sum_async(dialsort_ctx ctx, const uint32_t* recv, uint32_t G, uint32_t L,
-                             uint32_t* H_slice, dialsort_stream_t stream);
-/* CUDA IPC of a device allocation (cudaIpcGetMemHandle / cudaIpcOpenMemHandle with lazy peer
- * access / cudaIpcCloseMemHandle) on the context's device; handles are
- * DIALSORT_IPC_HANDLE_BYTES opaque bytes (host memory) exchanged by the caller. */
-#define DIALSORT_IPC_HANDLE_BYTES 64
-int dialsort_ipc_handle(dialsort_ctx ctx, const void* dev_ptr, void* handle_out);
-int dialsort_ipc_open(dialsort_ctx ctx, const void* handle, void** dev_ptr_out);
-int dialsort_ipc_close(dialsort_ctx ctx, void* dev_ptr);
+/* ---- multi-GPU over peer memory --------------------------- */
+/* One rank of G <= 8 per GPU.  Rank g holds a contiguous shard of the keys (thm:par proof, "distribute
+ * the n keys across k ingestion lanes").  Histogram path (reading R10): universe slice
+ * s = [s L, (s+1) L), L = U / G, is owned by rank s; each rank's local histogram slice s is stored
+ * into rank s's receive slot (the reduce-scatter of the local histograms, lem:crn lifted to whole
+ * histograms P:951-962; the WSE-3 "tile k owns H[k]" idea P:1449-1459 with GPUs as owners); rank s
+ * sums its G slots and projects its slice with key_base s L; the rank-order concatenation of the
+ * outputs is the sorted array (offset of rank g = Σ_{r<g} count_r).  Radix path (DialSort-Radix at
+ * G > 1): top-digit histograms all-gathered, contiguous top-byte ranges per rank balanced by counts,
+ * every key stored straight into its owner's receive buffer (the all-to-all), local 4-pass LSD.
+ *
+ * Communicator: a symmetric device workspace per rank (allocated by the library; completion flags
+ * tagged with the call's epoch, two parities of every buffer), mapped into every rank either by
+ * CUDA IPC (one process per GPU: exchange the DIALSORT_COMM_HANDLE_BYTES handle bytes with any host
+ * channel, e.g. torch.distributed.all_gather_object) or by pointer (several communicators of one
+ * process).  All ranks must issue the same sequence of sharded calls.  There is no host barrier:
+ * a rank's kernels wait on device flags for its peers (giving up after 20 s: DIALSORT_E_COMM at the
+ * next dialsort_sync).  Calls on one communicator must be serialised on one stream.
+ *
+ * dialsort_comm_create: G in [1, 8], rank < G.  max_U: the largest universe of a histogram call
+ *   (L = U / G <= ceil(max_U / G)); max_recv_keys: the radix receive capacity (keys a rank may
+ *   receive; 0 if the radix path is unused).  handle_out (host, nullable) receives this rank's
+ *   DIALSORT_COMM_HANDLE_BYTES handle bytes.
+ * dialsort_comm_connect_ipc: handles = the G ranks' handle bytes in rank order (host memory).
+ * dialsort_comm_connect_local: peers = the G communicators (rank order) of this process, e.g. G
+ *   virtual ranks on one GPU (the loopback test harness) or G GPUs driven by one process. */
+#define DIALSORT_COMM_HANDLE_BYTES 128
+typedef struct dialsort_comm_s* dialsort_comm; /* opaque */
+int dialsort_comm_create(dialsort_ctx ctx, uint32_t G, uint32_t rank, uint32_t max_U, uint64_t max_recv_keys,
+                         void* handle_out, dialsort_comm* out);
+int dialsort_comm_connect_ipc(dialsort_comm comm, const void* handles);
+int dialsort_comm_connect_local(dialsort_comm comm, const dialsort_comm* peers);
+int dialsort_comm_destroy(dialsort_comm comm);
+int dialsort_comm_info(dialsort_comm comm, uint32_t* G, uint32_t* rank, uint32_t* epoch);
+
+/* Sharded DialSort, step by step (each step enqueues on `stream` and returns; steps that wait for
+ * peers do so on the device):
+ *   scatter  (starts a call) local histogram of keys[n] (device; U % G == 0), slice s stored into
+ *            rank s's slot for this rank — the shared-memory and hierarchical universes store each
+ *            merged bin straight from the histogram kernel; larger ones push the local H — then this
+ *            rank's completion flag is raised in every peer;
+ *   gather   wait for the G slots, H_slice = their sum (uint32[U/G]; NULL: the communicator's own
+ *            buffer), the slice total all-gathered to every rank;
+ *   project  wait for the G totals, *d_count = ΣH_slice, *d_offset = Σ_{r<rank} count_r (device
+ *            uint64*, nullable), out[0 .. min(count, cap)) = projection of H_slice with key_base
+ *            rank * U/G; count > cap is DIALSORT_E_SIZE at the next sync.
+ * dialsort_sharded_sort_async = scatter + gather + project. */
+int dialsort_sharded_histogram_scatter_async(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n,
+                                             uint32_t U, dialsort_stream_t stream);
+int dialsort_sharded_histogram_gather_async(dialsort_ctx ctx, dialsort_comm comm, uint32_t U, uint32_t* H_slice,
+                                            dialsort_stream_t stream);
+int dialsort_sharded_project_async(dialsort_ctx ctx, dialsort_comm comm, uint32_t U, const uint32_t* H_slice,
+                                   int32_t* out, uint64_t cap, uint64_t* d_count, uint64_t* d_offset,
+                                   dialsort_stream_t stream);
+int dialsort_sharded_sort_async(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n, uint32_t U,
+                                int32_t* out, uint64_t cap, uint32_t* H_slice, uint64_t* d_count,
+                                uint64_t* d_offset, dialsort_stream_t stream);
+/* Sharded DialSort-Radix (full int32), step by step:
+ *   radix_hist   (starts a call) top-digit histogram of keys[n], all-gathered;
+ *   radix_split  wait for the G histograms, plan the top-byte ranges, d_count / d_offset (device,
+ *                nullable) = keys this rank receives / its global output offset, store every key
+ *                into its owner's receive buffer, raise this rank's flag;
+ *   radix_local  wait for every source, 4 LSD passes of the received keys into out (cap keys;
+ *                more than min(cap, max_recv_keys) received: DIALSORT_E_SIZE). */
+int dialsort_sharded_radix_hist_async(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n,
+                                      dialsort_stream_t stream);
+int dialsort_sharded_radix_split_async(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n,
+                                       uint64_t cap, uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream);
+int dialsort_sharded_radix_local_async(dialsort_ctx ctx, dialsort_comm comm, int32_t* out, uint64_t cap,
+                                       dialsort_stream_t stream);
+int dialsort_sharded_sort_int32_async(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n,
+                                      int32_t* out, uint64_t cap, uint64_t* d_count, uint64_t* d_offset,
+                                      dialsort_stream_t stream);
+/* Synchronous forms: as the async ones, then dialsort_sync; count / offset to host memory. */
+int dialsort_sharded_sort(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n, uint32_t U,
+                          int32_t* out, uint64_t cap, uint64_t* count_host, uint64_t* offset_host,
+                          dialsort_stream_t stream);
+int dialsort_sharded_sort_int32(dialsort_ctx ctx, dialsort_comm comm, const int32_t* keys, uint64_t n, int32_t* out,
+                                uint64_t cap, uint64_t* count_host, uint64_t* offset_host, dialsort_stream_t stream);
 
 /* ---- canonical-state queries on a device histogram (NEXT-1) ---------------- */
-/* d_result (device uint64*): Σ_{k=a}^{b} H[k], 0 <= a <= b < U. */
+/* The histogram is the canonical ordered state: "direct consumers of H can answer frequency(k)
+ * in O(1), presence(k) in O(1), and range-count(a,b) in O(b-a) without reconstructing a linear
+ * output array".  All buffers are device memory.
+ * dialsort_range_count_async: d_result (uint64*) = Σ_{k=a}^{b} H[k], 0 <= a <= b < U
+ *   (argument error otherwise, synchronous).
+ * dialsort_query_async (batched): op DIALSORT_Q_FREQUENCY / DIALSORT_Q_PRESENCE: q = m keys
+ *   (uint32), d_out[i] = H[q[i]] / (H[q[i]] > 0); op DIALSORT_Q_RANGE_COUNT: q = m pairs
+ *   (a_i, b_i) as uint32[2m], d_out[i] = Σ_{k=a_i}^{b_i} H[k] (one O(U) prefix, then O(1) per
+ *   query).  A query key outside [0,U) (or a_i > b_i) is a deferred DIALSORT_E_KEY_RANGE whose
+ *   info names the query index; its answer is 0.
+ * dialsort_support_set_async: the support set D = {k : H(k) > 0} ascending into
+ *   D_out (uint32[U]), |D| into *d_count (uint64), and into *d_iso (uint32, nullable) the
+ *   order-isomorphism condition of prop:iso: 1 iff D = [0, U-1]. */
+#define DIALSORT_Q_FREQUENCY 0
+#define DIALSORT_Q_PRESENCE 1
+#define DIALSORT_Q_RANGE_COUNT 2
 int dialsort_range_count_async(dialsort_ctx ctx, const uint32_t* H, uint32_t U, uint32_t a,
                                uint32_t b, uint64_t* d_result, dialsort_stream_t stream);
+int dialsort_query_async(dialsort_ctx ctx, const uint32_t* H, uint32_t U, int op, const uint32_t* q, uint64_t m,
+                         uint64_t* d_out, dialsort_stream_t stream);
+int dialsort_support_set_async(dialsort_ctx ctx, const uint32_t* H, uint32_t U, uint32_t* D_out, uint64_t* d_count,
+                               uint32_t* d_iso, dialsort_stream_t stream);
 
 /* ---- measurement hooks (bench.py's live per-kernel roofline) --------------------------- */
 /* enable != 0: record a CUDA event pair around every kernel this ctx launches (on the
@@ -171,6 +269,15 @@ int dialsort_debug_phase_ns(dialsort_ctx ctx, uint64_t* out16);
  * after the earliest start, 0 = not reached) into out[max_ctas * 17] (host); returns the number
  * of CTAs copied, or -status.  Reading resets the stamps (as dialsort_debug_phase_ns). */
 int dialsort_debug_phase_cta(dialsort_ctx ctx, uint64_t* out, int max_ctas);
+
+/* ---- test entry: DialSort-Radix pass buffers ------------------------------------------- */
+/* Runs the 4 passes of dialsort_sort_int32 on keys[n] with pass p writing pass_out + p n
+ * (device uint32[4n]) instead of ping-ponging: passes 0..2 hold the biased keys u = x ^ 0x80000000
+ * after the stable scatter by digits 0..p, pass 3 the sorted int32 keys (un-biased).  For the
+ * per-pass parity test against the oracle (after pass p the buffer is the stable sort by the low
+ * 8(p+1) bits, a unique array). */
+int dialsort_debug_radix_passes(dialsort_ctx ctx, const int32_t* keys, uint64_t n, uint32_t* pass_out,
+                                dialsort_stream_t stream);
 
 /* ---- test entry: the warp CRN primitive on explicit lane batches ---------------------- */
 /* lane_keys: int32[32*n_batches]; active: uint32[n_batches] lane masks.  For each batch, the

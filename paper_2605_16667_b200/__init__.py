@@ -17,8 +17,8 @@ from . import _lib
 from ._lib import ErrorInfo
 
 __all__ = [
-    "DialSortError", "Context", "histogram", "reconstruct", "sort", "sort_int32", "sort_host",
-    "range_count", "crn_resolve", "default_context", "LIB_PATH",
+    "DialSortError", "Context", "Comm", "histogram", "reconstruct", "sort", "sort_int32", "sort_host",
+    "range_count", "frequency", "presence", "support_set", "crn_resolve", "default_context", "LIB_PATH",
 ]
 
 LIB_PATH = _lib.LIB_PATH
@@ -49,6 +49,19 @@ def _stream(device: torch.device):
 def _keys(t: torch.Tensor, name: str = "keys") -> torch.Tensor:
     if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous int32 CUDA tensor")
+    return t
+
+
+def _dev_buf(t: torch.Tensor | None, name: str, like: torch.Tensor, min_numel: int,
+             dtypes=(torch.int32,)) -> torch.Tensor | None:
+    """Caller-provided device buffer: contiguous, of an allowed dtype, on `like`'s device, large
+    enough (the C ABI takes raw pointers: a short buffer would be overrun on the device)."""
+    if t is None:
+        return None
+    if t.dtype not in dtypes or not t.is_cuda or not t.is_contiguous() or t.device != like.device:
+        raise ValueError(f"{name} must be a contiguous {'/'.join(str(d) for d in dtypes)} tensor on {like.device}")
+    if t.numel() < min_numel:
+        raise ValueError(f"{name} holds {t.numel()} elements, needs >= {min_numel}")
     return t
 
 
@@ -88,6 +101,7 @@ class Context:
         _keys(keys)
         if H is None:
             H = torch.empty(int(U), dtype=torch.int32, device=keys.device)
+        _dev_buf(H, "H", keys, int(U))
         _check(_L.dialsort_histogram_async(self._h, _ptr(keys), keys.numel(), int(U), _ptr(H),
                                            _stream(keys.device)))
         return H
@@ -103,6 +117,8 @@ class Context:
                 n = int(H.to(torch.int64).sum().item())  # host-side sizing only
             out = torch.empty(int(n), dtype=torch.int32, device=H.device)
         cap = out.numel() if n is None else int(n)
+        _dev_buf(out, "out", H, cap)
+        _dev_buf(d_total, "d_total", H, 1, (torch.int64,))
         _check(_L.dialsort_reconstruct_async(self._h, _ptr(H), H.numel(), int(key_base), _ptr(out), cap,
                                              1 if exact else 0, _ptr(d_total), _stream(H.device)))
         return out
@@ -113,6 +129,8 @@ class Context:
         _keys(keys)
         if out is None:
             out = torch.empty_like(keys)
+        _dev_buf(out, "out", keys, keys.numel())
+        _dev_buf(H, "H", keys, int(U))
         _check(_L.dialsort_sort_async(self._h, _ptr(keys), keys.numel(), int(U), _ptr(out), _ptr(H),
                                       _stream(keys.device)))
         return out
@@ -122,6 +140,7 @@ class Context:
         _keys(keys)
         if out is None:
             out = torch.empty_like(keys)
+        _dev_buf(out, "out", keys, keys.numel())
         _check(_L.dialsort_sort_int32_async(self._h, _ptr(keys), keys.numel(), _ptr(out),
                                             _stream(keys.device)))
         return out
@@ -139,43 +158,59 @@ class Context:
         _check(fn(self._h, _ptr(keys_host), keys_host.numel(), int(U), _ptr(out_host), s))
         return out_host
 
-    # -- multi-GPU exchange over peer memory (sharded.py drives these) ----------------------------
-    def histogram_scatter(self, keys: torch.Tensor, U: int, G: int, rank: int, peers: torch.Tensor) -> None:
-        """Local histogram, universe slice s stored into peers[s] (device int64 array of G device
-        pointers to the owners' receive buffers) at slot `rank` (dialsort_histogram_scatter_async)."""
-        keys = _keys(keys)
-        if peers.dtype != torch.int64 or not peers.is_cuda or peers.numel() != G:
-            raise ValueError("peers must be a device int64 tensor of G pointers")
-        _check(_L.dialsort_histogram_scatter_async(self._h, _ptr(keys), keys.numel(), int(U), int(G), int(rank),
-                                                   _ptr(peers), _stream(self.device)))
+    # -- options -------------------------------------------------------------------------
+    def set_option(self, option: int, value: int) -> None:
+        _check(_L.dialsort_ctx_set_option(self._h, int(option), int(value)))
 
-    def slice_sum(self, recv: torch.Tensor, G: int, L: int, out: torch.Tensor | None = None) -> torch.Tensor:
-        """out[j] = Σ_src recv[src * L + j] (uint32 counts carried in int32 tensors)."""
-        if out is None:
-            out = torch.empty(L, dtype=torch.int32, device=recv.device)
-        _check(_L.dialsort_slice_sum_async(self._h, _ptr(recv), int(G), int(L), _ptr(out), _stream(self.device)))
-        return out
+    def get_option(self, option: int) -> int:
+        v = ctypes.c_int64()
+        _check(_L.dialsort_ctx_get_option(self._h, int(option), ctypes.byref(v)))
+        return int(v.value)
 
-    def ipc_handle(self, t: torch.Tensor) -> bytes:
-        buf = ctypes.create_string_buffer(64)
-        _check(_L.dialsort_ipc_handle(self._h, ctypes.c_void_p(t.data_ptr()), buf))
-        return buf.raw
+    @property
+    def radix_variant(self) -> int:
+        """The radix pass in use for aligned buffers: 4 (TMA, ranks from the counting atomic; only
+        on a device that passed the lane-order probe) or 3 (equality-grouped ranks)."""
+        return self.get_option(_lib.OPT_RADIX_ACTIVE)
 
-    def ipc_open(self, handle: bytes) -> int:
-        p = ctypes.c_void_p()
-        _check(_L.dialsort_ipc_open(self._h, ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
-        return int(p.value)
-
-    def ipc_close(self, ptr: int) -> None:
-        _check(_L.dialsort_ipc_close(self._h, ctypes.c_void_p(ptr)))
+    def debug_radix_passes(self, keys: torch.Tensor) -> torch.Tensor:
+        """The 4 pass buffers of DialSort-Radix (uint32 bits in an int32 [4, n] tensor): passes
+        0..2 biased keys, pass 3 the sorted int32 keys (dialsort_debug_radix_passes)."""
+        _keys(keys)
+        n = keys.numel()
+        out = torch.empty((4, max(n, 1)), dtype=torch.int32, device=keys.device)
+        _check(_L.dialsort_debug_radix_passes(self._h, _ptr(keys), n, _ptr(out), _stream(keys.device)))
+        return out[:, :n]
 
     def range_count(self, H: torch.Tensor, a: int, b: int, out: torch.Tensor | None = None) -> torch.Tensor:
         """range-count(a, b) = Σ_{k=a}^{b} H[k] on the canonical state."""
         if out is None:
             out = torch.empty(1, dtype=torch.int64, device=H.device)
+        _dev_buf(out, "out", H, 1, (torch.int64,))
         _check(_L.dialsort_range_count_async(self._h, _ptr(H), H.numel(), int(a), int(b), _ptr(out),
                                              _stream(H.device)))
         return out
+
+    def query(self, H: torch.Tensor, op: int, q: torch.Tensor) -> torch.Tensor:
+        """Batched canonical-state queries (dialsort_query_async): op Q_FREQUENCY / Q_PRESENCE with
+        m keys, or Q_RANGE_COUNT with m (a, b) pairs (q shaped [m, 2]); int64 answers."""
+        if q.dtype != torch.int32 or not q.is_cuda or not q.is_contiguous():
+            raise ValueError("q must be a contiguous int32 CUDA tensor")
+        m = q.numel() // 2 if op == _lib.Q_RANGE_COUNT else q.numel()
+        out = torch.empty(max(m, 1), dtype=torch.int64, device=H.device)
+        _check(_L.dialsort_query_async(self._h, _ptr(H), H.numel(), int(op), _ptr(q), m, _ptr(out),
+                                       _stream(H.device)))
+        return out[:m]
+
+    def support_set(self, H: torch.Tensor):
+        """(D, |D|, iso) on the device: D ascending occupied cells, iso = 1 iff D is
+        the whole universe (prop:iso).  D is valid in its first |D| entries."""
+        U = H.numel()
+        D = torch.empty(max(U, 1), dtype=torch.int32, device=H.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=H.device)
+        iso = torch.zeros(1, dtype=torch.int32, device=H.device)
+        _check(_L.dialsort_support_set_async(self._h, _ptr(H), U, _ptr(D), _ptr(cnt), _ptr(iso), _stream(H.device)))
+        return D, cnt, iso
 
     # -- measurement hooks ---------------------------------------------------------------
     def profile(self, enable: bool) -> None:
@@ -219,6 +254,97 @@ class Context:
         _check(_L.dialsort_crn_resolve_async(self._h, _ptr(lane_keys), _ptr(active), nb, _ptr(ok), _ptr(oc),
                                              _stream(lane_keys.device)))
         return ok, oc
+
+
+class Comm:
+    """A multi-GPU communicator (dialsort_comm) of one rank: a symmetric device workspace mapped
+    into every rank.  Build it with `create`, exchange `handle` bytes between the ranks (any host
+    channel), then `connect_ipc(all_handles)`; or, for several ranks in one process (the one-GPU
+    loopback harness), `connect_local(comms)`."""
+
+    def __init__(self, ctx: Context, G: int, rank: int, max_U: int, max_recv_keys: int = 0):
+        self.ctx, self.G, self.rank = ctx, int(G), int(rank)
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(_lib.COMM_HANDLE_BYTES)
+        with torch.cuda.device(ctx.device):
+            _check(_L.dialsort_comm_create(ctx._h, self.G, self.rank, int(max_U), int(max_recv_keys), buf,
+                                           ctypes.byref(h)))
+        self._h = h
+        self.handle = buf.raw
+
+    def connect_ipc(self, handles) -> None:
+        blob = b"".join(handles)
+        _check(_L.dialsort_comm_connect_ipc(self._h, ctypes.create_string_buffer(blob, len(blob))))
+
+    def connect_local(self, comms) -> None:
+        arr = (ctypes.c_void_p * len(comms))(*[c._h.value for c in comms])
+        _check(_L.dialsort_comm_connect_local(self._h, arr))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _L.dialsort_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def epoch(self) -> int:
+        e = ctypes.c_uint32()
+        _check(_L.dialsort_comm_info(self._h, None, None, ctypes.byref(e)))
+        return int(e.value)
+
+    def _s(self):
+        return _stream(self.ctx.device)
+
+    # histogram path (step by step, or sort = scatter + gather + project)
+    def scatter(self, keys: torch.Tensor, U: int) -> None:
+        _keys(keys)
+        _check(_L.dialsort_sharded_histogram_scatter_async(self.ctx._h, self._h, _ptr(keys), keys.numel(), int(U),
+                                                           self._s()))
+
+    def gather(self, U: int, H_slice: torch.Tensor | None = None) -> torch.Tensor | None:
+        """H_slice (uint32[U/G] as int32) = Σ of the G slots; None: the communicator's own buffer
+        (what `project(U, None, ...)` reads)."""
+        if H_slice is not None:
+            _dev_buf(H_slice, "H_slice", H_slice, int(U) // self.G)
+        _check(_L.dialsort_sharded_histogram_gather_async(self.ctx._h, self._h, int(U), _ptr(H_slice), self._s()))
+        return H_slice
+
+    def project(self, U: int, H_slice: torch.Tensor | None, out: torch.Tensor, count: torch.Tensor,
+                offset: torch.Tensor) -> None:
+        _check(_L.dialsort_sharded_project_async(self.ctx._h, self._h, int(U), _ptr(H_slice), _ptr(out), out.numel(),
+                                                 _ptr(count), _ptr(offset), self._s()))
+
+    def sort(self, keys: torch.Tensor, U: int, out: torch.Tensor, count: torch.Tensor, offset: torch.Tensor,
+             H_slice: torch.Tensor | None = None) -> None:
+        """Sharded DialSort of this rank's key shard: out[:count] = sorted keys of universe slice
+        `rank`, *offset = its position in the global order (all on the device, no host sync)."""
+        _keys(keys)
+        _check(_L.dialsort_sharded_sort_async(self.ctx._h, self._h, _ptr(keys), keys.numel(), int(U), _ptr(out),
+                                              out.numel(), _ptr(H_slice), _ptr(count), _ptr(offset), self._s()))
+
+    # radix path
+    def radix_hist(self, keys: torch.Tensor) -> None:
+        _keys(keys)
+        _check(_L.dialsort_sharded_radix_hist_async(self.ctx._h, self._h, _ptr(keys), keys.numel(), self._s()))
+
+    def radix_split(self, keys: torch.Tensor, cap: int, count: torch.Tensor, offset: torch.Tensor) -> None:
+        _keys(keys)
+        _check(_L.dialsort_sharded_radix_split_async(self.ctx._h, self._h, _ptr(keys), keys.numel(), int(cap),
+                                                     _ptr(count), _ptr(offset), self._s()))
+
+    def radix_local(self, out: torch.Tensor) -> None:
+        _check(_L.dialsort_sharded_radix_local_async(self.ctx._h, self._h, _ptr(out), out.numel(), self._s()))
+
+    def sort_int32(self, keys: torch.Tensor, out: torch.Tensor, count: torch.Tensor, offset: torch.Tensor) -> None:
+        """Sharded DialSort-Radix: out[:count] = this rank's contiguous part of the sorted array."""
+        _keys(keys)
+        _check(_L.dialsort_sharded_sort_int32_async(self.ctx._h, self._h, _ptr(keys), keys.numel(), _ptr(out),
+                                                    out.numel(), _ptr(count), _ptr(offset), self._s()))
 
 
 _default_lock = threading.Lock()
@@ -273,6 +399,18 @@ def sort_host(keys_host: torch.Tensor, U: int, out_host: torch.Tensor | None = N
 
 def range_count(H: torch.Tensor, a: int, b: int):
     return default_context(H.device).range_count(H, a, b)
+
+
+def frequency(H: torch.Tensor, keys: torch.Tensor):
+    return default_context(H.device).query(H, _lib.Q_FREQUENCY, keys)
+
+
+def presence(H: torch.Tensor, keys: torch.Tensor):
+    return default_context(H.device).query(H, _lib.Q_PRESENCE, keys)
+
+
+def support_set(H: torch.Tensor):
+    return default_context(H.device).support_set(H)
 
 
 def crn_resolve(lane_keys: torch.Tensor, active: torch.Tensor):

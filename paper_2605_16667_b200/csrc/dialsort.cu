@@ -1,10 +1,13 @@
 // dialsort.cu — C ABI (include/dialsort.h) and launch logic of the B200 DialSort hot path.
 //
 // Host side only decides paths, sizes grids and enqueues kernels; every step of the method
-// runs in the kernels of ds_hist.cuh / ds_scan.cuh / ds_expand.cuh / ds_radix.cuh.
-// All launches use programmatic dependent launch (PDL) so each kernel's launch overlaps
-// its predecessor's tail; every kernel calls griddepcontrol.wait before touching its
-// inputs, which keeps stream order exact.
+// runs in the kernels of ds_hist.cuh / ds_scan.cuh / ds_fused.cuh / ds_part.cuh /
+// ds_expand.cuh / ds_radix.cuh / ds_comm.cuh.
+// All launches use programmatic dependent launch (PDL) so each kernel's launch overlaps its
+// predecessor's tail; every kernel calls griddepcontrol.wait before touching its inputs, which
+// keeps stream order exact.  Kernels that synchronise their whole grid (software grid barriers,
+// ready flags) are launched cooperatively: a grid that cannot be fully co-resident (another
+// tenant, a concurrent barrier kernel of another context) fails to launch instead of hanging.
 #include "../../include/dialsort.h"
 
 #include <cuda_runtime.h>
@@ -18,12 +21,14 @@
 #include <string>
 #include <vector>
 
+#include "ds_comm.cuh"
 #include "ds_common.cuh"
 #include "ds_expand.cuh"
 #include "ds_fused.cuh"
 #include "ds_hist.cuh"
 #include "ds_part.cuh"
 #include "ds_peer.cuh"
+#include "ds_query.cuh"
 #include "ds_radix.cuh"
 #include "ds_scan.cuh"
 
@@ -41,19 +46,23 @@ int fail(int code, const std::string& msg) {
 #define DS_CUDA(expr)                                                                        \
   do {                                                                                       \
     cudaError_t e_ = (expr);                                                                 \
-    if (e_ != cudaSuccess)                                                                   \
+    if (e_ != cudaSuccess) {                                                                 \
+      cudaGetLastError();                                                                    \
       return fail(DIALSORT_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
+    }                                                                                        \
   } while (0)
 
 enum KernelId {
-  KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND,
-  KID_RADIX_HIST4, KID_RADIX_PASS, KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN,
-  KID_PART_SCATTER, KID_PUSH_SLICES, KID_SLICE_SUM, KID_COUNT
+  KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
+  KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
+  KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_COUNT
 };
-const char* const kKernelNames[KID_COUNT] = {"k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global",
-                                             "k_scan", "k_expand", "k_radix_hist0", "k_radix_pass",
-                                             "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count",
-                                             "k_part_scan", "k_part_scatter", "k_push_slices", "k_slice_sum"};
+const char* const kKernelNames[KID_COUNT] = {
+    "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
+    "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_scatter",
+    "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
+    "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -64,7 +73,27 @@ struct Profiler {
 };
 thread_local Profiler* g_prof = nullptr;  // set by the API entry for the ctx in use
 
-template <typename... KArgs, typename... Args>
+// COOP: the kernel waits on the rest of its grid (grid barrier / ready flags), so the whole
+// grid must be co-resident (grids are sized from the occupancy of an otherwise idle device).
+// Two such kernels running at once could each hold part of the SMs and wait forever for the
+// rest; they can only overlap when issued on different streams of one process (kernels of
+// different processes are time-sliced without MPS).  Default: the library keeps a per-device
+// FIFO of its co-resident launches — a launch on another stream than the previous one first
+// waits (cudaStreamWaitEvent) for everything that stream had enqueued, so two of them never
+// overlap; a single stream pays nothing.  DIALSORT_OPT_COOPERATIVE = 1 (per context) launches
+// them with cudaLaunchAttributeCooperative instead, which makes a grid that cannot be
+// co-resident fail to launch even against other tenants, at ~2 us per launch (measured: c2
+// 32.8 -> 35.0 us, the attribute gives up the PDL overlap with the previous kernel).
+struct CoopFifo {
+  std::mutex mu;
+  bool any = false;
+  cudaStream_t last = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+CoopFifo g_fifo[32];
+thread_local bool g_coop_attr = false;  // set per API call from the context's option
+
+template <bool COOP = false, typename... KArgs, typename... Args>
 cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -72,11 +101,33 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (COOP && g_coop_attr) ? 2 : 1;
+  std::unique_lock<std::mutex> lk;
+  CoopFifo* fifo = nullptr;
+  if (COOP && !g_coop_attr) {  // wait for the previous co-resident launch if it is on another stream
+    int dev = 0;
+    cudaGetDevice(&dev);
+    fifo = &g_fifo[dev & 31];
+    lk = std::unique_lock<std::mutex>(fifo->mu);
+    if (!fifo->ev) cudaEventCreateWithFlags(&fifo->ev, cudaEventDisableTiming);
+    if (fifo->any && fifo->last != s) cudaStreamWaitEvent(s, fifo->ev, 0);
+    fifo->any = true;
+    fifo->last = s;
+  }
+  // (and the event marks this launch for the next one: recorded after it, on its stream)
+  struct FifoMark {
+    CoopFifo* f;
+    cudaStream_t s;
+    ~FifoMark() {
+      if (f) cudaEventRecord(f->ev, s);
+    }
+  } mark{fifo, s};
   Profiler* P = g_prof;
   if (P && P->on) {
     if (2 * P->used + 2 > P->ev.size()) {
@@ -132,6 +183,11 @@ struct DBuf {
   }
 };
 
+// Result of the radix lane-order probe per device (k_radix_lane_probe): -1 unknown, else the
+// number of violating lanes (0: k_radix_pass4's in-warp ranks are stable on this device).
+std::mutex g_probe_mu;
+std::map<int, long long> g_probe;
+
 }  // namespace
 
 struct dialsort_ctx_s {
@@ -139,16 +195,75 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      radix_lb, fused_tiles, Hx, part, htmp;
+      fused_tiles, Hx, part, htmp, qtmp;
   DevStatus* host_status = nullptr;  // pinned mirror
   uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
   unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
+  unsigned long long qbar_base = 0;  // the same for the query kernels' barrier counter
   Profiler prof;
-  int expand_occ = 4, scan_occ = 2, radix_occ = 1, radix2_occ = 1, radix3_occ = 1, radix4_occ = 1;
-  PhaseTimes* pt = nullptr;  // debug phase timing (DIALSORT_PHASE_TIMING=1)
+  int expand_occ = 4, scan_occ = 2, radix3_occ = 1, radix4_occ = 1;
+  long long probe_violations = -1;   // radix lane-order probe of this device
+  int radix_force = 0;               // 0: auto (pass4 iff the probe passed), 3 / 4 forced
+  bool coop_attr = false;            // DIALSORT_OPT_COOPERATIVE
+  PhaseTimes* pt = nullptr;          // debug phase timing (DIALSORT_PHASE_TIMING=1)
+};
+
+struct dialsort_comm_s {
+  dialsort_ctx ctx = nullptr;
+  uint32_t G = 1, rank = 0;
+  CommLayout lay = {};
+  void* ws = nullptr;                    // own symmetric workspace (cudaMalloc: IPC handles at offset 0)
+  char* peer[kCommMaxRanks] = {};        // every rank's workspace as mapped here
+  bool ipc_mapped[kCommMaxRanks] = {};   // opened with cudaIpcOpenMemHandle (closed at destroy)
+  bool connected = false;
+  uint32_t epoch = 0;                    // calls so far (flags hold the epoch of the last call)
+  DBuf tables;                           // [2 parity][G] owner receive-slot pointers (histogram scatter)
+  DBuf scratch;                          // comm scalars: slice total + ticket, rhist ws, plan
+  DBuf hslice;                           // the owner's slice histogram (uint32[Lmax])
 };
 
 namespace {
+
+constexpr uint32_t kCommMagic = 0x44534331u;  // "DSC1"
+struct CommHandle {                            // DIALSORT_COMM_HANDLE_BYTES bytes
+  unsigned char ipc[64];
+  uint32_t magic, G, rank, Lmax;
+  uint64_t cap, bytes;
+  int32_t device;
+  unsigned char pad[128 - 64 - 16 - 16 - 4];
+};
+static_assert(sizeof(CommHandle) == 128, "comm handle size");
+constexpr uint64_t kScratchTot = 0, kScratchRh = 64, kScratchPlan = 64 + 4 * 260;  // byte offsets
+
+CommLayout comm_layout(uint32_t G, uint32_t Lmax, uint64_t cap) {
+  CommLayout l = {};
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t r = o;
+    o = round_up(o + bytes, 256);
+    return r;
+  };
+  l.flags = take(32ull * 2 * kFlagKinds * kCommMaxRanks);
+  l.tot = take(8ull * 2 * kCommMaxRanks);
+  l.rhist = take(4ull * 2 * kCommMaxRanks * 256);
+  l.recv = take(4ull * 2 * G * (uint64_t)Lmax);
+  l.rkeys = take(4ull * 2 * cap);
+  l.bytes = o;
+  l.Lmax = Lmax;
+  l.cap = cap;
+  return l;
+}
+
+CommDev comm_dev(dialsort_comm m) {
+  CommDev d = {};
+  for (uint32_t r = 0; r < m->G; ++r) d.ws[r] = m->peer[r];
+  d.lay = m->lay;
+  d.G = m->G;
+  d.rank = m->rank;
+  d.epoch = m->epoch;
+  d.parity = m->epoch & 1u;
+  return d;
+}
 
 int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaSetDevice(c->device));
@@ -173,16 +288,10 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
   int occ = 0;
-  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass, kRadixThreads, sizeof(RadixSmem)));
-  c->radix_occ = occ > 0 ? occ : 1;
-  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass2, kRadixThreads, sizeof(RadixSmem)));
-  c->radix2_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass3, kRadixThreads, sizeof(Radix3Smem)));
   c->radix3_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass4, kRadixThreads, sizeof(Radix4Smem)));
@@ -196,11 +305,32 @@ int ctx_init(dialsort_ctx c) {
     DS_CUDA(cudaMalloc(&c->pt, sizeof(PhaseTimes)));
     DS_CUDA(cudaMemset(c->pt, 0, sizeof(PhaseTimes)));
   }
+  // radix lane-order probe, once per device (k_radix_lane_probe, ds_radix.cuh)
+  {
+    std::lock_guard<std::mutex> lk(g_probe_mu);
+    auto it = g_probe.find(c->device);
+    if (it != g_probe.end()) {
+      c->probe_violations = it->second;
+    } else {
+      unsigned long long* dv = nullptr;
+      DS_CUDA(cudaMalloc(&dv, 8));
+      DS_CUDA(cudaMemset(dv, 0, 8));
+      k_radix_lane_probe<<<2 * c->nsm, kRadixThreads>>>(0x5eed1234u, 9 * 32, dv);
+      cudaError_t le = cudaGetLastError();
+      unsigned long long hv = 0;
+      cudaError_t ce = cudaMemcpy(&hv, dv, 8, cudaMemcpyDeviceToHost);
+      cudaFree(dv);
+      if (le != cudaSuccess || ce != cudaSuccess)
+        return fail(DIALSORT_E_CUDA, std::string("radix lane probe: ") + cudaGetErrorString(le != cudaSuccess ? le : ce));
+      c->probe_violations = (long long)hv;
+      g_probe[c->device] = c->probe_violations;
+    }
+  }
   return DIALSORT_OK;
 }
 
-// Bumps the call epoch (tags the packed-overflow flag and the radix look-back statuses).
-uint32_t next_epoch(dialsort_ctx c, cudaStream_t s) {
+// Bumps the call epoch (tags the packed-overflow flag).
+uint32_t next_epoch(dialsort_ctx c) {
   c->epoch = (c->epoch + 1) & 0xffffffu;
   if (c->epoch == 0) c->epoch = 1;
   return c->epoch;
@@ -217,22 +347,12 @@ int check_U(uint32_t U) {
   return DIALSORT_OK;
 }
 
-enum class HistPath { Smem32, Smem16, Global };
+enum class HistPath { Smem32, Smem16, Hier, Global };
 HistPath choose_path(uint32_t U) {
   if (U <= kSmem32MaxBins) return HistPath::Smem32;
   if (U <= kSmem16MaxBins) return HistPath::Smem16;
+  if ((uint64_t)U <= ((uint64_t)kPartMaxBlocks << kPartShift)) return HistPath::Hier;
   return HistPath::Global;
-}
-
-// Histogram ingestion variant: register pipeline (default) or TMA-fed ring (DIALSORT_HIST=tma,
-// kept for A/B: measured 12.7 vs 10.2 us ingest at c2 — 3 x 32 KB stages fit beside the
-// 128 KB histogram, fewer bytes in flight than 2 x 4 int4 per thread).
-bool hist_use_tma() {
-  static const bool tma = [] {
-    const char* e = getenv("DIALSORT_HIST");
-    return e && strcmp(e, "tma") == 0;
-  }();
-  return tma;
 }
 
 // Common scan arguments (workspace pointers, output tiling, size check).
@@ -262,113 +382,27 @@ int fill_scan_args(dialsort_ctx c, ScanArgs& a, uint32_t U, bool do_scan, uint64
   return DIALSORT_OK;
 }
 
-// Histogram of keys into H; when do_scan, also P / tfb for a projection of `cap` outputs.
-// Smem paths: one fused co-resident kernel.  Global path: zero + L2 ingest + k_scan.
-int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, bool do_scan,
-                      uint64_t cap, uint32_t epoch, cudaStream_t s, uint32_t* const* Hpeer = nullptr,
-                      uint32_t peerL = 0, uint32_t peerRank = 0) {
-  int rc;
-  ScanArgs a = {};
-  if ((rc = fill_scan_args(c, a, U, do_scan, cap, true, nullptr, epoch))) return rc;
-  a.Hpeer = Hpeer;  // (smem paths only: the merge stores into the owners' slots)
-  a.peerL = peerL;
-  a.peerRank = peerRank;
-  const HistPath path = choose_path(U);
-  if (path == HistPath::Global) {
-    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, H, (uint64_t)U));
-    const uint64_t want = cdiv(n / 4 + 1, 256ull * kHistUnroll);
-    const uint64_t capg = (uint64_t)c->nsm * 8;
-    const uint32_t grid = (uint32_t)(want < capg ? (want ? want : 1) : capg);
-    DS_CUDA(launch_k(KID_HIST_GLOBAL, k_hist_global, dim3(grid), dim3(256), 0, s, keys, n, U, H, a.st));
-    if (!do_scan) return DIALSORT_OK;
-    a.Hsrc = H;
-    const uint64_t ntiles = cdiv(U, kTileBins);
-    const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
-    DS_CUDA(launch_k(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
-    return DIALSORT_OK;
-  }
-  const bool pack = path == HistPath::Smem16;
-  const uint32_t W = pack ? (U + 1) / 2 : U;
-  const uint32_t ldw = (uint32_t)round_up(W, 8);
-  const size_t hist_bytes = std::max<size_t>(4ull * ldw, 32 * 1024);
-  // TMA-fed ingestion only on request (DIALSORT_HIST=tma)
-  uint32_t stages = 0;
-  if (hist_use_tma()) {
-    stages = (uint32_t)std::min<size_t>(kMaxStages, (kSmemBudget - hist_bytes) / kChunkBytes);
-    if (stages < 2) stages = 0;
-  }
-  const size_t smem = hist_bytes + (size_t)stages * kChunkBytes;
-  const uint64_t n4 = n / 4 + 1;
-  const uint64_t want = stages ? cdiv(4 * n4, kChunkBytes / 4) : cdiv(n4, 1024ull * kHistUnroll * 2);
-  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
-  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
-  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
-  if ((rc = c->tsums.ensure(4ull * C * cdiv(U, kTileBins)))) return rc;
-  a.tsums = c->tsums.as<uint32_t>();
-  a.partials = c->partials.as<uint32_t>();
-  a.C = C;
-  a.ldw = ldw;
-  a.pack16 = pack;
-  a.ovfH = c->ovfH.as<uint32_t>();
-  a.H = H;
-  const int kid = pack ? KID_HIST_SMEM16 : KID_HIST_SMEM32;
-  if (pack && stages)
-    DS_CUDA(launch_k(kid, k_hist_fused<true, true>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
-  else if (pack)
-    DS_CUDA(launch_k(kid, k_hist_fused<true, false>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
-  else if (stages)
-    DS_CUDA(launch_k(kid, k_hist_fused<false, true>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
-  else
-    DS_CUDA(launch_k(kid, k_hist_fused<false, false>, dim3(C), dim3(1024), smem, s, keys, n, a, stages));
-  return DIALSORT_OK;
-}
-
-// Scan of a caller histogram (reconstruct API).
-int enqueue_scan(dialsort_ctx c, const uint32_t* H, uint32_t U, uint64_t cap, bool exact, uint64_t* d_total,
-                 uint32_t epoch, cudaStream_t s) {
-  int rc;
-  ScanArgs a = {};
-  if ((rc = fill_scan_args(c, a, U, true, cap, exact, d_total, epoch))) return rc;
-  a.Hsrc = H;
-  const uint64_t ntiles = cdiv(U, kTileBins);
-  const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
-  DS_CUDA(launch_k(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
-  return DIALSORT_OK;
-}
-
-int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, int32_t* out, cudaStream_t s) {
-  if (cap == 0) return DIALSORT_OK;
-  const uint64_t ntiles_out = cdiv(cap, kExpandTile);
-  const uint64_t wave = (uint64_t)c->nsm * c->expand_occ;  // persistent grid: one wave
-  const uint32_t grid = (uint32_t)(ntiles_out < wave ? ntiles_out : wave);
-  DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3(grid), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
-                     c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out,
-                     c->pt));
-  return DIALSORT_OK;
-}
-
-// The whole sort step as one kernel (ds_fused.cuh) for the shared-memory paths.
-// DIALSORT_FUSED=0 selects the two-kernel pipeline (k_hist_fused + k_expand) for A/B.
-bool sort_fused_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("DIALSORT_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
-// d_n / d_off (nullable): the key count and the keys/out offset are on the device (a universe
-// block of the hierarchical path); n is then only the size hint for the grid and row format.
-// k16: keys are uint16 (the hierarchical path's universe blocks), else int32.
+// The whole sort step as one kernel (ds_fused.cuh) for the shared-memory universes, or — with
+// hist_only — the histogram only (merged H stored into H, or into the owners' slots when
+// Hpeer is set).  d_n / d_off (nullable): the key count and the keys/out offset are on the
+// device (a universe block of the hierarchical path); n is then only the size hint for the grid
+// and row format.  k16: keys are uint16 (the hierarchical path's universe blocks), else int32.
 int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
                        uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
-                       const uint64_t* d_off = nullptr, bool k16 = false) {
+                       const uint64_t* d_off = nullptr, bool k16 = false, bool hist_only = false,
+                       uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0, uint32_t peerRank = 0,
+                       uint32_t bin_base = 0) {
   int rc;
   ScanArgs a = {};
-  if ((rc = fill_scan_args(c, a, U, true, n, true, nullptr, epoch))) return rc;
+  if ((rc = fill_scan_args(c, a, U, !hist_only, n, true, nullptr, epoch))) return rc;
   a.d_n = d_n;
   a.d_off = d_off;
-  const bool pack = choose_path(U) == HistPath::Smem16;
+  a.hist_only = hist_only;
+  a.Hpeer = Hpeer;
+  a.peerL = peerL;
+  a.peerRank = peerRank;
+  a.bin_base = bin_base;
+  const bool pack = U > kSmem32MaxBins;
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
   const uint64_t n4 = n / 4 + 1;
@@ -411,8 +445,8 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);
   a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
   a.bar_base = c->bar64_base;
-#define DS_LAUNCH_FUSED(F, K)                                                                                 \
-  DS_CUDA(launch_k(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
+#define DS_LAUNCH_FUSED(F, K) \
+  DS_CUDA(launch_k<true>(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
   if (fmt == kRowN4) {
     if (k16) DS_LAUNCH_FUSED(kRowN4, true); else DS_LAUNCH_FUSED(kRowN4, false);
   } else if (fmt == kRowP16) {
@@ -427,29 +461,16 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
 }
 
 // Hierarchical DialSort for 98304 < U <= 2^22 (ds_part.cuh): MSD split into 65536-bin universe
-// blocks, then one k_sort_fused per block (device-resident block sizes / offsets: no host
-// round trip).  DIALSORT_HIER=0 selects the L2 path (one RED per distinct key per warp).
-bool hier_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("DIALSORT_HIER");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-bool hier_applies(uint32_t U) {
-  return U > kSmem16MaxBins && (uint64_t)U <= ((uint64_t)kPartMaxBlocks << kPartShift) && hier_enabled() &&
-         sort_fused_enabled();
-}
-
-int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
-                      cudaStream_t s) {
+// blocks, then one k_sort_fused per block (device-resident block sizes / offsets: no host round
+// trip).  hist_only: the blocks' launches stop after their merge (H, or the owners' slots).
+int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
+                 cudaStream_t s, bool hist_only = false, uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0,
+                 uint32_t peerRank = 0) {
   int rc;
   const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
-#ifndef DIALSORT_PART_CTAS_PER_SM
-#define DIALSORT_PART_CTAS_PER_SM (2048 / DIALSORT_PART_THREADS)
-#endif
-  const uint32_t Gp = (uint32_t)std::max<uint64_t>(
-      1, std::min<uint64_t>((uint64_t)DIALSORT_PART_CTAS_PER_SM * c->nsm, cdiv(n, kPartTile)));
+  constexpr uint32_t kCtasPerSm = 2048 / kPartThreads;
+  const uint32_t Gp =
+      (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)kCtasPerSm * c->nsm, cdiv(n, kPartTile)));
   if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
   if ((rc = c->htmp.ensure(2ull * n + 16))) return rc;  // uint16 block keys
   PartWs w;
@@ -463,87 +484,157 @@ int enqueue_sort_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
   DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
   for (uint32_t b = 0; b < B; ++b) {
     const uint32_t Ub = (uint32_t)std::min<uint64_t>(1ull << kPartShift, (uint64_t)U - ((uint64_t)b << kPartShift));
-    const uint32_t epoch = next_epoch(c, s);  // each block launch has its own ready-flag epoch
-    if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, H + ((uint64_t)b << kPartShift), out, epoch, s,
-                                 (int32_t)(b << kPartShift), w.bsz + b, w.boff + b, true)))
+    const uint32_t epoch = next_epoch(c);  // each block launch has its own ready-flag epoch
+    uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
+    if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, Hb, out, epoch, s, (int32_t)(b << kPartShift), w.bsz + b,
+                                 w.boff + b, true, hist_only, Hpeer, peerL, peerRank, b << kPartShift)))
       return rc;
   }
   return DIALSORT_OK;
 }
 
-// Host-side enqueue of DialSort-Radix.  Default: 4 reduce-then-scan passes with 8192-key
-// sub-tiles, TMA-staged when the buffers are 16-byte aligned (k_radix_pass4, else pass3;
-// co-resident grid).  DIALSORT_RADIX=pass3 / pass2 / onesweep select the other variants (A/B).
-const char* radix_variant() {
-  static const char* v = [] {
-    const char* e = getenv("DIALSORT_RADIX");
-    return e ? e : "pass4";
-  }();
-  return v;
+// Histogram of keys into H (or into the owners' slots: Hpeer); when do_scan, also P / tfb for a
+// projection of `cap` outputs (k_expand).  Smem universes: one fused co-resident kernel;
+// hierarchical universes: the MSD split + histogram-only block launches; larger: zero + L2
+// ingest (+ k_scan).
+int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H, bool do_scan,
+                      uint64_t cap, uint32_t epoch, cudaStream_t s, uint32_t* const* Hpeer = nullptr,
+                      uint32_t peerL = 0, uint32_t peerRank = 0) {
+  int rc;
+  ScanArgs a = {};
+  if ((rc = fill_scan_args(c, a, U, do_scan, cap, true, nullptr, epoch))) return rc;
+  a.Hpeer = Hpeer;  // (the merge stores into the owners' slots)
+  a.peerL = peerL;
+  a.peerRank = peerRank;
+  const HistPath path = choose_path(U);
+  if (path == HistPath::Hier && n > 0) {
+    if ((rc = enqueue_hier(c, keys, n, U, H, nullptr, s, true, Hpeer, peerL, peerRank))) return rc;
+    if (!do_scan) return DIALSORT_OK;
+    a.Hsrc = H;
+    const uint64_t ntiles = cdiv(U, kTileBins);
+    const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
+    DS_CUDA(launch_k<true>(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
+    return DIALSORT_OK;
+  }
+  if (path == HistPath::Global || path == HistPath::Hier) {
+    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm * 4), dim3(256), 0, s, H, (uint64_t)U));
+    const uint64_t want = cdiv(n / 4 + 1, 256ull * kHistUnroll);
+    const uint64_t capg = (uint64_t)c->nsm * 8;
+    const uint32_t grid = (uint32_t)(want < capg ? (want ? want : 1) : capg);
+    DS_CUDA(launch_k(KID_HIST_GLOBAL, k_hist_global, dim3(grid), dim3(256), 0, s, keys, n, U, H, a.st));
+    if (!do_scan) return DIALSORT_OK;
+    a.Hsrc = H;
+    const uint64_t ntiles = cdiv(U, kTileBins);
+    const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
+    DS_CUDA(launch_k<true>(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
+    return DIALSORT_OK;
+  }
+  const bool pack = path == HistPath::Smem16;
+  const uint32_t W = pack ? (U + 1) / 2 : U;
+  const uint32_t ldw = (uint32_t)round_up(W, 8);
+  const size_t smem = std::max<size_t>(4ull * ldw, 32 * 1024);
+  const uint64_t n4 = n / 4 + 1;
+  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);
+  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
+  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
+  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
+  if ((rc = c->tsums.ensure(4ull * C * cdiv(U, kTileBins)))) return rc;
+  a.tsums = c->tsums.as<uint32_t>();
+  a.partials = c->partials.as<uint32_t>();
+  a.C = C;
+  a.ldw = ldw;
+  a.pack16 = pack;
+  a.ovfH = c->ovfH.as<uint32_t>();
+  a.H = H;
+  const int kid = pack ? KID_HIST_SMEM16 : KID_HIST_SMEM32;
+  if (pack)
+    DS_CUDA(launch_k<true>(kid, k_hist_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a));
+  else
+    DS_CUDA(launch_k<true>(kid, k_hist_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a));
+  return DIALSORT_OK;
 }
-bool radix_onesweep() { return strcmp(radix_variant(), "onesweep") == 0; }
 
-int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, cudaStream_t s) {
+// Scan of a caller histogram (reconstruct API).
+int enqueue_scan(dialsort_ctx c, const uint32_t* H, uint32_t U, uint64_t cap, bool exact, uint64_t* d_total,
+                 uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a = {};
+  if ((rc = fill_scan_args(c, a, U, true, cap, exact, d_total, epoch))) return rc;
+  a.Hsrc = H;
+  const uint64_t ntiles = cdiv(U, kTileBins);
+  const uint64_t wave = (uint64_t)c->nsm * c->scan_occ;
+  DS_CUDA(launch_k<true>(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
+  return DIALSORT_OK;
+}
+
+int enqueue_expand(dialsort_ctx c, uint32_t U, uint64_t cap, int32_t key_base, int32_t* out, cudaStream_t s) {
+  if (cap == 0) return DIALSORT_OK;
+  const uint64_t ntiles_out = cdiv(cap, kExpandTile);
+  const uint64_t wave = (uint64_t)c->nsm * c->expand_occ;  // persistent grid: one wave
+  const uint32_t grid = (uint32_t)(ntiles_out < wave ? ntiles_out : wave);
+  DS_CUDA(launch_k(KID_EXPAND, k_expand, dim3(grid), dim3(kExpandThreads), 0, s, c->P.as<const uint32_t>(), U,
+                   c->tfb.as<const uint32_t>(), ntiles_out, c->ws_total.as<const uint64_t>(), cap, key_base, out,
+                   c->pt));
+  return DIALSORT_OK;
+}
+
+// The radix variant in use: pass4 (TMA sub-tiles, ranks from the counting atomic) when the
+// device passed the lane-order probe and the buffers are 16-byte aligned, else pass3.
+int radix_variant(dialsort_ctx c, bool aligned) {
+  if (c->radix_force == 3) return 3;
+  if (c->radix_force == 4) return aligned ? 4 : 3;
+  return (aligned && c->probe_violations == 0) ? 4 : 3;
+}
+
+// DialSort-Radix, 4 reduce-then-scan passes (ds_radix.cuh).  d_n (nullable): the key count is
+// on the device; n is then the bound the grid is sized for.  pass_out (nullable, debug): pass p
+// writes pass_out + p n instead of ping-ponging (pass buffers for the per-pass parity test).
+int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, int32_t* tmp, cudaStream_t s,
+                  const uint32_t* d_n = nullptr, uint32_t* pass_out = nullptr) {
   if (n >= (1ull << 30)) return fail(DIALSORT_E_INVALID_ARG, "radix path supports n < 2^30 per call");
   int rc;
   const uint32_t* src = reinterpret_cast<const uint32_t*>(keys);
   uint32_t* bufs[2] = {reinterpret_cast<uint32_t*>(tmp), reinterpret_cast<uint32_t*>(out)};
-  if (!radix_onesweep()) {
-    const bool p3 = strcmp(radix_variant(), "pass2") != 0;
-    // pass4 (TMA-staged) needs 16-byte aligned buffers: keys, tmp and out of every pass
-    const bool p4 = p3 && strcmp(radix_variant(), "pass3") != 0 && ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0) &&
-                    ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && ((reinterpret_cast<uintptr_t>(tmp) & 15u) == 0);
-    const uint32_t G = (uint32_t)std::max<uint64_t>(
-        1, std::min<uint64_t>(cdiv(n, p3 ? kR3Tile : kRadixTile),
-                              (uint64_t)c->nsm * (p4 ? c->radix4_occ : p3 ? c->radix3_occ : c->radix2_occ)));
-    if ((rc = c->radix_hist.ensure(8ull * 256 * G + 4 * 256 + 64))) return rc;
-    Radix2Ws w;
-    w.cnt = c->radix_hist.as<uint32_t>();
-    w.pre = w.cnt + 256 * G;
-    w.total = w.pre + 256 * G;
-    w.bar = reinterpret_cast<GridBarR*>(c->gridbar.as<char>() + 32);
-    w.pt = c->pt;
-    for (int p = 0; p < 4; ++p) {
-      uint32_t* dst = bufs[p & 1];
-      if (p4)
-        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass4, dim3(G), dim3(kRadixThreads), sizeof(Radix4Smem), s, src, dst,
-                         (uint32_t)n, p, w));
-      else if (p3)
-        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass3, dim3(G), dim3(kRadixThreads), sizeof(Radix3Smem), s, src, dst,
-                         (uint32_t)n, p, w));
-      else
-        DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass2, dim3(G), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
-                         (uint32_t)n, p, w));
-      src = dst;
-    }
-    return DIALSORT_OK;
-  }
-  const uint32_t ntiles = (uint32_t)cdiv(n, kRadixTile);
-  if ((rc = c->radix_hist.ensure(4 * 1024 + 64))) return rc;
-  if ((rc = c->radix_lb.ensure(2ull * 4 * 256 * ntiles + 16))) return rc;
-  RadixWs w;
-  w.ghist = c->radix_hist.as<uint32_t>();
-  w.ctrs = w.ghist + 1024;
-  w.status = c->radix_lb.as<uint32_t>();
-  w.ntiles = ntiles;
-  const uint32_t g0 = (uint32_t)std::min<uint64_t>(cdiv(n / 4 + 1, 512ull * 4), (uint64_t)c->nsm * 4);
-  DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(1), dim3(256), 0, s, w.ghist, (uint64_t)256));
-  DS_CUDA(launch_k(KID_RADIX_HIST4, k_radix_hist0, dim3(g0), dim3(512), 0, s, keys, n, w));
-  const uint32_t gp = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)c->nsm * c->radix_occ);
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool aligned = al(keys) && al(out) && al(tmp);
+  if (pass_out) aligned = al(keys) && al(pass_out) && (n % 4 == 0);
+  const int v = radix_variant(c, aligned);
+  const uint32_t G = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>(cdiv(n, kR3Tile), (uint64_t)c->nsm * (v == 4 ? c->radix4_occ : c->radix3_occ)));
+  if ((rc = c->radix_hist.ensure(8ull * 256 * G + 4 * 256 + 64))) return rc;
+  Radix2Ws w;
+  w.cnt = c->radix_hist.as<uint32_t>();
+  w.pre = w.cnt + 256 * G;
+  w.total = w.pre + 256 * G;
+  w.bar = reinterpret_cast<GridBarR*>(c->gridbar.as<char>() + 32);
+  w.pt = c->pt;
+  w.d_n = d_n;
   for (int p = 0; p < 4; ++p) {
-    uint32_t* dst = bufs[p & 1];
-    DS_CUDA(launch_k(KID_RADIX_PASS, k_radix_pass, dim3(gp), dim3(kRadixThreads), sizeof(RadixSmem), s, src, dst,
-                     (uint32_t)n, p, w));
+    uint32_t* dst = pass_out ? pass_out + (uint64_t)p * n : bufs[p & 1];
+    if (v == 4)
+      DS_CUDA(launch_k<true>(KID_RADIX_PASS, k_radix_pass4, dim3(G), dim3(kRadixThreads), sizeof(Radix4Smem), s, src,
+                             dst, (uint32_t)n, p, w));
+    else
+      DS_CUDA(launch_k<true>(KID_RADIX_PASS, k_radix_pass3, dim3(G), dim3(kRadixThreads), sizeof(Radix3Smem), s, src,
+                             dst, (uint32_t)n, p, w));
     src = dst;
   }
   return DIALSORT_OK;
 }
 
 // Makes `c`'s profiler the active one for launches made by this thread during an API call.
+// (and its cooperative-launch option)
 struct ProfScope {
   Profiler* prev;
-  explicit ProfScope(dialsort_ctx c) : prev(g_prof) { g_prof = c ? &c->prof : nullptr; }
-  ~ProfScope() { g_prof = prev; }
+  bool prev_coop;
+  explicit ProfScope(dialsort_ctx c) : prev(g_prof), prev_coop(g_coop_attr) {
+    g_prof = c ? &c->prof : nullptr;
+    g_coop_attr = c ? c->coop_attr : false;
+  }
+  ~ProfScope() {
+    g_prof = prev;
+    g_coop_attr = prev_coop;
+  }
 };
 
 std::mutex g_default_mu;
@@ -571,6 +662,13 @@ bool ranges_overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
   return a0 < b0 + nb && b0 < a0 + na;
 }
 
+int check_comm(dialsort_ctx c, dialsort_comm m) {
+  if (!c || !m) return fail(DIALSORT_E_INVALID_ARG, "ctx / comm is NULL");
+  if (m->ctx != c) return fail(DIALSORT_E_INVALID_ARG, "comm belongs to another context");
+  if (!m->connected) return fail(DIALSORT_E_INVALID_ARG, "comm is not connected");
+  return DIALSORT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -580,16 +678,17 @@ const char* dialsort_status_string(int s) {
     case DIALSORT_OK: return "ok";
     case DIALSORT_E_INVALID_ARG: return "invalid argument";
     case DIALSORT_E_KEY_RANGE: return "key outside [0,U)";
-    case DIALSORT_E_SIZE: return "size mismatch (sum(H) vs n)";
+    case DIALSORT_E_SIZE: return "size mismatch (sum(H) vs n / capacity)";
     case DIALSORT_E_OVERFLOW: return "count overflow";
     case DIALSORT_E_CUDA: return "CUDA error";
+    case DIALSORT_E_COMM: return "multi-GPU exchange timed out";
     case DIALSORT_E_NOMEM: return "out of device memory";
     default: return "unknown status";
   }
 }
 
 const char* dialsort_last_error(void) { return g_last_error.c_str(); }
-int dialsort_version(void) { return 100; }
+int dialsort_version(void) { return 200; }
 
 int dialsort_ctx_create(int device, uint64_t max_n, uint32_t max_U, dialsort_ctx* out) {
   if (!out) return fail(DIALSORT_E_INVALID_ARG, "out is NULL");
@@ -598,7 +697,7 @@ int dialsort_ctx_create(int device, uint64_t max_n, uint32_t max_U, dialsort_ctx
   int rc = ctx_init(c);
   if (!rc && max_U) {
     const HistPath path = choose_path(max_U);
-    if (path != HistPath::Global) {
+    if (path == HistPath::Smem32 || path == HistPath::Smem16) {
       const uint64_t W = path == HistPath::Smem16 ? (max_U + 1) / 2 : max_U;
       rc = c->partials.ensure(4ull * c->nsm * round_up(W, 8));
     }
@@ -620,14 +719,41 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
-                  &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->radix_lb,
-                  &c->fused_tiles, &c->Hx, &c->part, &c->htmp})
+                  &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->fused_tiles, &c->Hx,
+                  &c->part, &c->htmp, &c->qtmp})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt) cudaFree(c->pt);
   for (cudaEvent_t e : c->prof.ev) cudaEventDestroy(e);
   delete c;
   return DIALSORT_OK;
+}
+
+int dialsort_ctx_set_option(dialsort_ctx c, int option, int64_t value) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  switch (option) {
+    case DIALSORT_OPT_RADIX_VARIANT:
+      if (value != 0 && value != 3 && value != 4) return fail(DIALSORT_E_INVALID_ARG, "radix variant: 0, 3 or 4");
+      c->radix_force = (int)value;
+      return DIALSORT_OK;
+    case DIALSORT_OPT_COOPERATIVE:
+      c->coop_attr = value != 0;
+      return DIALSORT_OK;
+    default:
+      return fail(DIALSORT_E_INVALID_ARG, "unknown or read-only option");
+  }
+}
+
+int dialsort_ctx_get_option(dialsort_ctx c, int option, int64_t* value) {
+  if (!c || !value) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  switch (option) {
+    case DIALSORT_OPT_RADIX_VARIANT: *value = c->radix_force; return DIALSORT_OK;
+    case DIALSORT_OPT_RADIX_PROBE_VIOLATIONS: *value = c->probe_violations; return DIALSORT_OK;
+    case DIALSORT_OPT_RADIX_ACTIVE: *value = radix_variant(c, true); return DIALSORT_OK;
+    case DIALSORT_OPT_NUM_SMS: *value = c->nsm; return DIALSORT_OK;
+    case DIALSORT_OPT_COOPERATIVE: *value = c->coop_attr ? 1 : 0; return DIALSORT_OK;
+    default: return fail(DIALSORT_E_INVALID_ARG, "unknown option");
+  }
 }
 
 int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info* info) {
@@ -656,6 +782,7 @@ int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info*
              (int32_t)(uint32_t)(h.first_bad & 0xffffffffu));
     return fail(DIALSORT_E_KEY_RANGE, buf);
   }
+  if (h.flags & FLAG_COMM) return fail(DIALSORT_E_COMM, "a peer did not reach the exchange within the timeout");
   if (h.flags & FLAG_OVERFLOW) return fail(DIALSORT_E_OVERFLOW, "sum(H) >= 2^32");
   if (h.flags & FLAG_SIZE)
     return fail(DIALSORT_E_SIZE, "sum(H) = " + std::to_string(h.last_total) + " does not match n / capacity");
@@ -671,76 +798,12 @@ int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, ui
   if (!H) return fail(DIALSORT_E_INVALID_ARG, "H is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t epoch = next_epoch(c, s);
+  const uint32_t epoch = next_epoch(c);
   if (n == 0) {
     DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
     return DIALSORT_OK;
   }
   return enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s);
-}
-
-int dialsort_histogram_scatter_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t G,
-                                     uint32_t rank, uint32_t* const* peer_recv, dialsort_stream_t stream) {
-  int rc;
-  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
-  if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
-  if (G == 0 || U % G != 0 || rank >= G) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and rank < G");
-  if (!peer_recv) return fail(DIALSORT_E_INVALID_ARG, "peer_recv is NULL");
-  cudaStream_t s = (cudaStream_t)stream;
-  DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t epoch = next_epoch(c, s);
-  const uint32_t L = U / G;
-  if (n > 0 && choose_path(U) != HistPath::Global)  // one kernel: histogram, merge, P2P stores
-    return enqueue_hist_scan(c, keys, n, U, nullptr, false, 0, epoch, s, peer_recv, L, rank);
-  // L2 path (or no keys): the local histogram, then one push kernel
-  if ((rc = c->Hws.ensure(4ull * U + 16))) return rc;
-  uint32_t* H = c->Hws.as<uint32_t>();
-  if (n == 0)
-    DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
-  else if ((rc = enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s)))
-    return rc;
-  DS_CUDA(launch_k(KID_PUSH_SLICES, k_push_slices, dim3(2 * c->nsm), dim3(256), 0, s, (const uint32_t*)H, U, L, rank,
-                   peer_recv));
-  return DIALSORT_OK;
-}
-
-int dialsort_slice_sum_async(dialsort_ctx c, const uint32_t* recv, uint32_t G, uint32_t L, uint32_t* H_slice,
-                             dialsort_stream_t stream) {
-  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
-  if (!recv || !H_slice || G == 0 || L == 0) return fail(DIALSORT_E_INVALID_ARG, "bad slice-sum arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(2ull * c->nsm, cdiv(L, 256));
-  DS_CUDA(launch_k(KID_SLICE_SUM, k_slice_sum, dim3(grid), dim3(256), 0, s, recv, G, L, H_slice));
-  return DIALSORT_OK;
-}
-
-int dialsort_ipc_handle(dialsort_ctx c, const void* dev_ptr, void* handle_out) {
-  if (!c || !dev_ptr || !handle_out) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_handle arguments");
-  DS_CUDA(cudaSetDevice(c->device));
-  cudaIpcMemHandle_t h;
-  DS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
-  static_assert(sizeof(h) == DIALSORT_IPC_HANDLE_BYTES, "IPC handle size");
-  memcpy(handle_out, &h, sizeof(h));
-  return DIALSORT_OK;
-}
-
-int dialsort_ipc_open(dialsort_ctx c, const void* handle, void** dev_ptr_out) {
-  if (!c || !handle || !dev_ptr_out) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_open arguments");
-  DS_CUDA(cudaSetDevice(c->device));
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle, sizeof(h));
-  DS_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
-  return DIALSORT_OK;
-}
-
-int dialsort_ipc_close(dialsort_ctx c, void* dev_ptr) {
-  if (!c || !dev_ptr) return fail(DIALSORT_E_INVALID_ARG, "bad ipc_close arguments");
-  DS_CUDA(cudaSetDevice(c->device));
-  DS_CUDA(cudaIpcCloseMemHandle(dev_ptr));
-  return DIALSORT_OK;
 }
 
 int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int32_t key_base, int32_t* out,
@@ -754,7 +817,7 @@ int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, in
     return fail(DIALSORT_E_INVALID_ARG, "key_base + U - 1 exceeds INT32_MAX");
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t epoch = next_epoch(c, s);
+  const uint32_t epoch = next_epoch(c);
   if ((rc = enqueue_scan(c, H, U, cap, exact != 0, d_total, epoch, s))) return rc;
   return enqueue_expand(c, U, cap, key_base, out, s);
 }
@@ -769,7 +832,7 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t epoch = next_epoch(c, s);
+  const uint32_t epoch = next_epoch(c);
   if (n == 0) {
     if (H_out) DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H_out, (uint64_t)U));
     return DIALSORT_OK;
@@ -779,9 +842,9 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     if ((rc = c->Hws.ensure(4ull * U))) return rc;
     H = c->Hws.as<uint32_t>();
   }
-  if (choose_path(U) != HistPath::Global && sort_fused_enabled() && !hist_use_tma())
-    return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);
-  if (hier_applies(U)) return enqueue_sort_hier(c, keys, n, U, H, out, s);
+  const HistPath path = choose_path(U);
+  if (path == HistPath::Smem32 || path == HistPath::Smem16) return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);
+  if (path == HistPath::Hier) return enqueue_hier(c, keys, n, U, H, out, s);
   if ((rc = enqueue_hist_scan(c, keys, n, U, H, true, n, epoch, s))) return rc;
   return enqueue_expand(c, U, n, 0, out, s);
 }
@@ -795,11 +858,21 @@ int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, i
     return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
-  const uint32_t epoch = next_epoch(c, s);
   if (n == 0) return DIALSORT_OK;
   if ((rc = c->radix_tmp.ensure(4ull * n + 16))) return rc;
-  (void)epoch;
   return radix_enqueue(c, keys, n, out, c->radix_tmp.as<int32_t>(), s);
+}
+
+int dialsort_debug_radix_passes(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t* pass_out,
+                                dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(pass_out, 4 * n))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  if (n == 0) return DIALSORT_OK;
+  return radix_enqueue(c, keys, n, nullptr, nullptr, s, nullptr, pass_out);
 }
 
 int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, uint32_t a, uint32_t b,
@@ -816,7 +889,55 @@ int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, ui
   uint64_t len = (uint64_t)b - a + 1;
   uint32_t grid = (uint32_t)(cdiv(len, 1024) < (uint64_t)c->nsm * 4 ? cdiv(len, 1024) : (uint64_t)c->nsm * 4);
   DS_CUDA(launch_k(KID_RANGE_COUNT, k_range_count, dim3(grid), dim3(256), 0, s, H, a, b,
-                 reinterpret_cast<unsigned long long*>(d_result)));
+                   reinterpret_cast<unsigned long long*>(d_result)));
+  return DIALSORT_OK;
+}
+
+int dialsort_query_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int op, const uint32_t* q, uint64_t m,
+                         uint64_t* d_out, dialsort_stream_t stream) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  int rc;
+  if ((rc = check_U(U))) return rc;
+  if (op != DIALSORT_Q_FREQUENCY && op != DIALSORT_Q_PRESENCE && op != DIALSORT_Q_RANGE_COUNT)
+    return fail(DIALSORT_E_INVALID_ARG, "unknown query op");
+  if (m == 0) return DIALSORT_OK;
+  if (!H || !q || !d_out) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  if (op == DIALSORT_Q_RANGE_COUNT) {
+    // prefix of H (uint64, exclusive, U + 1 entries) in the context's query workspace
+    int rc2;
+    if ((rc2 = c->qtmp.ensure(8ull * (U + 1 + c->nsm) + 64))) return rc2;
+    uint64_t* pre = c->qtmp.as<uint64_t>();
+    const uint32_t g = (uint32_t)std::min<uint64_t>(c->nsm, cdiv(U, 4096));
+    c->qbar_base += g;
+    DS_CUDA(launch_k<true>(KID_QUERY, k_query_prefix, dim3(g), dim3(1024), 0, s, H, U, pre,
+                           reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 48), c->qbar_base));
+    DS_CUDA(launch_k(KID_QUERY, k_query_range, dim3((uint32_t)std::min<uint64_t>(cdiv(m, 256), 4ull * c->nsm)),
+                     dim3(256), 0, s, (const uint64_t*)pre, U, q, m, d_out, c->status.as<DevStatus>()));
+    return DIALSORT_OK;
+  }
+  DS_CUDA(launch_k(KID_QUERY, k_query_point, dim3((uint32_t)std::min<uint64_t>(cdiv(m, 256), 4ull * c->nsm)), dim3(256),
+                   0, s, H, U, op, q, m, d_out, c->status.as<DevStatus>()));
+  return DIALSORT_OK;
+}
+
+int dialsort_support_set_async(dialsort_ctx c, const uint32_t* H, uint32_t U, uint32_t* D_out, uint64_t* d_count,
+                               uint32_t* d_iso, dialsort_stream_t stream) {
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  int rc;
+  if ((rc = check_U(U))) return rc;
+  if (!H || !D_out || !d_count) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(c->nsm, cdiv(U, 4096));
+  if ((rc = c->qtmp.ensure(8ull * (grid + 1) + 64))) return rc;
+  c->qbar_base += grid;
+  DS_CUDA(launch_k<true>(KID_QUERY, k_support_set, dim3(grid), dim3(1024), 0, s, H, U, D_out,
+                         reinterpret_cast<unsigned long long*>(d_count), d_iso, c->qtmp.as<unsigned long long>(),
+                         reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 48), c->qbar_base));
   return DIALSORT_OK;
 }
 
@@ -909,8 +1030,267 @@ int dialsort_crn_resolve_async(dialsort_ctx c, const int32_t* lane_keys, const u
   uint64_t grid = cdiv(n_batches * 32, 256);
   if (grid > 0x7fffffffull) return fail(DIALSORT_E_INVALID_ARG, "too many batches");
   DS_CUDA(launch_k(KID_CRN, k_crn_resolve, dim3((uint32_t)grid), dim3(256), 0, s, lane_keys, active, n_batches, out_keys,
-                 out_counts));
+                   out_counts));
   return DIALSORT_OK;
+}
+
+// ---- multi-GPU: communicator over peer memory ----------------------------------------------
+
+int dialsort_comm_create(dialsort_ctx c, uint32_t G, uint32_t rank, uint32_t max_U, uint64_t max_recv_keys,
+                         void* handle_out, dialsort_comm* out) {
+  if (!c || !out) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  if (G == 0 || G > kCommMaxRanks || rank >= G) return fail(DIALSORT_E_INVALID_ARG, "need 1 <= G <= 8 and rank < G");
+  if (max_recv_keys > 0xffffffffull) return fail(DIALSORT_E_INVALID_ARG, "max_recv_keys exceeds 2^32-1");
+  DS_CUDA(cudaSetDevice(c->device));
+  dialsort_comm m = new dialsort_comm_s();
+  m->ctx = c;
+  m->G = G;
+  m->rank = rank;
+  const uint32_t Lmax = (uint32_t)cdiv(max_U ? max_U : 1, G);
+  m->lay = comm_layout(G, (uint32_t)round_up(Lmax, 4), round_up(max_recv_keys ? max_recv_keys : 4, 64));
+  int rc = DIALSORT_OK;
+  if (cudaMalloc(&m->ws, m->lay.bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete m;
+    return fail(DIALSORT_E_NOMEM, "comm workspace allocation failed");
+  }
+  if (cudaMemset(m->ws, 0, m->lay.bytes) != cudaSuccess) rc = fail(DIALSORT_E_CUDA, "cudaMemset failed");
+  if (!rc) rc = m->tables.ensure(8ull * 2 * kCommMaxRanks);
+  if (!rc) rc = m->scratch.ensure(kScratchPlan + 4 * 320, true);
+  if (!rc) rc = m->hslice.ensure(4ull * m->lay.Lmax);
+  if (!rc && handle_out) {
+    CommHandle h = {};
+    cudaIpcMemHandle_t ih;
+    if (cudaIpcGetMemHandle(&ih, m->ws) != cudaSuccess) {
+      cudaGetLastError();
+      memset(&ih, 0, sizeof ih);  // (single-process use: dialsort_comm_connect_local needs no handle)
+    }
+    memcpy(h.ipc, &ih, 64);
+    h.magic = kCommMagic;
+    h.G = G;
+    h.rank = rank;
+    h.Lmax = m->lay.Lmax;
+    h.cap = m->lay.cap;
+    h.bytes = m->lay.bytes;
+    h.device = c->device;
+    memcpy(handle_out, &h, sizeof h);
+  }
+  if (rc) {
+    dialsort_comm_destroy(m);
+    return rc;
+  }
+  m->peer[rank] = static_cast<char*>(m->ws);
+  *out = m;
+  return DIALSORT_OK;
+}
+
+static int comm_finish_connect(dialsort_comm m) {
+  // owner receive-slot tables for the two parities: owner s's recv region of parity p
+  std::vector<uint32_t*> t(2 * kCommMaxRanks, nullptr);
+  for (uint32_t p = 0; p < 2; ++p)
+    for (uint32_t s = 0; s < m->G; ++s)
+      t[p * kCommMaxRanks + s] =
+          reinterpret_cast<uint32_t*>(m->peer[s] + m->lay.recv) + (uint64_t)p * m->G * m->lay.Lmax;
+  DS_CUDA(cudaMemcpy(m->tables.p, t.data(), 8ull * t.size(), cudaMemcpyHostToDevice));
+  m->connected = true;
+  return DIALSORT_OK;
+}
+
+int dialsort_comm_connect_ipc(dialsort_comm m, const void* handles) {
+  if (!m || !handles) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  DS_CUDA(cudaSetDevice(m->ctx->device));
+  const CommHandle* h = static_cast<const CommHandle*>(handles);
+  for (uint32_t s = 0; s < m->G; ++s) {
+    if (h[s].magic != kCommMagic || h[s].G != m->G || h[s].rank != s || h[s].Lmax != m->lay.Lmax ||
+        h[s].cap != m->lay.cap || h[s].bytes != m->lay.bytes)
+      return fail(DIALSORT_E_INVALID_ARG, "comm handle " + std::to_string(s) + " does not match this communicator");
+  }
+  for (uint32_t s = 0; s < m->G; ++s) {
+    if (s == m->rank) continue;
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, h[s].ipc, 64);
+    void* p = nullptr;
+    DS_CUDA(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+    m->peer[s] = static_cast<char*>(p);
+    m->ipc_mapped[s] = true;
+  }
+  return comm_finish_connect(m);
+}
+
+int dialsort_comm_connect_local(dialsort_comm m, const dialsort_comm* peers) {
+  if (!m || !peers) return fail(DIALSORT_E_INVALID_ARG, "NULL argument");
+  DS_CUDA(cudaSetDevice(m->ctx->device));
+  for (uint32_t s = 0; s < m->G; ++s) {
+    const dialsort_comm q = peers[s];
+    if (!q || q->G != m->G || q->rank != s || q->lay.bytes != m->lay.bytes || q->lay.Lmax != m->lay.Lmax ||
+        q->lay.cap != m->lay.cap)
+      return fail(DIALSORT_E_INVALID_ARG, "peer comm " + std::to_string(s) + " does not match this communicator");
+    if (q->ctx->device != m->ctx->device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(q->ctx->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(DIALSORT_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    m->peer[s] = static_cast<char*>(q->ws);
+  }
+  return comm_finish_connect(m);
+}
+
+int dialsort_comm_destroy(dialsort_comm m) {
+  if (!m) return DIALSORT_OK;
+  cudaSetDevice(m->ctx->device);
+  cudaDeviceSynchronize();
+  for (uint32_t s = 0; s < kCommMaxRanks; ++s)
+    if (m->ipc_mapped[s]) cudaIpcCloseMemHandle(m->peer[s]);
+  if (m->ws) cudaFree(m->ws);
+  m->tables.release();
+  m->scratch.release();
+  m->hslice.release();
+  delete m;
+  return DIALSORT_OK;
+}
+
+int dialsort_comm_info(dialsort_comm m, uint32_t* G, uint32_t* rank, uint32_t* epoch) {
+  if (!m) return fail(DIALSORT_E_INVALID_ARG, "comm is NULL");
+  if (G) *G = m->G;
+  if (rank) *rank = m->rank;
+  if (epoch) *epoch = m->epoch;
+  return DIALSORT_OK;
+}
+
+int dialsort_sharded_histogram_scatter_async(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n,
+                                             uint32_t U, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
+  if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  m->epoch++;
+  const uint32_t L = U / m->G, par = m->epoch & 1u;
+  uint32_t* const* tbl = m->tables.as<uint32_t*>() + par * kCommMaxRanks;
+  const uint32_t epoch = next_epoch(c);
+  const HistPath path = choose_path(U);
+  if (n > 0 && path != HistPath::Global) {  // the merge stores each finished bin into its owner's slot
+    if ((rc = enqueue_hist_scan(c, keys, n, U, nullptr, false, 0, epoch, s, tbl, L, m->rank))) return rc;
+  } else {  // L2 path (or no keys): the local histogram, then one push kernel
+    if ((rc = c->Hws.ensure(4ull * U + 16))) return rc;
+    uint32_t* H = c->Hws.as<uint32_t>();
+    if (n == 0)
+      DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
+    else if ((rc = enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s)))
+      return rc;
+    DS_CUDA(launch_k(KID_PUSH_SLICES, k_push_slices, dim3(2 * c->nsm), dim3(256), 0, s, (const uint32_t*)H, U, L,
+                     m->rank, tbl));
+  }
+  DS_CUDA(launch_k(KID_COMM_SIGNAL, k_comm_signal, dim3(1), dim3(32), 0, s, comm_dev(m), kFlagHist));
+  return DIALSORT_OK;
+}
+
+int dialsort_sharded_histogram_gather_async(dialsort_ctx c, dialsort_comm m, uint32_t U, uint32_t* H_slice,
+                                            dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U))) return rc;
+  if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t L = U / m->G;
+  uint32_t* Hs = H_slice ? H_slice : m->hslice.as<uint32_t>();
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * c->nsm, cdiv(L, 256)));
+  DS_CUDA(launch_k(KID_COMM_SLICE_SUM, k_comm_slice_sum, dim3(grid), dim3(256), 0, s, comm_dev(m), L, Hs,
+                   reinterpret_cast<unsigned long long*>(m->scratch.as<char>() + kScratchTot),
+                   c->status.as<DevStatus>()));
+  return DIALSORT_OK;
+}
+
+int dialsort_sharded_project_async(dialsort_ctx c, dialsort_comm m, uint32_t U, const uint32_t* H_slice, int32_t* out,
+                                   uint64_t cap, uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(out, cap))) return rc;
+  if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t L = U / m->G;
+  const uint32_t* Hs = H_slice ? H_slice : m->hslice.as<const uint32_t>();
+  DS_CUDA(launch_k(KID_COMM_OFFSETS, k_comm_offsets, dim3(1), dim3(32), 0, s, comm_dev(m), cap, d_count, d_offset,
+                   c->status.as<DevStatus>()));
+  const uint32_t epoch = next_epoch(c);
+  if ((rc = enqueue_scan(c, Hs, L, cap, false, nullptr, epoch, s))) return rc;
+  return enqueue_expand(c, L, cap, (int32_t)(m->rank * L), out, s);
+}
+
+int dialsort_sharded_sort_async(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n, uint32_t U,
+                                int32_t* out, uint64_t cap, uint32_t* H_slice, uint64_t* d_count, uint64_t* d_offset,
+                                dialsort_stream_t stream) {
+  int rc;
+  if ((rc = dialsort_sharded_histogram_scatter_async(c, m, keys, n, U, stream))) return rc;
+  if ((rc = dialsort_sharded_histogram_gather_async(c, m, U, H_slice, stream))) return rc;
+  return dialsort_sharded_project_async(c, m, U, H_slice, out, cap, d_count, d_offset, stream);
+}
+
+int dialsort_sharded_radix_hist_async(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n,
+                                      dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(keys, n))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  m->epoch++;
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * c->nsm, cdiv(n, 8192)));
+  DS_CUDA(launch_k(KID_COMM_RHIST, k_comm_rhist, dim3(grid), dim3(512), 0, s, comm_dev(m), keys, n,
+                   reinterpret_cast<uint32_t*>(m->scratch.as<char>() + kScratchRh)));
+  return DIALSORT_OK;
+}
+
+int dialsort_sharded_radix_split_async(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n, uint64_t cap,
+                                       uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(keys, n))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  uint32_t* plan = reinterpret_cast<uint32_t*>(m->scratch.as<char>() + kScratchPlan);
+  DS_CUDA(launch_k(KID_COMM_RPLAN, k_comm_rplan, dim3(1), dim3(256), 0, s, comm_dev(m), plan, cap, d_count, d_offset,
+                   c->status.as<DevStatus>()));
+  if (n) {
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * c->nsm, cdiv(n, kSplitTile)));
+    DS_CUDA(launch_k(KID_COMM_RSPLIT, k_comm_rsplit, dim3(grid), dim3(kSplitThreads), 0, s, comm_dev(m), keys, n, plan));
+  }
+  DS_CUDA(launch_k(KID_COMM_SIGNAL, k_comm_signal, dim3(1), dim3(32), 0, s, comm_dev(m), kFlagRkeys));
+  return DIALSORT_OK;
+}
+
+int dialsort_sharded_radix_local_async(dialsort_ctx c, dialsort_comm m, int32_t* out, uint64_t cap,
+                                       dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  ProfScope prof_scope_(c);
+  if ((rc = check_keys_arg(out, cap))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(launch_k(KID_COMM_WAIT, k_comm_wait, dim3(1), dim3(32), 0, s, comm_dev(m), kFlagRkeys,
+                   c->status.as<DevStatus>()));
+  const uint64_t bound = std::min<uint64_t>(cap, m->lay.cap);
+  if (bound == 0) return DIALSORT_OK;
+  if ((rc = c->radix_tmp.ensure(4ull * bound + 16))) return rc;
+  const uint32_t* d_n = reinterpret_cast<const uint32_t*>(m->scratch.as<char>() + kScratchPlan) + 32;
+  const int32_t* rk = reinterpret_cast<const int32_t*>(m->peer[m->rank] + m->lay.rkeys) + (uint64_t)(m->epoch & 1u) * m->lay.cap;
+  return radix_enqueue(c, rk, bound, out, c->radix_tmp.as<int32_t>(), s, d_n);
+}
+
+int dialsort_sharded_sort_int32_async(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n, int32_t* out,
+                                      uint64_t cap, uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = dialsort_sharded_radix_hist_async(c, m, keys, n, stream))) return rc;
+  if ((rc = dialsort_sharded_radix_split_async(c, m, keys, n, cap, d_count, d_offset, stream))) return rc;
+  return dialsort_sharded_radix_local_async(c, m, out, cap, stream);
 }
 
 // ---- synchronous forms ----------------------------------------------------------------------
@@ -941,6 +1321,34 @@ int dialsort_sort_int32(const int32_t* keys, uint64_t n, int32_t* out) {
   if (rc) return rc;
   if ((rc = dialsort_sort_int32_async(c, keys, n, out, nullptr))) return rc;
   return dialsort_sync(c, nullptr, nullptr);
+}
+
+static int sharded_sync_read(dialsort_ctx c, dialsort_stream_t stream, uint64_t* d2, uint64_t* count_host,
+                             uint64_t* offset_host) {
+  int rc = dialsort_sync(c, stream, nullptr);
+  uint64_t h[2] = {0, 0};
+  DS_CUDA(cudaMemcpy(h, d2, 16, cudaMemcpyDeviceToHost));
+  if (count_host) *count_host = h[0];
+  if (offset_host) *offset_host = h[1];
+  return rc;
+}
+
+int dialsort_sharded_sort(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n, uint32_t U, int32_t* out,
+                          uint64_t cap, uint64_t* count_host, uint64_t* offset_host, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  uint64_t* d2 = reinterpret_cast<uint64_t*>(m->scratch.as<char>() + kScratchTot + 16);
+  if ((rc = dialsort_sharded_sort_async(c, m, keys, n, U, out, cap, nullptr, d2, d2 + 1, stream))) return rc;
+  return sharded_sync_read(c, stream, d2, count_host, offset_host);
+}
+
+int dialsort_sharded_sort_int32(dialsort_ctx c, dialsort_comm m, const int32_t* keys, uint64_t n, int32_t* out,
+                                uint64_t cap, uint64_t* count_host, uint64_t* offset_host, dialsort_stream_t stream) {
+  int rc;
+  if ((rc = check_comm(c, m))) return rc;
+  uint64_t* d2 = reinterpret_cast<uint64_t*>(m->scratch.as<char>() + kScratchTot + 16);
+  if ((rc = dialsort_sharded_sort_int32_async(c, m, keys, n, out, cap, d2, d2 + 1, stream))) return rc;
+  return sharded_sync_read(c, stream, d2, count_host, offset_host);
 }
 
 int dialsort_sort_host(dialsort_ctx c, const int32_t* keys_host, uint64_t n, uint32_t U, int32_t* out_host,

@@ -76,26 +76,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 //   key(p) = max{k : P[k] <= p} = ka - 1 + cnt(p),   cnt(p) = #{i : Ps[i] <= p}
 // (the bin whose run covers p; empty bins share their start with the next bin and are
 // skipped by the max); kbase = key_base + ka - 1.
-// project_warp (warp-level; the A/B reference of project_tbl below, DIALSORT_PROJ_WARP=1):
-// the range is cut into 512-position super-blocks aligned to absolute multiples of 512,
-// dealt round-robin to the CTA's 32 warps, so the CTA writes one contiguous front (measured:
-// 5.6 us for 40 MB of stores vs 8.8 us when each warp streams a range of its own — DRAM page
-// locality).  A super-block is 4 sub-blocks of 128 positions; lane l owns the quad at
-// positions sb + 128 s + 4 l .. +3 of sub-block s, and each sub-block leaves as one
-// coalesced 512-byte warp store.  A warp keeps c = #{i : Ps[i] < sb} and a register window
-// sreg = Ps[cb + lane] (cb <= c <= cb + 15); the bin starts of the super-block are window
-// lanes o = c-cb .. le-1, found with one ballot:
-//   none      every position has key kbase + c (four stores);
-//   distinct  (starts in distinct quads: bins longer than 4, the common case) four
-//             OR-reductions give per-sub-block quad occupancy masks M_s; lane l adds the
-//             starts of the quads before its own (popc) plus its own quad's start where that
-//             start's offset <= the position;
-//   otherwise (starts sharing a quad, or more than the window holds) sub-block by sub-block,
-//             each start adds a mark to the warp's 128-entry count array and a warp scan
-//             gives cnt — O(starts) in parallel (a per-start loop over the lanes' positions
-//             measured 10x slower on Zipf's short bins).
-// The projection is issue-bound (ncu ~70% issue-active at one 128-position block per
-// iteration), so the per-iteration bookkeeping is amortised over 4 quads per lane.
 // #{i : Ps[i] < x} for a warp, given that it lies in [x0, m] (Ps[m ..] are sentinels): rounds of
 // 32 lane probes narrow the range 32-fold each (two rounds for m <= 1024), a last round of
 // consecutive probes gives the count.
@@ -112,12 +92,8 @@ __device__ __forceinline__ uint32_t count_below(const uint32_t* Ps, uint32_t m, 
   return x0 + __popc(__ballot_sync(FULL, Ps[x0 + lane] < x));  // x0 + lane < m + 32: sentinels
 }
 
-// Projection stores: 1 = st.global.L1::no_allocate without an L2 hint (default: 0.3 us
-// faster than the evict-first hint on c2 / c3 in A/B runs, c4 -0.5 %), 2 = default policy,
-// 0 = L2 evict-first hint.
-#ifndef DIALSORT_PROJ_STORE
-#define DIALSORT_PROJ_STORE 1
-#endif
+// Projection stores: st.global.L1::no_allocate without an L2 hint (measured 0.3 us faster than
+// the evict-first hint on c2 / c3, and than the default policy).
 __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
                                            bool aligned, uint64_t pol, bool full = false) {
   const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
@@ -147,125 +123,12 @@ __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p
     return;
   }
   if (full || (aligned && p >= lo && p + 4 <= hi)) {
-#if DIALSORT_PROJ_STORE == 1
     st_stream4(reinterpret_cast<int4*>(out + p), v);  // no L2 hint
-#elif DIALSORT_PROJ_STORE == 2
-    *reinterpret_cast<int4*>(out + p) = v;  // default policy
-#else
-    st_stream4(reinterpret_cast<int4*>(out + p), v, pol);
-#endif
   } else {
     if (p >= lo && p < hi) out[p] = v.x;
     if (p + 1 >= lo && p + 1 < hi) out[p + 1] = v.y;
     if (p + 2 >= lo && p + 2 < hi) out[p + 2] = v.z;
     if (p + 3 >= lo && p + 3 < hi) out[p + 3] = v.w;
-  }
-}
-
-#if DIALSORT_EXP_PATHCNT
-__shared__ uint32_t s_pathcnt[4];  // debug: super-blocks per projection path
-#define DS_PATHCNT(i) \
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_pathcnt[i], 1u)
-#else
-#define DS_PATHCNT(i)
-#endif
-__device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
-                                             uint32_t* wc, int32_t* __restrict__ out, bool aligned, uint64_t pol) {
-  constexpr uint32_t QPL = 4;  // quads per lane and super-block (1 and 2 measured slower)
-  constexpr uint32_t NW = 32, SB = 128 * QPL;
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t ltmask = (1u << lane) - 1u;
-  uint32_t sb = (lo & ~(SB - 1)) + SB * w;
-  if (sb >= hi) return;
-  // c = #{i : Ps[i] < sb}  (sentinels are never < sb, so c <= m)
-  uint32_t c = count_below(Ps, m, 0, sb), cb = c;
-  uint32_t sreg = Ps[cb + lane];
-  for (;;) {
-    const uint32_t bend = hi - sb > SB ? sb + SB - 1 : hi - 1;
-    const bool full = sb >= lo && hi - sb >= SB;  // every quad in [lo, hi) (any alignment)
-    if (c - cb >= 16) {  // keep >= 16 lanes of look-ahead in the window
-      cb = c;
-      sreg = Ps[cb + lane];
-    }
-    const uint32_t o = c - cb;
-    const uint32_t le = __popc(__ballot_sync(FULL, sreg <= bend));
-    const uint32_t base = kbase + c;
-    if (le == o) {  // no bin starts in the super-block
-      DS_PATHCNT(0);
-      const uint4 q = make_uint4(base, base, base, base);
-#pragma unroll
-      for (uint32_t s = 0; s < QPL; ++s) store_quad(out, sb + 128 * s + 4 * lane, lo, hi, q, aligned, pol, full);
-    } else {
-      bool done = false;
-      if (le < 32) {
-        const bool mine = lane >= o && lane < le;
-        const uint32_t qi = (sreg - sb) >> 2;  // quad of the super-block (valid when mine)
-        uint32_t M[QPL], pc = 0;
-#pragma unroll
-        for (uint32_t s = 0; s < QPL; ++s) {
-          M[s] = __reduce_or_sync(FULL, (mine && (qi >> 5) == s) ? 1u << (qi & 31) : 0u);
-          pc += __popc(M[s]);
-        }
-        if (pc == le - o) {
-          uint32_t cum = 0;
-#pragma unroll
-          for (uint32_t s = 0; s < QPL; ++s) {
-            const uint32_t below = cum + __popc(M[s] & ltmask);
-            const uint32_t own = (M[s] >> lane) & 1u;
-            const uint32_t r = (__shfl_sync(FULL, sreg, min(o + below, 31u)) - sb) & 3u;
-            const uint32_t v = base + below;
-            store_quad(out, sb + 128 * s + 4 * lane, lo, hi,
-                       make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own),
-                       aligned, pol, full);
-            cum += __popc(M[s]);
-          }
-          done = true;
-          DS_PATHCNT(1);
-        }
-      }
-      if (!done) {
-        DS_PATHCNT(2);
-        // starts sharing quads, or more than the window holds: sub-block by sub-block, each
-        // start adds a mark to the warp's 128-entry count array (O(starts) in parallel)
-        uint32_t cs = c;  // #{i : Ps[i] < b0}
-#pragma unroll 1
-        for (uint32_t s = 0; s < QPL; ++s) {
-          const uint32_t b0 = sb + 128 * s;
-          if (b0 >= hi) break;
-          const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
-          uint32_t i1 = cs;
-          for (;;) {
-            const uint32_t sl = Ps[min(i1 + lane, m)];  // Ps[m] is a sentinel
-            const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= be));
-            if (lane < cnt) atomicAdd(&wc[sl - b0], 1u);
-            i1 += cnt;
-            if (cnt < 32) break;
-          }
-          __syncwarp();
-          uint4 mk = reinterpret_cast<uint4*>(wc)[lane];
-          reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
-          mk.y += mk.x;
-          mk.z += mk.y;
-          mk.w += mk.z;
-          const uint32_t v = kbase + cs + warp_incl_scan(mk.w) - mk.w;
-          store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol);
-          __syncwarp();
-          cs = i1;  // starts <= be counted: #{i : Ps[i] < b0 + 128}
-        }
-      }
-    }
-    if (hi - sb <= SB * NW) break;
-    sb += SB * NW;
-    // advance: c = #{i : Ps[i] < sb}
-    const uint32_t lt = __popc(__ballot_sync(FULL, sreg < sb));
-    if (lt < 32) {
-      c = cb + lt;
-    } else {
-      // the warp's next super-block is 16K positions away: in a start-dense region (short
-      // bins) thousands of starts lie between, so search rather than walk
-      c = cb = count_below(Ps, m, cb + 32, sb);
-      sreg = Ps[cb + lane];
-    }
   }
 }
 
@@ -278,7 +141,7 @@ __device__ __forceinline__ void project_warp(const uint32_t* Ps, uint32_t m, uin
 // its quad (2 bits per quad).  Warp w then writes sub-blocks w, w + 32, .. (the CTA writes one
 // contiguous front): lane l's quad holds keys kbase + c0 + popc(M & lanes below l), + 1 from
 // its start's offset on — about 25 instructions per quad, a third of the ballot / REDUX /
-// shuffle path of project_warp.  A sub-block whose quads hold several starts (bins shorter
+// shuffle projection it replaced.  A sub-block whose quads hold several starts (bins shorter
 // than 4 positions, empty bins) takes the count-mark path.
 constexpr uint32_t kFTblCap = kFSlot / 4;  // 4884 sub-blocks per window (one staging slot)
 __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
@@ -528,9 +391,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   __shared__ uint32_t wsum[32];
   pdl_wait();
   phase_mark(a.pt, -1);
-#if DIALSORT_EXP_PATHCNT
-  if (threadIdx.x < 4) s_pathcnt[threadIdx.x] = 0;
-#endif
   uint64_t n_exp = a.n_expected;
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
     const uint64_t off = *a.d_off;
@@ -561,7 +421,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   // (the ingestion's first __syncthreads orders this before the flush)
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
   for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
-  hist_ingest_flush<PACK16, false, K16>(keys, n, a, 0, sh, red64, nullptr, nullptr, sh + kFOffTsh);
+  hist_ingest_flush<PACK16, K16>(keys, n, a, sh, red64, sh + kFOffTsh);
   __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
     my_tiles(ntiles, s_own[0], s_own[1]);
@@ -584,18 +444,16 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     const uint32_t t0 = tb0 + k * tpb, nt = min(tpb, tb1 - t0);
     return nt >= 32 ? 0xffffffffu : (1u << nt) - 1u;
   };
-  // The owner totals, the overflow state and the first two batches' row segments (and their
-  // exception counts) are requested together, totals first: none depends on another, and the
-  // barrier ordered every CTA's flush before them.  Each CTA reads the G owner totals only
-  // (reading all ntiles strided tile counters from every CTA measured ~2.5 us: a 148-way
-  // fan-in on the same L2 lines); its own tiles' offsets come out of its merge.
-  // (warp 0, lane l: owners kOPL l .. kOPL l + kOPL - 1, scanned by that warp alone)
-  constexpr uint32_t kOPL = (kFMaxRows + 31) / 32;
-  uint32_t ov[kOPL];
-#pragma unroll
-  for (uint32_t j = 0; j < kOPL; ++j) {
-    const uint32_t c = kOPL * threadIdx.x + j;
-    ov[j] = threadIdx.x < 32 && c < G ? __ldcg(a.own_red + (uint64_t)c * S) : 0u;
+  // This CTA's offset counters (P_b, P_{b+1}: its tiles' first output position and the next
+  // owner's, flush_owner_totals), the skew vote, the overflow state and the first two batches'
+  // row segments (and their exception counts) are requested together: none depends on another,
+  // and the barrier ordered every CTA's flush before them.  Two counter lines per CTA, each read
+  // by two CTAs (all owner totals read by every CTA measured ~1.7 us: a 148-way fan-in).
+  __shared__ uint32_t s_pb[3];
+  if (threadIdx.x == 0) {
+    s_pb[0] = b ? __ldcg(a.own_red + (uint64_t)b * S) : 0u;
+    s_pb[1] = __ldcg(a.own_red + (uint64_t)(b + 1) * S);
+    s_pb[2] = __ldcg(a.own_red + (uint64_t)kFOwnVote * S);
   }
   const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
   for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
@@ -609,8 +467,20 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     return FMT == kRowN4 && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
+  // own-tile mode: every CTA projects exactly the tiles it merged (near-uniform histograms: no
+  // skew vote); otherwise (skew, or a packed-counter overflow) equal position shares, for which
+  // every owner offset oo[0..G] is read.
+  constexpr uint32_t kOPL = (kFMaxRows + 31) / 32;
+  uint32_t ov[kOPL];
+  bool own;
   if (!use_ovf) {
     barrier_skip(a.bar64);
+    __syncthreads();  // s_pb
+    own = ntiles <= kFPassTiles * G && s_pb[2] == 0;  // (every CTA's tiles fit one projection pass)
+    if (!own) {
+      for (uint32_t c = threadIdx.x; c <= G; c += blockDim.x) oo[c] = c ? __ldcg(a.own_red + (uint64_t)c * S) : 0u;
+      __syncthreads();
+    }
   } else {
     // a packed counter overflowed somewhere: the flushed owner sums miss the fallback keys
     uint64_t osd = 0;
@@ -622,28 +492,29 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
       const uint32_t c = kOPL * threadIdx.x + j;
       ov[j] = threadIdx.x < 32 && c < G ? __ldcg(a.own_alt + c) : 0u;
     }
-  }
-
-  // ---- owner offsets: oo[c] = first output position of owner c's tiles (one warp) ------------
-  if (threadIdx.x < 32) {  // (every count sum here is <= n < 2^32, R4)
-    uint32_t sum = 0;
+    // owner offsets: oo[c] = first output position of owner c's tiles (one warp)
+    if (threadIdx.x < 32) {  // (every count sum here is <= n < 2^32, R4)
+      uint32_t sum = 0;
 #pragma unroll
-    for (uint32_t j = 0; j < kOPL; ++j) sum += ov[j];
-    const uint32_t inc = warp_incl_scan(sum);
-    uint32_t ex = inc - sum;
+      for (uint32_t j = 0; j < kOPL; ++j) sum += ov[j];
+      const uint32_t inc = warp_incl_scan(sum);
+      uint32_t ex = inc - sum;
 #pragma unroll
-    for (uint32_t j = 0; j < kOPL; ++j) {
-      const uint32_t c = kOPL * threadIdx.x + j;
-      if (c < G) oo[c] = ex;
-      ex += ov[j];
+      for (uint32_t j = 0; j < kOPL; ++j) {
+        const uint32_t c = kOPL * threadIdx.x + j;
+        if (c < G) oo[c] = ex;
+        ex += ov[j];
+      }
+      if (threadIdx.x == 31) oo[G] = inc;
     }
-    if (threadIdx.x == 31) oo[G] = inc;
+    __syncthreads();
+    own = false;
   }
-  __syncthreads();
   phase_mark(a.pt, 4);
-  const uint64_t total = oo[G];
-  const uint32_t obase = oo[b];  // first output position of this CTA's tiles
-  if (b == 0 && threadIdx.x == 0) {
+  const uint32_t obase = own ? s_pb[0] : oo[b];    // first output position of this CTA's tiles
+  const uint32_t oend = own ? s_pb[1] : oo[b + 1];  // ... and of the next owner's (the last: the total)
+  if (b == G - 1 && threadIdx.x == 0) {
+    const uint64_t total = oend;
     unsigned flags = 0;
     if (a.exact ? (total != n_exp) : (total > n_exp)) flags |= FLAG_SIZE;
     if (flags) atomicOr(&a.st->flags, flags);
@@ -651,14 +522,8 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     if (a.d_total) *a.d_total = total;
     *a.ws_total = total;
   }
-  const uint32_t nw = (uint32_t)(total < n_exp ? total : n_exp);  // positions written
-  // Own-tile mode: when every CTA's own tiles hold about nw / G positions (near-uniform
-  // histograms), each CTA projects exactly the tiles it merged, from P in its shared memory —
-  // no cross-CTA flags, no P round trip through L2.  Otherwise (skew) equal position shares.
-  bool own = ntiles <= kFPassTiles * G;  // every CTA's tiles fit one projection pass
-  if (own)  // max owner total <= (17/16) nw / G + 1024
-    own = !__syncthreads_or(threadIdx.x < G &&
-                            16ull * G * (oo[threadIdx.x + 1] - oo[threadIdx.x]) > 17ull * nw + 16384ull * G);
+  // positions written: [0, min(total, n_exp)) (share mode needs the total: oo[G])
+  const uint32_t nw = own ? 0u : (uint32_t)(oo[G] < n_exp ? oo[G] : n_exp);
   // equal share [lo, hi) (share mode) and the owners oa..ob (tiles [x0, x1)) it overlaps
   uint32_t lo = 0, hi = 0;
   if (!own) {
@@ -720,14 +585,14 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     if (j < nbb && ((need >> (j / kFTileBins)) & 1u)) {
       const uint32_t wpre = obase + carry + wex[j >> 5];
       const uint32_t bin = t0 * kFTileBins + j;
-      const uint32_t p = bin < U ? wpre + inc - h : (uint32_t)total;
-      if (bin < U) a.H[bin] = h;
+      const uint32_t p = bin < U ? wpre + inc - h : oend;  // (bins >= U: the last tile; oend = total)
+      if (bin < U) store_H(a, bin, h);
       if (own) Ps[(t0 - tb0) * kFTileBins + j] = p;
-      else if (bin < U) a.P[bin] = p;
+      else if (bin < U && !a.hist_only) a.P[bin] = p;
     }
     carry += s_btot;  // (read before the next batch's scan rewrites it: two barriers apart)
     phase_mark(a.pt, 15);
-    if (!own) {
+    if (!own && !a.hist_only) {
       __syncthreads();  // the batch's H and P are written
       if (threadIdx.x < tpb && ((need >> threadIdx.x) & 1u))
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t0 + threadIdx.x), "r"(a.epoch) : "memory");
@@ -736,6 +601,10 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   if (use_ovf)  // only this CTA read ovfH for its tiles: clear them for the next call
     for (uint32_t k = tb0 * kFTileBins + threadIdx.x; k < min(tb1 * kFTileBins, U); k += blockDim.x) a.ovfH[k] = 0;
   phase_mark(a.pt, 6);
+  if (a.hist_only) {  // histogram-only launch (hierarchical histogram, multi-GPU exchange)
+    pdl_trigger();
+    return;
+  }
 
   const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
   const uint64_t pol = l2_evict_first_policy();
@@ -745,22 +614,11 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     if (threadIdx.x < 32) Ps[m + threadIdx.x] = 0xffffffffu;
     __syncthreads();
     phase_mark(a.pt, 9);
-    const uint32_t p0 = obase, p1 = min(oo[b + 1], nw);
-#if DIALSORT_PROJ_WARP
-    if (nown && p0 < p1) project_warp(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
-#else
+    const uint32_t p0 = obase, p1 = (uint32_t)(oend < n_exp ? oend : n_exp);
     if (nown && p0 < p1)  // (uniform per CTA) table in the second staging slot, dead after the merge
       project_tbl(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1,
                   reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
                   reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
-#endif
-#if DIALSORT_EXP_PATHCNT
-    __syncthreads();
-    if (a.pt && threadIdx.x == 0) {  // slot 12..14: t + count, slot 15: t (stamps are read relative)
-      const unsigned long long t = gtimer();
-      for (int i = 0; i < 4; ++i) a.pt->stamp[blockIdx.x][12 + i] = t + (i < 3 ? s_pathcnt[i] : 0u);
-    }
-#endif
     phase_mark(a.pt, 7);
     pdl_trigger();
     return;
@@ -807,29 +665,18 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
       if (b0 + m > U) {  // bins >= U of a last partial tile
-        for (uint32_t i = U - b0 + threadIdx.x; i < m; i += blockDim.x) Pw[i] = (uint32_t)total;
+        for (uint32_t i = U - b0 + threadIdx.x; i < m; i += blockDim.x) Pw[i] = oo[G];
         __syncthreads();
       }
       phase_mark(a.pt, 9);
       const uint32_t p0 = max(lo, ts[pt0 - x0]), p1 = min(hi, ts[pt1 - x0]);
-#if DIALSORT_PROJ_WARP
-      if (p0 < p1) project_warp(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1, wc, out, aligned, pol);
-#else
       if (p0 < p1)
         project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
                     reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
                     reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
-#endif
       __syncthreads();  // Pw is reused by the next pass
     }
   }
-#if DIALSORT_EXP_PATHCNT
-  __syncthreads();
-    if (a.pt && threadIdx.x == 0) {  // slot 12..14: t + count, slot 15: t (stamps are read relative)
-      const unsigned long long t = gtimer();
-      for (int i = 0; i < 4; ++i) a.pt->stamp[blockIdx.x][12 + i] = t + (i < 3 ? s_pathcnt[i] : 0u);
-    }
-#endif
   phase_mark(a.pt, 7);
   pdl_trigger();
 }

@@ -22,9 +22,7 @@ constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
 constexpr uint32_t kFTileBins = 64;         // scan-tile width of k_sort_fused (ds_fused.cuh)
 constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
-constexpr uint32_t kChunkBytes = 32768;     // TMA path: 8192 keys per chunk
-constexpr uint32_t kChunkVecs = kChunkBytes / 16;
-constexpr uint32_t kMaxStages = 4;
+constexpr uint32_t kFOwnVote = 255;         // k_sort_fused: owner-counter slot of the skew vote
 
 // Key layout shared by every pass over `keys`: `head` scalars before the first 16-byte
 // boundary, `n4` aligned int4 vectors, `tail` scalars.  CTA 0 takes the head, the last CTA
@@ -83,67 +81,6 @@ __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1
   }
 }
 
-// TMA-fed traversal: the aligned body is cut into kChunkBytes chunks; CTA c consumes chunks
-// c, c+G, ... through a ring of `stages` shared-memory slots filled by cp.async.bulk (one
-// elected thread issues, an mbarrier per slot signals "full", a second "empty" collects one
-// arrival per warp).  Each lane takes 2 vectors of each chunk; keys stream through the TMA
-// engine without occupying registers, so all 32 warps can issue atomics.
-
-template <typename F4, typename F1>
-__device__ __forceinline__ uint32_t for_each_key_tma(const KeySpan& s, unsigned char* ring, uint32_t stages,
-                                                 uint64_t* full_bar, uint64_t* empty_bar, F4&& f4, F1&& f1) {
-  const uint32_t G = gridDim.x;
-  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
-  if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
-    uint64_t i = s.head + 4 * s.n4 + threadIdx.x;
-    f1((uint32_t)s.keys[i], i);
-  }
-  const uint64_t nbytes = 16ull * s.n4;
-  const uint32_t nchunks = (uint32_t)((nbytes + kChunkBytes - 1) / kChunkBytes);
-  const uint32_t mine = blockIdx.x < nchunks ? (nchunks - blockIdx.x + G - 1) / G : 0;
-  const char* body = reinterpret_cast<const char*>(s.body());
-  const uint64_t pol = l2_evict_first_policy();
-  auto chunk_bytes = [&](uint32_t k) -> uint32_t {
-    const uint64_t off = (uint64_t)(blockIdx.x + k * G) * kChunkBytes;
-    const uint64_t rem = nbytes - off;
-    return (uint32_t)(rem < kChunkBytes ? rem : kChunkBytes);
-  };
-  auto issue = [&](uint32_t k) {
-    const uint32_t slot = k % stages, b = chunk_bytes(k);
-    mbar_arrive_expect_tx(&full_bar[slot], b);
-    tma_load_1d(ring + (size_t)slot * kChunkBytes, body + (uint64_t)(blockIdx.x + k * G) * kChunkBytes, b,
-                &full_bar[slot], pol);
-  };
-  if (threadIdx.x == 0)
-    for (uint32_t k = 0; k < mine && k < stages; ++k) issue(k);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t nvec = 0;
-  for (uint32_t k = 0; k < mine; ++k) {
-    const uint32_t slot = k % stages, parity = (k / stages) & 1u;
-    mbar_wait_sleep(&full_bar[slot], parity);
-    const uint32_t nv = chunk_bytes(k) / 16;
-    const int4* src = reinterpret_cast<const int4*>(ring + (size_t)slot * kChunkBytes);
-    const uint32_t v0 = warp * 64 + lane, v1 = v0 + 32;
-    const uint32_t i4 = (blockIdx.x + k * G) * (kChunkBytes / 16);
-    if (v1 < nv) {
-      const int4 x0 = src[v0], x1 = src[v1];
-      f4(x0, i4 + v0);
-      f4(x1, i4 + v1);
-      nvec += 2;
-    } else if (v0 < nv) {
-      f4(src[v0], i4 + v0);
-      nvec += 1;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[slot]);
-    if (threadIdx.x == 0 && k + stages < mine) {
-      mbar_wait_sleep(&empty_bar[slot], parity);  // every warp has read this slot
-      issue(k + stages);
-    }
-  }
-  return nvec;
-}
-
 // Slow path of an int4 group holding at least one key outside [0,U): ingest the valid keys
 // one by one and record the bad ones (never taken on valid input; kept out of line).
 template <bool PACK16>
@@ -162,29 +99,18 @@ __device__ __noinline__ uint32_t ingest4_checked(uint32_t* h, int4 v, uint64_t i
   return bad;
 }
 
-// Error path of the hot loop: re-read the vectors this thread owns and ingest, key by key,
-// those that hold an out-of-range key (the hot loop skipped them whole); returns #bad keys.
-// CHUNK: ownership of the TMA traversal (lane owns vectors warp*64+lane and +32 of each of its
-// CTA's chunks); otherwise the register traversal's grid stride.
-template <bool PACK16, bool CHUNK>
+// Error path of the hot loop: re-read the vectors this thread owns (the grid stride of
+// for_each_key4) and ingest, key by key, those that hold an out-of-range key (the hot loop
+// skipped them whole); returns #bad keys.
+template <bool PACK16>
 __device__ __noinline__ uint32_t ingest_deferred(uint32_t* h, const KeySpan& s, uint32_t U, DevStatus* st) {
   const uint32_t n4 = (uint32_t)s.n4;
   const int4* body = s.body();
   uint32_t bad = 0;
-  auto one = [&](uint32_t i) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const int4 v = body[i];
     if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)i, U, st);
-  };
-  if (CHUNK) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t c = blockIdx.x; c * kChunkVecs < n4; c += gridDim.x) {
-      const uint64_t i0 = c * kChunkVecs + warp * 64 + lane;
-      if (i0 < n4) one((uint32_t)i0);
-      if (i0 + 32 < n4) one((uint32_t)(i0 + 32));
-    }
-  } else {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) one(i);
   }
   return bad;
 }
@@ -199,10 +125,9 @@ __device__ __forceinline__ void crn_red(uint32_t* H, uint32_t k, bool valid) {
   }
 }
 
-// The keys this CTA owns, warp-synchronously (every lane runs every iteration), for the CRN
-// paths: f(key, index, valid).  CHUNK selects the TMA traversal's ownership (whole chunks
-// c, c+G, ...), otherwise the grid stride of the register traversal.
-template <bool CHUNK = false, typename F>
+// The keys this CTA owns (the grid stride of for_each_key4), warp-synchronously (every lane runs
+// every iteration), for the CRN paths: f(key, index, valid).
+template <typename F>
 __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
   const uint64_t T = blockDim.x, G = gridDim.x;
   {
@@ -223,27 +148,18 @@ __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
     f((uint32_t)v.z, b + 2, ok);
     f((uint32_t)v.w, b + 3, ok);
   };
-  if (CHUNK) {
-    for (uint64_t c = blockIdx.x; c * kChunkVecs < s.n4; c += G)
-      for (uint32_t j = 0; j < kChunkVecs; j += T) {
-        const uint64_t i = c * kChunkVecs + j + threadIdx.x;
-        vec(i, i < s.n4);
-      }
-  } else {
-    const uint64_t stride = G * T;
-    for (uint64_t w = blockIdx.x * T + (threadIdx.x & ~31u); w < s.n4; w += stride) {
-      const uint64_t i = w + (threadIdx.x & 31);
-      vec(i, i < s.n4);
-    }
+  const uint64_t stride = G * T;
+  for (uint64_t w = blockIdx.x * T + (threadIdx.x & ~31u); w < s.n4; w += stride) {
+    const uint64_t i = w + (threadIdx.x & 31);
+    vec(i, i < s.n4);
   }
 }
-template <bool CHUNK>
 __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
                                                     uint32_t U, DevStatus* st, uint32_t epoch) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
-  for_each_key_warp<CHUNK>(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
+  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
 }
 
 // ---- shared-memory paths: ingestion + merge + scan in one co-resident grid ------------------
@@ -258,16 +174,28 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
 // Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
 // writes the row and, per 512-bin tile, the row's tile sum into tsums[tile][row] — or, for
-// k_sort_fused (a.fused), the row's 64-bin tile sums into shared memory (tsum_sh), from
-// which thread b < G adds the row's sum over CTA b's tiles into the owner total own_red[b].
-__device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U) {
-  const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x;
-  for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) {
+// k_sort_fused (a.fused), the row's 64-bin tile sums into shared memory (tsum_sh), from which
+// the row's sum s_o over each owning CTA o's tiles is formed.  k_sort_fused needs, after its
+// grid barrier, only the first output position of its own tiles: P_o = Σ_rows Σ_{o' < o} s_o'.
+// So each row adds its inclusive prefix over owners into P_{o+1} (one RED per owner, counters
+// on separate L2 lines: same-line REDs serialise) and CTA o later reads just P_o and P_{o+1}
+// (two lines) instead of every owner total.  It also votes "skewed" (one RED into a per-launch
+// word) when some s_o exceeds 5/4 of its even share of the row: the own-tile projection is then
+// replaced by equal position shares (no vote anywhere bounds every owner's positions by
+// 5/4 n / G + 64 G, so own tiles stay balanced).
+__device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U,
+                                                   uint32_t* red) {
+  const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x, b = threadIdx.x;
+  uint32_t s = 0;
+  if (b < G) {
     const uint32_t t0 = (uint32_t)((uint64_t)ntf * b / G), t1 = (uint32_t)((uint64_t)ntf * (b + 1) / G);
-    uint32_t s = 0;
     for (uint32_t t = t0; t < t1; ++t) s += tsum_sh[t];
-    if (s) red_add_u32(a.own_red + (uint64_t)b * a.ctr_stride, s);
   }
+  uint32_t tot;
+  const uint32_t inc = block_excl_scan<uint32_t>(s, tot, red) + s;  // Σ_{o <= b} s_o
+  if (b < G && inc) red_add_u32(a.own_red + (uint64_t)(b + 1) * a.ctr_stride, inc);
+  const bool skew = b < G && 4ull * G * s > 5ull * tot + 256ull * G;  // (tot = the row's keys)
+  if (__syncthreads_or(skew) && threadIdx.x == 0) red_add_u32(a.own_red + (uint64_t)(kFOwnVote)*a.ctr_stride, 1u);
 }
 
 // ---- 16-bit keys (the hierarchical path's universe blocks, ds_part.cuh) -------------------
@@ -360,11 +288,9 @@ __device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4*
   }
 }
 
-template <bool PACK16, bool TMA, bool K16 = false>
+template <bool PACK16, bool K16 = false>
 __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_v, uint64_t n, const ScanArgs& a,
-                                                  uint32_t stages, uint32_t* sh_hist, uint64_t* red64,
-                                                  uint64_t* full_bar, uint64_t* empty_bar,
-                                                  uint32_t* tsum_sh = nullptr) {
+                                                  uint32_t* sh_hist, uint64_t* red64, uint32_t* tsum_sh = nullptr) {
   const uint32_t U = a.U, ldw = a.ldw;
 
   // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
@@ -464,17 +390,6 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   };
   if (K16) {
     seen += 8 * for_each_key8_u16(s16, f4, f1);  // (16-bit keys are < U by construction)
-  } else if (TMA) {
-    if (threadIdx.x == 0) {
-      for (uint32_t q = 0; q < stages; ++q) {
-        mbar_init(&full_bar[q], 1);
-        mbar_init(&empty_bar[q], blockDim.x / 32);
-      }
-      mbar_fence_init();
-    }
-    __syncthreads();
-    seen += 4 * for_each_key_tma(s, reinterpret_cast<unsigned char*>(sh_hist) + 4ull * max(ldw, 8192u), stages,
-                                 full_bar, empty_bar, f4, f1);
   } else {
     for_each_key4(s, f4, f1);
     // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
@@ -483,7 +398,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
     seen += 4 * cnt;
   }
-  if (!K16 && deferred) bad += ingest_deferred<PACK16, TMA>(sh_hist, s, U, st);
+  if (!K16 && deferred) bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
@@ -613,7 +528,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     const bool exact = dsum == 0u;
     // k_sort_fused: the row's owner totals (its tile sums summed per owning CTA) — only for
     // an exact row (an overflowed one is recounted after the barrier)
-    if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U);
+    if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64));
     if (!exact) {
       if (a.fused) {
         // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
@@ -632,27 +547,25 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
         }
         uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
         if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
-        else hist_overflow_fallback<TMA>(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
+        else hist_overflow_fallback(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
       } else {
-        hist_overflow_fallback<TMA>(s, row4, W4, a.ovfH, U, st, a.epoch);
+        hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch);
       }
     }
   } else if (tsum_sh) {  // 32-bit rows cannot overflow
     __syncthreads();
-    flush_owner_totals(a, tsum_sh, U);
+    flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64));
   }
   phase_mark(a.pt, 2);
 }
 
-template <bool PACK16, bool TMA>
-__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a,
-                                                       uint32_t stages) {
+template <bool PACK16>
+__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a) {
   extern __shared__ __align__(128) uint32_t sh_hist[];
   __shared__ uint64_t red64[34];
-  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
   phase_mark(a.pt, -1);
-  hist_ingest_flush<PACK16, TMA>(keys, n, a, stages, sh_hist, red64, full_bar, empty_bar);
+  hist_ingest_flush<PACK16>(keys, n, a, sh_hist, red64);
   const uint32_t U = a.U;
   DevStatus* st = a.st;
   grid_barrier(a.bar);  // every row, tile sum (and any fallback contribution) is in L2

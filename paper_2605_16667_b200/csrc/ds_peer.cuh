@@ -33,15 +33,4 @@ __global__ void k_push_slices(const uint32_t* __restrict__ H, uint32_t U, uint32
   pdl_trigger();
 }
 
-// Owner side: H_slice[j] = Σ_src recv[src * L + j] (uint32 sums; every count fits: n < 2^32).
-__global__ void k_slice_sum(const uint32_t* __restrict__ recv, uint32_t G, uint32_t L, uint32_t* __restrict__ Hs) {
-  pdl_wait();
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < L; j += gridDim.x * blockDim.x) {
-    uint32_t h = 0;
-    for (uint32_t src = 0; src < G; ++src) h += __ldcg(recv + (uint64_t)src * L + j);
-    Hs[j] = h;
-  }
-  pdl_trigger();
-}
-
 }  // namespace ds

@@ -61,6 +61,8 @@ struct ScanArgs {
   // Hpeer[s][peerRank * peerL + k - s * peerL] (P2P stores over NVLink / NVSwitch)
   uint32_t* const* Hpeer;    // device array of G device pointers, or null
   uint32_t peerL, peerRank;
+  uint32_t bin_base;         // universe bin of this launch's bin 0 (hierarchical blocks), for Hpeer
+  int hist_only;             // k_sort_fused: stop after the merge (H only, no projection)
   int do_scan;
   uint32_t* P;               // [U+1] exclusive prefix
   uint64_t* range_tot;       // [gridDim] per-CTA range totals
@@ -96,8 +98,8 @@ struct ScanArgs {
 // H[bin] = h, or — multi-GPU histogram — the owner rank's slot of this rank (see Hpeer).
 __device__ __forceinline__ void store_H(const ScanArgs& a, uint32_t bin, uint32_t h) {
   if (a.Hpeer) {
-    const uint32_t sl = bin / a.peerL;
-    a.Hpeer[sl][(uint64_t)a.peerRank * a.peerL + (bin - sl * a.peerL)] = h;
+    const uint32_t gb = a.bin_base + bin, sl = gb / a.peerL;
+    a.Hpeer[sl][(uint64_t)a.peerRank * a.peerL + (gb - sl * a.peerL)] = h;
   } else {
     a.H[bin] = h;
   }

@@ -24,21 +24,20 @@ import torch.distributed as dist
 class ShardedResult:
     out: torch.Tensor          # int32[capacity]; the first `count` entries are valid
     count: torch.Tensor        # int64[1] (device): keys of this rank's universe slice
-    all_counts: torch.Tensor   # int64[G] (device): every rank's slice count (rank order)
-    slice_lo: int              # first key of this rank's slice
-    slice_len: int             # U / G
+    offset_t: torch.Tensor     # int64[1] (device): global position of this rank's first key
+    slice_lo: int              # first key of this rank's slice (radix path: 0, ranges are data-driven)
+    slice_len: int             # U / G (0 on the radix path)
 
     def offset(self) -> int:
-        """Global output offset of this rank's slice (host read; not on the hot path)."""
-        g = self.slice_lo // self.slice_len if self.slice_len else 0
-        return int(self.all_counts[:g].sum().item())
+        """Global output offset of this rank's keys (host read; not on the hot path)."""
+        return int(self.offset_t.item())
 
     def valid(self) -> torch.Tensor:
         return self.out[: int(self.count.item())]
 
 
 class _DeviceOps:
-    """Device steps through the C ABI (the product path)."""
+    """Device steps of the NCCL baseline through the C ABI."""
 
     def __init__(self, ctx):
         self.ctx = ctx
@@ -48,31 +47,6 @@ class _DeviceOps:
 
     def reconstruct(self, H_slice: torch.Tensor, key_base: int, out: torch.Tensor, d_total: torch.Tensor):
         self.ctx.reconstruct(H_slice, out, key_base=key_base, exact=False, d_total=d_total)
-
-    # peer-memory exchange (PeerExchange / sharded_sort_p2p)
-    def alloc_recv(self, size: int, device):
-        t = torch.empty(size, dtype=torch.int32, device=device)
-        return t, self.ctx.ipc_handle(t)
-
-    def open(self, handle):
-        return self.ctx.ipc_open(handle)
-
-    def close(self, remote):
-        self.ctx.ipc_close(remote)
-
-    def peer_table(self, recv: torch.Tensor, remote: list, g: int, off: int, length: int):
-        ptrs = [(recv.data_ptr() if r is None else r) + 4 * off for r in remote]
-        return torch.tensor(ptrs, dtype=torch.int64, device=recv.device)
-
-    def histogram_scatter(self, keys: torch.Tensor, U: int, G: int, g: int, peers) -> None:
-        self.ctx.histogram_scatter(keys, U, G, g, peers)
-
-    def barrier(self, group) -> None:
-        torch.cuda.current_stream(self.ctx.device).synchronize()  # this rank's P2P stores landed
-        dist.barrier(group=group)                                  # ... and every other rank's
-
-    def slice_sum(self, recv: torch.Tensor, G: int, L: int) -> torch.Tensor:
-        return self.ctx.slice_sum(recv, G, L)
 
 
 def _reduce_scatter_sum(H_local: torch.Tensor, S: int, group) -> torch.Tensor:
@@ -89,7 +63,7 @@ def _reduce_scatter_sum(H_local: torch.Tensor, S: int, group) -> torch.Tensor:
 
 def sharded_sort(keys_local: torch.Tensor, U: int, capacity: int, group=None, ctx=None, ops=None,
                  out: torch.Tensor | None = None) -> ShardedResult:
-    """Sort the union of all ranks' key shards; rank g receives universe slice g.
+    """NCCL baseline: sort the union of all ranks' key shards; rank g receives universe slice g.
 
     capacity: room (keys) of this rank's output.  A slice with more keys than `capacity`
     raises DIALSORT_E_SIZE at the next sync (its first `capacity` keys are written).
@@ -115,64 +89,8 @@ def sharded_sort(keys_local: torch.Tensor, U: int, capacity: int, group=None, ct
     ops.reconstruct(H_slice, g * S, out, count)                # project slice g, key_base g*S
     all_counts = torch.empty(G, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(all_counts, count, group=group)  # slice totals -> offsets
-    return ShardedResult(out=out, count=count, all_counts=all_counts, slice_lo=g * S, slice_len=S)
-
-
-class PeerExchange:
-    """Receive buffers of the peer-memory exchange: rank g holds G slots of its universe slice
-    (one per source rank, uint32[G * L]), mapped into every rank with CUDA IPC once and reused
-    across calls.  Two parities alternate between calls: a rank one call ahead writes the other
-    parity while its peers still read this one (the per-call barrier bounds the lead to one)."""
-
-    def __init__(self, U: int, device, group=None, ctx=None, ops=None):
-        self.G = dist.get_world_size(group)
-        self.g = dist.get_rank(group)
-        if U % self.G != 0:
-            raise ValueError(f"U={U} must be divisible by the world size {self.G} (reading R10)")
-        self.U, self.L, self.group = U, U // self.G, group
-        if ops is None:
-            if ctx is None:
-                from . import default_context
-                ctx = default_context(device)
-            ops = _DeviceOps(ctx)
-        self.ops = ops
-        GL = self.G * self.L
-        self.recv_all, handle = ops.alloc_recv(2 * GL, device)
-        handles = [None] * self.G
-        dist.all_gather_object(handles, handle, group=group)
-        self.remote = [None if s == self.g else ops.open(handles[s]) for s in range(self.G)]
-        self.recv = [self.recv_all[p * GL:(p + 1) * GL] for p in range(2)]
-        self.peers = [ops.peer_table(self.recv_all, self.remote, self.g, p * GL, GL) for p in range(2)]
-        self.calls = 0
-
-    def close(self) -> None:
-        for r in self.remote:
-            if r is not None:
-                self.ops.close(r)
-        self.remote = []
-
-
-def sharded_sort_p2p(keys_local: torch.Tensor, ex: PeerExchange, capacity: int,
-                     out: torch.Tensor | None = None) -> ShardedResult:
-    """sharded_sort with the exchange over peer memory instead of an NCCL reduce-scatter: one
-    kernel builds the local histogram and stores each finished bin of universe slice s straight
-    into rank s's slot for this rank (NVLink / NVSwitch P2P stores, dialsort_histogram_scatter_async);
-    after every rank's kernel completed (stream sync + barrier), rank g sums its G slots and
-    projects its slice with key_base g L."""
-    G, g, L, ops = ex.G, ex.g, ex.L, ex.ops
-    dev = keys_local.device
-    par = ex.calls & 1
-    ex.calls += 1
-    ops.histogram_scatter(keys_local, ex.U, G, g, ex.peers[par])
-    ops.barrier(ex.group)
-    H_slice = ops.slice_sum(ex.recv[par], G, L)
-    if out is None:
-        out = torch.empty(int(capacity), dtype=torch.int32, device=dev)
-    count = torch.zeros(1, dtype=torch.int64, device=dev)
-    ops.reconstruct(H_slice, g * L, out, count)
-    all_counts = torch.empty(G, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_counts, count, group=ex.group)
-    return ShardedResult(out=out, count=count, all_counts=all_counts, slice_lo=g * L, slice_len=L)
+    offset = all_counts[:g].sum().reshape(1)
+    return ShardedResult(out=out, count=count, offset_t=offset, slice_lo=g * S, slice_len=S)
 
 
 def sharded_histogram(keys_local: torch.Tensor, U: int, group=None, ctx=None, ops=None) -> torch.Tensor:
@@ -186,3 +104,57 @@ def sharded_histogram(keys_local: torch.Tensor, U: int, group=None, ctx=None, op
             ctx = default_context(keys_local.device)
         ops = _DeviceOps(ctx)
     return _reduce_scatter_sum(ops.histogram(keys_local, U), U // G, group)
+
+
+def connect_comms(comm, group=None) -> None:
+    """One-time bootstrap of a communicator over torch.distributed: every rank's handle bytes,
+    all-gathered in rank order, then opened (CUDA IPC) by every rank."""
+    G = dist.get_world_size(group)
+    handles = [None] * G
+    dist.all_gather_object(handles, comm.handle, group=group)
+    comm.connect_ipc(handles)
+
+
+class PeerComm:
+    """This rank's communicator (dialsort_comm) for U <= max_U and up to max_recv_keys radix keys."""
+
+    def __init__(self, max_U: int, device, group=None, ctx=None, max_recv_keys: int = 0, comm_factory=None):
+        from . import Comm, default_context
+        self.G = dist.get_world_size(group)
+        self.g = dist.get_rank(group)
+        self.group = group
+        self.ctx = ctx if ctx is not None else default_context(device)
+        make = comm_factory if comm_factory is not None else Comm
+        self.comm = make(self.ctx, self.G, self.g, int(max_U), int(max_recv_keys))
+        connect_comms(self.comm, group)
+
+    def close(self) -> None:
+        self.comm.close()
+
+
+def sharded_sort_p2p(keys_local: torch.Tensor, pc: PeerComm, U: int, capacity: int,
+                     out: torch.Tensor | None = None) -> ShardedResult:
+    """Sharded DialSort with the exchange over peer memory (dialsort_sharded_sort_async): one
+    histogram kernel stores each merged bin of slice s into rank s's slot, rank g sums its slots
+    and projects slice g with key_base g U/G; count and offset stay on the device."""
+    if U % pc.G != 0:
+        raise ValueError(f"U={U} must be divisible by the world size {pc.G} (reading R10)")
+    dev = keys_local.device
+    if out is None:
+        out = torch.empty(int(capacity), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    pc.comm.sort(keys_local, U, out, cnt[0:1], cnt[1:2])
+    L = U // pc.G
+    return ShardedResult(out=out, count=cnt[0:1], offset_t=cnt[1:2], slice_lo=pc.g * L, slice_len=L)
+
+
+def sharded_sort_int32(keys_local: torch.Tensor, pc: PeerComm, capacity: int,
+                       out: torch.Tensor | None = None) -> ShardedResult:
+    """Sharded DialSort-Radix (dialsort_sharded_sort_int32_async): rank g ends with the sorted keys
+    of its contiguous top-byte range; the rank-order concatenation is the sorted array."""
+    dev = keys_local.device
+    if out is None:
+        out = torch.empty(int(capacity), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    pc.comm.sort_int32(keys_local, out, cnt[0:1], cnt[1:2])
+    return ShardedResult(out=out, count=cnt[0:1], offset_t=cnt[1:2], slice_lo=0, slice_len=0)

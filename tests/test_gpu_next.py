@@ -1,0 +1,164 @@
+"""GPU parity of the canonical-state queries (NEXT-1) and of DialSort-Radix's pass buffers and
+variant selection, through the C ABI, against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ds(cuda_dev):
+    import paper_2605_16667_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(ds, cuda_dev):
+    return ds.Context(0, max_n=1 << 22, max_U=1 << 20)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to("cuda:0")
+
+
+def u32_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).to("cuda:0")
+
+
+# ---- NEXT-1: frequency, presence, range-count, support set + prop:iso ---------------------------
+
+def test_queries_paper_example(ds, ctx):
+    """fig:viz state H = [0,2,0,4,0,2]: frequency(3) = 4, presence(2) = false,
+    presence(5) = true, range-count(0,5) = 8, (3,5) = 6, (2,2) = 0; D = {1,3,5}, not an isomorphism."""
+    keys = to_dev([3, 1, 3, 5, 1, 3, 5, 3])
+    H = ctx.histogram(keys, 6)
+    f = ctx.query(H, ds._lib.Q_FREQUENCY, to_dev([3, 0, 5]))
+    p = ctx.query(H, ds._lib.Q_PRESENCE, to_dev([2, 5, 1]))
+    r = ctx.query(H, ds._lib.Q_RANGE_COUNT, to_dev([[0, 5], [3, 5], [2, 2]]))
+    D, cnt, iso = ctx.support_set(H)
+    ctx.sync()
+    assert f.cpu().tolist() == [4, 0, 2] and p.cpu().tolist() == [0, 1, 1] and r.cpu().tolist() == [8, 6, 0]
+    assert int(cnt) == 3 and D[:3].cpu().tolist() == [1, 3, 5] and int(iso) == 0
+
+
+@pytest.mark.parametrize("U,dist", [(1, "uniform"), (256, "uniform"), (5000, "zipf"), (65536, "sorted"),
+                                    (300_007, "hot1"), (1 << 20, "uniform")])
+def test_queries_random_vs_oracle(ds, ctx, U, dist):
+    n = 400_003
+    x = synth.hot1(n, U, seed=U) if dist == "hot1" else synth.make(dist, n, U, seed=U)
+    H = ctx.histogram(to_dev(x), U)
+    Hr = oracle.histogram(x, U)
+    rng = np.random.default_rng(U)
+    q = rng.integers(0, U, size=10_001)
+    a = rng.integers(0, U, size=5003)
+    b = np.minimum(U - 1, a + rng.integers(0, max(U // 3, 1), size=a.size))
+    pairs = np.stack([a, b], 1)
+    f = ctx.query(H, ds._lib.Q_FREQUENCY, to_dev(q))
+    p = ctx.query(H, ds._lib.Q_PRESENCE, to_dev(q))
+    r = ctx.query(H, ds._lib.Q_RANGE_COUNT, to_dev(pairs))
+    D, cnt, iso = ctx.support_set(H)
+    ctx.sync()
+    assert np.array_equal(f.cpu().numpy(), Hr[q].astype(np.int64))
+    assert np.array_equal(p.cpu().numpy(), (Hr[q] > 0).astype(np.int64))
+    assert r.cpu().tolist() == [oracle.range_count(Hr, int(i), int(j)) for i, j in pairs]
+    Dr = oracle.support_set(Hr)
+    assert int(cnt) == Dr.size and np.array_equal(D[:Dr.size].cpu().numpy().view(np.uint32), Dr)
+    assert int(iso) == int(Dr.size == U)
+
+
+def test_support_set_isomorphism_condition(ds, ctx):
+    """prop:iso: phi is an order-isomorphism iff D = [0, U-1]; every key once (U = 4, the SPEC
+    example) and a full universe of 65536 with one key removed."""
+    for keys, U, want in [([2, 0, 3, 1], 4, 1), (list(range(65536)), 65536, 1), (list(range(1, 65536)), 65536, 0)]:
+        H = ctx.histogram(to_dev(keys), U)
+        D, cnt, iso = ctx.support_set(H)
+        ctx.sync()
+        assert int(iso) == want and int(cnt) == len(set(keys))
+        assert D[:int(cnt)].cpu().tolist() == sorted(set(keys))
+
+
+def test_query_range_errors(ds, ctx):
+    H = ctx.histogram(to_dev([0, 1, 1]), 4)
+    ctx.query(H, ds._lib.Q_FREQUENCY, to_dev([1, 4, 2]))      # 4 is outside [0, 4)
+    with pytest.raises(ds.DialSortError) as e:
+        ctx.sync()
+    assert e.value.code == 2 and e.value.info.first_bad_index == 1 and e.value.info.first_bad_key == 4
+    ctx.query(H, ds._lib.Q_RANGE_COUNT, to_dev([[0, 3], [3, 1]]))  # a > b
+    with pytest.raises(ds.DialSortError) as e:
+        ctx.sync()
+    assert e.value.code == 2 and e.value.info.first_bad_index == 1
+
+
+# ---- DialSort-Radix: per-pass buffers and the two pass variants ---------------------------------
+
+@pytest.mark.parametrize("variant", [3, 4])
+@pytest.mark.parametrize("n,shape", [(8, "full"), (100_000, "full"), (1_000_004, "full"), (524_288, "lowbyte"),
+                                     (262_144, "equal_hi")])
+def test_radix_pass_buffers_vs_oracle(ds, cuda_dev, variant, n, shape):
+    """After pass p the buffer is the stable sort of the input by its low 8(p+1) bits — a unique
+    array — compared with the oracle's pass buffers for each variant."""
+    c = ds.Context(0)
+    c.set_option(ds._lib.OPT_RADIX_VARIANT, variant)
+    rng = np.random.default_rng(n)
+    if shape == "full":
+        x = synth.full_int32(n, seed=n)
+    elif shape == "lowbyte":  # equal high bytes, whole warps of equal digits in passes 1..3
+        x = ((rng.integers(-4, 4, size=n) << 8) | rng.integers(0, 256, size=n)).astype(np.int32)
+    else:
+        x = (0x7f000000 | rng.integers(0, 1 << 16, size=n)).astype(np.int32)
+    passes = c.debug_radix_passes(to_dev(x))
+    c.sync()
+    ref_out, ref_passes = oracle.radix_sort_i32(x, return_passes=True)
+    got = passes.cpu().numpy().view(np.uint32)
+    for p in range(3):
+        assert np.array_equal(got[p], ref_passes[p]), p
+    assert np.array_equal(got[3].view(np.int32), ref_out)
+
+
+def test_radix_lane_probe_and_variant_selection(ds, cuda_dev):
+    """The context probes the ATOMS lane order once per device; automatic selection uses pass4
+    only when the probe found no violation; forced variants are honoured."""
+    c = ds.Context(0)
+    v = c.get_option(ds._lib.OPT_RADIX_PROBE_VIOLATIONS)
+    assert v >= 0
+    assert c.radix_variant == (4 if v == 0 else 3)
+    c.set_option(ds._lib.OPT_RADIX_VARIANT, 3)
+    assert c.radix_variant == 3
+    c.set_option(ds._lib.OPT_RADIX_VARIANT, 4)
+    assert c.radix_variant == 4
+    with pytest.raises(ds.DialSortError):
+        c.set_option(ds._lib.OPT_RADIX_VARIANT, 5)
+    x = synth.full_int32(300_001, seed=9)
+    for var in (3, 4):
+        c.set_option(ds._lib.OPT_RADIX_VARIANT, var)
+        y = c.sort_int32(to_dev(x))
+        c.sync()
+        assert np.array_equal(y.cpu().numpy(), oracle.radix_sort_i32(x)), var
+
+
+def test_concurrent_contexts_two_streams(ds, cuda_dev):
+    """Two contexts issue grid-barrier kernels on two streams at once (the e2e pipeline's shape):
+    cooperative launches keep each grid co-resident (no deadlock), results exact."""
+    cs = [ds.Context(0, max_n=4_000_000, max_U=65536) for _ in range(2)]
+    sts = [torch.cuda.Stream(cuda_dev) for _ in range(2)]
+    xs = [synth.uniform(3_000_001, 65536, seed=60 + i) for i in range(6)]
+    rs = [synth.full_int32(2_000_003, seed=70 + i) for i in range(6)]
+    dx = [to_dev(x) for x in xs]
+    dr = [to_dev(r) for r in rs]
+    torch.cuda.synchronize()
+    outs, routs = [], []
+    for i in range(6):
+        with torch.cuda.stream(sts[i % 2]):
+            outs.append(cs[i % 2].sort(dx[i], 65536))
+            routs.append(cs[i % 2].sort_int32(dr[i]))
+    for i in range(2):
+        with torch.cuda.stream(sts[i]):
+            cs[i].sync()
+    torch.cuda.synchronize()
+    for i in range(6):
+        assert np.array_equal(outs[i].cpu().numpy(), oracle.sort(xs[i], 65536)), i
+        assert np.array_equal(routs[i].cpu().numpy(), oracle.radix_sort_i32(rs[i])), i

@@ -20,10 +20,9 @@ dev = torch.device("cuda:0")
 keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
 outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
-fused = os.environ.get("DIALSORT_FUSED") != "0"
-names = (["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
-          "proj_start", "m_reduced", "flush_loop", "r_rows", "r_synced", "m_scanned", "m_Pwritten"] if fused else
-         ["ingest", "sync", "flush", "barrier1", "merge_scan", "offsets_issued", "rows_summed", "expand_start"] + [""] * 8)
+fused = True
+names = ["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
+         "proj_start", "m_reduced", "flush_loop", "r_rows", "r_synced", "m_scanned", "m_Pwritten"]
 for rep in range(4):
     ctx.debug_phase_cta()
     for _ in range(int(os.environ.get("PHASE_BACK_TO_BACK", "1"))):  # stamps: the last launch
