@@ -62,6 +62,7 @@ def _L():
         lib.oracle_radix_pass.restype = None
         lib.oracle_radix_sort_i32.argtypes = [P, u64, P, P]
         lib.oracle_sharded_radix_rank.argtypes = [P, u64, ci, ci, P, u64, P, P, P]
+        lib.oracle_sort_domain.argtypes = [P, ci, u64, u64, P, P, P, P]
         lib.oracle_range_count.argtypes = [P, u64, u64]
         lib.oracle_range_count.restype = u64
         lib.oracle_support_set.argtypes = [P, u64, P]
@@ -207,6 +208,24 @@ def sharded_radix_rank(keys, G: int, g: int):
         raise OracleError(rc, f"oracle_sharded_radix_rank rc={rc}")
     c = int(cnt[0])
     return out[:c], c, int(off[0]), D[: int(G) + 1].astype(np.int64)
+
+
+def sort_domain(items, U: int, encode=None, decode=None) -> np.ndarray:
+    """A2 Proposition 2: items (uint8 / uint16 / int32 array), phi = encode table (1-byte items)
+    or identity, phi^-1 = decode table or identity.  Returns the emitted int32 sequence."""
+    it = np.ascontiguousarray(items)
+    width = {np.dtype(np.uint8): 1, np.dtype(np.uint16): 2, np.dtype(np.int32): 4}[it.dtype]
+    enc = None if encode is None else np.ascontiguousarray(encode, dtype=np.uint32)
+    dec = None if decode is None else np.ascontiguousarray(decode, dtype=np.int32)
+    out = np.empty(max(it.size, 1), dtype=np.int32)
+    bad = np.zeros(1, dtype=np.uint64)
+    rc = _L().oracle_sort_domain(_ptr(it), width, it.size, int(U), _ptr(enc) if enc is not None else None,
+                                 _ptr(dec) if dec is not None else None, _ptr(out), _ptr(bad))
+    if rc == E_KEY_RANGE:
+        raise OracleError(rc, f"item {int(bad[0])} maps outside [0,{U})")
+    if rc != OK:
+        raise OracleError(rc, f"oracle_sort_domain rc={rc}")
+    return out[: it.size]
 
 
 def range_count(H, a: int, b: int) -> int:

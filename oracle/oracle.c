@@ -269,6 +269,44 @@ int oracle_sharded_radix_rank(const int32_t *keys, uint64_t n, int G, int g, int
   }
 }
 
+/* A2 — general self-indexing, Proposition 2 (constructive proof): S a finite totally
+ * ordered set with a known order-isomorphism phi : S -> {0..U-1}.
+ *   1. "For each s in K, compute i = phi(s) and increment H[i]" — items are item_bytes = 1, 2
+ *      or 4 byte values; phi(s) = encode[s] when an encode table is given (1-byte items), else
+ *      s itself (the direct-address case); i outside [0,U) is a key-range error (R5);
+ *   2. "Sweep i = 0..U-1 and emit phi^-1(i) exactly H[i] times" — phi^-1(i) = decode[i] when a
+ *      decode table is given ("for other domains a lookup table suffices"), else i. */
+int oracle_sort_domain(const void *items, int item_bytes, uint64_t n, uint64_t U, const uint32_t *encode,
+                       const int32_t *decode, int32_t *out, uint64_t *bad_index) {
+  uint64_t i, k, c, pos = 0;
+  uint64_t *H;
+  if (U == 0 || (item_bytes != 1 && item_bytes != 2 && item_bytes != 4)) return ORACLE_E_INVALID_ARG;
+  if (encode && item_bytes != 1) return ORACLE_E_INVALID_ARG;
+  H = (uint64_t *)malloc(U * sizeof(uint64_t));
+  if (!H) return ORACLE_E_INVALID_ARG;
+  for (k = 0; k < U; k++) H[k] = 0;
+  for (i = 0; i < n; i++) {
+    uint64_t s;
+    if (item_bytes == 1) s = ((const uint8_t *)items)[i];
+    else if (item_bytes == 2) s = ((const uint16_t *)items)[i];
+    else s = (uint32_t)((const int32_t *)items)[i];
+    k = encode ? encode[s] : s;
+    if (k >= U) {
+      if (bad_index) *bad_index = i;
+      free(H);
+      return ORACLE_E_KEY_RANGE;
+    }
+    H[k] = H[k] + 1;
+  }
+  for (k = 0; k < U; k++)
+    for (c = 0; c < H[k]; c++) {
+      out[pos] = decode ? decode[k] : (int32_t)k;
+      pos = pos + 1;
+    }
+  free(H);
+  return ORACLE_OK;
+}
+
 /* NEXT-1 canonical-state queries on H: frequency(k) = H[k], presence(k) =
  * H[k] > 0, range-count(a,b) = Σ_{k=a}^{b} H[k] (O(b-a)), support set D = {k : H(k) > 0}
  * (P:326-329).  Returns |D| and writes D ascending into D_out (capacity U). */

@@ -272,3 +272,43 @@ def test_sharded_radix_balance():
         for g in range(G):
             _, cnt, _, _ = oracle.sharded_radix_rank(x, G, g)
             assert abs(cnt - 100_000 / G) <= C.max() + 1
+
+
+# ---- A2 Proposition 2: general self-indexing through phi -----------------------------------------
+
+def test_domain_spec_examples():
+    """SPEC generic-domain examples: ASCII "dcba" with phi = code point (U = 256) -> "abcd";
+    MIDI notes {60, 0, 127} with U = 128 -> {0, 60, 127}."""
+    out = oracle.sort_domain(np.frombuffer(b"dcba", dtype=np.uint8), 256)
+    assert bytes(out.astype(np.uint8)) == b"abcd"
+    assert oracle.sort_domain(np.array([60, 0, 127], dtype=np.uint8), 128).tolist() == [0, 60, 127]
+
+
+def test_domain_table_driven_enumeration():
+    """A 7-element enumerated domain whose order is not the symbols' numeric order: phi = rank
+    table (encode), phi^-1 = symbol table (decode).  Equals a comparison sort under <_S
+    (Python's sorted with key = rank), and decode(encode(s)) = s."""
+    rng = np.random.default_rng(5)
+    symbols = rng.permutation(np.arange(10, 250))[:7].astype(np.uint8)   # arbitrary symbol bytes
+    order = {int(s): r for r, s in enumerate(symbols)}                   # <_S: the table order
+    enc = np.zeros(256, dtype=np.uint32)
+    for s, r in order.items():
+        enc[s] = r
+    dec = symbols.astype(np.int32)
+    for trial in range(50):
+        items = rng.choice(symbols, size=int(rng.integers(0, 400))).astype(np.uint8)
+        got = oracle.sort_domain(items, 7, encode=enc, decode=dec)
+        assert got.tolist() == sorted(items.tolist(), key=lambda s: order[s])
+    assert all(int(dec[enc[s]]) == s for s in symbols.tolist())
+
+
+def test_domain_day_numbers_and_identity():
+    """Calendar days (phi = day number, U = 366) as 2-byte items equal the sorted days; with
+    identity maps the domain sort is the integer DialSort (A1) itself."""
+    rng = np.random.default_rng(6)
+    days = rng.integers(0, 366, size=5000).astype(np.uint16)
+    assert oracle.sort_domain(days, 366).tolist() == sorted(days.tolist())
+    x = synth.uniform(3001, 1000, seed=2)
+    assert np.array_equal(oracle.sort_domain(x, 1000), oracle.sort(x, 1000))
+    with pytest.raises(oracle.OracleError):
+        oracle.sort_domain(np.array([1, 400], dtype=np.uint16), 366)
