@@ -20,6 +20,8 @@ from __future__ import annotations
 
 import argparse
 import json
+
+import numpy as np
 import os
 import statistics
 import sys
@@ -136,6 +138,12 @@ def alg_bytes(cfg, G=1):
     return G * (8 * n // G + 8 * U + 8 * U // G)
 
 
+def config_dict(cfg, args, G):
+    """The workload (identical in both arms, so the driver can match them)."""
+    return {"workload": cfg["desc"], "n": cfg["n"], "U": cfg["U"], "dist": cfg["dist"], "seed": args.seed,
+            "parallelism": f"dp{G}"}
+
+
 def run_reference(args, cfg):
     """The CPU oracle as it stands, one thread, on this host: each step = one bounded sample."""
     import numpy as np
@@ -161,7 +169,7 @@ def run_reference(args, cfg):
         "metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": cfg["desc"], "n": cfg["n"], "U": cfg["U"], "dist": cfg["dist"], "seed": args.seed},
+        "config": config_dict(cfg, args, args.gpus),
         "cpu_baseline": {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
                          "sample": f"first {m} keys of the {args.config} input per step, oracle/oracle.c single thread"},
         "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -191,6 +199,99 @@ def cpu_baseline(cfg, seed, budget_s=10.0):
             "sample": f"{reps} x oracle sort of the first {m} keys of the {cfg['desc']} input ({el:.1f} s, 1 thread)"}
 
 
+def host_parallel_baseline(cfg, seed, budget_s=5.0):
+    """The DS-Parallel analog (baseline/ds_parallel.c: private histograms per thread, cell-wise
+    merge, parallel emit) on all host cores this process may use: context, not the target."""
+    if cfg["dist"] == "int32":
+        return None
+    import baseline
+    m = min(cfg["n"], 10_000_000)
+    x = make_host_input(cfg, seed)[:m] if cfg["n"] <= 100_000_000 else __import__("synth").uniform(m, cfg["U"], seed)
+    T = baseline.threads()
+    out = np.empty(m, dtype=np.int32)
+    baseline.sort(x, cfg["U"], T, out)
+    ts = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(ts) < 3:
+        t0 = time.perf_counter()
+        baseline.sort(x, cfg["U"], T, out)
+        ts.append(time.perf_counter() - t0)
+    best = min(ts)
+    return {"value": m / best, "unit": "keys/s", "cores": T, "kind": "ds_parallel (host threads)",
+            "cpu": baseline.cpu_model(), "mean_keys_s": m / (sum(ts) / len(ts)),
+            "sample": f"best of {len(ts)} DS-Parallel sorts of the first {m} keys ({T} threads)"}
+
+
+def run_grid(args):
+    """NEXT-2: the paper's own grid on one B200 (N in {1e4..1e7} x U in {256, 1024,
+    65536} x {uniform, skewed, sorted, reverse}, seed 20260321).  Per config: the device-resident
+    sort (best of 7 blocks of back-to-back steps, CUDA events), the e2e host-buffer sort
+    (dialsort_sort_host, pinned, H2D + sort + D2H per call, wall clock), the oracle (1 thread)
+    and the DS-Parallel host baseline, each verified against the oracle; one JSON line each."""
+    import torch
+    import oracle
+    import baseline
+    import paper_2605_16667_b200 as dsl
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    ctx = dsl.Context(0, max_n=10_000_000, max_U=65536)
+    T = baseline.threads()
+    for n in (10_000, 100_000, 1_000_000, 10_000_000):
+        for U in (256, 1024, 65536):
+            for dist_name in ("uniform", "skewed", "sorted", "reverse"):
+                x = __import__("synth").make(dist_name, n, U, args.seed)
+                ref = oracle.sort(x, U)
+                R = max(2, min(16, -(-3 * (126 << 20) // (8 * n))))
+                ins = [torch.from_numpy(x).to(dev) for _ in range(R)]
+                outs = [torch.empty_like(ins[0]) for _ in range(R)]
+                for i in range(5):
+                    ctx.sort(ins[i % R], U, out=outs[i % R])
+                ctx.sync()
+                ok = bool(np.array_equal(outs[4 % R].cpu().numpy(), ref))
+                kb = max(20, min(400, 2_000_000 // n))
+                blk = []
+                for r in range(7):
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for i in range(kb):
+                        ctx.sort(ins[i % R], U, out=outs[i % R])
+                    e1.record()
+                    torch.cuda.synchronize()
+                    blk.append(e0.elapsed_time(e1) / kb)
+                ctx.sync()
+                xh = torch.from_numpy(x).pin_memory()
+                oh = torch.empty_like(xh).pin_memory()
+                ctx.sort_host(xh, U, oh)
+                te = []
+                for r in range(7):
+                    t0 = time.perf_counter()
+                    ctx.sort_host(xh, U, oh)
+                    te.append(time.perf_counter() - t0)
+                ok = ok and bool(np.array_equal(oh.numpy(), ref))
+                to = []
+                for r in range(3 if n >= 10_000_000 else 7):
+                    t0 = time.perf_counter()
+                    oracle.sort(x, U)
+                    to.append(time.perf_counter() - t0)
+                po = np.empty(n, dtype=np.int32)
+                baseline.sort(x, U, T, po)
+                ok = ok and bool(np.array_equal(po, ref))
+                tp = []
+                for r in range(7):
+                    t0 = time.perf_counter()
+                    baseline.sort(x, U, T, po)
+                    tp.append(time.perf_counter() - t0)
+                line = {"grid": "paper P:1591-1598", "n": n, "U": U, "dist": dist_name, "verified": ok,
+                        "gpu_best_keys_s": n / (min(blk) * 1e-3), "gpu_mean_ms": statistics.mean(blk),
+                        "gpu_cv": statistics.stdev(blk) / statistics.mean(blk),
+                        "e2e_best_keys_s": n / min(te), "oracle_keys_s": n / min(to),
+                        "ds_parallel_keys_s": n / min(tp), "ds_parallel_threads": T,
+                        "l2": "inputs of n <= 4M keys are L2-resident between steps (latency regime)"
+                        if 8 * n * R < (126 << 20) else f"rotation over {R} copies"}
+                print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,6 +302,7 @@ def main():
     ap.add_argument("--seed", type=int, default=20260321)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--grid", action="store_true", help="NEXT-2: the paper's 48-config grid (one JSON line each)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: histogram exchange over peer memory (default) or NCCL reduce-scatter")
     args = ap.parse_args()
@@ -209,6 +311,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.grid:
+        return run_grid(args)
 
     import numpy as np
     import torch
@@ -258,25 +362,57 @@ def main():
         if radix and G == 1:
             ctx.sort_int32(ins[j], out=outs[j])
         elif radix:
-            sharded_sort_int32(ins[j], ex, capacity=cap, out=outs[j])
+            return sharded_sort_int32(ins[j], ex, capacity=cap, out=outs[j])
         elif G == 1:
             ctx.sort(ins[j], U, out=outs[j])
         elif ex is not None:
-            sharded_sort_p2p(ins[j], ex, U, capacity=cap, out=outs[j])
+            return sharded_sort_p2p(ins[j], ex, U, capacity=cap, out=outs[j])
         else:
-            sharded_sort(ins[j], U, capacity=cap, ctx=ctx, out=outs[j])
+            return sharded_sort(ins[j], U, capacity=cap, ctx=ctx, out=outs[j])
 
-    # ---- correctness gate before timing (bit-exact vs oracle at N=1) -----------------------
+    # ---- correctness gate before timing, and again on the last timed step (bit-exact vs the
+    # oracle: the whole output at N=1, every rank's piece vs the oracle's sharded reading at N>1)
     verified = None
-    step(0)
-    ctx.sync()
-    if G == 1 and n <= 100_000_000:
+    ref = None
+    if n <= 100_000_000:
         import oracle
         xh = make_host_input(cfg, args.seed)
-        ref = oracle.radix_sort_i32(xh) if radix else oracle.sort(xh, U)
-        verified = bool(np.array_equal(outs[0][:n].cpu().numpy(), ref))
-        if not verified:
-            raise SystemExit("bench: GPU output differs from the oracle")
+        if G == 1:
+            ref = oracle.radix_sort_i32(xh) if radix else oracle.sort(xh, U)
+        elif radix:
+            r_out, r_cnt, r_off, _ = oracle.sharded_radix_rank(xh, G, rank)
+            ref = (r_out, r_cnt, r_off)
+        else:
+            _, r_out, r_cnt, r_off = oracle.sharded_rank(xh, U, G, rank)
+            ref = (r_out, r_cnt, r_off)
+
+    last_result = [None]
+
+    def check(j):
+        """Output of the step that wrote outs[j] against the oracle (this rank's piece)."""
+        if ref is None:
+            return None
+        if G == 1:
+            return bool(np.array_equal(outs[j][:n].cpu().numpy(), ref))
+        res = last_result[0]
+        cnt, off = int(res.count.item()), res.offset()
+        ok = cnt == ref[1] and off == ref[2] and bool(np.array_equal(outs[j][:cnt].cpu().numpy(), ref[0]))
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    _step = step
+
+    def step(i):  # (keeps the sharded result handle of the last call for check())
+        r = _step(i)
+        last_result[0] = r
+        return r
+
+    step(0)
+    ctx.sync()
+    verified = check(0)
+    if verified is False:
+        raise SystemExit("bench: GPU output differs from the oracle")
 
     # ---- warm-up + timed region ------------------------------------------------------------
     stream = torch.cuda.current_stream(dev)
@@ -305,6 +441,36 @@ def main():
     ms_step = ms / args.steps
     value = n / (ms_step * 1e-3)
     peak, peak_kind = load_peaks()
+    verified_last = check((args.steps - 1) % R)  # the last timed step's output
+    if verified_last is False:
+        raise SystemExit("bench: the last timed step's output differs from the oracle")
+
+    # ---- repetition statistics (the paper reports best of 7 with mean / std / CV):
+    # 7 blocks of the same back-to-back steps, each timed on the device (max over ranks)
+    nb, kb = 7, max(10, args.steps // 7)
+    blk = []
+    for r in range(nb):
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for i in range(kb):
+            step(r * kb + i)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        t = b0.elapsed_time(b1) / kb
+        if G > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        blk.append(t)
+    ctx.sync()
+    mean_b = statistics.mean(blk)
+    std_b = statistics.stdev(blk) if len(blk) > 1 else 0.0
+    reps = {"blocks": nb, "steps_per_block": kb, "best_ms_per_step": min(blk), "mean_ms_per_step": mean_b,
+            "std_ms_per_step": std_b, "cv": std_b / mean_b if mean_b else None,
+            "best_value": n / (min(blk) * 1e-3)}
 
     # ---- per-kernel live timing (separate pass: event pairs disable the PDL overlap) -------
     ctx.profile(True)
@@ -396,32 +562,28 @@ def main():
         e2e = {"value": n / wall, "unit": "keys/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                "ms_per_step": wall * 1e3, "api": "dialsort_sort_host_async",
                "pipeline": "2 contexts x 2 streams: batch i+1's H2D overlaps batch i's sort + D2H (wall clock)"}
-        ref = torch.empty_like(ins[0][:n])  # the e2e output against the device path's own
-        if U:
-            ctx.sort(ins[0][:n], U, out=ref)
-        else:
-            ctx.sort_int32(ins[0][:n], out=ref)
-        ctx.sync()
-        e2e["verified"] = bool(torch.equal(ohs[(k2 - 1) % 2], ref.cpu()))
+        e2e["verified"] = bool(np.array_equal(ohs[(k2 - 1) % 2].numpy(), ref)) if ref is not None else None
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.seed)
+        cpu["host_parallel"] = host_parallel_baseline(cfg, args.seed)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": n, "U": U, "dist": cfg["dist"], "seed": args.seed,
-                       "parallelism": (f"dp{G}: keys sharded, H slices stored into the owners' slots over "
-                                       "peer memory by the histogram kernel, per-slice projection"
-                                       if ex is not None else
-                                       f"dp{G}: keys sharded, H reduce-scatter (NCCL), per-slice projection")
-                       if G > 1 else "single GPU",
-                       "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)"},
-            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary(), "verified": verified,
+            "config": config_dict(cfg, args, G),
+            "layout": (("radix: keys sharded, top-byte ranges, keys stored into the owners' buffers over peer "
+                        "memory, local LSD" if radix else
+                        "keys sharded, H slices stored into the owners' slots over peer memory by the histogram "
+                        "kernel, per-slice projection") if ex is not None else
+                       "keys sharded, H reduce-scatter (NCCL), per-slice projection") if G > 1 else "single GPU",
+            "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)",
+            "roofline": roof, "step_roofline": step_roof, "reps": reps, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary(),
+            "verified": verified, "verified_last_step": verified_last,
         }
         print(json.dumps(line), flush=True)
     if G > 1:

@@ -127,6 +127,20 @@ int dialsort_sort_async(dialsort_ctx ctx, const int32_t* keys, uint64_t n, uint3
 int dialsort_sort_int32_async(dialsort_ctx ctx, const int32_t* keys, uint64_t n, int32_t* out,
                               dialsort_stream_t stream);
 
+/* General self-indexing, Proposition 2: a finite totally ordered domain S with a
+ * known order-isomorphism phi : S -> [0, U) is sorted by ingesting phi(s) and emitting
+ * phi^-1(i) exactly H[i] times ("for other domains a lookup table suffices").
+ * items: device array of n elements of item_bytes = 1 (uint8), 2 (uint16) or 4 (int32) bytes.
+ * encode (device uint32[256], nullable, 1-byte items only): phi of each byte value; NULL: phi is
+ *   the identity on the item value (bytes / code points, day numbers, MIDI notes, ...).
+ * decode (device int32[U], nullable): phi^-1, the value emitted for code i; NULL: i itself.
+ * out: int32[n] (may not overlap items unless item_bytes == 4 and out == items).
+ * U <= 8192 (1-byte items), 65536 (2-byte), 98304 (4-byte).  A code outside [0, U) is a deferred
+ * DIALSORT_E_KEY_RANGE naming the item index.  Narrow items cut the ingestion's bytes 2-4x. */
+int dialsort_sort_domain_async(dialsort_ctx ctx, const void* items, int item_bytes, uint64_t n, uint32_t U,
+                               const uint32_t* encode, const int32_t* decode, int32_t* out,
+                               dialsort_stream_t stream);
+
 /* ---- synchronous forms (per-device default context, legacy default stream) ------------ */
 int dialsort_histogram(const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H);
 int dialsort_reconstruct(const uint32_t* H, uint32_t U, int32_t* out, uint64_t n);

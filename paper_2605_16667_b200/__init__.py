@@ -173,6 +173,23 @@ class Context:
         on a device that passed the lane-order probe) or 3 (equality-grouped ranks)."""
         return self.get_option(_lib.OPT_RADIX_ACTIVE)
 
+    def sort_domain(self, items: torch.Tensor, U: int, encode: torch.Tensor | None = None,
+                    decode: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Proposition 2: sort items of a finite ordered domain through phi (encode:
+        uint8 -> code table of 256 entries, uint8 items only; None = identity) and emit phi^-1
+        (decode: int32[U] table; None = the code).  items: uint8 / int16 (uint16 bits) / int32."""
+        widths = {torch.uint8: 1, torch.int16: 2, torch.uint16: 2, torch.int32: 4}
+        if items.dtype not in widths or not items.is_cuda or not items.is_contiguous():
+            raise ValueError("items must be a contiguous uint8 / (u)int16 / int32 CUDA tensor")
+        if out is None:
+            out = torch.empty(items.numel(), dtype=torch.int32, device=items.device)
+        _dev_buf(out, "out", items, items.numel())
+        _dev_buf(encode, "encode", items, 256, (torch.int32,))
+        _dev_buf(decode, "decode", items, int(U), (torch.int32,))
+        _check(_L.dialsort_sort_domain_async(self._h, _ptr(items), widths[items.dtype], items.numel(), int(U),
+                                             _ptr(encode), _ptr(decode), _ptr(out), _stream(items.device)))
+        return out
+
     def debug_radix_passes(self, keys: torch.Tensor) -> torch.Tensor:
         """The 4 pass buffers of DialSort-Radix (uint32 bits in an int32 [4, n] tensor): passes
         0..2 biased keys, pass 3 the sorted int32 keys (dialsort_debug_radix_passes)."""

@@ -30,7 +30,7 @@ EXPORTS = (
     "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host", "dialsort_sort_host_async",
     "dialsort_range_count_async", "dialsort_query_async", "dialsort_support_set_async",
     "dialsort_crn_resolve_async", "dialsort_ctx_set_option", "dialsort_ctx_get_option",
-    "dialsort_debug_radix_passes",
+    "dialsort_debug_radix_passes", "dialsort_sort_domain_async",
     "dialsort_comm_create", "dialsort_comm_connect_ipc", "dialsort_comm_connect_local",
     "dialsort_comm_destroy", "dialsort_comm_info",
     "dialsort_sharded_histogram_scatter_async", "dialsort_sharded_histogram_gather_async",
@@ -85,6 +85,7 @@ def load() -> ctypes.CDLL:
         "dialsort_ctx_set_option": ([P, ci, i64], ci),
         "dialsort_ctx_get_option": ([P, ci, ctypes.POINTER(i64)], ci),
         "dialsort_debug_radix_passes": ([P, P, u64, P, P], ci),
+        "dialsort_sort_domain_async": ([P, P, ci, u64, u32, P, P, P, P], ci),
         "dialsort_comm_create": ([P, u32, u32, u32, u64, P, ctypes.POINTER(P)], ci),
         "dialsort_comm_connect_ipc": ([P, P], ci),
         "dialsort_comm_connect_local": ([P, P], ci),

@@ -282,12 +282,13 @@ int ctx_init(dialsort_ctx c) {
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
   // k_sort_fused: tile totals (2 parities), fallback tile totals
   if ((rc = c->fused_tiles.ensure(4ull * kFusedTileWords, true))) return rc;
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
@@ -386,12 +387,14 @@ int fill_scan_args(dialsort_ctx c, ScanArgs& a, uint32_t U, bool do_scan, uint64
 // hist_only — the histogram only (merged H stored into H, or into the owners' slots when
 // Hpeer is set).  d_n / d_off (nullable): the key count and the keys/out offset are on the
 // device (a universe block of the hierarchical path); n is then only the size hint for the grid
-// and row format.  k16: keys are uint16 (the hierarchical path's universe blocks), else int32.
+// and row format.  kb: key bytes (4 int32; 2 uint16: the hierarchical path's universe blocks or a
+// 2-byte coded domain; 1 uint8: a 1-byte coded domain, U <= 8192).  enc / dec: the coded-domain
+// maps phi (1-byte keys) and phi^-1 (emitted values), nullable.
 int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
                        uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
-                       const uint64_t* d_off = nullptr, bool k16 = false, bool hist_only = false,
+                       const uint64_t* d_off = nullptr, int kb = 4, bool hist_only = false,
                        uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0, uint32_t peerRank = 0,
-                       uint32_t bin_base = 0) {
+                       uint32_t bin_base = 0, const uint32_t* enc = nullptr, const int32_t* dec = nullptr) {
   int rc;
   ScanArgs a = {};
   if ((rc = fill_scan_args(c, a, U, !hist_only, n, true, nullptr, epoch))) return rc;
@@ -402,6 +405,9 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.peerL = peerL;
   a.peerRank = peerRank;
   a.bin_base = bin_base;
+  a.enc = enc;
+  a.dec = dec;
+  if (kb == 1 && U > kSmem32MaxBins) return fail(DIALSORT_E_INVALID_ARG, "1-byte keys need U <= 8192");
   const bool pack = U > kSmem32MaxBins;
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
@@ -448,11 +454,11 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
 #define DS_LAUNCH_FUSED(F, K) \
   DS_CUDA(launch_k<true>(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
   if (fmt == kRowN4) {
-    if (k16) DS_LAUNCH_FUSED(kRowN4, true); else DS_LAUNCH_FUSED(kRowN4, false);
+    if (kb == 2) DS_LAUNCH_FUSED(kRowN4, 2); else DS_LAUNCH_FUSED(kRowN4, 4);
   } else if (fmt == kRowP16) {
-    if (k16) DS_LAUNCH_FUSED(kRowP16, true); else DS_LAUNCH_FUSED(kRowP16, false);
+    if (kb == 2) DS_LAUNCH_FUSED(kRowP16, 2); else DS_LAUNCH_FUSED(kRowP16, 4);
   } else {
-    if (k16) DS_LAUNCH_FUSED(kRowU32, true); else DS_LAUNCH_FUSED(kRowU32, false);
+    if (kb == 2) DS_LAUNCH_FUSED(kRowU32, 2); else if (kb == 1) DS_LAUNCH_FUSED(kRowU32, 1); else DS_LAUNCH_FUSED(kRowU32, 4);
   }
 #undef DS_LAUNCH_FUSED
   c->fused_seq++;
@@ -487,7 +493,7 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
     const uint32_t epoch = next_epoch(c);  // each block launch has its own ready-flag epoch
     uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
     if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, Hb, out, epoch, s, (int32_t)(b << kPartShift), w.bsz + b,
-                                 w.boff + b, true, hist_only, Hpeer, peerL, peerRank, b << kPartShift)))
+                                 w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift)))
       return rc;
   }
   return DIALSORT_OK;
@@ -861,6 +867,30 @@ int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, i
   if (n == 0) return DIALSORT_OK;
   if ((rc = c->radix_tmp.ensure(4ull * n + 16))) return rc;
   return radix_enqueue(c, keys, n, out, c->radix_tmp.as<int32_t>(), s);
+}
+
+int dialsort_sort_domain_async(dialsort_ctx c, const void* items, int item_bytes, uint64_t n, uint32_t U,
+                               const uint32_t* encode, const int32_t* decode, int32_t* out, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U)) || (rc = check_keys_arg(out, n))) return rc;
+  if (item_bytes != 1 && item_bytes != 2 && item_bytes != 4) return fail(DIALSORT_E_INVALID_ARG, "item_bytes: 1, 2 or 4");
+  if (n > 0xffffffffull) return fail(DIALSORT_E_INVALID_ARG, "n exceeds 2^32-1");
+  if (n && !items) return fail(DIALSORT_E_INVALID_ARG, "NULL items with n > 0");
+  if (reinterpret_cast<uintptr_t>(items) & (item_bytes - 1)) return fail(DIALSORT_E_INVALID_ARG, "items misaligned");
+  if (encode && item_bytes != 1) return fail(DIALSORT_E_INVALID_ARG, "an encode table needs 1-byte items");
+  if ((item_bytes == 1 && U > kSmem32MaxBins) || (item_bytes == 2 && U > 65536) || (item_bytes == 4 && U > kSmem16MaxBins))
+    return fail(DIALSORT_E_INVALID_ARG, "U too large for the item width (1 B: 8192, 2 B: 65536, 4 B: 98304)");
+  if (n && ranges_overlap(items, (uint64_t)item_bytes * n, out, 4 * n) && (item_bytes != 4 || items != out))
+    return fail(DIALSORT_E_INVALID_ARG, "out overlaps the items");
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const uint32_t epoch = next_epoch(c);
+  if (n == 0) return DIALSORT_OK;
+  if ((rc = c->Hws.ensure(4ull * U))) return rc;
+  return enqueue_sort_fused(c, items, n, U, c->Hws.as<uint32_t>(), out, epoch, s, 0, nullptr, nullptr, item_bytes,
+                            false, nullptr, 0, 0, 0, encode, decode);
 }
 
 int dialsort_debug_radix_passes(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t* pass_out,

@@ -95,8 +95,12 @@ __device__ __forceinline__ uint32_t count_below(const uint32_t* Ps, uint32_t m, 
 // Projection stores: st.global.L1::no_allocate without an L2 hint (measured 0.3 us faster than
 // the evict-first hint on c2 / c3, and than the default policy).
 __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
-                                           bool aligned, uint64_t pol, bool full = false) {
-  const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
+                                           bool aligned, uint64_t pol, bool full = false,
+                                           const int32_t* __restrict__ dec = nullptr) {
+  // (coded domain: the emitted value of code k is phi^-1(k) = dec[k]; consecutive
+  //  positions mostly share a code, so the table reads hit L1)
+  const int4 v = dec ? make_int4(__ldg(dec + q.x), __ldg(dec + q.y), __ldg(dec + q.z), __ldg(dec + q.w))
+                     : make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
   if (full && !aligned) {
     // Warp-cooperative (all 32 lanes, p = p_0 + 4 lane, the 128 positions inside [lo, hi)):
     // out is 4-byte but not 16-byte aligned (a hierarchical block's output starts at the
@@ -146,7 +150,7 @@ __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p
 constexpr uint32_t kFTblCap = kFSlot / 4;  // 4884 sub-blocks per window (one staging slot)
 __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
                                             uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out,
-                                            bool aligned, uint64_t pol) {
+                                            bool aligned, uint64_t pol, const int32_t* __restrict__ dec = nullptr) {
   __shared__ uint32_t s_ib[2];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t ltmask = (1u << lane) - 1u;
@@ -199,7 +203,7 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         const uint32_t v = kbase + c0 + below;
         store_quad(out, b0 + 4 * lane, lo, hi,
                    make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own), aligned,
-                   pol, full);
+                   pol, full, dec);
       } else {  // count marks of the sub-block's starts, then a warp scan
         const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
         uint32_t i1 = c0;
@@ -217,7 +221,8 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         mk.z += mk.y;
         mk.w += mk.z;
         const uint32_t v = kbase + c0 + warp_incl_scan(mk.w) - mk.w;
-        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol);
+        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol,
+                   false, dec);
         __syncwarp();
       }
     }
@@ -381,10 +386,11 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
 // Grid: C <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic
 // smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch (the
 // second one is only waited for after a packed-counter overflow).
-template <int FMT, bool K16 = false>
+template <int FMT, int KB = 4>
 __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
-  // (K16: uint16 keys, the hierarchical path's universe blocks; otherwise int32)
+  // (KB: key bytes — 4 int32 keys; 2 uint16 keys, the hierarchical path's universe blocks or a
+  //  2-byte coded domain; 1 uint8 keys, a 1-byte coded domain)
   // (keys, out, n are adjusted below for hierarchical blocks)
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
@@ -393,9 +399,12 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   phase_mark(a.pt, -1);
   uint64_t n_exp = a.n_expected;
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
-    const uint64_t off = *a.d_off;
-    n = *a.d_n;
-    keys = static_cast<const char*>(keys) + off * (K16 ? 2 : 4);
+    __shared__ uint64_t s_noff[2];  // (one load per CTA, not one per thread: a 148k-way fan-in)
+    if (threadIdx.x == 0) s_noff[0] = *a.d_n, s_noff[1] = *a.d_off;
+    __syncthreads();
+    const uint64_t off = s_noff[1];
+    n = s_noff[0];
+    keys = static_cast<const char*>(keys) + off * KB;
     out += off;
     n_exp = n;
   }
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   // (the ingestion's first __syncthreads orders this before the flush)
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
   for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
-  hist_ingest_flush<PACK16, K16>(keys, n, a, sh, red64, sh + kFOffTsh);
+  hist_ingest_flush<PACK16, KB>(keys, n, a, sh, red64, sh + kFOffTsh);
   __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
     my_tiles(ntiles, s_own[0], s_own[1]);
@@ -449,13 +458,15 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   // row segments (and their exception counts) are requested together: none depends on another,
   // and the barrier ordered every CTA's flush before them.  Two counter lines per CTA, each read
   // by two CTAs (all owner totals read by every CTA measured ~1.7 us: a 148-way fan-in).
-  __shared__ uint32_t s_pb[3];
+  // (one thread loads each shared word — every thread loading the overflow epoch measured as the
+  // top stall of the kernel: 151k loads of one L2 line)
+  __shared__ uint32_t s_pb[4];
   if (threadIdx.x == 0) {
     s_pb[0] = b ? __ldcg(a.own_red + (uint64_t)b * S) : 0u;
     s_pb[1] = __ldcg(a.own_red + (uint64_t)(b + 1) * S);
     s_pb[2] = __ldcg(a.own_red + (uint64_t)kFOwnVote * S);
+    s_pb[3] = __ldcg(&a.st->ovf_epoch);
   }
-  const bool use_ovf = __ldcg(&a.st->ovf_epoch) == a.epoch;
   for (uint32_t k = 0; k < 2 && k < nbt; ++k) {
     stage_batch<FMT>(a, tb0 + k * tpb, need_of(k), slot(k));
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -467,6 +478,8 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     return FMT == kRowN4 && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
+  __syncthreads();  // s_pb
+  const bool use_ovf = s_pb[3] == a.epoch;
   // own-tile mode: every CTA projects exactly the tiles it merged (near-uniform histograms: no
   // skew vote); otherwise (skew, or a packed-counter overflow) equal position shares, for which
   // every owner offset oo[0..G] is read.
@@ -475,7 +488,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   bool own;
   if (!use_ovf) {
     barrier_skip(a.bar64);
-    __syncthreads();  // s_pb
     own = ntiles <= kFPassTiles * G && s_pb[2] == 0;  // (every CTA's tiles fit one projection pass)
     if (!own) {
       for (uint32_t c = threadIdx.x; c <= G; c += blockDim.x) oo[c] = c ? __ldcg(a.own_red + (uint64_t)c * S) : 0u;
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     if (nown && p0 < p1)  // (uniform per CTA) table in the second staging slot, dead after the merge
       project_tbl(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1,
                   reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
-                  reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
+                  reinterpret_cast<uint32_t*>(red64), out, aligned, pol, a.dec);
     phase_mark(a.pt, 7);
     pdl_trigger();
     return;
@@ -673,7 +685,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
       if (p0 < p1)
         project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
                     reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
-                    reinterpret_cast<uint32_t*>(red64), out, aligned, pol);
+                    reinterpret_cast<uint32_t*>(red64), out, aligned, pol, a.dec);
       __syncthreads();  // Pw is reused by the next pass
     }
   }

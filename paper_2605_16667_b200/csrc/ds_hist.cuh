@@ -207,34 +207,59 @@ struct KeySpan16 {
   const uint16_t* keys;
   uint64_t n, head, n8, tail;
 };
-__device__ __forceinline__ KeySpan16 make_span16(const uint16_t* keys, uint64_t n) {
+// Narrow keys of KB bytes (KB = 2: the hierarchical path's uint16 block keys and 2-byte coded
+// domains; KB = 1: 1-byte coded domains, Proposition 2), optionally mapped through
+// the encode table phi (enc, device uint32[256], 1-byte keys only).  The aligned body is visited
+// as 16-byte vectors of 16 / KB keys, grid-strided like for_each_key4; the unaligned head (CTA 0)
+// and tail (last CTA) go through f1.  Returns this thread's vectors.
+template <int KB>
+__device__ __forceinline__ uint32_t narrow_key(const uint16_t* keys, uint64_t i, const uint32_t* enc) {
+  const uint32_t k = KB == 1 ? (uint32_t)reinterpret_cast<const uint8_t*>(keys)[i] : (uint32_t)keys[i];
+  return enc ? __ldg(enc + k) : k;
+}
+template <int KB>
+__device__ __forceinline__ KeySpan16 make_span_narrow(const uint16_t* keys, uint64_t n) {
   KeySpan16 s;
   s.keys = keys;
   s.n = n;
-  const uint64_t mis = (reinterpret_cast<uintptr_t>(keys) >> 1) & 7u;
-  s.head = mis ? 8 - mis : 0;
+  constexpr uint32_t per = 16 / KB;  // keys per vector
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(keys) & 15u) / KB;
+  s.head = mis ? per - mis : 0;
   if (s.head > n) s.head = n;
-  s.n8 = (n - s.head) / 8;
-  s.tail = n - s.head - 8 * s.n8;
+  s.n8 = (n - s.head) / per;
+  s.tail = n - s.head - per * s.n8;
   return s;
 }
-template <typename F4, typename F1>
-__device__ __forceinline__ uint32_t for_each_key8_u16(const KeySpan16& s, F4&& f4, F1&& f1) {
+// 16 bytes -> 16 / KB keys -> vectors of 4 for f4(int4, index of the 4-key group)
+template <int KB, typename F4>
+__device__ __forceinline__ void expand_narrow(const int4& x, uint32_t v, const uint32_t* enc, F4&& f4) {
+  const uint32_t w[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+  if (KB == 2) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      f4(make_int4((int)(w[2 * h] & 0xffffu), (int)(w[2 * h] >> 16), (int)(w[2 * h + 1] & 0xffffu),
+                   (int)(w[2 * h + 1] >> 16)), 2 * v + h);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t b0 = w[q] & 0xffu, b1 = (w[q] >> 8) & 0xffu, b2 = (w[q] >> 16) & 0xffu, b3 = w[q] >> 24;
+      if (enc) b0 = __ldg(enc + b0), b1 = __ldg(enc + b1), b2 = __ldg(enc + b2), b3 = __ldg(enc + b3);
+      f4(make_int4((int)b0, (int)b1, (int)b2, (int)b3), 4 * v + q);
+    }
+  }
+}
+template <int KB, typename F4, typename F1>
+__device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, const uint32_t* enc, F4&& f4, F1&& f1) {
+  constexpr uint32_t per = 16 / KB;
   const uint32_t T = blockDim.x, G = gridDim.x;
-  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
+  if (blockIdx.x == 0 && threadIdx.x < s.head) f1(narrow_key<KB>(s.keys, threadIdx.x, enc), (uint64_t)threadIdx.x);
   if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
-    const uint64_t i = s.head + 8 * s.n8 + threadIdx.x;
-    f1((uint32_t)s.keys[i], i);
+    const uint64_t i = s.head + per * s.n8 + threadIdx.x;
+    f1(narrow_key<KB>(s.keys, i, enc), i);
   }
   const uint64_t pol = l2_evict_first_policy();
-  const int4* __restrict__ body = reinterpret_cast<const int4*>(s.keys + s.head);
+  const int4* __restrict__ body = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s.keys) + KB * s.head);
   const uint32_t n8 = (uint32_t)s.n8, stride = G * T;
-  auto expand = [&](const int4& x, uint32_t v) {  // 8 keys -> two vectors of 4
-    f4(make_int4((int)((uint32_t)x.x & 0xffffu), (int)((uint32_t)x.x >> 16), (int)((uint32_t)x.y & 0xffffu),
-                 (int)((uint32_t)x.y >> 16)), 2 * v);
-    f4(make_int4((int)((uint32_t)x.z & 0xffffu), (int)((uint32_t)x.z >> 16), (int)((uint32_t)x.w & 0xffffu),
-                 (int)((uint32_t)x.w >> 16)), 2 * v + 1);
-  };
   uint32_t cnt = 0;
   uint32_t i = blockIdx.x * T + threadIdx.x;
   int4 a[kHistUnroll / 2];
@@ -250,7 +275,7 @@ __device__ __forceinline__ uint32_t for_each_key8_u16(const KeySpan16& s, F4&& f
 #pragma unroll
     for (int u = 0; u < kHistUnroll / 2; ++u)
       if (i + u * stride < n8) {
-        expand(a[u], i + u * stride);
+        expand_narrow<KB>(a[u], i + u * stride, enc, f4);
         ++cnt;
       }
 #pragma unroll
@@ -258,6 +283,20 @@ __device__ __forceinline__ uint32_t for_each_key8_u16(const KeySpan16& s, F4&& f
     i = in;
   }
   return cnt;
+}
+// Error path of the narrow traversal: re-read this thread's vectors, ingest key by key those
+// 4-key groups holding a key outside [0, U) (skipped whole by the hot loop); returns #bad keys.
+template <bool PACK16, int KB>
+__device__ __noinline__ uint32_t ingest_deferred_narrow(uint32_t* h, const KeySpan16& s, const uint32_t* enc,
+                                                        uint32_t U, DevStatus* st) {
+  const int4* body = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s.keys) + KB * s.head);
+  uint32_t bad = 0;
+  const uint32_t stride = gridDim.x * blockDim.x, n8 = (uint32_t)s.n8;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride)
+    expand_narrow<KB>(body[i], i, enc, [&](int4 v, uint32_t g) {
+      if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)g, U, st);
+    });
+  return bad;
 }
 // Overflow fallback of a 16-bit-key CTA: zero the row, re-ingest this CTA's keys (the same
 // head / tail / grid-strided vectors) into ovfH through the warp CRN.
@@ -288,9 +327,11 @@ __device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4*
   }
 }
 
-template <bool PACK16, bool K16 = false>
+template <bool PACK16, int KB = 4>
 __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_v, uint64_t n, const ScanArgs& a,
                                                   uint32_t* sh_hist, uint64_t* red64, uint32_t* tsum_sh = nullptr) {
+  constexpr bool K16 = KB == 2;  // (uint16 keys; KB == 1: uint8 keys)
+  constexpr bool NARROW = KB != 4;
   const uint32_t U = a.U, ldw = a.ldw;
 
   // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
@@ -302,8 +343,9 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
 
   // Ingestion (eq:ingestion): one shared atomic per key; equal addresses inside one warp
   // instruction are merged by the shared-memory atomic unit (the CRN's equality merge).
-  const KeySpan s = make_span(K16 ? nullptr : static_cast<const int32_t*>(keys_v), K16 ? 0 : n);
-  const KeySpan16 s16 = make_span16(K16 ? static_cast<const uint16_t*>(keys_v) : nullptr, K16 ? n : 0);
+  const KeySpan s = make_span(NARROW ? nullptr : static_cast<const int32_t*>(keys_v), NARROW ? 0 : n);
+  const KeySpan16 s16 =
+      make_span_narrow<NARROW ? KB : 2>(NARROW ? static_cast<const uint16_t*>(keys_v) : nullptr, NARROW ? n : 0);
   DevStatus* st = a.st;
   uint32_t seen = 0, bad = 0, deferred = 0;
   // packed word of key k: k >> 1 at byte offset (2k) & ~3; increment 1 or 65536
@@ -388,8 +430,8 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
       ++bad;
     }
   };
-  if (K16) {
-    seen += 8 * for_each_key8_u16(s16, f4, f1);  // (16-bit keys are < U by construction)
+  if (NARROW) {
+    seen += (16 / KB) * for_each_key_narrow<NARROW ? KB : 2>(s16, a.enc, f4, f1);
   } else {
     for_each_key4(s, f4, f1);
     // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
@@ -398,7 +440,10 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
     seen += 4 * cnt;
   }
-  if (!K16 && deferred) bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
+  if (deferred) {
+    if (NARROW) bad += ingest_deferred_narrow<PACK16, NARROW ? KB : 2>(sh_hist, s16, a.enc, U, st);
+    else bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
+  }
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
@@ -573,7 +618,10 @@ __global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restric
 
   // Merge + scan this CTA's tile range.
   const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
-  const bool use_ovf = ld_acquire_u32(&st->ovf_epoch) == a.epoch;
+  __shared__ uint32_t s_ovf;
+  if (threadIdx.x == 0) s_ovf = ld_acquire_u32(&st->ovf_epoch);
+  __syncthreads();
+  const bool use_ovf = s_ovf == a.epoch;
   uint32_t tb0, tb1;
   my_tiles(ntiles, tb0, tb1);
   if (a.do_scan && !use_ovf) {

@@ -103,7 +103,12 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass3(const uint32_t
   extern __shared__ __align__(16) unsigned char radix_smem_raw[];
   Radix3Smem& S = *reinterpret_cast<Radix3Smem*>(radix_smem_raw);
   pdl_wait();
-  if (w.d_n) n = *w.d_n;
+  if (w.d_n) {  // (one load per CTA)
+    __shared__ uint32_t s_n;
+    if (threadIdx.x == 0) s_n = *w.d_n;
+    __syncthreads();
+    n = s_n;
+  }
   phase_mark(w.pt, -1);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
   const uint32_t dsel = 0x4440u | (uint32_t)p;
@@ -285,7 +290,12 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
   extern __shared__ __align__(16) unsigned char radix_smem_raw[];
   Radix4Smem& S = *reinterpret_cast<Radix4Smem*>(radix_smem_raw);
   pdl_wait();
-  if (w.d_n) n = *w.d_n;
+  if (w.d_n) {  // (one load per CTA)
+    __shared__ uint32_t s_n;
+    if (threadIdx.x == 0) s_n = *w.d_n;
+    __syncthreads();
+    n = s_n;
+  }
   phase_mark(w.pt, -1);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
   const uint32_t dsel = 0x4440u | (uint32_t)p;

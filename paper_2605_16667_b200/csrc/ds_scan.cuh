@@ -63,6 +63,8 @@ struct ScanArgs {
   uint32_t peerL, peerRank;
   uint32_t bin_base;         // universe bin of this launch's bin 0 (hierarchical blocks), for Hpeer
   int hist_only;             // k_sort_fused: stop after the merge (H only, no projection)
+  const uint32_t* enc;       // coded domains (Proposition 2): phi of a 1-byte item, device uint32[256], or null
+  const int32_t* dec;        // coded domains: phi^-1, the value emitted for code k (device int32[U]), or null
   int do_scan;
   uint32_t* P;               // [U+1] exclusive prefix
   uint64_t* range_tot;       // [gridDim] per-CTA range totals

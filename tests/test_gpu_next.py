@@ -162,3 +162,56 @@ def test_concurrent_contexts_two_streams(ds, cuda_dev):
     for i in range(6):
         assert np.array_equal(outs[i].cpu().numpy(), oracle.sort(xs[i], 65536)), i
         assert np.array_equal(routs[i].cpu().numpy(), oracle.radix_sort_i32(rs[i])), i
+
+
+# ---- NEXT-3: Proposition 2 coded domains -------------------------------------------------------
+
+@pytest.mark.parametrize("width,U,n", [(1, 256, 1_000_003), (1, 7, 99_999), (2, 366, 2_000_001), (2, 65536, 3_000_017),
+                                       (4, 128, 500_001)])
+def test_sort_domain_vs_oracle(ds, ctx, width, U, n):
+    """Items of 1 / 2 / 4 bytes through phi (an encode table for bytes) and phi^-1 (a decode
+    table) against the oracle's A2, including unaligned item pointers (odd offsets)."""
+    rng = np.random.default_rng(width * 1000 + U)
+    enc = dec = None
+    if width == 1 and U == 7:  # table-driven 7-element enumeration (symbols are arbitrary bytes)
+        symbols = rng.permutation(np.arange(256))[:7]
+        enc_h = np.zeros(256, dtype=np.uint32)
+        enc_h[symbols] = np.arange(7)
+        items = rng.choice(symbols, size=n).astype(np.uint8)
+        dec_h = (symbols * 1000 + 7).astype(np.int32)
+        enc, dec = u32_dev(enc_h), to_dev(dec_h)
+        ref = oracle.sort_domain(items, U, encode=enc_h, decode=dec_h)
+    else:
+        dt = {1: np.uint8, 2: np.uint16, 4: np.int32}[width]
+        items = rng.integers(0, U, size=n).astype(dt)
+        dec_h = (np.arange(U) * 3 - 5).astype(np.int32)  # a decode table (order-preserving)
+        dec = to_dev(dec_h)
+        ref = oracle.sort_domain(items, U, decode=dec_h)
+    tdt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[width]
+    buf = torch.empty(n + 8, dtype=tdt, device="cuda:0")
+    off = 3 if width < 4 else 1
+    it = buf[off:off + n]
+    it.copy_(torch.from_numpy(items.view({1: np.uint8, 2: np.int16, 4: np.int32}[width])))
+    out = ctx.sort_domain(it, U, encode=enc, decode=dec)
+    ctx.sync()
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_sort_domain_ascii_and_range_error(ds, ctx):
+    s = b"the quick brown fox jumps over the lazy dog" * 1000
+    items = torch.from_numpy(np.frombuffer(s, dtype=np.uint8).copy()).to("cuda:0")
+    out = ctx.sort_domain(items, 256)
+    ctx.sync()
+    assert bytes(out.cpu().numpy().astype(np.uint8)) == bytes(sorted(s))
+    bad = torch.tensor([1, 2, 300, 4], dtype=torch.int16, device="cuda:0")
+    ctx.sort_domain(bad, 256)
+    with pytest.raises(ds.DialSortError) as e:
+        ctx.sync()
+    assert e.value.code == 2 and e.value.info.first_bad_index == 2
+    big = np.random.default_rng(1).integers(0, 256, size=100_003).astype(np.int16)
+    big[50_001] = 999                         # inside the vectorised body
+    big[77_777] = 1000
+    ctx.sort_domain(torch.from_numpy(big).to("cuda:0"), 256)
+    with pytest.raises(ds.DialSortError) as e:
+        ctx.sync()
+    assert e.value.code == 2 and e.value.info.first_bad_index == 50_001 and e.value.info.bad_count == 2
