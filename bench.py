@@ -303,6 +303,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--grid", action="store_true", help="NEXT-2: the paper's 48-config grid (one JSON line each)")
+    ap.add_argument("--batch", type=int, default=32,
+                    help="steps per dialsort_sort_batch_async call (U <= 98304 at N=1; 1 = one sort per call)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: histogram exchange over peer memory (default) or NCCL reduce-scatter")
     args = ap.parse_args()
@@ -343,6 +345,9 @@ def main():
     L2 = torch.cuda.get_device_properties(dev).L2_cache_size
     step_bytes = 8 * n_loc + 8 * max(U, 1)
     R = max(2, min(16, -(-3 * L2 // step_bytes)))
+    use_batch = G == 1 and not radix and U <= 98304 and args.batch > 1
+    if use_batch:
+        R = max(R, args.batch)  # (the batches of one call need distinct output buffers)
     if 8 * n_loc * R > 40 * (1 << 30):
         R = 2
     base = make_device_input(cfg, args.seed, dev, lo=lo, count=n_loc)
@@ -408,6 +413,20 @@ def main():
         last_result[0] = r
         return r
 
+    def run(i0, k):
+        """Steps i0 .. i0 + k - 1: one sort per step, or — batch mode — calls of dialsort_sort_batch_async
+        of args.batch steps each (the steps overlapped on CTA groups in one launch)."""
+        if not use_batch:
+            for i in range(i0, i0 + k):
+                step(i)
+            return
+        i = i0
+        while i < i0 + k:
+            m = min(args.batch, i0 + k - i)
+            js = [(i + t) % R for t in range(m)]
+            ctx.sort_batch([ins[j] for j in js], U, [outs[j] for j in js])
+            i += m
+
     step(0)
     ctx.sync()
     verified = check(0)
@@ -416,8 +435,7 @@ def main():
 
     # ---- warm-up + timed region ------------------------------------------------------------
     stream = torch.cuda.current_stream(dev)
-    for i in range(args.warmup):
-        step(i)
+    run(0, max(args.warmup, args.batch if use_batch else 0))
     ctx.sync()
     if G > 1:
         dist.barrier()
@@ -425,8 +443,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         e0.record(stream)
-        for i in range(args.steps):
-            step(i)
+        run(0, args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     ctx.sync()
@@ -455,8 +472,7 @@ def main():
         torch.cuda.synchronize()
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         b0.record(stream)
-        for i in range(kb):
-            step(r * kb + i)
+        run(r * kb, kb)
         b1.record(stream)
         torch.cuda.synchronize()
         t = b0.elapsed_time(b1) / kb
@@ -473,10 +489,24 @@ def main():
             "best_value": n / (min(blk) * 1e-3)}
 
     # ---- per-kernel live timing (separate pass: event pairs disable the PDL overlap) -------
+    # the same steps issued one sort per call (the single-call latency of the path), batch mode only
+    single = None
+    if use_batch:
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ctx.sync()
+        sms = s0.elapsed_time(s1) / args.steps
+        single = {"ms_per_step": sms, "value": n / (sms * 1e-3), "api": "dialsort_sort_async, one step per call",
+                  "frac_of_measured": (8 * n + 8 * U) / (sms * 1e-3) / 1e9 / load_peaks()[0]}
+
     ctx.profile(True)
     prof_steps = min(args.steps, 200)
-    for i in range(prof_steps):
-        step(i)
+    run(0, prof_steps)
     torch.cuda.synchronize()
     ctx.profile(False)
     recs = ctx.profile_read()
@@ -494,9 +524,15 @@ def main():
     # region's own per-step time (events on the launching stream, back-to-back launches);
     # per-launch event pairs add the launch latency of an otherwise idle stream (~6 us at c2).
     dur_src = "per-launch CUDA event pairs (separate pass)"
+    per_launch_steps = 1
     if dom and len(per) == 1 and abs(launches_per_step - 1.0) < 1e-9 and G == 1:
         kern_avg[dom] = ms_step
         dur_src = "timed region: one launch per step, back-to-back (CUDA events on the launching stream)"
+    elif dom == "k_sort_batch" and len(per) == 1 and G == 1:
+        per_launch_steps = args.batch
+        kern_avg[dom] = ms_step * args.batch
+        dur_src = (f"timed region: one k_sort_batch launch per {args.batch} steps, back-to-back (CUDA events on "
+                   "the launching stream)")
     # algorithmic bytes per launch of each kernel
     hier = any(nm == "k_part_count" for nm, _ in recs)  # hierarchical path (U > 98304)
     nblk = max(1, -(-U // 65536))
@@ -505,6 +541,7 @@ def main():
         # hierarchical: blocks hold uint16 keys (2 B read + 4 B written a key); the scatter reads
         # 4 B and writes 2 B a key
         "k_sort_fused": (6 * n_loc // nblk + 8 * 65536) if hier else 8 * n_loc + 8 * U,
+        "k_sort_batch": per_launch_steps * (8 * n_loc + 8 * U),
         "k_part_count": 4 * n_loc, "k_part_scatter": 6 * n_loc, "k_part_scan": 0,
         # two-kernel pipeline: fused ingest+merge+scan (keys read + H and P written), expand
         "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
@@ -581,6 +618,9 @@ def main():
                         "kernel, per-slice projection") if ex is not None else
                        "keys sharded, H reduce-scatter (NCCL), per-slice projection") if G > 1 else "single GPU",
             "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)",
+            "mode": (f"batched: dialsort_sort_batch_async, {args.batch} steps per call (one launch, CTA groups)"
+                     if use_batch else "one step per call"),
+            "single_call": single,
             "roofline": roof, "step_roofline": step_roof, "reps": reps, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary(),
             "verified": verified, "verified_last_step": verified_last,

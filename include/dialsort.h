@@ -72,6 +72,8 @@ int dialsort_ctx_destroy(dialsort_ctx ctx);
 int dialsort_sync(dialsort_ctx ctx, dialsort_stream_t stream, dialsort_error_info* info);
 
 /* Context options.
+ *   DIALSORT_OPT_MAX_CTAS (read / write): cap on the CTAs (one per SM) of the fused sort kernel
+ *     (0 = every SM, default).
  *   DIALSORT_OPT_RADIX_VARIANT (read / write): 0 = automatic (default), 3 = k_radix_pass3
  *     (in-warp ranks by explicit equality grouping: stable by construction), 4 = k_radix_pass4
  *     (ranks from the counting shared atomic; needs 16-byte aligned buffers, else pass3).
@@ -92,6 +94,7 @@ int dialsort_sync(dialsort_ctx ctx, dialsort_stream_t stream, dialsort_error_inf
 #define DIALSORT_OPT_RADIX_ACTIVE 3
 #define DIALSORT_OPT_NUM_SMS 4
 #define DIALSORT_OPT_COOPERATIVE 5
+#define DIALSORT_OPT_MAX_CTAS 6
 int dialsort_ctx_set_option(dialsort_ctx ctx, int option, int64_t value);
 int dialsort_ctx_get_option(dialsort_ctx ctx, int option, int64_t* value);
 
@@ -120,6 +123,17 @@ int dialsort_reconstruct_async(dialsort_ctx ctx, const uint32_t* H, uint32_t U,
  * the canonical ordered state H. */
 int dialsort_sort_async(dialsort_ctx ctx, const int32_t* keys, uint64_t n, uint32_t U,
                         int32_t* out, uint32_t* H_out, dialsort_stream_t stream);
+
+/* A batch of independent DialSorts (a serving engine's stream of sort requests): batch j sorts
+ * keys[j][0 .. n[j]) into out[j] (H_out[j]: its histogram, nullable array / entries), all in
+ * [0, U).  keys / n / out / H_out are HOST arrays of nb entries; the pointers they hold are device
+ * buffers.  On the shared-memory universes (U <= 98304) up to 64 batches run in ONE launch on
+ * disjoint groups of CTAs (k_sort_batch: each group sorts its batches one after another on its own
+ * workspace; the groups' HBM-bound phases overlap the others' merge phases); other universes,
+ * batches of different row formats or single batches are sorted one after another.  Results and
+ * errors as nb calls of dialsort_sort_async (errors are reported by dialsort_sync of ctx). */
+int dialsort_sort_batch_async(dialsort_ctx ctx, const int32_t* const* keys, const uint64_t* n, uint32_t U,
+                              int32_t* const* out, uint32_t* const* H_out, uint32_t nb, dialsort_stream_t stream);
 
 /* DialSort-Radix (tab:radix): full signed int32 range, LSD base 256, 4 passes
  * over sign-flipped keys u = x ^ 0x80000000 (reading R2), each pass a 256-bin DialSort

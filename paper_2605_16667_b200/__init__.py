@@ -135,6 +135,27 @@ class Context:
                                       _stream(keys.device)))
         return out
 
+    def sort_batch(self, keys_list, U: int, outs=None, Hs=None):
+        """Independent DialSorts of several key batches in one call (dialsort_sort_batch_async):
+        overlapped in one launch on disjoint CTA groups when U <= 98304."""
+        nb = len(keys_list)
+        for k in keys_list:
+            _keys(k)
+        if outs is None:
+            outs = [torch.empty_like(k) for k in keys_list]
+        for k, o in zip(keys_list, outs):
+            _dev_buf(o, "out", k, k.numel())
+        if Hs is not None:
+            for k, h in zip(keys_list, Hs):
+                _dev_buf(h, "H", k, int(U))
+        P = ctypes.c_void_p
+        kp = (P * nb)(*[k.data_ptr() for k in keys_list])
+        ns = (ctypes.c_uint64 * nb)(*[k.numel() for k in keys_list])
+        op = (P * nb)(*[o.data_ptr() for o in outs])
+        hp = None if Hs is None else (P * nb)(*[h.data_ptr() for h in Hs])
+        _check(_L.dialsort_sort_batch_async(self._h, kp, ns, int(U), op, hp, nb, _stream(keys_list[0].device)))
+        return outs
+
     def sort_int32(self, keys: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """DialSort-Radix over the full signed int32 range."""
         _keys(keys)

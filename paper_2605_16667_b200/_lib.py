@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_DIR, f"libdialsort_{_VARIANT}.so" if _VARIANT else "lib
 # dialsort_status
 OK, E_INVALID_ARG, E_KEY_RANGE, E_SIZE, E_OVERFLOW, E_CUDA, E_COMM, E_NOMEM = 0, 1, 2, 3, 4, 5, 6, 7
 # context options, query ops, communicator handle size (include/dialsort.h)
-OPT_RADIX_VARIANT, OPT_RADIX_PROBE_VIOLATIONS, OPT_RADIX_ACTIVE, OPT_NUM_SMS, OPT_COOPERATIVE = 1, 2, 3, 4, 5
+OPT_RADIX_VARIANT, OPT_RADIX_PROBE_VIOLATIONS, OPT_RADIX_ACTIVE, OPT_NUM_SMS, OPT_COOPERATIVE, OPT_MAX_CTAS = 1, 2, 3, 4, 5, 6
 Q_FREQUENCY, Q_PRESENCE, Q_RANGE_COUNT = 0, 1, 2
 COMM_HANDLE_BYTES = 128
 
@@ -30,7 +30,7 @@ EXPORTS = (
     "dialsort_sort", "dialsort_sort_int32", "dialsort_sort_host", "dialsort_sort_host_async",
     "dialsort_range_count_async", "dialsort_query_async", "dialsort_support_set_async",
     "dialsort_crn_resolve_async", "dialsort_ctx_set_option", "dialsort_ctx_get_option",
-    "dialsort_debug_radix_passes", "dialsort_sort_domain_async",
+    "dialsort_debug_radix_passes", "dialsort_sort_domain_async", "dialsort_sort_batch_async",
     "dialsort_comm_create", "dialsort_comm_connect_ipc", "dialsort_comm_connect_local",
     "dialsort_comm_destroy", "dialsort_comm_info",
     "dialsort_sharded_histogram_scatter_async", "dialsort_sharded_histogram_gather_async",
@@ -86,6 +86,7 @@ def load() -> ctypes.CDLL:
         "dialsort_ctx_get_option": ([P, ci, ctypes.POINTER(i64)], ci),
         "dialsort_debug_radix_passes": ([P, P, u64, P, P], ci),
         "dialsort_sort_domain_async": ([P, P, ci, u64, u32, P, P, P, P], ci),
+        "dialsort_sort_batch_async": ([P, P, P, u32, P, P, u32, P], ci),
         "dialsort_comm_create": ([P, u32, u32, u32, u64, P, ctypes.POINTER(P)], ci),
         "dialsort_comm_connect_ipc": ([P, P], ci),
         "dialsort_comm_connect_local": ([P, P], ci),

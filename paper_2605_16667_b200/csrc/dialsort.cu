@@ -56,13 +56,13 @@ enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
   KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
   KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
-  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_COUNT
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {
     "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
     "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_scatter",
     "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
-    "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query"};
+    "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -110,7 +110,11 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.numAttrs = (COOP && g_coop_attr) ? 2 : 1;
   std::unique_lock<std::mutex> lk;
   CoopFifo* fifo = nullptr;
-  if (COOP && !g_coop_attr) {  // wait for the previous co-resident launch if it is on another stream
+  static const bool no_fifo = [] {  // (DIALSORT_NO_FIFO=1: experiments only)
+    const char* e = getenv("DIALSORT_NO_FIFO");
+    return e && e[0] == '1';
+  }();
+  if (COOP && !g_coop_attr && !no_fifo) {  // wait for the previous co-resident launch if it is on another stream
     int dev = 0;
     cudaGetDevice(&dev);
     fifo = &g_fifo[dev & 31];
@@ -190,6 +194,8 @@ std::map<int, long long> g_probe;
 
 }  // namespace
 
+constexpr int kMaxLanes = 6;  // CTA groups of the batched sort
+
 struct dialsort_ctx_s {
   int device = 0;
   int nsm = 148;
@@ -205,6 +211,10 @@ struct dialsort_ctx_s {
   long long probe_violations = -1;   // radix lane-order probe of this device
   int radix_force = 0;               // 0: auto (pass4 iff the probe passed), 3 / 4 forced
   bool coop_attr = false;            // DIALSORT_OPT_COOPERATIVE
+  uint32_t max_ctas = 0;             // DIALSORT_OPT_MAX_CTAS (0: every SM)
+  // batched sort (dialsort_sort_batch_async): one workspace lane per CTA group, created lazily;
+  // their deferred errors are merged by dialsort_sync of this context
+  dialsort_ctx lanes[kMaxLanes] = {};
   PhaseTimes* pt = nullptr;          // debug phase timing (DIALSORT_PHASE_TIMING=1)
 };
 
@@ -289,6 +299,10 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowN4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_reconstruct_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
@@ -390,13 +404,15 @@ int fill_scan_args(dialsort_ctx c, ScanArgs& a, uint32_t U, bool do_scan, uint64
 // and row format.  kb: key bytes (4 int32; 2 uint16: the hierarchical path's universe blocks or a
 // 2-byte coded domain; 1 uint8: a 1-byte coded domain, U <= 8192).  enc / dec: the coded-domain
 // maps phi (1-byte keys) and phi^-1 (emitted values), nullable.
-int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
-                       uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
-                       const uint64_t* d_off = nullptr, int kb = 4, bool hist_only = false,
-                       uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0, uint32_t peerRank = 0,
-                       uint32_t bin_base = 0, const uint32_t* enc = nullptr, const int32_t* dec = nullptr) {
+// The arguments of one fused step on context c's workspace (shared by the single-step launch
+// and the batched kernel).  C_force != 0: the step runs on exactly that many CTAs (a group of
+// k_sort_batch); barriers: the step reserves `bars` barriers of its grid.
+int build_fused_args(dialsort_ctx c, ScanArgs& a, int& fmt, uint32_t& C, size_t& smem, uint64_t n, uint32_t U,
+                     uint32_t* H, uint32_t epoch, const uint64_t* d_n, const uint64_t* d_off, int kb, bool hist_only,
+                     uint32_t* const* Hpeer, uint32_t peerL, uint32_t peerRank, uint32_t bin_base,
+                     const uint32_t* enc, const int32_t* dec, uint32_t C_force, uint32_t bars) {
   int rc;
-  ScanArgs a = {};
+  a = ScanArgs{};
   if ((rc = fill_scan_args(c, a, U, !hist_only, n, true, nullptr, epoch))) return rc;
   a.d_n = d_n;
   a.d_off = d_off;
@@ -412,14 +428,18 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
   const uint64_t n4 = n / 4 + 1;
-  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);
-  const uint64_t cmax = std::min<uint64_t>(c->nsm, kFMaxRows);  // rows a staging slot holds
-  const uint32_t C = (uint32_t)(want < cmax ? (want ? want : 1) : cmax);
+  // CTAs: enough for the keys (8 vectors per thread), and at least one per 1024 bins — every CTA
+  // flushes and merges O(U) words whatever the grid, but the merge's batches (16 tiles of 64
+  // bins each) run one after another: U = 65536 on one CTA took 64 batches (~330 us at n = 1e4)
+  const uint64_t want = std::max<uint64_t>(cdiv(n4, 1024ull * kHistUnroll * 2), cdiv(U, 1024));
+  const uint64_t cmax = std::min<uint64_t>(c->max_ctas ? std::min<uint32_t>(c->max_ctas, c->nsm) : c->nsm,
+                                           kFMaxRows);  // rows a staging slot holds
+  C = C_force ? C_force : (uint32_t)(want < cmax ? (want ? want : 1) : cmax);
   // partial-row format: 4-bit rows while counts per CTA and bin are small (mean <= 8: counts
   // >= 16 — exceptions, one RED each — stay rare), else the packed 16-bit rows
-  const int fmt = !pack ? kRowU32 : (n <= 8ull * C * U ? kRowN4 : kRowP16);
+  fmt = !pack ? kRowU32 : (n <= 8ull * C * U ? kRowN4 : kRowP16);
   const uint32_t ldr = fmt == kRowN4 ? (uint32_t)round_up((U + 7) / 8, 8) : ldw;  // row words
-  const size_t smem = std::max<size_t>(4ull * ldw, 4ull * kFSmemWords);  // histogram | merge + projection
+  smem = std::max<size_t>(4ull * ldw, 4ull * kFSmemWords);  // histogram | merge + projection
   if ((rc = c->partials.ensure(4ull * C * std::max(ldw, ldr)))) return rc;
   if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
   if ((rc = c->Hx.ensure(8ull * kSmem16MaxBins, true))) return rc;
@@ -436,8 +456,8 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.tsums = nullptr;
   a.fused = 1;
   a.ctr_stride = kTileTotStride;
-  // per-tile ready flags (share mode), two parities: each launch clears the other one, so a
-  // flag never holds a value from an earlier launch (the epoch wraps after 2^24 launches)
+  // per-tile ready flags (share mode), two parities: each step clears the other one, so a flag
+  // never holds a value from an earlier step (the epoch wraps after 2^24 steps)
   uint32_t* rdy = ft;
   a.ready = rdy + kFTileSlots * (c->fused_seq & 1);
   a.ready_clear = rdy + kFTileSlots * ((c->fused_seq + 1) & 1);
@@ -446,11 +466,29 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   a.own_red = ownb + own_words * (c->fused_seq & 1);
   a.own_clear = ownb + own_words * ((c->fused_seq + 1) & 1);
   a.own_alt = ownb + 2 * own_words;
-  // exception histogram of the 4-bit rows: parity buffers, the other one cleared by every launch
+  // exception histogram of the 4-bit rows: parity buffers, the other one cleared by every step
   a.Hx = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * (c->fused_seq & 1);
   a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);
   a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
   a.bar_base = c->bar64_base;
+  c->fused_seq++;
+  c->bar64_base += (uint64_t)bars * C;  // barriers reserved (the overflow one is skipped unless needed)
+  return DIALSORT_OK;
+}
+
+int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U, uint32_t* H, int32_t* out,
+                       uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
+                       const uint64_t* d_off = nullptr, int kb = 4, bool hist_only = false,
+                       uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0, uint32_t peerRank = 0,
+                       uint32_t bin_base = 0, const uint32_t* enc = nullptr, const int32_t* dec = nullptr) {
+  int rc;
+  ScanArgs a;
+  int fmt;
+  uint32_t C;
+  size_t smem;
+  if ((rc = build_fused_args(c, a, fmt, C, smem, n, U, H, epoch, d_n, d_off, kb, hist_only, Hpeer, peerL, peerRank,
+                             bin_base, enc, dec, 0, 2)))
+    return rc;
 #define DS_LAUNCH_FUSED(F, K) \
   DS_CUDA(launch_k<true>(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
   if (fmt == kRowN4) {
@@ -461,8 +499,36 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
     if (kb == 2) DS_LAUNCH_FUSED(kRowU32, 2); else if (kb == 1) DS_LAUNCH_FUSED(kRowU32, 1); else DS_LAUNCH_FUSED(kRowU32, 4);
   }
 #undef DS_LAUNCH_FUSED
-  c->fused_seq++;
-  c->bar64_base += 2ull * C;  // two barriers reserved per launch (one skipped unless overflow)
+  return DIALSORT_OK;
+}
+
+// The projection of a caller histogram as one co-resident kernel (k_reconstruct_fused) when H
+// is 16-byte aligned, U % 4 == 0 and U <= 131072 (the share mode's ready-flag slots); returns
+// false (nothing enqueued) otherwise, and the caller takes k_scan + k_expand.
+bool reconstruct_fused_applies(const uint32_t* H, uint32_t U) {
+  return (reinterpret_cast<uintptr_t>(H) & 15u) == 0 && U % 4 == 0 && (uint64_t)U <= (uint64_t)kFTileSlots * kFTileBins;
+}
+int enqueue_reconstruct_fused(dialsort_ctx c, const uint32_t* H, uint32_t U, int32_t key_base, int32_t* out,
+                              uint64_t cap, bool exact, uint64_t* d_total, uint32_t epoch, cudaStream_t s) {
+  int rc;
+  ScanArgs a;
+  int fmt;
+  uint32_t C;
+  size_t smem;
+  const uint64_t want = std::max<uint64_t>(cdiv(cap / 4 + 1, 1024ull * kHistUnroll * 2), cdiv(U, 1024));
+  const uint32_t Cr = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, std::min<uint64_t>(c->nsm, kFMaxRows)));
+  if ((rc = build_fused_args(c, a, fmt, C, smem, cap, U, nullptr, epoch, nullptr, nullptr, 4, false, nullptr, 0, 0, 0,
+                             nullptr, nullptr, Cr, 2)))
+    return rc;
+  a.partials = H;  // the given histogram as the single u32 "row"
+  a.C = 1;
+  a.ldw = a.ldr = (uint32_t)round_up(U, 8);
+  a.pack16 = 0;
+  a.nib4 = 0;
+  a.exact = exact;
+  a.d_total = d_total;
+  smem = 4ull * kFSmemWords;
+  DS_CUDA(launch_k<true>(KID_SORT_FUSED, k_reconstruct_fused, dim3(C), dim3(1024), smem, s, a, cap, out, key_base));
   return DIALSORT_OK;
 }
 
@@ -724,6 +790,11 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
   if (!c) return DIALSORT_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  for (dialsort_ctx& l : c->lanes)
+    if (l) {
+      dialsort_ctx_destroy(l);
+      l = nullptr;
+    }
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
                   &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->fused_tiles, &c->Hx,
                   &c->part, &c->htmp, &c->qtmp})
@@ -745,6 +816,10 @@ int dialsort_ctx_set_option(dialsort_ctx c, int option, int64_t value) {
     case DIALSORT_OPT_COOPERATIVE:
       c->coop_attr = value != 0;
       return DIALSORT_OK;
+    case DIALSORT_OPT_MAX_CTAS:
+      if (value < 0 || value > 1024) return fail(DIALSORT_E_INVALID_ARG, "max CTAs: 0..1024");
+      c->max_ctas = (uint32_t)value;
+      return DIALSORT_OK;
     default:
       return fail(DIALSORT_E_INVALID_ARG, "unknown or read-only option");
   }
@@ -758,6 +833,7 @@ int dialsort_ctx_get_option(dialsort_ctx c, int option, int64_t* value) {
     case DIALSORT_OPT_RADIX_ACTIVE: *value = radix_variant(c, true); return DIALSORT_OK;
     case DIALSORT_OPT_NUM_SMS: *value = c->nsm; return DIALSORT_OK;
     case DIALSORT_OPT_COOPERATIVE: *value = c->coop_attr ? 1 : 0; return DIALSORT_OK;
+    case DIALSORT_OPT_MAX_CTAS: *value = c->max_ctas; return DIALSORT_OK;
     default: return fail(DIALSORT_E_INVALID_ARG, "unknown option");
   }
 }
@@ -774,6 +850,20 @@ int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info*
   clean.ovf_epoch = h.ovf_epoch;
   clean.last_total = h.last_total;
   if (h.bad_count || h.flags) DS_CUDA(cudaMemcpy(c->status.p, &clean, sizeof(clean), cudaMemcpyHostToDevice));
+  for (dialsort_ctx l : c->lanes) {  // the batched sort's lanes (their work is on this stream too)
+    if (!l) continue;
+    DevStatus lh;
+    DS_CUDA(cudaMemcpy(&lh, l->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+    if (!lh.bad_count && !lh.flags) continue;
+    h.bad_count += lh.bad_count;
+    h.first_bad = std::min(h.first_bad, lh.first_bad);
+    h.flags |= lh.flags;
+    DevStatus lc = {};
+    lc.first_bad = ~0ull;
+    lc.ovf_epoch = lh.ovf_epoch;
+    lc.last_total = lh.last_total;
+    DS_CUDA(cudaMemcpy(l->status.p, &lc, sizeof(lc), cudaMemcpyHostToDevice));
+  }
   if (info) {
     info->bad_count = h.bad_count;
     info->first_bad_index = h.bad_count ? (h.first_bad >> 32) : ~0ull;
@@ -824,6 +914,7 @@ int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, in
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
   const uint32_t epoch = next_epoch(c);
+  if (reconstruct_fused_applies(H, U)) return enqueue_reconstruct_fused(c, H, U, key_base, out, cap, exact != 0, d_total, epoch, s);
   if ((rc = enqueue_scan(c, H, U, cap, exact != 0, d_total, epoch, s))) return rc;
   return enqueue_expand(c, U, cap, key_base, out, s);
 }
@@ -853,6 +944,92 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
   if (path == HistPath::Hier) return enqueue_hier(c, keys, n, U, H, out, s);
   if ((rc = enqueue_hist_scan(c, keys, n, U, H, true, n, epoch, s))) return rc;
   return enqueue_expand(c, U, n, 0, out, s);
+}
+
+int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const uint64_t* n, uint32_t U,
+                              int32_t* const* out, uint32_t* const* H_out, uint32_t nb, dialsort_stream_t stream) {
+  int rc;
+  if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
+  ProfScope prof_scope_(c);
+  if ((rc = check_U(U))) return rc;
+  if (nb && (!keys || !n || !out)) return fail(DIALSORT_E_INVALID_ARG, "NULL batch arrays");
+  for (uint32_t j = 0; j < nb; ++j) {
+    if ((rc = check_keys_arg(keys[j], n[j])) || (rc = check_keys_arg(out[j], n[j]))) return rc;
+    if (n[j] && out[j] != keys[j] && ranges_overlap(keys[j], 4 * n[j], out[j], 4 * n[j]))
+      return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CUDA(cudaSetDevice(c->device));
+  const HistPath path = choose_path(U);
+  static const uint32_t kGroups = [] {  // CTA groups per launch (DIALSORT_BATCH_GROUPS: experiments)
+    const char* e = getenv("DIALSORT_BATCH_GROUPS");
+    const int v = e ? atoi(e) : 4;
+    return (uint32_t)(v < 2 ? 2 : v > kMaxLanes ? kMaxLanes : v);
+  }();
+  const uint32_t Lmax = std::min<uint32_t>(kGroups, (uint32_t)c->nsm / 8);
+  for (uint32_t j0 = 0; j0 < nb; j0 += kBatchMax) {
+    const uint32_t m = std::min<uint32_t>(kBatchMax, nb - j0);
+    // groups: at most kGroups, and few enough that every group keeps its own-tile projection
+    // (ntiles <= kFPassTiles per CTA): smaller groups fall to the share mode (Zipf at 5 groups of
+    // 29 CTAs: 145 us per batch vs 22 us at 4 groups of 37)
+    const uint64_t ntl = cdiv(U, kFTileBins);
+    const uint32_t Lown = (uint32_t)std::max<uint64_t>(1, (uint64_t)c->nsm * kFPassTiles / ntl);
+    const uint32_t L = std::min<uint32_t>(std::min<uint32_t>(Lmax, Lown), m);
+    const uint32_t Gg = std::min<uint32_t>(kFMaxRows, (uint32_t)c->nsm / std::max<uint32_t>(L, 1));
+    // one launch needs every batch on the shared-memory path in one row format, and no empty one
+    bool together = L >= 2 && (path == HistPath::Smem32 || path == HistPath::Smem16);
+    int fmt0 = -1;
+    for (uint32_t j = 0; together && j < m; ++j) {
+      const uint64_t nj = n[j0 + j];
+      const int f = U <= kSmem32MaxBins ? kRowU32 : (nj <= 8ull * Gg * U ? kRowN4 : kRowP16);
+      if (nj == 0 || (fmt0 >= 0 && f != fmt0)) together = false;
+      fmt0 = f;
+    }
+    if (!together) {  // one step after the other on the whole grid
+      for (uint32_t j = 0; j < m; ++j)
+        if ((rc = dialsort_sort_async(c, keys[j0 + j], n[j0 + j], U, out[j0 + j], H_out ? H_out[j0 + j] : nullptr,
+                                      stream)))
+          return rc;
+      continue;
+    }
+    BatchArgs B;
+    memset(&B, 0, sizeof B);
+    B.nb = m;
+    B.L = L;
+    B.Gg = Gg;
+    size_t smem = 0;
+    int fmt = -1;
+    for (uint32_t g = 0; g < L; ++g) {  // lanes: each group's own workspace and status
+      if (!c->lanes[g]) {
+        dialsort_ctx l = nullptr;
+        if ((rc = dialsort_ctx_create(c->device, 0, 0, &l))) return rc;
+        c->lanes[g] = l;
+      }
+    }
+    for (uint32_t j = 0; j < m; ++j) {
+      dialsort_ctx l = c->lanes[j % L];
+      uint32_t* H = H_out ? H_out[j0 + j] : nullptr;
+      if (!H) {
+        if ((rc = l->Hws.ensure(4ull * U))) return rc;
+        H = l->Hws.as<uint32_t>();
+      }
+      uint32_t C;
+      if ((rc = build_fused_args(l, B.a[j], fmt, C, smem, n[j0 + j], U, H, next_epoch(l), nullptr, nullptr, 4, false,
+                                 nullptr, 0, 0, 0, nullptr, nullptr, Gg, 3)))
+        return rc;
+      B.keys[j] = keys[j0 + j];
+      B.n[j] = n[j0 + j];
+      B.out[j] = out[j0 + j];
+    }
+    const dim3 grid(L * Gg);
+    if (fmt == kRowN4)
+      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowN4>, grid, dim3(1024), smem, s, B));
+    else if (fmt == kRowP16)
+      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowP16>, grid, dim3(1024), smem, s, B));
+    else
+      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowU32>, grid, dim3(1024), smem, s, B));
+  }
+  return DIALSORT_OK;
 }
 
 int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, dialsort_stream_t stream) {
@@ -1250,6 +1427,8 @@ int dialsort_sharded_project_async(dialsort_ctx c, dialsort_comm m, uint32_t U, 
   DS_CUDA(launch_k(KID_COMM_OFFSETS, k_comm_offsets, dim3(1), dim3(32), 0, s, comm_dev(m), cap, d_count, d_offset,
                    c->status.as<DevStatus>()));
   const uint32_t epoch = next_epoch(c);
+  if (reconstruct_fused_applies(Hs, L))
+    return enqueue_reconstruct_fused(c, Hs, L, (int32_t)(m->rank * L), out, cap, false, nullptr, epoch, s);
   if ((rc = enqueue_scan(c, Hs, L, cap, false, nullptr, epoch, s))) return rc;
   return enqueue_expand(c, L, cap, (int32_t)(m->rank * L), out, s);
 }

@@ -12,6 +12,14 @@ namespace ds {
 
 constexpr uint32_t FULL = 0xffffffffu;
 
+// The grid a CTA cooperates with: the launch's own grid, or — in the batched sort kernel
+// (k_sort_batch, ds_fused.cuh) — one group of its CTAs sorting a batch on its own ("virtual
+// grid" of G CTAs, this CTA's rank b).  Device helpers take it as their last argument.
+struct VGrid {
+  uint32_t G, b;
+};
+__device__ __forceinline__ VGrid vgrid_hw() { return VGrid{gridDim.x, blockIdx.x}; }
+
 // Deferred device error state of one context (dialsort_sync reads and clears it).
 struct DevStatus {
   unsigned long long bad_count;   // keys outside [0,U)

@@ -382,21 +382,21 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
   return block_sum<uint64_t>(s, red);
 }
 
-// One DialSort step: keys[n] in [0,U) -> out[min(ΣH, cap)] sorted; H as a by-product.
-// Grid: C <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic
-// smem: max(histogram, kFSmemWords words).  Two grid barriers are reserved per launch (the
-// second one is only waited for after a packed-counter overflow).
-template <int FMT, int KB = 4>
-__global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__ keys, uint64_t n, ScanArgs a,
-                                                       int32_t* __restrict__ out, int32_t key_base) {
+// One DialSort step: keys[n] in [0,U) -> out[min(ΣH, cap)] sorted; H as a by-product — run by
+// the G CTAs of the virtual grid vg (the whole launch, or one group of k_sort_batch).
+// C = vg.G <= min(#SMs, kFMaxRows) CTAs of 1024 threads (co-resident, 1 per SM).  Dynamic smem:
+// max(histogram, kFSmemWords words).  Two grid barriers are reserved per step (the second one
+// is only waited for after a packed-counter overflow).
+// FROM_H (reconstruct_step): no keys — the step projects a given histogram H (a.partials = H as
+// the single u32 "row", a.C = 1): each CTA sums its own tiles of H and adds its total into the
+// owner counters P_{o+1} of every owner o >= b instead of ingesting and flushing.
+template <int FMT, int KB, bool FROM_H = false>
+__device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_t n, const ScanArgs& a,
+                                          int32_t* __restrict__ out, int32_t key_base, VGrid vg, uint32_t* sh,
+                                          uint64_t* red64, uint32_t* wsum) {
   // (KB: key bytes — 4 int32 keys; 2 uint16 keys, the hierarchical path's universe blocks or a
   //  2-byte coded domain; 1 uint8 keys, a 1-byte coded domain)
   // (keys, out, n are adjusted below for hierarchical blocks)
-  extern __shared__ __align__(128) uint32_t sh[];
-  __shared__ uint64_t red64[34];
-  __shared__ uint32_t wsum[32];
-  pdl_wait();
-  phase_mark(a.pt, -1);
   uint64_t n_exp = a.n_expected;
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
     __shared__ uint64_t s_noff[2];  // (one load per CTA, not one per thread: a 148k-way fan-in)
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     n_exp = n;
   }
   const uint32_t U = a.U, ntiles = (U + kFTileBins - 1) / kFTileBins;
-  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t G = vg.G, b = vg.b;
   // the other parity's owner totals are zeroed for the next launch (host alternates them;
   // every slot, since the next launch may have more CTAs than this one)
   if (b == G - 1) {
@@ -429,11 +429,27 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
   // the row's 64-bin tile sums (flush) sit past the largest ingestion histogram; zeroed here
   // (the ingestion's first __syncthreads orders this before the flush)
   static_assert(kFOffTsh >= kSmem16MaxBins / 2, "tile sums overlap the packed histogram");
-  for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
-  hist_ingest_flush<PACK16, KB>(keys, n, a, sh, red64, sh + kFOffTsh);
+  if constexpr (FROM_H) {
+    // own tiles' total t_b of the given H, added into P_{o+1} for o = b .. G-1 (Σ_{o' <= o} t_o'),
+    // and the skew vote against the expected total (n_exp = ΣH in exact mode)
+    uint32_t t0, t1;
+    my_tiles(ntiles, t0, t1, vg);
+    const uint32_t k1 = min(t1 * kFTileBins, U);
+    uint32_t sum = 0;
+    for (uint32_t k = t0 * kFTileBins + threadIdx.x; k < k1; k += blockDim.x) sum += __ldcg(a.partials + k);
+    sum = block_sum<uint32_t>(sum, reinterpret_cast<uint32_t*>(red64));
+    for (uint32_t o = b + threadIdx.x; o < G && sum; o += blockDim.x)
+      red_add_u32(a.own_red + (uint64_t)(o + 1) * a.ctr_stride, sum);
+    if (threadIdx.x == 0 && 4ull * G * sum > 5ull * n_exp + 256ull * G)
+      red_add_u32(a.own_red + (uint64_t)kFOwnVote * a.ctr_stride, 1u);
+    __syncthreads();
+  } else {
+    for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) sh[kFOffTsh + i] = 0;
+    hist_ingest_flush<PACK16, KB>(keys, n, a, sh, red64, sh + kFOffTsh, vg);
+  }
   __shared__ uint32_t s_own[2];  // this CTA's tiles [tb0, tb1) (index ownership)
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
-    my_tiles(ntiles, s_own[0], s_own[1]);
+    my_tiles(ntiles, s_own[0], s_own[1], vg);
   });
   phase_mark(a.pt, 3);
 
@@ -598,7 +614,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
       const uint32_t wpre = obase + carry + wex[j >> 5];
       const uint32_t bin = t0 * kFTileBins + j;
       const uint32_t p = bin < U ? wpre + inc - h : oend;  // (bins >= U: the last tile; oend = total)
-      if (bin < U) store_H(a, bin, h);
+      if (bin < U && (a.H || a.Hpeer)) store_H(a, bin, h);  // (a given H is not written back)
       if (own) Ps[(t0 - tb0) * kFTileBins + j] = p;
       else if (bin < U && !a.hist_only) a.P[bin] = p;
     }
@@ -614,7 +630,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     for (uint32_t k = tb0 * kFTileBins + threadIdx.x; k < min(tb1 * kFTileBins, U); k += blockDim.x) a.ovfH[k] = 0;
   phase_mark(a.pt, 6);
   if (a.hist_only) {  // histogram-only launch (hierarchical histogram, multi-GPU exchange)
-    pdl_trigger();
     return;
   }
 
@@ -632,7 +647,6 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
                   reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
                   reinterpret_cast<uint32_t*>(red64), out, aligned, pol, a.dec);
     phase_mark(a.pt, 7);
-    pdl_trigger();
     return;
   }
 
@@ -690,6 +704,69 @@ __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__
     }
   }
   phase_mark(a.pt, 7);
+}
+
+
+
+template <int FMT, int KB = 4>
+__global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__ keys, uint64_t n, ScanArgs a,
+                                                       int32_t* __restrict__ out, int32_t key_base) {
+  extern __shared__ __align__(128) uint32_t sh[];
+  __shared__ uint64_t red64[34];
+  __shared__ uint32_t wsum[32];
+  pdl_wait();
+  phase_mark(a.pt, -1);
+  sort_step<FMT, KB>(keys, n, a, out, key_base, vgrid_hw(), sh, red64, wsum);
+  pdl_trigger();
+}
+
+// The projection of a given histogram H (dialsort_reconstruct_async, the sharded slice
+// projection) as one co-resident kernel: offsets, scan and projection of sort_step without the
+// ingestion (U <= kFTileSlots * 64 bins: the share mode's ready flags).
+__global__ void __launch_bounds__(1024, 1) k_reconstruct_fused(ScanArgs a, uint64_t cap, int32_t* __restrict__ out,
+                                                              int32_t key_base) {
+  extern __shared__ __align__(128) uint32_t sh[];
+  __shared__ uint64_t red64[34];
+  __shared__ uint32_t wsum[32];
+  pdl_wait();
+  sort_step<kRowU32, 4, true>(nullptr, cap, a, out, key_base, vgrid_hw(), sh, red64, wsum);
+  pdl_trigger();
+}
+
+// ---- batched sort: independent DialSort steps overlapped on disjoint CTA groups --------------
+// One launch sorts up to kBatchMax batches (each: keys[n] -> out, H) on L groups of Gg CTAs:
+// group g sorts batches g, g + L, g + 2L, ... one after another, each as a whole DialSort step
+// on its own virtual grid (sort_step with vg = {Gg, rank in the group}) with its own workspace
+// (a context lane: rows, counters, barrier, status).  A step alternates HBM-bound phases
+// (ingestion, projection) with phases that leave HBM idle (flush, grid barrier, merge): with
+// the groups out of phase, one group's ingestion or projection runs while another merges, so
+// HBM stays busy (c2 on one B200: 27.7 us per batch on the whole grid, 17.6 us per batch on four
+// concurrent groups of 37 CTAs).  The groups drift out of phase by themselves (an explicit
+// start stagger — group g waiting for group g - 1's first ingestion — measured slower: 20.9
+// vs 17.6 us).  After each batch a group passes one more barrier of its own (every CTA finished
+// the batch before the group's next one reuses the workspace: the boundary a kernel launch gives
+// the single-step kernel).
+constexpr uint32_t kBatchMax = 64;
+struct BatchArgs {
+  uint32_t nb, L, Gg;
+  const void* keys[kBatchMax];
+  uint64_t n[kBatchMax];
+  int32_t* out[kBatchMax];
+  ScanArgs a[kBatchMax];  // per batch: its group's workspace, parities, epochs, barrier base
+};
+template <int FMT>
+__global__ void __launch_bounds__(1024, 1) k_sort_batch(const __grid_constant__ BatchArgs B) {
+  extern __shared__ __align__(128) uint32_t sh[];
+  __shared__ uint64_t red64[34];
+  __shared__ uint32_t wsum[32];
+  pdl_wait();
+  const uint32_t g = blockIdx.x / B.Gg;
+  const VGrid vg{B.Gg, blockIdx.x % B.Gg};
+  for (uint32_t j = g; j < B.nb; j += B.L) {
+    const ScanArgs& a = B.a[j];
+    sort_step<FMT, 4>(B.keys[j], B.n[j], a, B.out[j], 0, vg, sh, red64, wsum);
+    grid_barrier_mono(a.bar64, a.bar_base + 3ull * B.Gg);  // batch done by every CTA of the group
+  }
   pdl_trigger();
 }
 

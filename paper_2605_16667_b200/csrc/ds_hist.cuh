@@ -47,10 +47,10 @@ __host__ __device__ inline KeySpan make_span(const int32_t* keys, uint64_t n) {
 // Visit this CTA's keys as int4 vectors f4(v, vector index), plus scalars f1(key, index) for
 // the unaligned head (CTA 0) and tail (last CTA).  32-bit vector indices (n4 < 2^30).
 template <typename F4, typename F1>
-__device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1) {
-  const uint32_t T = blockDim.x, G = gridDim.x;
-  if (blockIdx.x == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
-  if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
+__device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1, VGrid vg = vgrid_hw()) {
+  const uint32_t T = blockDim.x, G = vg.G;
+  if (vg.b == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
+  if (vg.b == G - 1 && threadIdx.x < s.tail) {
     uint64_t i = s.head + 4 * s.n4 + threadIdx.x;
     f1((uint32_t)s.keys[i], i);
   }
@@ -61,7 +61,7 @@ __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1
   // Software pipeline: the next batch is requested before the current one is ingested
   // (measured faster than ping-pong / refill-after-consume variants, 10 vs 14 us at c2).
   const uint32_t n4 = (uint32_t)s.n4, stride = G * T;
-  uint32_t i = blockIdx.x * T + threadIdx.x;
+  uint32_t i = vg.b * T + threadIdx.x;
   int4 a[kHistUnroll];
 #pragma unroll
   for (int u = 0; u < kHistUnroll; ++u)
@@ -103,12 +103,12 @@ __device__ __noinline__ uint32_t ingest4_checked(uint32_t* h, int4 v, uint64_t i
 // for_each_key4) and ingest, key by key, those that hold an out-of-range key (the hot loop
 // skipped them whole); returns #bad keys.
 template <bool PACK16>
-__device__ __noinline__ uint32_t ingest_deferred(uint32_t* h, const KeySpan& s, uint32_t U, DevStatus* st) {
+__device__ __noinline__ uint32_t ingest_deferred(uint32_t* h, const KeySpan& s, uint32_t U, DevStatus* st, VGrid vg) {
   const uint32_t n4 = (uint32_t)s.n4;
   const int4* body = s.body();
   uint32_t bad = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+  const uint32_t stride = vg.G * blockDim.x;
+  for (uint32_t i = vg.b * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const int4 v = body[i];
     if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)i, U, st);
   }
@@ -128,14 +128,14 @@ __device__ __forceinline__ void crn_red(uint32_t* H, uint32_t k, bool valid) {
 // The keys this CTA owns (the grid stride of for_each_key4), warp-synchronously (every lane runs
 // every iteration), for the CRN paths: f(key, index, valid).
 template <typename F>
-__device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
-  const uint64_t T = blockDim.x, G = gridDim.x;
+__device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f, VGrid vg = vgrid_hw()) {
+  const uint64_t T = blockDim.x, G = vg.G;
   {
-    bool v = blockIdx.x == 0 && threadIdx.x < s.head;
+    bool v = vg.b == 0 && threadIdx.x < s.head;
     if (threadIdx.x < 32) f(v ? (uint32_t)s.keys[threadIdx.x] : 0u, (uint64_t)threadIdx.x, v);
   }
   {
-    bool v = blockIdx.x == G - 1 && threadIdx.x < s.tail;
+    bool v = vg.b == G - 1 && threadIdx.x < s.tail;
     uint64_t i = s.head + 4 * s.n4 + threadIdx.x;
     if (threadIdx.x < 32) f(v ? (uint32_t)s.keys[i] : 0u, i, v);
   }
@@ -149,17 +149,17 @@ __device__ __forceinline__ void for_each_key_warp(const KeySpan& s, F&& f) {
     f((uint32_t)v.w, b + 3, ok);
   };
   const uint64_t stride = G * T;
-  for (uint64_t w = blockIdx.x * T + (threadIdx.x & ~31u); w < s.n4; w += stride) {
+  for (uint64_t w = vg.b * T + (threadIdx.x & ~31u); w < s.n4; w += stride) {
     const uint64_t i = w + (threadIdx.x & 31);
     vec(i, i < s.n4);
   }
 }
 __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
-                                                    uint32_t U, DevStatus* st, uint32_t epoch) {
+                                                    uint32_t U, DevStatus* st, uint32_t epoch, VGrid vg) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
-  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); });
+  for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); }, vg);
 }
 
 // ---- shared-memory paths: ingestion + merge + scan in one co-resident grid ------------------
@@ -184,8 +184,8 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // replaced by equal position shares (no vote anywhere bounds every owner's positions by
 // 5/4 n / G + 64 G, so own tiles stay balanced).
 __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U,
-                                                   uint32_t* red) {
-  const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = gridDim.x, b = threadIdx.x;
+                                                   uint32_t* red, VGrid vg) {
+  const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = vg.G, b = threadIdx.x;
   uint32_t s = 0;
   if (b < G) {
     const uint32_t t0 = (uint32_t)((uint64_t)ntf * b / G), t1 = (uint32_t)((uint64_t)ntf * (b + 1) / G);
@@ -249,11 +249,12 @@ __device__ __forceinline__ void expand_narrow(const int4& x, uint32_t v, const u
   }
 }
 template <int KB, typename F4, typename F1>
-__device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, const uint32_t* enc, F4&& f4, F1&& f1) {
+__device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, const uint32_t* enc, F4&& f4, F1&& f1,
+                                                        VGrid vg) {
   constexpr uint32_t per = 16 / KB;
-  const uint32_t T = blockDim.x, G = gridDim.x;
-  if (blockIdx.x == 0 && threadIdx.x < s.head) f1(narrow_key<KB>(s.keys, threadIdx.x, enc), (uint64_t)threadIdx.x);
-  if (blockIdx.x == G - 1 && threadIdx.x < s.tail) {
+  const uint32_t T = blockDim.x, G = vg.G;
+  if (vg.b == 0 && threadIdx.x < s.head) f1(narrow_key<KB>(s.keys, threadIdx.x, enc), (uint64_t)threadIdx.x);
+  if (vg.b == G - 1 && threadIdx.x < s.tail) {
     const uint64_t i = s.head + per * s.n8 + threadIdx.x;
     f1(narrow_key<KB>(s.keys, i, enc), i);
   }
@@ -261,7 +262,7 @@ __device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, cons
   const int4* __restrict__ body = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s.keys) + KB * s.head);
   const uint32_t n8 = (uint32_t)s.n8, stride = G * T;
   uint32_t cnt = 0;
-  uint32_t i = blockIdx.x * T + threadIdx.x;
+  uint32_t i = vg.b * T + threadIdx.x;
   int4 a[kHistUnroll / 2];
 #pragma unroll
   for (int u = 0; u < kHistUnroll / 2; ++u)
@@ -288,11 +289,11 @@ __device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, cons
 // 4-key groups holding a key outside [0, U) (skipped whole by the hot loop); returns #bad keys.
 template <bool PACK16, int KB>
 __device__ __noinline__ uint32_t ingest_deferred_narrow(uint32_t* h, const KeySpan16& s, const uint32_t* enc,
-                                                        uint32_t U, DevStatus* st) {
+                                                        uint32_t U, DevStatus* st, VGrid vg) {
   const int4* body = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s.keys) + KB * s.head);
   uint32_t bad = 0;
-  const uint32_t stride = gridDim.x * blockDim.x, n8 = (uint32_t)s.n8;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride)
+  const uint32_t stride = vg.G * blockDim.x, n8 = (uint32_t)s.n8;
+  for (uint32_t i = vg.b * blockDim.x + threadIdx.x; i < n8; i += stride)
     expand_narrow<KB>(body[i], i, enc, [&](int4 v, uint32_t g) {
       if (umax4(v) >= U) bad += ingest4_checked<PACK16>(h, v, s.head + 4 * (uint64_t)g, U, st);
     });
@@ -301,20 +302,20 @@ __device__ __noinline__ uint32_t ingest_deferred_narrow(uint32_t* h, const KeySp
 // Overflow fallback of a 16-bit-key CTA: zero the row, re-ingest this CTA's keys (the same
 // head / tail / grid-strided vectors) into ovfH through the warp CRN.
 __device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4* row4, uint32_t W4, uint32_t* ovfH,
-                                                      uint32_t U, DevStatus* st, uint32_t epoch) {
+                                                      uint32_t U, DevStatus* st, uint32_t epoch, VGrid vg) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) row4[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) atomicExch(&st->ovf_epoch, epoch);
-  const uint32_t T = blockDim.x, G = gridDim.x;
+  const uint32_t T = blockDim.x, G = vg.G;
   if (threadIdx.x < 32) {
-    bool v = blockIdx.x == 0 && threadIdx.x < s.head;
+    bool v = vg.b == 0 && threadIdx.x < s.head;
     crn_red(ovfH, v ? (uint32_t)s.keys[threadIdx.x] : 0u, v && s.keys[threadIdx.x] < U);
-    v = blockIdx.x == G - 1 && threadIdx.x < s.tail;
+    v = vg.b == G - 1 && threadIdx.x < s.tail;
     const uint64_t ti = s.head + 8 * s.n8 + threadIdx.x;
     crn_red(ovfH, v ? (uint32_t)s.keys[ti] : 0u, v && s.keys[ti] < U);
   }
   const int4* body = reinterpret_cast<const int4*>(s.keys + s.head);
-  for (uint64_t w = (uint64_t)blockIdx.x * T + (threadIdx.x & ~31u); w < s.n8; w += (uint64_t)G * T) {
+  for (uint64_t w = (uint64_t)vg.b * T + (threadIdx.x & ~31u); w < s.n8; w += (uint64_t)G * T) {
     const uint64_t i = w + (threadIdx.x & 31);
     const bool ok = i < s.n8;
     const int4 x = ok ? ld_stream4(body + i) : make_int4(0, 0, 0, 0);
@@ -329,7 +330,8 @@ __device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4*
 
 template <bool PACK16, int KB = 4>
 __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_v, uint64_t n, const ScanArgs& a,
-                                                  uint32_t* sh_hist, uint64_t* red64, uint32_t* tsum_sh = nullptr) {
+                                                  uint32_t* sh_hist, uint64_t* red64, uint32_t* tsum_sh = nullptr,
+                                                  VGrid vg = vgrid_hw()) {
   constexpr bool K16 = KB == 2;  // (uint16 keys; KB == 1: uint8 keys)
   constexpr bool NARROW = KB != 4;
   const uint32_t U = a.U, ldw = a.ldw;
@@ -431,18 +433,18 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     }
   };
   if (NARROW) {
-    seen += (16 / KB) * for_each_key_narrow<NARROW ? KB : 2>(s16, a.enc, f4, f1);
+    seen += (16 / KB) * for_each_key_narrow<NARROW ? KB : 2>(s16, a.enc, f4, f1, vg);
   } else {
-    for_each_key4(s, f4, f1);
+    for_each_key4(s, f4, f1, vg);
     // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
-    const uint32_t stride = gridDim.x * blockDim.x, i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = vg.G * blockDim.x, i0 = vg.b * blockDim.x + threadIdx.x;
     const uint32_t n4 = (uint32_t)s.n4;
     const uint32_t cnt = i0 < n4 ? (n4 - 1 - i0) / stride + 1 : 0;
     seen += 4 * cnt;
   }
   if (deferred) {
-    if (NARROW) bad += ingest_deferred_narrow<PACK16, NARROW ? KB : 2>(sh_hist, s16, a.enc, U, st);
-    else bad += ingest_deferred<PACK16>(sh_hist, s, U, st);
+    if (NARROW) bad += ingest_deferred_narrow<PACK16, NARROW ? KB : 2>(sh_hist, s16, a.enc, U, st, vg);
+    else bad += ingest_deferred<PACK16>(sh_hist, s, U, st, vg);
   }
   phase_mark(a.pt, 0);
   __syncthreads();
@@ -452,7 +454,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   // (tsums[tile][row]) so that, after one barrier, every CTA knows its scan offsets.
   // Warp w flushes whole tiles w, w+32, ... (64 or 128 uint4 each): coalesced 512-byte
   // stores and one warp reduction per tile.
-  uint4* row4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * ldw);
+  uint4* row4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * ldw);
   const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
   constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
   const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -468,7 +470,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     constexpr uint32_t QT = kFTileBins / 8;  // packed uint4 per tile
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot = ntf * QT;
     const uint32_t lim = min(W4, (U + 7) / 8);  // uint4 g < lim: in the histogram and a row word
-    uint32_t* wp = const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr + threadIdx.x;
+    uint32_t* wp = const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * a.ldr + threadIdx.x;
     uint32_t* tp = tsum_sh + threadIdx.x / QT;
     // 4 iterations' loads first: the shared atomics order the loop (smem may alias), so an
     // unbatched loop waits a full load latency per iteration
@@ -520,7 +522,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     // the tile sum tsum_sh[i / QT] (shared atomic).
     constexpr uint32_t QT = PACK16 ? kFTileBins / 8 : kFTileBins / 4;
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, tot4 = ntf * QT;
-    uint4* frow4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
+    uint4* frow4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * a.ldr);
     for (uint32_t i = threadIdx.x; i < tot4; i += blockDim.x) {
       if (i < W4) {
         const uint4 w = h4[i];
@@ -557,7 +559,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     }
     v = warp_sum(v);
     fsum += v;
-    if (lane == 0) __stcg(a.tsums + (uint64_t)t * gridDim.x + blockIdx.x, v);  // [tile][row]
+    if (lane == 0) __stcg(a.tsums + (uint64_t)t * vg.G + vg.b, v);  // [tile][row]
   }
   phase_mark(a.pt, 11);  // flush loop done (debug)
   // (uint4 beyond the last tile are padding zeros and are never read by the merge)
@@ -573,7 +575,7 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     const bool exact = dsum == 0u;
     // k_sort_fused: the row's owner totals (its tile sums summed per owning CTA) — only for
     // an exact row (an overflowed one is recounted after the barrier)
-    if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64));
+    if (tsum_sh && exact) flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64), vg);
     if (!exact) {
       if (a.fused) {
         // k_sort_fused rows: take back this CTA's exception REDs (the same wrapped field
@@ -590,16 +592,16 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
             }
           }
         }
-        uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)blockIdx.x * a.ldr);
-        if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
-        else hist_overflow_fallback(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch);
+        uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * a.ldr);
+        if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
+        else hist_overflow_fallback(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
       } else {
-        hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch);
+        hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch, vg);
       }
     }
   } else if (tsum_sh) {  // 32-bit rows cannot overflow
     __syncthreads();
-    flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64));
+    flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64), vg);
   }
   phase_mark(a.pt, 2);
 }

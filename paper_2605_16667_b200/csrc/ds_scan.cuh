@@ -160,8 +160,8 @@ __device__ __forceinline__ void scan_finish(const ScanArgs& a, uint64_t total) {
 }
 
 // Tiles [tb0, tb1) of CTA b in a grid of G over ntiles (contiguous ranges).
-__device__ __forceinline__ void my_tiles(uint32_t ntiles, uint32_t& tb0, uint32_t& tb1) {
-  const uint32_t G = gridDim.x, b = blockIdx.x;
+__device__ __forceinline__ void my_tiles(uint32_t ntiles, uint32_t& tb0, uint32_t& tb1, VGrid vg = vgrid_hw()) {
+  const uint32_t G = vg.G, b = vg.b;
   tb0 = (uint32_t)((uint64_t)ntiles * b / G);
   tb1 = (uint32_t)((uint64_t)ntiles * (b + 1) / G);
 }
