@@ -303,8 +303,8 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_reconstruct_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-  DS_CUDA(cudaFuncSetAttribute(k_hist_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   radix_configure();
   int occ = 0;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass3, kRadixThreads, sizeof(Radix3Smem)));
@@ -532,6 +532,14 @@ int enqueue_reconstruct_fused(dialsort_ctx c, const uint32_t* H, uint32_t U, int
   return DIALSORT_OK;
 }
 
+bool hier_batched() {  // (DIALSORT_HIER_BATCH=0: one launch per block, A/B only)
+  static const bool v = [] {
+    const char* e = getenv("DIALSORT_HIER_BATCH");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // Hierarchical DialSort for 98304 < U <= 2^22 (ds_part.cuh): MSD split into 65536-bin universe
 // blocks, then one k_sort_fused per block (device-resident block sizes / offsets: no host round
 // trip).  hist_only: the blocks' launches stop after their merge (H, or the owners' slots).
@@ -554,11 +562,50 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
   DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
   DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
   DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
+  // the B block steps: overlapped on CTA groups in one k_sort_batch launch (their HBM phases
+  // overlap the others' merges, as the batched sort) when every block is a full 65536-bin block
+  // of one row format; else one k_sort_fused launch per block
+  const uint32_t L = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(B, (uint64_t)c->nsm * kFPassTiles / 1024), 4);
+  const uint32_t Gg = std::min<uint32_t>(kFMaxRows, (uint32_t)c->nsm / std::max<uint32_t>(L, 1));
+  const uint64_t nb_hint = cdiv(n, B);
+  if (hier_batched() && L >= 2 && U % (1u << kPartShift) == 0 && B <= kBatchMax) {
+    BatchArgs BA;
+    memset(&BA, 0, sizeof BA);
+    BA.nb = B;
+    BA.L = L;
+    BA.Gg = Gg;
+    int fmt = -1;
+    size_t smem = 0;
+    for (uint32_t g = 0; g < L; ++g)
+      if (!c->lanes[g]) {
+        dialsort_ctx l = nullptr;
+        if ((rc = dialsort_ctx_create(c->device, 0, 0, &l))) return rc;
+        c->lanes[g] = l;
+      }
+    for (uint32_t b = 0; b < B; ++b) {
+      dialsort_ctx l = c->lanes[b % L];
+      uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
+      uint32_t C;
+      if ((rc = build_fused_args(l, BA.a[b], fmt, C, smem, nb_hint, 1u << kPartShift, Hb, next_epoch(l), w.bsz + b,
+                                 w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift, nullptr, nullptr,
+                                 Gg, 3)))
+        return rc;
+      BA.keys[b] = tmp;
+      BA.n[b] = nb_hint;
+      BA.out[b] = out;
+      BA.key_base[b] = (int32_t)(b << kPartShift);
+    }
+    if (fmt == kRowN4)
+      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowN4, 2>, dim3(L * Gg), dim3(1024), smem, s, BA));
+    else
+      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowP16, 2>, dim3(L * Gg), dim3(1024), smem, s, BA));
+    return DIALSORT_OK;
+  }
   for (uint32_t b = 0; b < B; ++b) {
     const uint32_t Ub = (uint32_t)std::min<uint64_t>(1ull << kPartShift, (uint64_t)U - ((uint64_t)b << kPartShift));
     const uint32_t epoch = next_epoch(c);  // each block launch has its own ready-flag epoch
     uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
-    if ((rc = enqueue_sort_fused(c, tmp, cdiv(n, B), Ub, Hb, out, epoch, s, (int32_t)(b << kPartShift), w.bsz + b,
+    if ((rc = enqueue_sort_fused(c, tmp, nb_hint, Ub, Hb, out, epoch, s, (int32_t)(b << kPartShift), w.bsz + b,
                                  w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift)))
       return rc;
   }
@@ -601,29 +648,10 @@ int enqueue_hist_scan(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t 
     DS_CUDA(launch_k<true>(KID_SCAN, k_scan, dim3((uint32_t)(ntiles < wave ? ntiles : wave)), dim3(kTileBins), 0, s, a));
     return DIALSORT_OK;
   }
-  const bool pack = path == HistPath::Smem16;
-  const uint32_t W = pack ? (U + 1) / 2 : U;
-  const uint32_t ldw = (uint32_t)round_up(W, 8);
-  const size_t smem = std::max<size_t>(4ull * ldw, 32 * 1024);
-  const uint64_t n4 = n / 4 + 1;
-  const uint64_t want = cdiv(n4, 1024ull * kHistUnroll * 2);
-  const uint32_t C = (uint32_t)(want < (uint64_t)c->nsm ? (want ? want : 1) : c->nsm);
-  if ((rc = c->partials.ensure(4ull * C * ldw))) return rc;
-  if ((rc = c->ovfH.ensure(4ull * U, true))) return rc;
-  if ((rc = c->tsums.ensure(4ull * C * cdiv(U, kTileBins)))) return rc;
-  a.tsums = c->tsums.as<uint32_t>();
-  a.partials = c->partials.as<uint32_t>();
-  a.C = C;
-  a.ldw = ldw;
-  a.pack16 = pack;
-  a.ovfH = c->ovfH.as<uint32_t>();
-  a.H = H;
-  const int kid = pack ? KID_HIST_SMEM16 : KID_HIST_SMEM32;
-  if (pack)
-    DS_CUDA(launch_k<true>(kid, k_hist_fused<true>, dim3(C), dim3(1024), smem, s, keys, n, a));
-  else
-    DS_CUDA(launch_k<true>(kid, k_hist_fused<false>, dim3(C), dim3(1024), smem, s, keys, n, a));
-  return DIALSORT_OK;
+  // shared-memory universes: the fused step in histogram-only mode (k_sort_fused, hist_only:
+  // ingestion, flush, merge; the merged bins stored into H or straight into the owners' slots)
+  if (do_scan) return fail(DIALSORT_E_INVALID_ARG, "internal: scan of a shared-memory histogram");
+  return enqueue_sort_fused(c, keys, n, U, H, nullptr, epoch, s, 0, nullptr, nullptr, 4, true, Hpeer, peerL, peerRank, 0);
 }
 
 // Scan of a caller histogram (reconstruct API).

@@ -752,9 +752,11 @@ struct BatchArgs {
   const void* keys[kBatchMax];
   uint64_t n[kBatchMax];
   int32_t* out[kBatchMax];
+  int32_t key_base[kBatchMax];
   ScanArgs a[kBatchMax];  // per batch: its group's workspace, parities, epochs, barrier base
 };
-template <int FMT>
+// (KB = 2: the hierarchical path's universe blocks — uint16 keys, sizes and offsets on the device)
+template <int FMT, int KB = 4>
 __global__ void __launch_bounds__(1024, 1) k_sort_batch(const __grid_constant__ BatchArgs B) {
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
@@ -764,7 +766,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_batch(const __grid_constant__ 
   const VGrid vg{B.Gg, blockIdx.x % B.Gg};
   for (uint32_t j = g; j < B.nb; j += B.L) {
     const ScanArgs& a = B.a[j];
-    sort_step<FMT, 4>(B.keys[j], B.n[j], a, B.out[j], 0, vg, sh, red64, wsum);
+    sort_step<FMT, KB>(B.keys[j], B.n[j], a, B.out[j], B.key_base[j], vg, sh, red64, wsum);
     grid_barrier_mono(a.bar64, a.bar_base + 3ull * B.Gg);  // batch done by every CTA of the group
   }
   pdl_trigger();

@@ -162,27 +162,19 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
   for_each_key_warp(s, [&](uint32_t k, uint64_t, bool v) { crn_red(ovfH, k, v && k < U); }, vg);
 }
 
-// ---- shared-memory paths: ingestion + merge + scan in one co-resident grid ------------------
-// Phase 0: CTA c ingests its keys into a private shared-memory histogram (uint32, or packed
-//          2 x 16-bit with exact overflow detection) and writes it as partial row c
-//          (plain coalesced stores; no zeroing of H, no global atomics).
-// Phase A: after a grid barrier, CTA c merges the rows of its contiguous range of 512-bin
-//          tiles into H (ds_scan.cuh merge_tile) and its range total.
-// Phase B: after a second barrier, offsets from the range totals and the tile scans give P
-//          and the expand index tfb (skipped for the histogram-only API).
-// One CTA per SM (1024 threads); the grid (<= #SMs) is co-resident by construction.
-// Dynamic smem = max(4*ldw, 32 KB): the histogram, later reused as merge scratch.
-// Ingestion + flush (phase 0 above), shared by k_hist_fused and k_sort_fused.  The flush
-// writes the row and, per 512-bin tile, the row's tile sum into tsums[tile][row] — or, for
-// k_sort_fused (a.fused), the row's 64-bin tile sums into shared memory (tsum_sh), from which
-// the row's sum s_o over each owning CTA o's tiles is formed.  k_sort_fused needs, after its
-// grid barrier, only the first output position of its own tiles: P_o = Σ_rows Σ_{o' < o} s_o'.
-// So each row adds its inclusive prefix over owners into P_{o+1} (one RED per owner, counters
-// on separate L2 lines: same-line REDs serialise) and CTA o later reads just P_o and P_{o+1}
-// (two lines) instead of every owner total.  It also votes "skewed" (one RED into a per-launch
-// word) when some s_o exceeds 5/4 of its even share of the row: the own-tile projection is then
-// replaced by equal position shares (no vote anywhere bounds every owner's positions by
-// 5/4 n / G + 64 G, so own tiles stay balanced).
+// ---- shared-memory paths: ingestion and flush of the fused step (ds_fused.cuh sort_step) -------
+// Every CTA ingests its keys into a private shared-memory histogram (uint32, or packed 2 x 16-bit
+// with exact overflow detection) and flushes it as partial row c (4-bit, 16-bit or 32-bit
+// counts; plain coalesced stores, no zeroing of H, no global atomics on the hot path), with the
+// row's 64-bin tile sums in shared memory (tsum_sh), from which the row's sum s_o over each
+// owning CTA o's tiles is formed.  The step needs, after its grid barrier, only the first output
+// position of each CTA's own tiles: P_o = Σ_rows Σ_{o' < o} s_o'.  So each row adds its
+// inclusive prefix over owners into P_{o+1} (one RED per owner, counters on separate L2 lines:
+// same-line REDs serialise) and CTA o later reads just P_o and P_{o+1} (two lines) instead of
+// every owner total.  It also votes "skewed" (one RED into a per-launch word) when some s_o
+// exceeds 5/4 of its even share of the row: the own-tile projection is then replaced by equal
+// position shares (no vote anywhere bounds every owner's positions by 5/4 n / G + 64 G, so own
+// tiles stay balanced).
 __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U,
                                                    uint32_t* red, VGrid vg) {
   const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = vg.G, b = threadIdx.x;
@@ -450,14 +442,9 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   __syncthreads();
   phase_mark(a.pt, 1);
 
-  // Flush the private histogram as partial row blockIdx.x, and this row's per-tile sums
-  // (tsums[tile][row]) so that, after one barrier, every CTA knows its scan offsets.
-  // Warp w flushes whole tiles w, w+32, ... (64 or 128 uint4 each): coalesced 512-byte
-  // stores and one warp reduction per tile.
-  uint4* row4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * ldw);
-  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
-  constexpr uint32_t q_per_tile = PACK16 ? kTileBins / 8 : kTileBins / 4;  // uint4 per tile (64 or 128)
-  const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // Flush the private histogram as partial row vg.b (4-, 16- or 32-bit counts) and this row's
+  // 64-bin tile sums (tsum_sh) for the owner counters.
+  const uint32_t lane = threadIdx.x & 31;
   uint32_t fsum = 0;  // <= the CTA's keys < 2^32
   if (a.fused && PACK16 && a.nib4) {
     // k_sort_fused, 4-bit rows: the partial row keeps counts <= 15 — 8 bins
@@ -542,25 +529,6 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins;
     for (uint32_t t = threadIdx.x; t < ntf; t += blockDim.x) fsum += tsum_sh[t];
   }
-  for (uint32_t t = threadIdx.x >> 5; !a.fused && t < ntiles; t += nwarps) {
-    uint32_t v = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < q_per_tile; j += 32) {
-      const uint32_t i = t * q_per_tile + j + lane;
-      if (i < W4) {
-        const uint4 w = h4[i];
-        __stcg(row4 + i, w);
-        if (PACK16)
-          v += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) + (w.z >> 16) +
-               (w.w & 0xffffu) + (w.w >> 16);
-        else
-          v += w.x + w.y + w.z + w.w;
-      }
-    }
-    v = warp_sum(v);
-    fsum += v;
-    if (lane == 0) __stcg(a.tsums + (uint64_t)t * vg.G + vg.b, v);  // [tile][row]
-  }
   phase_mark(a.pt, 11);  // flush loop done (debug)
   // (uint4 beyond the last tile are padding zeros and are never read by the merge)
   if (PACK16) {
@@ -595,8 +563,6 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
         uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * a.ldr);
         if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
         else hist_overflow_fallback(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
-      } else {
-        hist_overflow_fallback(s, row4, W4, a.ovfH, U, st, a.epoch, vg);
       }
     }
   } else if (tsum_sh) {  // 32-bit rows cannot overflow
@@ -604,39 +570,6 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     flush_owner_totals(a, tsum_sh, U, reinterpret_cast<uint32_t*>(red64), vg);
   }
   phase_mark(a.pt, 2);
-}
-
-template <bool PACK16>
-__global__ void __launch_bounds__(1024, 1) k_hist_fused(const int32_t* __restrict__ keys, uint64_t n, ScanArgs a) {
-  extern __shared__ __align__(128) uint32_t sh_hist[];
-  __shared__ uint64_t red64[34];
-  pdl_wait();  // previous work on the stream (e.g. the caller's producer of keys)
-  phase_mark(a.pt, -1);
-  hist_ingest_flush<PACK16>(keys, n, a, sh_hist, red64);
-  const uint32_t U = a.U;
-  DevStatus* st = a.st;
-  grid_barrier(a.bar);  // every row, tile sum (and any fallback contribution) is in L2
-  phase_mark(a.pt, 3);
-
-  // Merge + scan this CTA's tile range.
-  const uint32_t ntiles = (U + kTileBins - 1) / kTileBins;
-  __shared__ uint32_t s_ovf;
-  if (threadIdx.x == 0) s_ovf = ld_acquire_u32(&st->ovf_epoch);
-  __syncthreads();
-  const bool use_ovf = s_ovf == a.epoch;
-  uint32_t tb0, tb1;
-  my_tiles(ntiles, tb0, tb1);
-  if (a.do_scan && !use_ovf) {
-    merge_scan_range(a, tb0, tb1, false, sh_hist, red64);  // one barrier in total
-  } else {
-    // histogram-only API, or a packed-counter overflow somewhere (tile sums incomplete):
-    // merge, then offsets from range totals after a second barrier
-    uint64_t range = 0;
-    for (uint32_t t = tb0; t < tb1; ++t) range += merge_tile(a, t, use_ovf, sh_hist, red64);
-    if (a.do_scan) scan_phase_b(a, a.H, tb0, tb1, range, red64);
-  }
-  phase_mark(a.pt, 4);
-  pdl_trigger();
 }
 
 // ---- L2 path -----------------------------------------------------------------------------

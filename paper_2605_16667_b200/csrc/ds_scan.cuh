@@ -173,61 +173,6 @@ __device__ __forceinline__ uint32_t owner_of(uint32_t t, uint32_t ntiles, uint32
   return b;
 }
 
-// Phase A for one tile: H[tile] = Σ_rows partial[row][tile] (+ ovfH), written to a.H.
-// Returns the tile total (valid in every thread).  scratch: >= (blockDim/64)*2 KB of smem.
-__device__ __forceinline__ uint64_t merge_tile(const ScanArgs& a, uint32_t tile, bool use_ovf, uint32_t* scratch,
-                                               uint64_t* red) {
-  const uint32_t words = a.pack16 ? kTileBins / 2 : kTileBins;  // partial words per tile
-  const uint32_t lanes_per_row = words / 4;                      // one uint4 per lane per row
-  const uint32_t ngroups = blockDim.x / lanes_per_row;
-  const uint32_t grp = threadIdx.x / lanes_per_row, l = threadIdx.x % lanes_per_row;
-  const uint32_t Wtot = a.pack16 ? (a.U + 1) / 2 : a.U;
-  const uint64_t word0 = (uint64_t)tile * words + 4 * l;
-  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (grp < ngroups && word0 < Wtot) {
-    const uint32_t* base = a.partials + word0;
-    for (uint32_t r0 = grp; r0 < a.C; r0 += 8 * ngroups) {
-      uint4 x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t r = r0 + u * ngroups;
-        x[u] = r < a.C ? __ldcg(reinterpret_cast<const uint4*>(base + (uint64_t)r * a.ldw)) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (a.pack16) {
-          acc[0] += x[u].x & 0xffffu; acc[1] += x[u].x >> 16; acc[2] += x[u].y & 0xffffu; acc[3] += x[u].y >> 16;
-          acc[4] += x[u].z & 0xffffu; acc[5] += x[u].z >> 16; acc[6] += x[u].w & 0xffffu; acc[7] += x[u].w >> 16;
-        } else {
-          acc[0] += x[u].x; acc[1] += x[u].y; acc[2] += x[u].z; acc[3] += x[u].w;
-        }
-      }
-    }
-  }
-  // cross-group reduction through shared memory: scratch[g][bin]
-  __syncthreads();
-  if (grp < ngroups) {
-    uint32_t* dst = scratch + grp * kTileBins + (a.pack16 ? 8 * l : 4 * l);
-    reinterpret_cast<uint4*>(dst)[0] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-    if (a.pack16) reinterpret_cast<uint4*>(dst)[1] = make_uint4(acc[4], acc[5], acc[6], acc[7]);
-  }
-  __syncthreads();
-  uint64_t tile_sum = 0;
-  for (uint32_t j = threadIdx.x; j < kTileBins; j += blockDim.x) {
-    const uint64_t bin = (uint64_t)tile * kTileBins + j;
-    if (bin >= a.U) break;
-    uint32_t h = 0;
-    for (uint32_t g = 0; g < ngroups; ++g) h += scratch[g * kTileBins + j];
-    if (use_ovf) {
-      h += a.ovfH[bin];
-      a.ovfH[bin] = 0;  // consumed: ovfH is zero again for the next call
-    }
-    store_H(a, bin, h);
-    tile_sum += h;
-  }
-  return block_sum<uint64_t>(tile_sum, red);
-}
-
 // Sum of H over one tile (phase A when H is given).
 __device__ __forceinline__ uint64_t sum_tile(const uint32_t* H, uint32_t U, uint32_t tile, uint64_t* red) {
   uint64_t s = 0;
@@ -271,172 +216,6 @@ __device__ __forceinline__ void scan_phase_b(const ScanArgs& a, const uint32_t* 
   uint64_t off = block_sum<uint64_t>(s, red);
   for (uint32_t t = tb0; t < tb1; ++t) off = scan_tile(a, H, t, off, red);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) scan_finish(a, off);
-}
-
-// Merge + scan of tiles [tb0, tb1) whose first bin has exclusive prefix `off`: each tile's
-// rows are summed in registers (all row loads of a thread in flight together), the groups
-// combined through shared memory, and H, P (and tfb when given) written; when a.ready is
-// set, tile t is published (ready[t] = epoch, release) once its P is in memory.  Returns
-// the prefix after tb1.
-// `first_off()` is called once, after the first tile's row loads are issued (so that whatever
-// it reads shares their L2 round trip), and returns the prefix before tb0.
-//
-// STAGE (packed rows, 1024 threads): the C row segments of a tile (1 KB each) are copied into
-// shared memory `stage` with cp.async — all of them in flight at once without holding
-// registers (the register path fits only 8 x 16 B loads per thread under the 64-register cap,
-// i.e. two L2 round trips for 148 rows) — then summed from shared memory by 4 row groups.
-template <bool STAGE = false, typename OffFn>
-__device__ __forceinline__ uint64_t merge_scan_tiles(const ScanArgs& a, uint32_t tb0, uint32_t tb1, OffFn&& first_off,
-                                                     bool use_ovf, uint32_t* scratch, uint64_t* red,
-                                                     uint32_t* stage = nullptr) {
-  uint64_t off = 0;
-  if (tb0 == tb1) return first_off();
-  for (uint32_t t = tb0; t < tb1; ++t) {
-    if (STAGE) {
-      // rows r of tile t: partials[r][t*256 .. t*256+256) -> stage[r*256 ..]
-      const uint32_t Wtot4 = ((a.U + 1) / 2 + 3) / 4;  // uint4 groups holding packed words
-      const uint32_t q0 = t * (kTileBins / 8);          // first uint4 of the tile in a row
-      for (uint32_t i = threadIdx.x; i < a.C * 64; i += blockDim.x) {
-        const uint32_t r = i >> 6, l = i & 63;
-        const uint32_t* src = a.partials + (uint64_t)r * a.ldw + 4ull * (q0 + l);
-        const uint32_t dst = smem_addr(stage + r * 256 + 4 * l);
-        const uint32_t bytes = (q0 + l < Wtot4) ? 16u : 0u;  // zero-fill past the last word
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (t == tb0) off = first_off();
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
-      phase_mark(a.pt, 6);  // partial rows in shared memory (debug)
-      // thread j: packed word column w = j & 255 over rows r = j >> 8 (mod 4)
-      const uint32_t w = threadIdx.x & 255, qg = threadIdx.x >> 8;
-      uint32_t lo = 0, hi = 0;
-      for (uint32_t r = qg; r < a.C; r += 4) {
-        const uint32_t x = stage[r * 256 + w];
-        lo += x & 0xffffu;
-        hi += x >> 16;
-      }
-      scratch[qg * kTileBins + 2 * w] = lo;
-      scratch[qg * kTileBins + 2 * w + 1] = hi;
-      __syncthreads();
-      const uint64_t bin = (uint64_t)t * kTileBins + threadIdx.x;
-      const bool own = threadIdx.x < kTileBins && bin < a.U;
-      uint32_t h = 0;
-      if (own) {
-        h = scratch[threadIdx.x] + scratch[kTileBins + threadIdx.x] + scratch[2 * kTileBins + threadIdx.x] +
-            scratch[3 * kTileBins + threadIdx.x];
-        if (use_ovf) {
-          h += a.ovfH[bin];
-          a.ovfH[bin] = 0;
-        }
-        store_H(a, bin, h);
-      }
-      uint64_t tile_total;
-      const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
-      if (own) a.P[bin] = (uint32_t)(off + ex);
-      if (a.ready) {
-        __syncthreads();  // every P of the tile is written
-        if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t), "r"(a.epoch) : "memory");
-      }
-      off += tile_total;
-      continue;
-    }
-    // merge: per-group partial sums into scratch[g][bin] (as merge_tile)
-    const uint32_t words = a.pack16 ? kTileBins / 2 : kTileBins;
-    const uint32_t lanes_per_row = words / 4;
-    const uint32_t ngroups = blockDim.x / lanes_per_row;
-    const uint32_t grp = threadIdx.x / lanes_per_row, l = threadIdx.x % lanes_per_row;
-    const uint32_t Wtot = a.pack16 ? (a.U + 1) / 2 : a.U;
-    const uint64_t word0 = (uint64_t)t * words + 4 * l;
-    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (grp < ngroups && word0 < Wtot) {
-      const uint32_t* base = a.partials + word0;
-      for (uint32_t r0 = grp; r0 < a.C; r0 += 10 * ngroups) {  // 148 rows / 16 groups: one round
-        uint4 x[10];
-#pragma unroll
-        for (int u = 0; u < 10; ++u) {
-          const uint32_t r = r0 + u * ngroups;
-          x[u] = r < a.C ? __ldcg(reinterpret_cast<const uint4*>(base + (uint64_t)r * a.ldw)) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < 10; ++u) {
-          if (a.pack16) {
-            acc[0] += x[u].x & 0xffffu; acc[1] += x[u].x >> 16; acc[2] += x[u].y & 0xffffu; acc[3] += x[u].y >> 16;
-            acc[4] += x[u].z & 0xffffu; acc[5] += x[u].z >> 16; acc[6] += x[u].w & 0xffffu; acc[7] += x[u].w >> 16;
-          } else {
-            acc[0] += x[u].x; acc[1] += x[u].y; acc[2] += x[u].z; acc[3] += x[u].w;
-          }
-        }
-      }
-    }
-    if (t == tb0) off = first_off();
-    phase_mark(a.pt, 6);  // partial rows summed in registers (debug)
-    __syncthreads();
-    if (grp < ngroups) {
-      uint32_t* dst = scratch + grp * kTileBins + (a.pack16 ? 8 * l : 4 * l);
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-      if (a.pack16) reinterpret_cast<uint4*>(dst)[1] = make_uint4(acc[4], acc[5], acc[6], acc[7]);
-    }
-    __syncthreads();
-    // thread j owns bin j of the tile: sum the groups, scan, write H and P, index tfb
-    const uint64_t bin = (uint64_t)t * kTileBins + threadIdx.x;
-    const bool own = threadIdx.x < kTileBins && bin < a.U;
-    uint32_t h = 0;
-    if (own) {
-      for (uint32_t g = 0; g < ngroups; ++g) h += scratch[g * kTileBins + threadIdx.x];
-      if (use_ovf) {
-        h += a.ovfH[bin];
-        a.ovfH[bin] = 0;
-      }
-      store_H(a, bin, h);
-    }
-    uint64_t tile_total;
-    const uint64_t ex = block_excl_scan<uint64_t>(h, tile_total, red);
-    if (own) {
-      const uint64_t pk = off + ex;
-      a.P[bin] = (uint32_t)pk;
-      if (a.tfb && h > 0) {
-        const uint64_t t0 = (pk + a.T - 1) / a.T, t1 = (pk + h - 1) / a.T;
-        for (uint64_t q = t0; q <= t1 && q < a.ntiles_out; ++q) a.tfb[q] = (uint32_t)bin;
-      }
-    }
-    if (a.ready) {
-      __syncthreads();  // every P of the tile is written
-      if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + t), "r"(a.epoch) : "memory");
-    }
-    off += tile_total;
-  }
-  return off;
-}
-
-// Fused path, after the single grid barrier: this CTA's tile offset is the sum of every
-// row's tile sums over the tiles before its range (tsums, written during the flush); the
-// offset loads are issued before the partial-row loads so both share one L2 round trip,
-// and each tile is merged and scanned straight from registers (no re-read of H).
-__device__ __forceinline__ void merge_scan_range(const ScanArgs& a, uint32_t tb0, uint32_t tb1, bool use_ovf,
-                                                 uint32_t* scratch, uint64_t* red) {
-  const uint32_t ntiles = (a.U + kTileBins - 1) / kTileBins;
-  // tsums is [tile][row]: the entries of tiles < tb0 are one contiguous block, read as uint4
-  // with all loads of a thread in flight together.
-  uint64_t s = 0;
-  const uint32_t cnt = a.C * tb0;
-  const uint32_t cnt4 = cnt / 4;
-  const uint4* ts4 = reinterpret_cast<const uint4*>(a.tsums);
-  for (uint32_t j0 = threadIdx.x; j0 < cnt4; j0 += 4 * blockDim.x) {
-    uint4 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t j = j0 + u * blockDim.x;
-      x[u] = j < cnt4 ? __ldcg(ts4 + j) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) s += (uint64_t)x[u].x + x[u].y + x[u].z + x[u].w;
-  }
-  for (uint32_t j = 4 * cnt4 + threadIdx.x; j < cnt; j += blockDim.x) s += __ldcg(a.tsums + j);
-  phase_mark(a.pt, 5);  // offset loads issued (debug)
-  const uint64_t off0 = block_sum<uint64_t>(s, red);
-  const uint64_t off = merge_scan_tiles(a, tb0, tb1, [&] { return off0; }, use_ovf, scratch, red);
-  if (tb1 == ntiles && tb1 > tb0 && threadIdx.x == 0) scan_finish(a, off);
 }
 
 // Standalone scan of a given H (global path, reconstruct API): persistent co-resident grid.

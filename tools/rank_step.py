@@ -28,7 +28,6 @@ for name, n, U in [("c2/8", 10_000_000, 65536), ("c4/8", 1_000_000_000, 1 << 20)
     L = U // G
     out = torch.empty(2 * nl + (1 << 20), dtype=torch.int32, device=dev)
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
-    Hs = torch.empty(L, dtype=torch.int32, device=dev)
     times = {"scatter": [], "gather": [], "project": []}
     for it in range(6):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -41,7 +40,7 @@ for name, n, U in [("c2/8", 10_000_000, 65536), ("c4/8", 1_000_000_000, 1 << 20)
         for g in range(G):
             if g == 0:
                 ev[2].record()
-            comms[g].gather(U, Hs if g == 0 else torch.empty(L, dtype=torch.int32, device=dev))
+            comms[g].gather(U)  # (into the communicator's own slice buffer, which project(U, None) reads)
             if g == 0:
                 ev[3].record()
         for g in range(G):
