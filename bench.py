@@ -42,6 +42,8 @@ CONFIGS = {
     "c3-hot1": dict(n=10_000_000, U=65536, dist="hot1", desc="c3: n=1e7 uniform + 1% hot key, U=65536"),
     "c4": dict(n=1_000_000_000, U=1 << 20, dist="uniform", desc="c4: n=1e9 uniform, U=2^20"),
     "c5": dict(n=100_000_000, U=0, dist="int32", desc="c5: n=1e8 full-range int32, radix"),
+    # NEXT-4 (not a BASELINE config): U beyond 2^22, the wide hierarchical partition
+    "c4-wide": dict(n=1_000_000_000, U=1 << 24, dist="uniform", desc="NEXT-4: n=1e9 uniform, U=2^24"),
 }
 
 

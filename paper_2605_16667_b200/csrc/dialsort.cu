@@ -216,6 +216,7 @@ struct dialsort_ctx_s {
   // their deferred errors are merged by dialsort_sync of this context
   dialsort_ctx lanes[kMaxLanes] = {};
   PhaseTimes* pt = nullptr;          // debug phase timing (DIALSORT_PHASE_TIMING=1)
+  bool owns_pt = true;               // (a lane writes into its parent's stamps)
 };
 
 struct dialsort_comm_s {
@@ -301,6 +302,8 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_sort_fused<kRowU32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_reconstruct_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  DS_CUDA(cudaFuncSetAttribute(k_part_scatter_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)part_wide_smem(kPartMaxBlocksWide)));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -366,7 +369,8 @@ enum class HistPath { Smem32, Smem16, Hier, Global };
 HistPath choose_path(uint32_t U) {
   if (U <= kSmem32MaxBins) return HistPath::Smem32;
   if (U <= kSmem16MaxBins) return HistPath::Smem16;
-  if ((uint64_t)U <= ((uint64_t)kPartMaxBlocks << kPartShift)) return HistPath::Hier;
+  static const bool no_hier = getenv("DIALSORT_NO_HIER") != nullptr;  // (A/B against the L2 path only)
+  if (!no_hier && (uint64_t)U <= ((uint64_t)kPartMaxBlocksWide << kPartShift)) return HistPath::Hier;
   return HistPath::Global;
 }
 
@@ -548,9 +552,10 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
                  uint32_t peerRank = 0) {
   int rc;
   const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
+  const bool wide = B > kPartMaxBlocks;  // 2^22 < U <= 2^26: per-CTA block counters
   constexpr uint32_t kCtasPerSm = 2048 / kPartThreads;
-  const uint32_t Gp =
-      (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)kCtasPerSm * c->nsm, cdiv(n, kPartTile)));
+  const uint32_t Gp = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t)kCtasPerSm * c->nsm, cdiv(n, wide ? kPartWideTile : kPartTile)));
   if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
   if ((rc = c->htmp.ensure(2ull * n + 16))) return rc;  // uint16 block keys
   PartWs w;
@@ -559,49 +564,66 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
   w.cnt = reinterpret_cast<uint32_t*>(w.boff + B);
   w.st = c->status.as<DevStatus>();
   uint16_t* tmp = c->htmp.as<uint16_t>();
-  DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
-  DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
-  DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
-  // the B block steps: overlapped on CTA groups in one k_sort_batch launch (their HBM phases
-  // overlap the others' merges, as the batched sort) when every block is a full 65536-bin block
-  // of one row format; else one k_sort_fused launch per block
-  const uint32_t L = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(B, (uint64_t)c->nsm * kFPassTiles / 1024), 4);
+  if (wide) {
+    DS_CUDA(launch_k(KID_PART_COUNT, k_part_count_wide, dim3(Gp), dim3(kPartThreads), 4ull * B, s, keys, n, U, B, w));
+    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
+    DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter_wide, dim3(Gp), dim3(kPartThreads), part_wide_smem(B), s, keys,
+                     n, U, B, w, tmp));
+  } else {
+    DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
+    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
+    DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
+  }
+  // the block steps: the full 65536-bin blocks overlapped on CTA groups, up to kBatchMax per
+  // k_sort_batch launch (their HBM phases overlap the others' merges, as the batched sort); a
+  // last partial block (U % 65536 != 0) by its own k_sort_fused launch
+  const uint32_t Bfull = (uint32_t)(U >> kPartShift);
+  const uint32_t L = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(Bfull, (uint64_t)c->nsm * kFPassTiles / 1024), 4);
   const uint32_t Gg = std::min<uint32_t>(kFMaxRows, (uint32_t)c->nsm / std::max<uint32_t>(L, 1));
   const uint64_t nb_hint = cdiv(n, B);
-  if (hier_batched() && L >= 2 && U % (1u << kPartShift) == 0 && B <= kBatchMax) {
-    BatchArgs BA;
-    memset(&BA, 0, sizeof BA);
-    BA.nb = B;
-    BA.L = L;
-    BA.Gg = Gg;
-    int fmt = -1;
-    size_t smem = 0;
+  uint32_t b_done = 0;
+  if (hier_batched() && L >= 2) {
     for (uint32_t g = 0; g < L; ++g)
       if (!c->lanes[g]) {
         dialsort_ctx l = nullptr;
         if ((rc = dialsort_ctx_create(c->device, 0, 0, &l))) return rc;
+        if (l->pt) cudaFree(l->pt);
+        l->pt = c->pt;
+        l->owns_pt = false;
         c->lanes[g] = l;
       }
-    for (uint32_t b = 0; b < B; ++b) {
-      dialsort_ctx l = c->lanes[b % L];
-      uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
-      uint32_t C;
-      if ((rc = build_fused_args(l, BA.a[b], fmt, C, smem, nb_hint, 1u << kPartShift, Hb, next_epoch(l), w.bsz + b,
-                                 w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift, nullptr, nullptr,
-                                 Gg, 3)))
-        return rc;
-      BA.keys[b] = tmp;
-      BA.n[b] = nb_hint;
-      BA.out[b] = out;
-      BA.key_base[b] = (int32_t)(b << kPartShift);
+    for (uint32_t b0 = 0; b0 < Bfull; b0 += kBatchMax) {
+      const uint32_t m = std::min<uint32_t>(kBatchMax, Bfull - b0);
+      BatchArgs BA;
+      memset(&BA, 0, sizeof BA);
+      BA.nb = m;
+      BA.L = std::min<uint32_t>(L, m);
+      BA.Gg = Gg;
+      int fmt = -1;
+      size_t smem = 0;
+      for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t b = b0 + j;
+        dialsort_ctx l = c->lanes[j % BA.L];
+        uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
+        uint32_t C;
+        if ((rc = build_fused_args(l, BA.a[j], fmt, C, smem, nb_hint, 1u << kPartShift, Hb, next_epoch(l), w.bsz + b,
+                                   w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift, nullptr, nullptr,
+                                   Gg, 3)))
+          return rc;
+        BA.keys[j] = tmp;
+        BA.n[j] = nb_hint;
+        BA.out[j] = out;
+        BA.key_base[j] = (int32_t)(b << kPartShift);
+      }
+      const dim3 grid(BA.L * Gg);
+      if (fmt == kRowN4)
+        DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowN4, 2>, grid, dim3(1024), smem, s, BA));
+      else
+        DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowP16, 2>, grid, dim3(1024), smem, s, BA));
     }
-    if (fmt == kRowN4)
-      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowN4, 2>, dim3(L * Gg), dim3(1024), smem, s, BA));
-    else
-      DS_CUDA(launch_k<true>(KID_SORT_BATCH, k_sort_batch<kRowP16, 2>, dim3(L * Gg), dim3(1024), smem, s, BA));
-    return DIALSORT_OK;
+    b_done = Bfull;
   }
-  for (uint32_t b = 0; b < B; ++b) {
+  for (uint32_t b = b_done; b < B; ++b) {
     const uint32_t Ub = (uint32_t)std::min<uint64_t>(1ull << kPartShift, (uint64_t)U - ((uint64_t)b << kPartShift));
     const uint32_t epoch = next_epoch(c);  // each block launch has its own ready-flag epoch
     uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
@@ -828,7 +850,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
                   &c->part, &c->htmp, &c->qtmp})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
-  if (c->pt) cudaFree(c->pt);
+  if (c->pt && c->owns_pt) cudaFree(c->pt);
   for (cudaEvent_t e : c->prof.ev) cudaEventDestroy(e);
   delete c;
   return DIALSORT_OK;
@@ -1031,6 +1053,9 @@ int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const 
       if (!c->lanes[g]) {
         dialsort_ctx l = nullptr;
         if ((rc = dialsort_ctx_create(c->device, 0, 0, &l))) return rc;
+        if (l->pt) cudaFree(l->pt);
+        l->pt = c->pt;
+        l->owns_pt = false;
         c->lanes[g] = l;
       }
     }

@@ -21,7 +21,8 @@
 namespace ds {
 
 constexpr uint32_t kPartShift = 16;         // 65536-bin universe blocks
-constexpr uint32_t kPartMaxBlocks = 64;     // U <= 2^22 take this path (larger: the L2 path)
+constexpr uint32_t kPartMaxBlocks = 64;     // U <= 2^22: per-warp block counters (below)
+constexpr uint32_t kPartMaxBlocksWide = 1024;  // 2^22 < U <= 2^26: per-CTA counters (k_part_*_wide)
 #ifndef DIALSORT_PART_THREADS
 #define DIALSORT_PART_THREADS 512
 #endif
@@ -110,21 +111,18 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __re
   pdl_trigger();
 }
 
-// One CTA: off[c][b] = start(b) + Σ_{c' < c} cnt[c'][b], start(b) = Σ_{b' < b} size(b').
+// One CTA: off[c][b] = start(b) + Σ_{c' < c} cnt[c'][b], start(b) = Σ_{b' < b} size(b')
+// (B <= 1024 blocks: thread b owns column b; one block scan of the sizes gives the starts).
 __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, PartWs w) {
-  __shared__ uint64_t sz[kPartMaxBlocks];
+  __shared__ unsigned long long red[34];
   pdl_wait();
-  // thread b sums its column (B <= 64 columns, G <= a few hundred rows)
+  unsigned long long sz = 0;
+  if (threadIdx.x < B)
+    for (uint32_t c = 0; c < G; ++c) sz += w.cnt[(uint64_t)c * B + threadIdx.x];
+  unsigned long long tot;
+  const unsigned long long start = block_excl_scan<unsigned long long>(sz, tot, red);
   if (threadIdx.x < B) {
-    uint64_t s = 0;
-    for (uint32_t c = 0; c < G; ++c) s += w.cnt[(uint64_t)c * B + threadIdx.x];
-    sz[threadIdx.x] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < B) {
-    uint64_t start = 0;
-    for (uint32_t b = 0; b < threadIdx.x; ++b) start += sz[b];
-    w.bsz[threadIdx.x] = sz[threadIdx.x];
+    w.bsz[threadIdx.x] = sz;
     w.boff[threadIdx.x] = start;
     uint64_t run = start;
     for (uint32_t c = 0; c < G; ++c) {
@@ -265,6 +263,144 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
     // scan warp and the staging rewrite them
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = kn[i];
+  }
+  pdl_trigger();
+}
+
+
+// ---- wide partition (2^22 < U <= 2^26: up to 1024 universe blocks, NEXT-4) -----------------
+// Per-CTA block counters in (dynamic) shared memory instead of per-warp ones: the rank a key
+// takes inside its block of the sub-tile comes from the counting atomic (order inside a block is
+// free), one block scan over the B counters gives the staged runs.  8192-key sub-tiles (16 keys
+// per thread, 4 x 16-byte loads), so a block's run in a sub-tile averages 8192 / B keys.
+constexpr uint32_t kPartWideKPT = 16;
+constexpr uint32_t kPartWideTile = kPartThreads * kPartWideKPT;  // 8192 keys
+__host__ __device__ constexpr size_t part_wide_smem(uint32_t B) {
+  return 4ull * (4 * B + kPartWideTile) + 64;  // cnt, bstart, delta, gpos, stage
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_count_wide(const int32_t* __restrict__ keys, uint64_t n,
+                                                                  uint32_t U, uint32_t B, PartWs w) {
+  extern __shared__ uint32_t ccnt[];
+  pdl_wait();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) ccnt[i] = 0;
+  __syncthreads();
+  uint64_t lo, hi;
+  part_chunk(keys, n, lo, hi);
+  auto one = [&](uint32_t k, uint64_t idx) {
+    if (k < U) atomicAdd(&ccnt[k >> kPartShift], 1u);
+    else record_bad(w.st, idx, k);
+  };
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(keys + lo) >> 2) & 3u;
+  const uint64_t a4 = min(hi, lo + ((4u - mis) & 3u));
+  const uint64_t b4 = a4 + ((hi - a4) & ~3ull);
+  for (uint64_t i = lo + threadIdx.x; i < a4; i += blockDim.x) one((uint32_t)keys[i], i);
+  for (uint64_t i = b4 + threadIdx.x; i < hi; i += blockDim.x) one((uint32_t)keys[i], i);
+  const int4* body = reinterpret_cast<const int4*>(keys + a4);
+  const uint64_t nv = (b4 - a4) / 4;
+  const uint64_t pol = l2_evict_first_policy();
+  uint64_t v = threadIdx.x;
+  for (; v + 3 * blockDim.x < nv; v += 4 * blockDim.x) {
+    int4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = ld_stream4(body + v + u * blockDim.x, pol);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i0 = a4 + 4 * (v + u * blockDim.x);
+      if (umax4(x[u]) < U) {
+        atomicAdd(&ccnt[(uint32_t)x[u].x >> kPartShift], 1u);
+        atomicAdd(&ccnt[(uint32_t)x[u].y >> kPartShift], 1u);
+        atomicAdd(&ccnt[(uint32_t)x[u].z >> kPartShift], 1u);
+        atomicAdd(&ccnt[(uint32_t)x[u].w >> kPartShift], 1u);
+      } else {
+        one((uint32_t)x[u].x, i0); one((uint32_t)x[u].y, i0 + 1); one((uint32_t)x[u].z, i0 + 2); one((uint32_t)x[u].w, i0 + 3);
+      }
+    }
+  }
+  for (; v < nv; v += blockDim.x) {
+    const int4 x = ld_stream4(body + v, pol);
+    const uint64_t i0 = a4 + 4 * v;
+    one((uint32_t)x.x, i0); one((uint32_t)x.y, i0 + 1); one((uint32_t)x.z, i0 + 2); one((uint32_t)x.w, i0 + 3);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) w.cnt[(uint64_t)blockIdx.x * B + b] = ccnt[b];
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter_wide(const int32_t* __restrict__ keys, uint64_t n,
+                                                                    uint32_t U, uint32_t B, PartWs w,
+                                                                    uint16_t* __restrict__ tmp) {
+  extern __shared__ uint32_t psh[];
+  __shared__ uint32_t red[34];
+  uint32_t* cnt = psh;             // [B] this sub-tile's block counts (zero between sub-tiles)
+  uint32_t* bstart = cnt + B;      // [B] staged run starts
+  int32_t* delta = reinterpret_cast<int32_t*>(bstart + B);  // [B] output index of staged slot j: delta + j
+  uint32_t* gpos = reinterpret_cast<uint32_t*>(delta + B);  // [B] running output position of block b
+  uint32_t* stage = gpos + B;      // [kPartWideTile] keys by block
+  constexpr uint32_t kBad = 0xffffffffu;
+  pdl_wait();
+  uint64_t lo, hi;
+  part_chunk(keys, n, lo, hi);
+  for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+    cnt[b] = 0;
+    gpos[b] = w.cnt[(uint64_t)blockIdx.x * B + b];
+  }
+  const bool vec = ((reinterpret_cast<uintptr_t>(keys + lo)) & 15u) == 0;
+  __syncthreads();
+  uint16_t* const out = tmp;
+  for (uint64_t t0 = lo; t0 < hi; t0 += kPartWideTile) {
+    // thread t holds sub-tile keys 16t .. 16t+15
+    uint32_t k[kPartWideKPT];
+    uint16_t r[kPartWideKPT];
+    const uint64_t i0 = t0 + (uint64_t)kPartWideKPT * threadIdx.x;
+    if (vec && i0 + kPartWideKPT <= hi) {
+#pragma unroll
+      for (uint32_t q = 0; q < kPartWideKPT / 4; ++q) {
+        const int4 x = __ldcs(reinterpret_cast<const int4*>(keys + i0) + q);
+        k[4 * q] = x.x; k[4 * q + 1] = x.y; k[4 * q + 2] = x.z; k[4 * q + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (uint32_t i = 0; i < kPartWideKPT; ++i) k[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : kBad;
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < kPartWideKPT; ++i) {
+      if (k[i] >= U) k[i] = kBad;  // (bad keys were recorded by the count pass)
+      r[i] = k[i] != kBad ? (uint16_t)atomicAdd(&cnt[k[i] >> kPartShift], 1u) : (uint16_t)0;
+    }
+    __syncthreads();
+    // exclusive scan of the counts over the blocks (2 per thread at 512 threads, B <= 1024)
+    {
+      const uint32_t b0 = 2 * threadIdx.x;
+      const uint32_t c0 = b0 < B ? cnt[b0] : 0u, c1 = b0 + 1 < B ? cnt[b0 + 1] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t>(c0 + c1, tot, red);
+      if (b0 < B) {
+        bstart[b0] = ex;
+        delta[b0] = (int32_t)(gpos[b0] - ex);
+        gpos[b0] += c0;
+        cnt[b0] = 0;
+      }
+      if (b0 + 1 < B) {
+        bstart[b0 + 1] = ex + c0;
+        delta[b0 + 1] = (int32_t)(gpos[b0 + 1] - ex - c0);
+        gpos[b0 + 1] += c1;
+        cnt[b0 + 1] = 0;
+      }
+      if (threadIdx.x == 0) red[33] = tot;
+    }
+    __syncthreads();
+    const uint32_t nvld = red[33];
+#pragma unroll
+    for (uint32_t i = 0; i < kPartWideKPT; ++i)
+      if (k[i] != kBad) stage[bstart[k[i] >> kPartShift] + r[i]] = k[i];
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
+      const uint32_t key = stage[j];
+      __stcs(reinterpret_cast<unsigned short*>(out) + (delta[key >> kPartShift] + (int32_t)j),
+             (unsigned short)(key & 0xffffu));
+    }
+    __syncthreads();  // stage / delta are rewritten by the next sub-tile
   }
   pdl_trigger();
 }
