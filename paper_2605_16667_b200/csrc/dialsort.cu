@@ -722,7 +722,7 @@ int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out,
   if (pass_out) aligned = al(keys) && al(pass_out) && (n % 4 == 0);
   const int v = radix_variant(c, aligned);
   const uint32_t G = (uint32_t)std::max<uint64_t>(
-      1, std::min<uint64_t>(cdiv(n, kR3Tile), (uint64_t)c->nsm * (v == 4 ? c->radix4_occ : c->radix3_occ)));
+      1, std::min<uint64_t>(cdiv(n, v == 4 ? kR4Tile : kR3Tile), (uint64_t)c->nsm * (v == 4 ? c->radix4_occ : c->radix3_occ)));
   if ((rc = c->radix_hist.ensure(8ull * 256 * G + 4 * 256 + 64))) return rc;
   Radix2Ws w;
   w.cnt = c->radix_hist.as<uint32_t>();

@@ -271,11 +271,27 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass3(const uint32_t
 // k+1 is issued as soon as sub-tile k's keys are in registers (after its counting), so it
 // overlaps the ranking and the write-out.  Ranking is the counting atomic itself: its
 // returned value is the key's rank among its warp's keys of the digit (no lane-mask
-// grouping pass).  One stage buffer, ~82 KB (2 CTAs per SM).  Requires src 16-byte aligned.
+// grouping pass).  One stage buffer, ~98 KB (2 CTAs per SM).  Requires src 16-byte aligned.
+// 10240-key sub-tiles with 16-bit per-warp counters (2 CTAs per SM): measured c5 1.335 ms vs
+// 1.418 ms for 8192-key sub-tiles with 32-bit counters; 4096 / 6144-key sub-tiles at 3-4 CTAs
+// per SM were slower (1.53 - 1.88 ms): per-sub-tile fixed costs, not occupancy, bound the pass.
+#ifndef DIALSORT_R4_KPT
+#define DIALSORT_R4_KPT 20
+#endif
+#ifndef DIALSORT_R4_MINB
+#define DIALSORT_R4_MINB 2
+#endif
+#ifndef DIALSORT_R4_W16
+#define DIALSORT_R4_W16 1
+#endif
+
+constexpr int kR4KPT = DIALSORT_R4_KPT;
+constexpr int kR4Tile = kRadixThreads * kR4KPT;
+constexpr bool kR4W16 = DIALSORT_R4_W16 != 0;  // per-warp digit counters as 16-bit halves
 struct Radix4Smem {
-  uint32_t wcur[kRadixWarps][256];   // per-warp digit counts -> slot bases (16 KB)
-  uint32_t sorted[kR3Tile];          // sub-tile sorted by digit (32 KB)
-  uint32_t stage[kR3Tile + 4];       // staged sub-tile (+ alignment shift) (32 KB)
+  uint32_t wcur[kRadixWarps][kR4W16 ? 128 : 256];  // per-warp digit counts -> slot bases
+  uint32_t sorted[kR4Tile];          // sub-tile sorted by digit
+  uint32_t stage[kR4Tile + 4];       // staged sub-tile (+ alignment shift)
   uint32_t dstart[257];
   uint32_t grun[256];
   int32_t gdel[256];                 // grun[d] - dstart[d]: output index of sorted slot j is gdel[d] + j
@@ -284,7 +300,23 @@ struct Radix4Smem {
   uint64_t bar;
 };
 
-__global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t* __restrict__ src,
+// counter of digit d of warp w: a 32-bit word, or one 16-bit half of word d / 2
+__device__ __forceinline__ uint32_t r4_count(Radix4Smem& S, uint32_t w, uint32_t d) {
+  if (kR4W16) {
+    const uint32_t old = atomicAdd(&S.wcur[w][d >> 1], 1u << (16 * (d & 1u)));
+    return (old >> (16 * (d & 1u))) & 0xffffu;
+  }
+  return atomicAdd(&S.wcur[w][d], 1u);
+}
+__device__ __forceinline__ uint32_t r4_get(const Radix4Smem& S, uint32_t w, uint32_t d) {
+  if (kR4W16) return reinterpret_cast<const uint16_t*>(&S.wcur[w][0])[d];
+  return S.wcur[w][d];
+}
+__device__ __forceinline__ void r4_set(Radix4Smem& S, uint32_t w, uint32_t d, uint32_t v) {
+  if (kR4W16) reinterpret_cast<uint16_t*>(&S.wcur[w][0])[d] = (uint16_t)v;
+  else S.wcur[w][d] = v;
+}
+__global__ void __launch_bounds__(kRadixThreads, DIALSORT_R4_MINB) k_radix_pass4(const uint32_t* __restrict__ src,
                                                                    uint32_t* __restrict__ dst, uint32_t n, int p,
                                                                    Radix2Ws w) {
   extern __shared__ __align__(16) unsigned char radix_smem_raw[];
@@ -309,6 +341,9 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
   if (threadIdx.x < 256) S.hnext[threadIdx.x] = 0;
   __syncthreads();
   {
+    // (counting the chunk back to front with L2-normal loads, so that its front is still in L2
+    //  when the scatter starts, measured no faster: 1.3346 vs 1.3337 ms — the scatter is bound
+    //  by shared memory, not by the second read)
     const uint64_t pol = l2_evict_first_policy();
     const uint32_t a4 = min(hi, (lo + 3u) & ~3u), b4 = max(a4, hi & ~3u);
     for (uint32_t i = lo + threadIdx.x; i < a4; i += blockDim.x)
@@ -370,7 +405,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
   // 16-byte aligned body [ab, ae) arrives by one bulk copy at the 16-byte aligned
   // stage + (ab - (t0 & ~3)); the at most 3 keys before ab and after ae are loaded by threads
   auto bounds = [&](uint32_t t0, uint32_t& tn, uint32_t& ab, uint32_t& ae) {
-    tn = min((uint32_t)kR3Tile, hi - t0);
+    tn = min((uint32_t)kR4Tile, hi - t0);
     ab = min(t0 + tn, (t0 + 3u) & ~3u);
     ae = max(ab, (t0 + tn) & ~3u);
   };
@@ -386,10 +421,10 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
   uint32_t phase = 0;
   __syncthreads();
   if (lo < hi) issue(lo);
-  for (uint32_t t0 = lo; t0 < hi; t0 += kR3Tile) {
+  for (uint32_t t0 = lo; t0 < hi; t0 += kR4Tile) {
     uint32_t tn, ab, ae;
     bounds(t0, tn, ab, ae);
-    for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&S.wcur[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kRadixWarps * (kR4W16 ? 128 : 256); i += blockDim.x) (&S.wcur[0][0])[i] = 0;
     const uint32_t sft = t0 & 3u;
     if (threadIdx.x < ab - t0) S.stage[sft + threadIdx.x] = __ldcs(src + t0 + threadIdx.x);
     if (threadIdx.x >= 8 && threadIdx.x - 8 < t0 + tn - ae)
@@ -397,37 +432,37 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
     mbar_wait_sleep(&S.bar, phase);
     phase ^= 1u;
     __syncthreads();  // staged keys (bulk + edges) visible; wcur cleared
-    const uint32_t wseg = warp * 32 * kR3KPT;
+    const uint32_t wseg = warp * 32 * kR4KPT;
     // the returned counter value is the key's rank among its warp's keys of that digit
-    // (< 32 kR3KPT), two ranks per register; slot = the warp's digit base + rank
-    uint32_t k[kR3KPT], rk[kR3KPT / 2];
-    if (wseg + 32 * kR3KPT <= tn) {
+    // (< 32 kR4KPT), two ranks per register; slot = the warp's digit base + rank
+    uint32_t k[kR4KPT], rk[kR4KPT / 2];
+    if (wseg + 32 * kR4KPT <= tn) {
       const uint32_t* sk = S.stage + sft + wseg + lane;
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i) {
+      for (int i = 0; i < kR4KPT; ++i) {
         k[i] = sk[i * 32] ^ flip_in;
-        const uint32_t r = atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u);
+        const uint32_t r = r4_count(S, warp, __byte_perm(k[i], 0, dsel));
         if (i & 1) rk[i >> 1] |= r << 16;
         else rk[i >> 1] = r;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i) {
+      for (int i = 0; i < kR4KPT; ++i) {
         const uint32_t j = wseg + i * 32 + lane;
         k[i] = j < tn ? (S.stage[sft + j] ^ flip_in) : 0u;
-        const uint32_t r = j < tn ? atomicAdd(&S.wcur[warp][__byte_perm(k[i], 0, dsel)], 1u) : 0u;
+        const uint32_t r = j < tn ? r4_count(S, warp, __byte_perm(k[i], 0, dsel)) : 0u;
         if (i & 1) rk[i >> 1] |= r << 16;
         else rk[i >> 1] = r;
       }
     }
     __syncthreads();  // counts complete; the stage buffer is free
-    if (t0 + kR3Tile < hi) issue(t0 + kR3Tile);
+    if (t0 + kR4Tile < hi) issue(t0 + kR4Tile);
     {  // exclusive scan over (digit, warp): thread t has digit t >> 1, warps (t & 1) * 8 .. + 7
       const uint32_t d = threadIdx.x >> 1, w0 = (threadIdx.x & 1u) * (kRadixWarps / 2);
       uint32_t v[kRadixWarps / 2], s = 0;
 #pragma unroll
       for (int j = 0; j < kRadixWarps / 2; ++j) {
-        v[j] = S.wcur[w0 + j][d];
+        v[j] = r4_get(S, w0 + j, d);
         s += v[j];
       }
       uint32_t tot;
@@ -436,26 +471,26 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass4(const uint32_t
       if (threadIdx.x == 0) S.dstart[256] = tot;
 #pragma unroll
       for (int j = 0; j < kRadixWarps / 2; ++j) {
-        S.wcur[w0 + j][d] = ex;
+        r4_set(S, w0 + j, d, ex);
         ex += v[j];
       }
     }
     __syncthreads();
     if (threadIdx.x < 256) S.gdel[threadIdx.x] = (int32_t)(S.grun[threadIdx.x] - S.dstart[threadIdx.x]);
-    if (wseg + 32 * kR3KPT <= tn) {
+    if (wseg + 32 * kR4KPT <= tn) {
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i)
-        S.sorted[S.wcur[warp][__byte_perm(k[i], 0, dsel)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+      for (int i = 0; i < kR4KPT; ++i)
+        S.sorted[r4_get(S, warp, __byte_perm(k[i], 0, dsel)) + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     } else {
 #pragma unroll
-      for (int i = 0; i < kR3KPT; ++i)
+      for (int i = 0; i < kR4KPT; ++i)
         if (wseg + i * 32 + lane < tn)
-          S.sorted[S.wcur[warp][__byte_perm(k[i], 0, dsel)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+          S.sorted[r4_get(S, warp, __byte_perm(k[i], 0, dsel)) + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     }
     __syncthreads();
-    if (tn == (uint32_t)kR3Tile) {  // full sub-tile: unrolled, 32-bit output index (n < 2^32)
+    if (tn == (uint32_t)kR4Tile) {  // full sub-tile: unrolled, 32-bit output index (n < 2^32)
 #pragma unroll
-      for (int r = 0; r < kR3KPT; ++r) {
+      for (int r = 0; r < kR4KPT; ++r) {
         const uint32_t j = r * kRadixThreads + threadIdx.x, u = S.sorted[j];
         __stcs(dst + (uint32_t)(S.gdel[__byte_perm(u, 0, dsel)] + (int32_t)j), u ^ flip_out);
       }
