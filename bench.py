@@ -467,6 +467,8 @@ def main():
     # ---- repetition statistics (the paper reports best of 7 with mean / std / CV):
     # 7 blocks of the same back-to-back steps, each timed on the device (max over ranks)
     nb, kb = 7, max(10, args.steps // 7)
+    if use_batch:  # whole calls of args.batch steps per block
+        kb = max(args.batch, kb // args.batch * args.batch)
     blk = []
     for r in range(nb):
         if G > 1:

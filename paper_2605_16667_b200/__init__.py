@@ -113,8 +113,9 @@ class Context:
         if H.dtype != torch.int32 or not H.is_cuda or not H.is_contiguous():
             raise ValueError("H must be a contiguous int32 (uint32 bits) CUDA tensor")
         if out is None:
-            if n is None:
-                n = int(H.to(torch.int64).sum().item())  # host-side sizing only
+            if n is None:  # ΣH by the library (range-count over the whole universe), read back to size out
+                tot = self.range_count(H, 0, H.numel() - 1)
+                n = int(tot.item())
             out = torch.empty(int(n), dtype=torch.int32, device=H.device)
         cap = out.numel() if n is None else int(n)
         _dev_buf(out, "out", H, cap)

@@ -552,7 +552,8 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
                  uint32_t peerRank = 0) {
   int rc;
   const uint32_t B = (uint32_t)cdiv(U, 1ull << kPartShift);
-  const bool wide = B > kPartMaxBlocks;  // 2^22 < U <= 2^26: per-CTA block counters
+  static const bool force_wide = getenv("DIALSORT_PART_WIDE") != nullptr;  // (A/B only)
+  const bool wide = B > kPartMaxBlocks || force_wide;  // 2^22 < U <= 2^26: per-CTA block counters
   constexpr uint32_t kCtasPerSm = 2048 / kPartThreads;
   const uint32_t Gp = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t)kCtasPerSm * c->nsm, cdiv(n, wide ? kPartWideTile : kPartTile)));

@@ -21,7 +21,9 @@ namespace ds {
 constexpr uint32_t kSmem32MaxBins = 8192;   // 32 KB of uint32 counters
 constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 words)
 constexpr uint32_t kFTileBins = 64;         // scan-tile width of k_sort_fused (ds_fused.cuh)
-constexpr int kHistUnroll = 4;              // int4 loads per batch (2 batches in flight)
+// int4 loads per batch, 2 batches in flight (5 or 6 per batch measured slower: c2 27.4 -> 28.6 /
+// 29.2 us single call, 17.8 -> 18.4 / 18.1 us batched — register pressure at 1024 threads)
+constexpr int kHistUnroll = 4;
 constexpr uint32_t kFOwnVote = 255;         // k_sort_fused: owner-counter slot of the skew vote
 
 // Key layout shared by every pass over `keys`: `head` scalars before the first 16-byte
