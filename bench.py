@@ -309,6 +309,8 @@ def main():
                     help="steps per dialsort_sort_batch_async call (U <= 98304 at N=1; 1 = one sort per call)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: histogram exchange over peer memory (default) or NCCL reduce-scatter")
+    ap.add_argument("--part-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="hierarchical partition (DIALSORT_OPT_PART_MODE): 0 sampled (default), 1 exact (A/B)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.warmup < 3:
@@ -342,6 +344,8 @@ def main():
     lo, hi = rank * n // G, (rank + 1) * n // G
     n_loc = hi - lo
     ctx = dsl.Context(local, max_n=n_loc, max_U=max(U, 256))
+    if args.part_mode:
+        ctx.set_option(dsl._lib.OPT_PART_MODE, args.part_mode)
 
     # ---- inputs: rotation of R copies so that no step's input is L2-resident ------------
     L2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -508,6 +512,38 @@ def main():
         single = {"ms_per_step": sms, "value": n / (sms * 1e-3), "api": "dialsort_sort_async, one step per call",
                   "frac_of_measured": (8 * n + 8 * U) / (sms * 1e-3) / 1e9 / load_peaks()[0]}
 
+    # the single-call steps captured in a CUDA graph (launch overhead out of the
+    # picture for the latency-bound configs); N = 1, U <= 98304
+    graph = None
+    if G == 1 and not radix and U <= 98304:
+        try:
+            gsteps = max(R, min(64, args.steps) // R * R)
+            for i in range(gsteps):  # (workspace sized before capture)
+                step(i)
+            ctx.sync()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for i in range(gsteps):
+                    step(i)
+            torch.cuda.synchronize()
+            reps_g = max(1, args.steps // gsteps)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            gr.replay()
+            torch.cuda.synchronize()
+            g0.record(stream)
+            for _ in range(reps_g):
+                gr.replay()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            ctx.sync()
+            gms = g0.elapsed_time(g1) / (reps_g * gsteps)
+            graph = {"ms_per_step": gms, "value": n / (gms * 1e-3), "steps_per_graph": gsteps, "replays": reps_g,
+                     "api": "dialsort_sort_async per step, captured once (torch.cuda.CUDAGraph) and replayed",
+                     "verified_last_step": check((gsteps - 1) % R)}
+            del gr
+        except Exception as e:  # (reported, never silent)
+            graph = {"error": str(e)[:200]}
+
     ctx.profile(True)
     prof_steps = min(args.steps, 200)
     run(0, prof_steps)
@@ -538,15 +574,17 @@ def main():
         dur_src = (f"timed region: one k_sort_batch launch per {args.batch} steps, back-to-back (CUDA events on "
                    "the launching stream)")
     # algorithmic bytes per launch of each kernel
-    hier = any(nm == "k_part_count" for nm, _ in recs)  # hierarchical path (U > 98304)
+    hier = any(nm in ("k_part_count", "k_part_sample") for nm, _ in recs)  # hierarchical path (U > 98304)
     nblk = max(1, -(-U // 65536))
     kb = {  # k_sort_fused = the whole step (keys read, out written, H and P written + read);
         # hierarchical path: one launch per 65536-bin block, plus the partition kernels
         # hierarchical: blocks hold uint16 keys (2 B read + 4 B written a key); the scatter reads
         # 4 B and writes 2 B a key
         "k_sort_fused": (6 * n_loc // nblk + 8 * 65536) if hier else 8 * n_loc + 8 * U,
-        "k_sort_batch": per_launch_steps * (8 * n_loc + 8 * U),
+        # (hierarchical: one launch holds up to 64 block steps — c4's 16 — 2 B read + 4 B written a key)
+        "k_sort_batch": ((6 * n_loc + 8 * U) // -(-nblk // 64)) if hier else per_launch_steps * (8 * n_loc + 8 * U),
         "k_part_count": 4 * n_loc, "k_part_scatter": 6 * n_loc, "k_part_scan": 0,
+        "k_part_scatter_est": 6 * n_loc, "k_part_sample": 0, "k_part_fin": 0,
         # two-kernel pipeline: fused ingest+merge+scan (keys read + H and P written), expand
         "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
         "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),
@@ -586,6 +624,8 @@ def main():
         xh.copy_(ins[0][:n].cpu())
         ohs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
         ctxs = [ctx, dsl.Context(local, max_n=n, max_U=max(U, 256))]
+        if args.part_mode:
+            ctxs[1].set_option(dsl._lib.OPT_PART_MODE, args.part_mode)
         sts = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
         for c in range(2):  # warm-up (and the staging buffers)
             with torch.cuda.stream(sts[c]):
@@ -624,7 +664,7 @@ def main():
             "l2": f"input/output rotation over {R} copies ({R * step_bytes / 2**20:.0f} MB > 3x L2)",
             "mode": (f"batched: dialsort_sort_batch_async, {args.batch} steps per call (one launch, CTA groups)"
                      if use_batch else "one step per call"),
-            "single_call": single,
+            "single_call": single, "cuda_graph": graph,
             "roofline": roof, "step_roofline": step_roof, "reps": reps, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary(),
             "verified": verified, "verified_last_step": verified_last,

@@ -23,6 +23,8 @@
  *     after such an error the contents of H / out are unspecified.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *   - A context may be used by one host thread / stream at a time (no internal locking).
+ *   - The single-GPU entries keep their sequencing state on the device, so a CUDA graph that
+ *     captured them replays correctly (after one uncaptured call has sized the workspace).
  */
 #ifndef DIALSORT_H_
 #define DIALSORT_H_
@@ -88,13 +90,19 @@ int dialsort_sync(dialsort_ctx ctx, dialsort_stream_t stream, dialsort_error_inf
  *     device in one FIFO (a launch on another stream than the previous one waits for that stream's
  *     enqueued work), so two of them never overlap; 1: cudaLaunchAttributeCooperative, which also
  *     rejects a grid another tenant keeps from being co-resident (DIALSORT_E_CUDA) at ~2 us per
- *     launch. */
+ *     launch.
+ *   DIALSORT_OPT_PART_MODE (read / write): the hierarchical path's partition (98304 < U <= 2^22).
+ *     0 (default): sampled — a 65536-key stratified sample sizes each universe block's key
+ *     region (estimate + 6 sigma), one pass places the keys, and a region overflow runs the exact
+ *     schedule on the device (no host round trip); 1: exact — a count pass, then the placement;
+ *     2: sampled without margins (overflows: exercises the exact schedule behind it; tests). */
 #define DIALSORT_OPT_RADIX_VARIANT 1
 #define DIALSORT_OPT_RADIX_PROBE_VIOLATIONS 2
 #define DIALSORT_OPT_RADIX_ACTIVE 3
 #define DIALSORT_OPT_NUM_SMS 4
 #define DIALSORT_OPT_COOPERATIVE 5
 #define DIALSORT_OPT_MAX_CTAS 6
+#define DIALSORT_OPT_PART_MODE 7
 int dialsort_ctx_set_option(dialsort_ctx ctx, int option, int64_t value);
 int dialsort_ctx_get_option(dialsort_ctx ctx, int option, int64_t* value);
 
@@ -189,7 +197,9 @@ int dialsort_sort_host_async(dialsort_ctx ctx, const int32_t* keys_host, uint64_
  * tagged with the call's epoch, two parities of every buffer), mapped into every rank either by
  * CUDA IPC (one process per GPU: exchange the DIALSORT_COMM_HANDLE_BYTES handle bytes with any host
  * channel, e.g. torch.distributed.all_gather_object) or by pointer (several communicators of one
- * process).  All ranks must issue the same sequence of sharded calls.  There is no host barrier:
+ * process).  All ranks must issue the same sequence of sharded calls (they are sequenced by host-side
+ * call epochs, so — unlike the single-GPU entries — they must not be captured in a CUDA graph).
+ * There is no host barrier:
  * a rank's kernels wait on device flags for its peers (giving up after 20 s: DIALSORT_E_COMM at the
  * next dialsort_sync).  Calls on one communicator must be serialised on one stream.
  *

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_DIR, f"libdialsort_{_VARIANT}.so" if _VARIANT else "lib
 # dialsort_status
 OK, E_INVALID_ARG, E_KEY_RANGE, E_SIZE, E_OVERFLOW, E_CUDA, E_COMM, E_NOMEM = 0, 1, 2, 3, 4, 5, 6, 7
 # context options, query ops, communicator handle size (include/dialsort.h)
-OPT_RADIX_VARIANT, OPT_RADIX_PROBE_VIOLATIONS, OPT_RADIX_ACTIVE, OPT_NUM_SMS, OPT_COOPERATIVE, OPT_MAX_CTAS = 1, 2, 3, 4, 5, 6
+(OPT_RADIX_VARIANT, OPT_RADIX_PROBE_VIOLATIONS, OPT_RADIX_ACTIVE, OPT_NUM_SMS, OPT_COOPERATIVE, OPT_MAX_CTAS,
+ OPT_PART_MODE) = 1, 2, 3, 4, 5, 6, 7
 Q_FREQUENCY, Q_PRESENCE, Q_RANGE_COUNT = 0, 1, 2
 COMM_HANDLE_BYTES = 128
 

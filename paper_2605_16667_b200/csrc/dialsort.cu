@@ -56,13 +56,14 @@ enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
   KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
   KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
-  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_COUNT
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {
     "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
     "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_scatter",
     "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
-    "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch"};
+    "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch", "k_part_sample",
+    "k_part_scatter_est", "k_part_fin"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -101,9 +102,10 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
+  static const int pdl = getenv("DIALSORT_NO_PDL") ? 0 : 1;  // (debug: launches without PDL)
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl;
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
@@ -117,12 +119,22 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   if (COOP && !g_coop_attr && !no_fifo) {  // wait for the previous co-resident launch if it is on another stream
     int dev = 0;
     cudaGetDevice(&dev);
-    fifo = &g_fifo[dev & 31];
-    lk = std::unique_lock<std::mutex>(fifo->mu);
-    if (!fifo->ev) cudaEventCreateWithFlags(&fifo->ev, cudaEventDisableTiming);
-    if (fifo->any && fifo->last != s) cudaStreamWaitEvent(s, fifo->ev, 0);
-    fifo->any = true;
-    fifo->last = s;
+    CoopFifo* f = &g_fifo[dev & 31];
+    lk = std::unique_lock<std::mutex>(f->mu);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (cap != cudaStreamCaptureStatusNone) {
+      // (a stream being captured into a graph may not wait on an event recorded outside the
+      //  capture, nor leave one for uncaptured streams: the graph's launches are ordered by the
+      //  graph itself; the FIFO restarts after it)
+      f->any = false;
+    } else {
+      fifo = f;
+      if (!f->ev) cudaEventCreateWithFlags(&f->ev, cudaEventDisableTiming);
+      if (f->any && f->last != s) cudaStreamWaitEvent(s, f->ev, 0);
+      f->any = true;
+      f->last = s;
+    }
   }
   // (and the event marks this launch for the next one: recorded after it, on its stream)
   struct FifoMark {
@@ -201,17 +213,18 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      fused_tiles, Hx, part, htmp, qtmp;
+      fused_tiles, Hx, part, htmp, qtmp, psamp;
   DevStatus* host_status = nullptr;  // pinned mirror
-  uint64_t fused_seq = 0;            // k_sort_fused launches (parity of the tile-total buffers)
-  unsigned long long bar64_base = 0; // value of the monotonic barrier counter after the last launch
-  unsigned long long qbar_base = 0;  // the same for the query kernels' barrier counter
+  // gridbar layout: [0] GridBar of k_scan, [32] GridBarR of the radix passes, [64] FusedState of
+  // the fused step, [128] GridBar of the query kernels (all zero at creation)
+  FusedState* fused_state() { return reinterpret_cast<FusedState*>(gridbar.as<char>() + 64); }
   Profiler prof;
   int expand_occ = 4, scan_occ = 2, radix3_occ = 1, radix4_occ = 1;
   long long probe_violations = -1;   // radix lane-order probe of this device
   int radix_force = 0;               // 0: auto (pass4 iff the probe passed), 3 / 4 forced
   bool coop_attr = false;            // DIALSORT_OPT_COOPERATIVE
   uint32_t max_ctas = 0;             // DIALSORT_OPT_MAX_CTAS (0: every SM)
+  int part_mode = 0;                 // DIALSORT_OPT_PART_MODE
   // batched sort (dialsort_sort_batch_async): one workspace lane per CTA group, created lazily;
   // their deferred errors are merged by dialsort_sync of this context
   dialsort_ctx lanes[kMaxLanes] = {};
@@ -289,7 +302,8 @@ int ctx_init(dialsort_ctx c) {
   clean.ovf_epoch = ~0u;
   DS_CUDA(cudaMemcpy(c->status.p, &clean, sizeof(clean), cudaMemcpyHostToDevice));
   if ((rc = c->ws_total.ensure(64, true))) return rc;
-  if ((rc = c->gridbar.ensure(64, true))) return rc;
+  if ((rc = c->gridbar.ensure(256, true))) return rc;
+  if ((rc = c->psamp.ensure(8ull * kPartMaxBlocks, true))) return rc;
   if ((rc = c->range_tot.ensure(8ull * 8 * c->nsm, true))) return rc;
   // k_sort_fused: tile totals (2 parities), fallback tile totals
   if ((rc = c->fused_tiles.ensure(4ull * kFusedTileWords, true))) return rc;
@@ -432,10 +446,17 @@ int build_fused_args(dialsort_ctx c, ScanArgs& a, int& fmt, uint32_t& C, size_t&
   const uint32_t W = pack ? (U + 1) / 2 : U;
   const uint32_t ldw = (uint32_t)round_up(W, 8);  // shared-memory histogram words
   const uint64_t n4 = n / 4 + 1;
-  // CTAs: enough for the keys (8 vectors per thread), and at least one per 1024 bins — every CTA
-  // flushes and merges O(U) words whatever the grid, but the merge's batches (16 tiles of 64
-  // bins each) run one after another: U = 65536 on one CTA took 64 batches (~330 us at n = 1e4)
-  const uint64_t want = std::max<uint64_t>(cdiv(n4, 1024ull * kHistUnroll * 2), cdiv(U, 1024));
+  // CTAs: one per 4096 keys (4 per thread), and at least one per 1024 bins — every CTA flushes
+  // and merges O(U) words whatever the grid, but the merge's batches (16 tiles of 64 bins each)
+  // run one after another: U = 65536 on one CTA took 64 batches (~330 us at n = 1e4).  4096 keys
+  // per CTA against round 1's 32768 (tools/kpc_ab.py, single-call device time): n = 1e5 U = 256
+  // 14.8 -> 13.9 us, n = 1e6 18.9 -> 15.1, n = 1e4 U = 1024 28.6 -> 15.7, n = 1e6 U = 65536
+  // skewed 27.9 -> 22.3; n >= 6e5 uses every SM either way.
+  static const uint64_t kpc = [] {  // keys per CTA the grid is sized for (DIALSORT_FUSED_KPC: A/B only)
+    const char* e = getenv("DIALSORT_FUSED_KPC");
+    return e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 4096ull;
+  }();
+  const uint64_t want = std::max<uint64_t>(cdiv(4 * n4, kpc), cdiv(U, 1024));
   const uint64_t cmax = std::min<uint64_t>(c->max_ctas ? std::min<uint32_t>(c->max_ctas, c->nsm) : c->nsm,
                                            kFMaxRows);  // rows a staging slot holds
   C = C_force ? C_force : (uint32_t)(want < cmax ? (want ? want : 1) : cmax);
@@ -460,23 +481,15 @@ int build_fused_args(dialsort_ctx c, ScanArgs& a, int& fmt, uint32_t& C, size_t&
   a.tsums = nullptr;
   a.fused = 1;
   a.ctr_stride = kTileTotStride;
-  // per-tile ready flags (share mode), two parities: each step clears the other one, so a flag
-  // never holds a value from an earlier step (the epoch wraps after 2^24 steps)
-  uint32_t* rdy = ft;
-  a.ready = rdy + kFTileSlots * (c->fused_seq & 1);
-  a.ready_clear = rdy + kFTileSlots * ((c->fused_seq + 1) & 1);
-  uint32_t* ownb = rdy + 2 * kFTileSlots;
-  const uint64_t own_words = (uint64_t)kFOwnSlots * kTileTotStride;  // per parity
-  a.own_red = ownb + own_words * (c->fused_seq & 1);
-  a.own_clear = ownb + own_words * ((c->fused_seq + 1) & 1);
-  a.own_alt = ownb + 2 * own_words;
-  // exception histogram of the 4-bit rows: parity buffers, the other one cleared by every step
-  a.Hx = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * (c->fused_seq & 1);
-  a.Hx_clear = c->Hx.as<uint32_t>() + (uint64_t)kSmem16MaxBins * ((c->fused_seq + 1) & 1);
-  a.bar64 = reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 16);
-  a.bar_base = c->bar64_base;
-  c->fused_seq++;
-  c->bar64_base += (uint64_t)bars * C;  // barriers reserved (the overflow one is skipped unless needed)
+  // two-parity workspaces (per-tile ready flags, owner counters, the 4-bit rows' exception
+  // histogram): each step uses parity seq & 1 and clears the other one; the parity, the epoch and
+  // the barrier base are derived on the device from the workspace's FusedState (sort_step)
+  a.ready_base = ft;
+  a.own_base = ft + 2 * kFTileSlots;
+  a.Hx_base = c->Hx.as<uint32_t>();
+  a.fstate = c->fused_state();
+  a.bar64 = &a.fstate->bar;
+  (void)bars;
   return DIALSORT_OK;
 }
 
@@ -484,7 +497,8 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
                        uint32_t epoch, cudaStream_t s, int32_t key_base = 0, const uint64_t* d_n = nullptr,
                        const uint64_t* d_off = nullptr, int kb = 4, bool hist_only = false,
                        uint32_t* const* Hpeer = nullptr, uint32_t peerL = 0, uint32_t peerRank = 0,
-                       uint32_t bin_base = 0, const uint32_t* enc = nullptr, const int32_t* dec = nullptr) {
+                       uint32_t bin_base = 0, const uint32_t* enc = nullptr, const int32_t* dec = nullptr,
+                       const uint64_t* d_koff = nullptr) {
   int rc;
   ScanArgs a;
   int fmt;
@@ -493,6 +507,7 @@ int enqueue_sort_fused(dialsort_ctx c, const void* keys, uint64_t n, uint32_t U,
   if ((rc = build_fused_args(c, a, fmt, C, smem, n, U, H, epoch, d_n, d_off, kb, hist_only, Hpeer, peerL, peerRank,
                              bin_base, enc, dec, 0, 2)))
     return rc;
+  a.d_koff = d_koff;
 #define DS_LAUNCH_FUSED(F, K) \
   DS_CUDA(launch_k<true>(KID_SORT_FUSED, k_sort_fused<F, K>, dim3(C), dim3(1024), smem, s, keys, n, a, out, key_base))
   if (fmt == kRowN4) {
@@ -557,23 +572,42 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
   constexpr uint32_t kCtasPerSm = 2048 / kPartThreads;
   const uint32_t Gp = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t)kCtasPerSm * c->nsm, cdiv(n, wide ? kPartWideTile : kPartTile)));
-  if ((rc = c->part.ensure(4ull * Gp * B + 16ull * B + 64))) return rc;
-  if ((rc = c->htmp.ensure(2ull * n + 16))) return rc;  // uint16 block keys
+  // sampled schedule (default for up to 64 blocks): the keys' regions in tmp carry the
+  // estimate's margins (at most n / 4 + 512 B extra keys)
+  // (+ a 4096-key trash area for the runs of an overflowed region; positions stay below 2^32)
+  const uint64_t tcap = n + n / 4 + 512ull * B;
+  const bool sampled = !wide && c->part_mode != 1 && tcap + kPartTile < (1ull << 32);
+  if ((rc = c->part.ensure(4ull * Gp * B + 160ull * B + 64))) return rc;
+  if ((rc = c->htmp.ensure(2ull * (sampled ? tcap + kPartTile : n) + 16))) return rc;  // uint16 block keys
   PartWs w;
   w.bsz = c->part.as<uint64_t>();
   w.boff = w.bsz + B;
-  w.cnt = reinterpret_cast<uint32_t*>(w.boff + B);
+  w.koff = w.boff + B;
+  w.cap = w.koff + B;
+  w.fill = reinterpret_cast<uint32_t*>(w.cap + B);
+  w.ovf = w.fill + (uint64_t)kFillStride * B;
+  w.cnt = w.ovf + 16;
   w.st = c->status.as<DevStatus>();
   uint16_t* tmp = c->htmp.as<uint16_t>();
   if (wide) {
     DS_CUDA(launch_k(KID_PART_COUNT, k_part_count_wide, dim3(Gp), dim3(kPartThreads), 4ull * B, s, keys, n, U, B, w));
-    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
+    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w, (const uint32_t*)nullptr));
     DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter_wide, dim3(Gp), dim3(kPartThreads), part_wide_smem(B), s, keys,
                      n, U, B, w, tmp));
   } else {
-    DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w));
-    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w));
-    DS_CUDA(launch_k(KID_PART_SCATTER, k_part_scatter, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, tmp));
+    const uint32_t* gate = nullptr;
+    if (sampled) {  // (part_mode 2: no margins — overflows, tests the exact schedule behind it)
+      DS_CUDA(launch_k(KID_PART_SAMPLE, k_part_sample, dim3(kSampleCtas), dim3(kSampleThreads), 0, s, keys, n, U, B,
+                       w, c->part_mode == 2 ? (uint64_t)0 : tcap, c->psamp.as<uint32_t>()));
+      DS_CUDA(launch_k(KID_PART_SCATTER_EST, k_part_place<true>, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w,
+                       tmp, (const uint32_t*)nullptr, (uint32_t)tcap));
+      DS_CUDA(launch_k(KID_PART_FIN, k_part_fin, dim3(1), dim3(1024), 0, s, B, w));
+      gate = w.ovf;  // the exact schedule below runs only after an overflow
+    }
+    DS_CUDA(launch_k(KID_PART_COUNT, k_part_count, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w, gate));
+    DS_CUDA(launch_k(KID_PART_SCAN, k_part_scan, dim3(1), dim3(1024), 0, s, Gp, B, w, gate));
+    DS_CUDA(launch_k(KID_PART_SCATTER, k_part_place<false>, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w,
+                     tmp, gate, 0u));
   }
   // the block steps: the full 65536-bin blocks overlapped on CTA groups, up to kBatchMax per
   // k_sort_batch launch (their HBM phases overlap the others' merges, as the batched sort); a
@@ -611,6 +645,7 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
                                    w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift, nullptr, nullptr,
                                    Gg, 3)))
           return rc;
+        BA.a[j].d_koff = w.koff + b;
         BA.keys[j] = tmp;
         BA.n[j] = nb_hint;
         BA.out[j] = out;
@@ -629,7 +664,8 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
     const uint32_t epoch = next_epoch(c);  // each block launch has its own ready-flag epoch
     uint32_t* Hb = H ? H + ((uint64_t)b << kPartShift) : nullptr;
     if ((rc = enqueue_sort_fused(c, tmp, nb_hint, Ub, Hb, out, epoch, s, (int32_t)(b << kPartShift), w.bsz + b,
-                                 w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift)))
+                                 w.boff + b, 2, hist_only, Hpeer, peerL, peerRank, b << kPartShift, nullptr, nullptr,
+                                 w.koff + b)))
       return rc;
   }
   return DIALSORT_OK;
@@ -848,7 +884,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
     }
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
                   &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->fused_tiles, &c->Hx,
-                  &c->part, &c->htmp, &c->qtmp})
+                  &c->part, &c->htmp, &c->qtmp, &c->psamp})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt && c->owns_pt) cudaFree(c->pt);
@@ -871,6 +907,10 @@ int dialsort_ctx_set_option(dialsort_ctx c, int option, int64_t value) {
       if (value < 0 || value > 1024) return fail(DIALSORT_E_INVALID_ARG, "max CTAs: 0..1024");
       c->max_ctas = (uint32_t)value;
       return DIALSORT_OK;
+    case DIALSORT_OPT_PART_MODE:
+      if (value < 0 || value > 2) return fail(DIALSORT_E_INVALID_ARG, "partition mode: 0, 1 or 2");
+      c->part_mode = (int)value;
+      return DIALSORT_OK;
     default:
       return fail(DIALSORT_E_INVALID_ARG, "unknown or read-only option");
   }
@@ -885,6 +925,7 @@ int dialsort_ctx_get_option(dialsort_ctx c, int option, int64_t* value) {
     case DIALSORT_OPT_NUM_SMS: *value = c->nsm; return DIALSORT_OK;
     case DIALSORT_OPT_COOPERATIVE: *value = c->coop_attr ? 1 : 0; return DIALSORT_OK;
     case DIALSORT_OPT_MAX_CTAS: *value = c->max_ctas; return DIALSORT_OK;
+    case DIALSORT_OPT_PART_MODE: *value = c->part_mode; return DIALSORT_OK;
     default: return fail(DIALSORT_E_INVALID_ARG, "unknown option");
   }
 }
@@ -1172,9 +1213,8 @@ int dialsort_query_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int op, 
     if ((rc2 = c->qtmp.ensure(8ull * (U + 1 + c->nsm) + 64))) return rc2;
     uint64_t* pre = c->qtmp.as<uint64_t>();
     const uint32_t g = (uint32_t)std::min<uint64_t>(c->nsm, cdiv(U, 4096));
-    c->qbar_base += g;
     DS_CUDA(launch_k<true>(KID_QUERY, k_query_prefix, dim3(g), dim3(1024), 0, s, H, U, pre,
-                           reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 48), c->qbar_base));
+                           reinterpret_cast<GridBar*>(c->gridbar.as<char>() + 128)));
     DS_CUDA(launch_k(KID_QUERY, k_query_range, dim3((uint32_t)std::min<uint64_t>(cdiv(m, 256), 4ull * c->nsm)),
                      dim3(256), 0, s, (const uint64_t*)pre, U, q, m, d_out, c->status.as<DevStatus>()));
     return DIALSORT_OK;
@@ -1195,10 +1235,9 @@ int dialsort_support_set_async(dialsort_ctx c, const uint32_t* H, uint32_t U, ui
   DS_CUDA(cudaSetDevice(c->device));
   const uint32_t grid = (uint32_t)std::min<uint64_t>(c->nsm, cdiv(U, 4096));
   if ((rc = c->qtmp.ensure(8ull * (grid + 1) + 64))) return rc;
-  c->qbar_base += grid;
   DS_CUDA(launch_k<true>(KID_QUERY, k_support_set, dim3(grid), dim3(1024), 0, s, H, U, D_out,
                          reinterpret_cast<unsigned long long*>(d_count), d_iso, c->qtmp.as<unsigned long long>(),
-                         reinterpret_cast<unsigned long long*>(c->gridbar.as<char>() + 48), c->qbar_base));
+                         reinterpret_cast<GridBar*>(c->gridbar.as<char>() + 128)));
   return DIALSORT_OK;
 }
 

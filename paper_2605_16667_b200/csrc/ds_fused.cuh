@@ -390,21 +390,41 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
 // FROM_H (reconstruct_step): no keys — the step projects a given histogram H (a.partials = H as
 // the single u32 "row", a.C = 1): each CTA sums its own tiles of H and adds its total into the
 // owner counters P_{o+1} of every owner o >= b instead of ingesting and flushing.
+// (fbase, fseq: the step's barrier base and sequence number, from FusedState; fs_adv: the state
+//  CTA 0 advances to {adv_base, adv_seq} once the first barrier shows every CTA has read it — no
+//  exit ticket, and the next launch reads it after this grid completes)
 template <int FMT, int KB, bool FROM_H = false>
-__device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_t n, const ScanArgs& a,
+__device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_t n, const ScanArgs& a_in,
                                           int32_t* __restrict__ out, int32_t key_base, VGrid vg, uint32_t* sh,
-                                          uint64_t* red64, uint32_t* wsum) {
+                                          uint64_t* red64, uint32_t* wsum, unsigned long long fbase, uint32_t fseq,
+                                          FusedState* fs_adv = nullptr, unsigned long long adv_base = 0,
+                                          uint32_t adv_seq = 0) {
+  // the step's parity buffers, epoch and barrier base (derived from the device-side sequence)
+  ScanArgs a = a_in;
+  {
+    const uint32_t par = fseq & 1u;
+    const uint64_t own_words = (uint64_t)kFOwnSlots * kTileTotStride;
+    a.own_red = a.own_base + own_words * par;
+    a.own_clear = a.own_base + own_words * (par ^ 1u);
+    a.own_alt = a.own_base + 2 * own_words;
+    a.ready = a.ready_base + (uint64_t)kFTileSlots * par;
+    a.ready_clear = a.ready_base + (uint64_t)kFTileSlots * (par ^ 1u);
+    a.Hx = a.Hx_base + (uint64_t)kSmem16MaxBins * par;
+    a.Hx_clear = a.Hx_base + (uint64_t)kSmem16MaxBins * (par ^ 1u);
+    a.epoch = (fseq % 0xffffffu) + 1u;
+    a.bar_base = fbase;
+  }
   // (KB: key bytes — 4 int32 keys; 2 uint16 keys, the hierarchical path's universe blocks or a
   //  2-byte coded domain; 1 uint8 keys, a 1-byte coded domain)
   // (keys, out, n are adjusted below for hierarchical blocks)
   uint64_t n_exp = a.n_expected;
   if (a.d_n) {  // a universe block of the hierarchical path: size and offset on the device
-    __shared__ uint64_t s_noff[2];  // (one load per CTA, not one per thread: a 148k-way fan-in)
-    if (threadIdx.x == 0) s_noff[0] = *a.d_n, s_noff[1] = *a.d_off;
+    __shared__ uint64_t s_noff[3];  // (one load per CTA, not one per thread: a 148k-way fan-in)
+    if (threadIdx.x == 0) s_noff[0] = *a.d_n, s_noff[1] = *a.d_off, s_noff[2] = a.d_koff ? *a.d_koff : s_noff[1];
     __syncthreads();
     const uint64_t off = s_noff[1];
     n = s_noff[0];
-    keys = static_cast<const char*>(keys) + off * KB;
+    keys = static_cast<const char*>(keys) + s_noff[2] * KB;
     out += off;
     n_exp = n;
   }
@@ -451,6 +471,10 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
   grid_barrier_mono_side(a.bar64, a.bar_base + G, [&] {  // rows, tile / owner totals, overflow fallback in L2
     my_tiles(ntiles, s_own[0], s_own[1], vg);
   });
+  if (fs_adv && b == 0 && threadIdx.x == 0) {
+    fs_adv->base = adv_base;
+    fs_adv->seq = adv_seq;
+  }
   phase_mark(a.pt, 3);
 
   const uint32_t tb0 = s_own[0], tb1 = s_own[1];  // tiles this CTA merges
@@ -708,15 +732,28 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
 
 
 
+// Start of a launch: every CTA reads the workspace's barrier base and step sequence.
+__device__ __forceinline__ void fused_state_read(const FusedState* fs, unsigned long long* s2) {
+  if (threadIdx.x == 0) {
+    s2[0] = *reinterpret_cast<const volatile unsigned long long*>(&fs->base);
+    s2[1] = *reinterpret_cast<const volatile unsigned int*>(&fs->seq);
+  }
+  __syncthreads();
+}
 template <int FMT, int KB = 4>
 __global__ void __launch_bounds__(1024, 1) k_sort_fused(const void* __restrict__ keys, uint64_t n, ScanArgs a,
                                                        int32_t* __restrict__ out, int32_t key_base) {
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
   __shared__ uint32_t wsum[32];
+  __shared__ unsigned long long s_fs[2];
   pdl_wait();
   phase_mark(a.pt, -1);
-  sort_step<FMT, KB>(keys, n, a, out, key_base, vgrid_hw(), sh, red64, wsum);
+  fused_state_read(a.fstate, s_fs);
+  const unsigned long long base = s_fs[0];
+  const uint32_t seq = (uint32_t)s_fs[1];
+  sort_step<FMT, KB>(keys, n, a, out, key_base, vgrid_hw(), sh, red64, wsum, base, seq, a.fstate,
+                     base + 2ull * gridDim.x, seq + 1);
   pdl_trigger();
 }
 
@@ -728,8 +765,13 @@ __global__ void __launch_bounds__(1024, 1) k_reconstruct_fused(ScanArgs a, uint6
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
   __shared__ uint32_t wsum[32];
+  __shared__ unsigned long long s_fs[2];
   pdl_wait();
-  sort_step<kRowU32, 4, true>(nullptr, cap, a, out, key_base, vgrid_hw(), sh, red64, wsum);
+  fused_state_read(a.fstate, s_fs);
+  const unsigned long long base = s_fs[0];
+  const uint32_t seq = (uint32_t)s_fs[1];
+  sort_step<kRowU32, 4, true>(nullptr, cap, a, out, key_base, vgrid_hw(), sh, red64, wsum, base, seq, a.fstate,
+                              base + 2ull * gridDim.x, seq + 1);
   pdl_trigger();
 }
 
@@ -761,13 +803,22 @@ __global__ void __launch_bounds__(1024, 1) k_sort_batch(const __grid_constant__ 
   extern __shared__ __align__(128) uint32_t sh[];
   __shared__ uint64_t red64[34];
   __shared__ uint32_t wsum[32];
+  __shared__ unsigned long long s_fs[2];
   pdl_wait();
   const uint32_t g = blockIdx.x / B.Gg;
   const VGrid vg{B.Gg, blockIdx.x % B.Gg};
-  for (uint32_t j = g; j < B.nb; j += B.L) {
+  FusedState* fs = B.a[g].fstate;  // the group's workspace lane
+  fused_state_read(fs, s_fs);
+  const unsigned long long base = s_fs[0];
+  const uint32_t seq = (uint32_t)s_fs[1];
+  const uint32_t steps = g < B.nb ? (B.nb - g + B.L - 1) / B.L : 0u;  // this group's batches
+  uint32_t k = 0;  // this group's steps so far
+  for (uint32_t j = g; j < B.nb; j += B.L, ++k) {
     const ScanArgs& a = B.a[j];
-    sort_step<FMT, KB>(B.keys[j], B.n[j], a, B.out[j], B.key_base[j], vg, sh, red64, wsum);
-    grid_barrier_mono(a.bar64, a.bar_base + 3ull * B.Gg);  // batch done by every CTA of the group
+    const unsigned long long bj = base + 3ull * B.Gg * k;
+    sort_step<FMT, KB>(B.keys[j], B.n[j], a, B.out[j], B.key_base[j], vg, sh, red64, wsum, bj, seq + k,
+                       k == 0 ? fs : nullptr, base + 3ull * B.Gg * steps, seq + steps);
+    grid_barrier_mono(a.bar64, bj + 3ull * B.Gg);  // batch done by every CTA of the group
   }
   pdl_trigger();
 }

@@ -11,10 +11,18 @@
 // 10 bytes per key of streaming traffic (count read 4, scatter read 4 + write 2: the blocks
 // hold their keys' low 16 bits as uint16) plus the shared-memory path of each block.
 //
-//   k_part_count    per-CTA chunk: block counts (per-warp shared counters)      [G][B]
-//   k_part_scan     exclusive offsets off[c][b] (block-major), block sizes and starts
-//   k_part_scatter  per-CTA chunk again, 4096-key sub-tiles staged in shared memory by
-//                   block and written as contiguous runs at the CTA's offsets
+// Two schedules place the blocks' keys (U <= 2^22, up to 64 blocks):
+//   sampled (default): 6 bytes per key, one pass over the keys
+//     k_part_sample   a stratified sample of 65536 keys -> each block's key-region capacity
+//                     (estimate + 6 sigma) and start in tmp
+//     k_part_place<true>  4096-key sub-tiles staged by block; each run claims its place in
+//                     its block's region with one global atomic (regions fill densely; a
+//                     region that would overflow sets ovf and drops the run)
+//     k_part_fin      block sizes and output starts from the fills (skipped after ovf)
+//   exact (after ovf — gated on it, no host round trip — or DIALSORT_OPT_PART_MODE = 1):
+//     k_part_count    per-CTA chunk: block counts (per-warp shared counters)      [G][B]
+//     k_part_scan     exclusive offsets off[c][b] (block-major), block sizes and starts
+//     k_part_place<false>  per-CTA chunk again, runs written at the CTA's offsets
 #pragma once
 #include "ds_common.cuh"
 
@@ -30,12 +38,23 @@ constexpr uint32_t kPartThreads = DIALSORT_PART_THREADS;
 constexpr uint32_t kPartKPT = 8;            // keys per thread per scatter sub-tile
 constexpr uint32_t kPartTile = kPartThreads * kPartKPT;  // 4096
 
+constexpr uint32_t kPartSample = 65536;     // keys sampled for the block-size estimate
+constexpr uint32_t kFillStride = 32;        // one 128-byte line per block's fill counter
 struct PartWs {
   uint32_t* cnt;   // [G][B] block counts of each CTA chunk, then offsets (in place)
   uint64_t* bsz;   // [B] block sizes
-  uint64_t* boff;  // [B] block starts
+  uint64_t* boff;  // [B] block starts in the output
   DevStatus* st;
+  uint64_t* koff;  // [B] block key-region starts in tmp (= boff on the exact schedule)
+  uint64_t* cap;   // [B] sampled schedule: region capacities
+  uint32_t* fill;  // [B * kFillStride] sampled schedule: keys placed per block so far
+  uint32_t* ovf;   // sampled schedule: a region overflowed -> the exact schedule runs
 };
+// Gate of the exact schedule's kernels when they back up the sampled one: run only after an
+// overflow (nullptr: always run).
+__device__ __forceinline__ bool part_gated_off(const uint32_t* gate) {
+  return gate && *reinterpret_cast<const volatile uint32_t*>(gate) == 0u;
+}
 
 // Chunk [lo, hi) of CTA c in a grid of G over n keys.  Interior cuts sit on 256-byte
 // boundaries of the key array (64 keys past its first 16-byte aligned element), so every
@@ -55,10 +74,16 @@ __device__ __forceinline__ void part_chunk(const int32_t* keys, uint64_t n, uint
   hi = cut(blockIdx.x + 1);
 }
 
+// (gate: see part_gated_off; a gated run does not record bad keys again — the sampled
+//  scatter did)
 __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
-                                                             uint32_t B, PartWs w) {
+                                                             uint32_t B, PartWs w, const uint32_t* gate) {
   __shared__ uint32_t wcnt[kPartThreads / 32][kPartMaxBlocks];
   pdl_wait();
+  if (part_gated_off(gate)) {
+    pdl_trigger();
+    return;
+  }
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < (kPartThreads / 32) * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
@@ -67,7 +92,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __re
   uint32_t* wc = wcnt[warp];
   auto one = [&](uint32_t k, uint64_t idx) {
     if (k < U) atomicAdd(&wc[k >> kPartShift], 1u);
-    else record_bad(w.st, idx, k);
+    else if (!gate) record_bad(w.st, idx, k);
   };
   // 16-byte aligned interior as int4, scalar head / tail
   const uint64_t mis = (reinterpret_cast<uintptr_t>(keys + lo) >> 2) & 3u;
@@ -113,9 +138,13 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int32_t* __re
 
 // One CTA: off[c][b] = start(b) + Σ_{c' < c} cnt[c'][b], start(b) = Σ_{b' < b} size(b')
 // (B <= 1024 blocks: thread b owns column b; one block scan of the sizes gives the starts).
-__global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, PartWs w) {
+__global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, PartWs w, const uint32_t* gate) {
   __shared__ unsigned long long red[34];
   pdl_wait();
+  if (part_gated_off(gate)) {
+    pdl_trigger();
+    return;
+  }
   unsigned long long sz = 0;
   if (threadIdx.x < B)
     for (uint32_t c = 0; c < G; ++c) sz += w.cnt[(uint64_t)c * B + threadIdx.x];
@@ -124,6 +153,7 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
   if (threadIdx.x < B) {
     w.bsz[threadIdx.x] = sz;
     w.boff[threadIdx.x] = start;
+    w.koff[threadIdx.x] = start;
     uint64_t run = start;
     for (uint32_t c = 0; c < G; ++c) {
       const uint64_t x = w.cnt[(uint64_t)c * B + threadIdx.x];
@@ -134,72 +164,212 @@ __global__ void __launch_bounds__(1024) k_part_scan(uint32_t G, uint32_t B, Part
   pdl_trigger();
 }
 
-// Re-reads the CTA's chunk and writes every valid key's low 16 bits into its universe block,
-// sub-tile by sub-tile (4096 keys, 8 per thread as two 16-byte loads; the next sub-tile's
-// loads are in flight while the current one is placed).  One shared atomic per key: the
-// returned value of the per-warp block counter is the key's rank among the warp's keys of
-// that block in this sub-tile (< 256), kept in the key's register next to the key itself
-// (key < U <= 2^22 fills 22 bits, rank bits 22..29, bit 31 marks a dropped bad key).  A scan
-// over (block, warp) turns the counters into slot bases, every key lands at base + rank in
-// the staged sub-tile (order inside a block is free), and the sub-tile leaves as contiguous
-// runs (~4096 / B keys per block) at the CTA's running block offsets.
-// The chunk interior must be 16-byte aligned for the vector loads; other chunks take the
-// scalar path (keys of an unaligned base).
+// Sampled schedule, step 1 (64 CTAs; the last one to finish sizes the regions): a stratified sample — one key at a hashed position in each
+// of S = min(n, 65536) equal strata of the input — counts the keys of each block; capacity of
+// block b = its estimate c_b n / S + 6 sqrt(c_b + 1) n / S + 256 (margins scaled down if their
+// sum would pass tcap - sum of the estimates), exact when S = n.  Region starts = exclusive
+// scan of the capacities; fills and the overflow flag are reset.
+__device__ __forceinline__ uint32_t part_hash(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+constexpr uint32_t kSampleCtas = 64, kSampleThreads = 256;  // 4 samples per thread
+__global__ void __launch_bounds__(kSampleThreads) k_part_sample(const int32_t* __restrict__ keys, uint64_t n,
+                                                                uint32_t U, uint32_t B, PartWs w, uint64_t tcap,
+                                                                uint32_t* __restrict__ sacc) {
+  // sacc: [kPartMaxBlocks] sample counts of the whole grid, [kPartMaxBlocks] the CTA ticket —
+  // zero between launches (the last CTA resets them)
+  constexpr uint32_t kPer = kPartSample / (kSampleCtas * kSampleThreads);
+  __shared__ uint32_t cnt[kPartMaxBlocks];
+  __shared__ unsigned long long red[34];
+  __shared__ double s_scale;
+  __shared__ uint32_t s_last;
+  pdl_wait();
+  if (threadIdx.x < kPartMaxBlocks) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t S = n < kPartSample ? n : kPartSample;
+  uint32_t k[kPer];
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {  // (loads first: all in flight together)
+    const uint64_t j = (uint64_t)(q * kSampleCtas + blockIdx.x) * kSampleThreads + threadIdx.x;
+    k[q] = 0xffffffffu;
+    if (j < S) {
+      const uint64_t lo = j * n / S, hi = (j + 1) * n / S;  // (hi > lo: S <= n)
+      k[q] = (uint32_t)__ldg(keys + lo + part_hash((uint32_t)j) % (hi - lo));
+    }
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q)
+    if (k[q] < U) atomicAdd(&cnt[k[q] >> kPartShift], 1u);
+  __syncthreads();
+  if (threadIdx.x < B && cnt[threadIdx.x]) atomicAdd(sacc + threadIdx.x, cnt[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(sacc + kPartMaxBlocks, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) {
+    pdl_trigger();
+    return;
+  }
+  __threadfence();
+  uint64_t est = 0, mar = 0;
+  if (threadIdx.x < B) {
+    const uint64_t cb = *reinterpret_cast<volatile uint32_t*>(sacc + threadIdx.x);
+    sacc[threadIdx.x] = 0;
+    if (S == n) {
+      est = cb;
+    } else {
+      const double r = (double)n / (double)S;
+      est = (uint64_t)ceil((double)cb * r);
+      mar = (uint64_t)ceil(6.0 * sqrt((double)cb + 1.0) * r) + 256;
+    }
+  }
+  if (threadIdx.x == 0) sacc[kPartMaxBlocks] = 0;
+  unsigned long long tot_est, tot_mar;
+  block_excl_scan<unsigned long long>(est, tot_est, red);
+  block_excl_scan<unsigned long long>(mar, tot_mar, red);
+  if (threadIdx.x == 0)
+    s_scale = tot_est + tot_mar <= tcap ? 1.0 : (tot_est < tcap ? (double)(tcap - tot_est) / (double)tot_mar : 0.0);
+  __syncthreads();
+  uint64_t cap = est + (uint64_t)((double)mar * s_scale);
+  if (cap > n) cap = n;
+  if (threadIdx.x >= B) cap = 0;
+  unsigned long long tot_cap;
+  const uint64_t start = block_excl_scan<unsigned long long>(cap, tot_cap, red);
+  if (threadIdx.x < B) {
+    w.cap[threadIdx.x] = cap;
+    w.koff[threadIdx.x] = start;
+    w.fill[threadIdx.x * kFillStride] = 0;
+  }
+  if (threadIdx.x == 0) *w.ovf = 0;
+  pdl_trigger();
+}
+
+// Sampled schedule, step 3 (one CTA): block sizes = the fills, output starts = their exclusive
+// scan.  After an overflow it does nothing (the exact schedule writes them).
+__global__ void __launch_bounds__(1024) k_part_fin(uint32_t B, PartWs w) {
+  __shared__ unsigned long long red[34];
+  pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(w.ovf)) {
+    pdl_trigger();
+    return;
+  }
+  const uint64_t sz = threadIdx.x < B ? w.fill[threadIdx.x * kFillStride] : 0u;
+  unsigned long long tot;
+  const uint64_t start = block_excl_scan<unsigned long long>(sz, tot, red);
+  if (threadIdx.x < B) {
+    w.bsz[threadIdx.x] = sz;
+    w.boff[threadIdx.x] = start;
+  }
+  pdl_trigger();
+}
+
+// The placement (both schedules): re-reads the CTA's chunk and writes every valid key's low 16
+// bits into its universe block, sub-tile by sub-tile (4096 keys, 8 per thread as two 16-byte
+// loads; the next sub-tile's loads are in flight while the current one is ranked).  One shared
+// atomic per key: the returned value of the per-warp block counter is the key's rank among the
+// warp's keys of that block in this sub-tile (< 256), kept in the key's register next to the
+// key (key < U <= 2^22 fills 22 bits, rank bits 22..29; kBad marks a dropped bad key).  The
+// scan warp turns the counters into slot bases; every key lands at base + rank in the staged
+// sub-tile (order inside a block is free), which leaves as contiguous runs (~4096 / B keys per
+// block).  Two stage buffers, two barriers per sub-tile:
+//   count(i) | B1 | scan(i) (warp 0) | B2 | stage(i) + write-out(i-1) (+ warp 0: deltas(i))
+// so the write-out of one sub-tile overlaps the staging of the next and the counting after it.
+// EST (sampled schedule): the scan warp claims each run's place in its block's region (one
+// global atomic per run, read back after the staging: its round trip overlaps the write-out); a
+// run whose claim would pass the region's capacity sets ovf and goes to the 4096-key trash area
+// past the regions.  Positions are 32-bit (mod 2^32; tmp holds < 2^32 keys, checked by the
+// host).  Bad keys are recorded here.
+// !EST (exact schedule): the runs go to the CTA's running block offsets (k_part_scan); gate as
+// k_part_count.
+// The chunk interior must be 16-byte aligned for the vector loads; other chunks take the scalar
+// path (keys of an unaligned base).
 #ifndef DIALSORT_PART_MINB
 #define DIALSORT_PART_MINB (2048 / DIALSORT_PART_THREADS)  // 4 CTAs per SM (32 registers): more loads in flight (c4 6.44 -> 6.19 ms)
 #endif
-__global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatter(const int32_t* __restrict__ keys, uint64_t n, uint32_t U,
-                                                               uint32_t B, PartWs w, uint16_t* __restrict__ tmp) {
+template <bool EST>
+__global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place(const int32_t* __restrict__ keys, uint64_t n,
+                                                             uint32_t U, uint32_t B, PartWs w,
+                                                             uint16_t* __restrict__ tmp, const uint32_t* gate,
+                                                             uint32_t trash) {
   constexpr uint32_t NW = kPartThreads / 32;
   constexpr uint32_t kBad = 0xffffffffu;
   __shared__ uint32_t wcnt[NW][kPartMaxBlocks];   // per-warp block counts of the sub-tile
   __shared__ uint32_t wbase[NW][kPartMaxBlocks];  // their slot bases in the staged sub-tile
-  __shared__ uint32_t bofs[kPartMaxBlocks + 1], gpos[kPartMaxBlocks], delta[kPartMaxBlocks];
-  __shared__ uint32_t stage[kPartTile];
+  __shared__ uint32_t bofs[2][kPartMaxBlocks + 1];  // run starts in the staged sub-tile, + total
+  __shared__ uint32_t delta[2][kPartMaxBlocks];     // staged slot j of block b goes to delta + j
+  __shared__ uint32_t gpos[kPartMaxBlocks];         // (exact) running output position of block b
+  __shared__ uint32_t stage[2][kPartTile];
   pdl_wait();
-  const uint32_t warp = threadIdx.x >> 5;
+  if (!EST && part_gated_off(gate)) {
+    pdl_trigger();
+    return;
+  }
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t lo, hi;
   part_chunk(keys, n, lo, hi);
-  if (threadIdx.x < B) gpos[threadIdx.x] = w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x];
+  if (!EST && threadIdx.x < B) gpos[threadIdx.x] = w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x];
   const bool vec = ((reinterpret_cast<uintptr_t>(keys + lo)) & 15u) == 0;
-  // thread t holds sub-tile keys 8t .. 8t+7 (blocked: two int4)
-  auto load = [&](uint64_t t0, uint32_t (&k)[kPartKPT]) {
-    const uint64_t i0 = t0 + (uint64_t)kPartKPT * threadIdx.x;
-    if (vec && i0 + kPartKPT <= hi) {
-      const int4 x0 = __ldcs(reinterpret_cast<const int4*>(keys + i0));
-      const int4 x1 = __ldcs(reinterpret_cast<const int4*>(keys + i0) + 1);
-      k[0] = x0.x; k[1] = x0.y; k[2] = x0.z; k[3] = x0.w; k[4] = x1.x; k[5] = x1.y; k[6] = x1.z; k[7] = x1.w;
-    } else {
-#pragma unroll
-      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : kBad;
-    }
-  };
   unsigned short* const out = reinterpret_cast<unsigned short*>(tmp);
   for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
+  if (lo >= hi) {
+    pdl_trigger();
+    return;
+  }
   uint32_t k[kPartKPT], kn[kPartKPT];
-  if (lo < hi) load(lo, k);
-  // Three barriers per sub-tile: count | scan (warp 0) | stage | write-out + next count.
-  // wcnt is zeroed by the scan warp once read, so the next sub-tile's counting (which
-  // touches only wcnt) follows the write-out without a barrier between them.
-  for (uint64_t t0 = lo; t0 < hi; t0 += kPartTile) {
-    if (t0 + kPartTile < hi) load(t0 + kPartTile, kn);  // next sub-tile in flight
+  uint32_t pos0 = 0, pos1 = 0;  // (EST, warp 0) claims of blocks lane, lane + 32
+#define DS_PART_LOAD(T0, K)                                                                                 \
+  {                                                                                                         \
+    const uint64_t i0 = (T0) + (uint64_t)kPartKPT * threadIdx.x;                                            \
+    if (vec && i0 + kPartKPT <= hi) {                                                                       \
+      const int4 x0 = __ldcs(reinterpret_cast<const int4*>(keys + i0));                                     \
+      const int4 x1 = __ldcs(reinterpret_cast<const int4*>(keys + i0) + 1);                                 \
+      K[0] = x0.x; K[1] = x0.y; K[2] = x0.z; K[3] = x0.w; K[4] = x1.x; K[5] = x1.y; K[6] = x1.z; K[7] = x1.w; \
+    } else {                                                                                                \
+      _Pragma("unroll") for (uint32_t i = 0; i < kPartKPT; ++i) K[i] = i0 + i < hi ? (uint32_t)keys[i0 + i] : kBad; \
+    }                                                                                                       \
+  }
+  // one 4096-key write-out of staged buffer q (runs at delta[q][block] + slot)
+  auto write_out = [&](uint32_t q) {
+    const uint32_t nvld = bofs[q][B];  // valid keys of the sub-tile (bad keys were dropped)
+    if (nvld == kPartTile) {
+#pragma unroll
+      for (uint32_t r = 0; r < kPartKPT; ++r) {
+        const uint32_t j = r * kPartThreads + threadIdx.x, key = stage[q][j];
+        __stcs(out + (uint32_t)(delta[q][key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
+        const uint32_t key = stage[q][j];
+        __stcs(out + (uint32_t)(delta[q][key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
+      }
+    }
+  };
+  DS_PART_LOAD(lo, k);
+  uint32_t p = 0;
+  for (uint64_t t0 = lo;; t0 += kPartTile, p ^= 1u) {
+    const bool nxt = t0 + kPartTile < hi;
+    if (nxt) DS_PART_LOAD(t0 + kPartTile, kn);  // next sub-tile in flight
     uint32_t kmax = 0;
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) kmax = max(kmax, k[i]);
-    if (kmax < U) {  // every key valid: no per-key test
+    const bool allv = kmax < U;
+    if (allv) {  // every key valid: no per-key test
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i) k[i] |= atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22;
     } else {
 #pragma unroll
-      for (uint32_t i = 0; i < kPartKPT; ++i)
+      for (uint32_t i = 0; i < kPartKPT; ++i) {
+        if (EST && k[i] >= U && t0 + (uint64_t)kPartKPT * threadIdx.x + i < hi)  // (past the end: kBad)
+          record_bad(w.st, t0 + (uint64_t)kPartKPT * threadIdx.x + i, k[i]);
         k[i] = k[i] < U ? k[i] | (atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22) : kBad;
+      }
     }
-    __syncthreads();
+    __syncthreads();  // B1: counts of sub-tile i complete
     if (warp == 0) {
-      // lane l owns blocks l and l + 32: block totals over the NW warps, one warp scan of
-      // the totals (block order), then the per-warp slot bases of each owned block.
-      const uint32_t lane = threadIdx.x & 31;
+      // lane l owns blocks l and l + 32: block totals over the NW warps, one warp scan of the
+      // totals (block order), then the per-warp slot bases of each owned block
       uint32_t t[2] = {0u, 0u};
       const uint32_t nh = B > 32 ? 2u : 1u;
       for (uint32_t h = 0; h < nh; ++h) {
@@ -216,9 +386,16 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
         const uint32_t b = lane + 32 * h;
         if (b < B) {
           uint32_t base = ex[h];
-          bofs[b] = base;
-          delta[b] = gpos[b] - base;  // staged slot j of block b goes to position delta[b] + j
-          gpos[b] += t[h];
+          bofs[p][b] = base;
+          if (EST) {
+            if (t[h]) {
+              const uint32_t c = atomicAdd(w.fill + b * kFillStride, t[h]);  // (read after the staging)
+              if (h) pos1 = c; else pos0 = c;
+            }
+          } else {
+            delta[p][b] = gpos[b] - base;
+            gpos[b] += t[h];
+          }
 #pragma unroll
           for (uint32_t q = 0; q < NW; ++q) {
             const uint32_t x = wcnt[q][b];
@@ -228,45 +405,47 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_scatt
           }
         }
       }
-      if (lane == 31) bofs[B] = s0 + (nh > 1 ? i1 : 0u);  // lane 31 holds both totals
+      if (lane == 31) bofs[p][B] = s0 + (nh > 1 ? i1 : 0u);  // lane 31 holds both totals
     }
-    __syncthreads();
-    if (kmax < U) {
+    __syncthreads();  // B2: slot bases of sub-tile i
+    if (allv) {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i) {
         const uint32_t key = k[i] & 0x3fffffu;
-        stage[wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+        stage[p][wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
       }
     } else {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i)
         if (k[i] != kBad) {
           const uint32_t key = k[i] & 0x3fffffu;
-          stage[wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+          stage[p][wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
         }
     }
-    __syncthreads();
-    const uint32_t nvld = bofs[B];  // valid keys of the sub-tile (bad keys were dropped)
-    if (nvld == kPartTile) {
-#pragma unroll
-      for (uint32_t r = 0; r < kPartKPT; ++r) {
-        const uint32_t j = r * kPartThreads + threadIdx.x, key = stage[j];
-        __stcs(out + (delta[key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
-      }
-    } else {
-      for (uint32_t j = threadIdx.x; j < nvld; j += blockDim.x) {
-        const uint32_t key = stage[j];
-        __stcs(out + (delta[key >> kPartShift] + j), (unsigned short)(key & 0xffffu));
+    if (t0 != lo) write_out(p ^ 1u);  // sub-tile i-1
+    if (EST && warp == 0) {  // the claims of sub-tile i -> its runs' deltas
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t b = lane + 32 * h;
+        if (b < B) {
+          const uint32_t ex = bofs[p][b], tb = bofs[p][b + 1] - ex, c = h ? pos1 : pos0;
+          uint32_t d = trash - ex;  // (an empty run: never read)
+          if (tb) {
+            if ((uint64_t)c + tb <= w.cap[b]) d = (uint32_t)(w.koff[b] + c) - ex;
+            else atomicOr(w.ovf, 1u);
+          }
+          delta[p][b] = d;
+        }
       }
     }
-    // the next sub-tile's count barrier orders these stage / delta / bofs reads before the
-    // scan warp and the staging rewrite them
+    if (!nxt) break;
 #pragma unroll
     for (uint32_t i = 0; i < kPartKPT; ++i) k[i] = kn[i];
   }
+  __syncthreads();  // the last sub-tile's staging and deltas
+  write_out(p);
+#undef DS_PART_LOAD
   pdl_trigger();
 }
-
 
 // ---- wide partition (2^22 < U <= 2^26: up to 1024 universe blocks, NEXT-4) -----------------
 // Per-CTA block counters in (dynamic) shared memory instead of per-warp ones: the rank a key

@@ -15,6 +15,7 @@
 // deferred status (index = query index) and answered 0.
 #pragma once
 #include "ds_common.cuh"
+#include "ds_scan.cuh"
 
 namespace ds {
 
@@ -38,26 +39,10 @@ __global__ void __launch_bounds__(256) k_query_point(const uint32_t* __restrict_
   pdl_trigger();
 }
 
-// Monotonic grid barrier on a 64-bit counter that only grows (co-resident grid): every CTA
-// arrives with a release add and waits until the counter reaches `target` (the host tracks the
-// counter: target = its value before the launch + gridDim).
-__device__ __forceinline__ void query_grid_sync(unsigned long long* bar, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned long long v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
 // pre[k] = Σ_{j<k} H[j] for k = 0..U (uint64).  CTA b owns a contiguous range of bins; its
 // total goes to part[b]; after one grid barrier each CTA adds the totals of lower CTAs.
 __global__ void __launch_bounds__(1024) k_query_prefix(const uint32_t* __restrict__ H, uint32_t U,
-                                                       uint64_t* __restrict__ pre, unsigned long long* bar,
-                                                       unsigned long long target) {
+                                                       uint64_t* __restrict__ pre, GridBar* bar) {
   __shared__ unsigned long long red[34];
   pdl_wait();
   const uint32_t G = gridDim.x, b = blockIdx.x;
@@ -69,7 +54,7 @@ __global__ void __launch_bounds__(1024) k_query_prefix(const uint32_t* __restric
   unsigned long long tot;
   s = block_excl_scan<unsigned long long>(s, tot, red);
   if (threadIdx.x == 0) __stcg(part + b, (uint64_t)tot);
-  query_grid_sync(bar, target);
+  grid_barrier(bar);  // (sense-reversing: replay-safe in CUDA graphs)
   unsigned long long off = 0;
   for (uint32_t j = threadIdx.x; j < b; j += blockDim.x) off += __ldcg(part + j);
   off = block_sum<unsigned long long>(off, red);
@@ -105,8 +90,7 @@ __global__ void __launch_bounds__(256) k_query_range(const uint64_t* __restrict_
 // ws: [G] per-CTA counts.
 __global__ void __launch_bounds__(1024) k_support_set(const uint32_t* __restrict__ H, uint32_t U,
                                                       uint32_t* __restrict__ D_out, unsigned long long* count,
-                                                      uint32_t* iso, unsigned long long* ws, unsigned long long* bar,
-                                                      unsigned long long target) {
+                                                      uint32_t* iso, unsigned long long* ws, GridBar* bar) {
   __shared__ unsigned long long red[34];
   pdl_wait();
   const uint32_t G = gridDim.x, b = blockIdx.x;
@@ -115,7 +99,7 @@ __global__ void __launch_bounds__(1024) k_support_set(const uint32_t* __restrict
   for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x) s += __ldg(H + k) > 0u ? 1ull : 0ull;
   s = block_sum<unsigned long long>(s, red);
   if (threadIdx.x == 0) __stcg(ws + b, (uint64_t)s);
-  query_grid_sync(bar, target);
+  grid_barrier(bar);  // (sense-reversing: replay-safe in CUDA graphs)
   unsigned long long off = 0;
   for (uint32_t j = threadIdx.x; j < b; j += blockDim.x) off += __ldcg(ws + j);
   off = block_sum<unsigned long long>(off, red);

@@ -88,13 +88,34 @@ struct ScanArgs {
   uint32_t* Hx_clear;        // the other parity's Hx, zeroed for the next launch
   const uint64_t* d_n;       // nullable: key count on the device (hierarchical blocks); then
   const uint64_t* d_off;     //   keys and out start at *d_off and n_expected = *d_n
+  const uint64_t* d_koff;    // nullable: the keys start at *d_koff instead (sampled partition)
   uint32_t* own_red;         // [G x ctr_stride] per-owner totals (tiles of CTA b) reduced during the flush
   uint32_t* own_clear;       // the other parity's own_red, zeroed for the next launch
   uint32_t* own_alt;         // [G] owner totals of the overflow fallback path
   uint32_t* ready_clear;     // k_sort_fused: the other parity's ready flags, zeroed for the next launch
   uint32_t* ready;           // [ntiles] per-tile "P published" flags (= epoch)
-  unsigned long long* bar64; // monotonic grid-barrier counter
-  unsigned long long bar_base;  // its value at launch (host-tracked: += 2 * gridDim per launch)
+  unsigned long long* bar64; // monotonic grid-barrier counter (= &fstate->bar)
+  unsigned long long bar_base;  // its value at the step's start (derived on the device, see FusedState)
+  // two-parity workspaces of the fused step; the parity, the epoch and bar_base of a step are
+  // derived ON THE DEVICE from FusedState (so a captured CUDA graph replays correctly)
+  uint32_t* own_base;        // [2][kFOwnSlots * ctr_stride] owner counters, then [kFOwnSlots] own_alt
+  uint32_t* ready_base;      // [2][kFTileSlots] per-tile ready flags
+  uint32_t* Hx_base;         // [2][kSmem16MaxBins] 4-bit rows' exception histograms
+  struct FusedState* fstate;
+};
+
+// Device-side sequencing of the fused step's launches on one workspace: the monotonic barrier
+// counter, its value at the start of the next launch and the steps run so far (parity = seq & 1,
+// epoch = seq mod 2^24 + 1).  Each launch reads base and seq at its start (after
+// griddepcontrol.wait); once its first grid barrier shows every CTA has read them, CTA 0 advances
+// them to the launch's end values (the next launch reads them after this grid completes).  No
+// host-side bookkeeping: a captured launch replays correctly and a launch that never ran leaves
+// the state as it was.
+struct FusedState {
+  unsigned long long bar;   // monotonic barrier counter
+  unsigned long long base;  // bar at the start of the next launch
+  unsigned int seq;         // fused steps run so far
+  unsigned int pad;
 };
 
 // H[bin] = h, or — multi-GPU histogram — the owner rank's slot of this rank (see Hpeer).

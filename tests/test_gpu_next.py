@@ -265,3 +265,68 @@ def test_sort_batch_range_error(ds, cuda_dev):
     assert e.value.code == 2 and e.value.info.first_bad_index == 123_457
     c.sort_batch(ks[:2], 65536)
     c.sync()  # (cleared)
+
+
+# ---- CUDA graphs: captured once, replayed with new inputs ---------------------------------------
+
+def test_cuda_graph_replay(ds, cuda_dev):
+    """The fused step, the batched sort, the reconstruct of a given H, DialSort-Radix, the
+    hierarchical path (U = 2^20) and the queries keep their sequencing state on the device
+    (FusedState, sense-reversing barriers, self-resetting counters), so a CUDA graph captured
+    once replays correctly: three replays with fresh inputs copied into the captured buffers,
+    every output against the oracle."""
+    c = ds.Context(0, max_n=2_000_000, max_U=65536)
+    U = 65536
+    n1, nb = 1_500_007, [700_001, 900_003, 650_000]
+    k1 = torch.empty(n1, dtype=torch.int32, device=cuda_dev)
+    kb = [torch.empty(m, dtype=torch.int32, device=cuda_dev) for m in nb]
+    kr = torch.empty(1_000_003, dtype=torch.int32, device=cuda_dev)
+    H = torch.empty(U, dtype=torch.int32, device=cuda_dev)
+    o1 = torch.empty_like(k1)
+    ob = [torch.empty_like(k) for k in kb]
+    orad = torch.empty_like(kr)
+    orec = torch.empty(n1, dtype=torch.int32, device=cuda_dev)
+    q = torch.arange(0, U, 97, dtype=torch.int32, device=cuda_dev)
+    Uh = 1 << 20  # the hierarchical path (sampled partition + batched block steps)
+    kh = torch.empty(1_200_001, dtype=torch.int32, device=cuda_dev)
+    oh = torch.empty_like(kh)
+
+    def fill(seed):
+        xs = [synth.uniform(n1, U, seed=seed)] + [synth.zipf(m, U, seed=seed + j + 1) for j, m in enumerate(nb)]
+        xr = synth.full_int32(kr.numel(), seed=seed + 9)
+        k1.copy_(torch.from_numpy(xs[0]))
+        for k, x in zip(kb, xs[1:]):
+            k.copy_(torch.from_numpy(x))
+        kr.copy_(torch.from_numpy(xr))
+        xh = synth.uniform(kh.numel(), Uh, seed=seed + 5)
+        kh.copy_(torch.from_numpy(xh))
+        torch.cuda.synchronize()
+        return xs, xr, xh
+
+    def work():
+        c.sort(k1, U, out=o1, H=H)
+        c.sort_batch(kb, U, ob)
+        c.reconstruct(H, orec)
+        c.sort_int32(kr, out=orad)
+        c.sort(kh, Uh, out=oh)
+        return c.query(H, ds._lib.Q_FREQUENCY, q)
+
+    fill(1)
+    work()  # (workspaces sized before the capture)
+    c.sync()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        f = work()
+    for rep in range(3):
+        xs, xr, xh = fill(100 + rep)
+        g.replay()
+        torch.cuda.synchronize()
+        c.sync()
+        Hr = oracle.histogram(xs[0], U)
+        assert np.array_equal(o1.cpu().numpy(), oracle.project(Hr)), rep
+        assert np.array_equal(orec.cpu().numpy(), oracle.project(Hr)), rep
+        for o, x in zip(ob, xs[1:]):
+            assert np.array_equal(o.cpu().numpy(), oracle.sort(x, U)), rep
+        assert np.array_equal(orad.cpu().numpy(), oracle.radix_sort_i32(xr)), rep
+        assert np.array_equal(f.cpu().numpy(), Hr[::97].astype(np.int64)), rep
+        assert np.array_equal(oh.cpu().numpy(), oracle.sort(xh, Uh)), rep
