@@ -93,40 +93,12 @@ __device__ __forceinline__ uint32_t count_below(const uint32_t* Ps, uint32_t m, 
 }
 
 // Projection stores: st.global.L1::no_allocate without an L2 hint (measured 0.3 us faster than
-// the evict-first hint on c2 / c3, and than the default policy).
+// the evict-first hint on c2 / c3, and than the default policy).  full: the 128 positions of the
+// warp lie inside [lo, hi); aligned: out + p is 16-byte aligned for every quad start p.
 __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p, uint32_t lo, uint32_t hi, uint4 q,
-                                           bool aligned, uint64_t pol, bool full = false,
-                                           const int32_t* __restrict__ dec = nullptr) {
-  // (coded domain: the emitted value of code k is phi^-1(k) = dec[k]; consecutive
-  //  positions mostly share a code, so the table reads hit L1)
-  const int4 v = dec ? make_int4(__ldg(dec + q.x), __ldg(dec + q.y), __ldg(dec + q.z), __ldg(dec + q.w))
-                     : make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
-  if (full && !aligned) {
-    // Warp-cooperative (all 32 lanes, p = p_0 + 4 lane, the 128 positions inside [lo, hi)):
-    // out is 4-byte but not 16-byte aligned (a hierarchical block's output starts at the
-    // block's offset), shifted by sh elements.  Lane L stores the aligned quad at
-    // p + 4 - sh: its own last sh values and lane L+1's first 4 - sh; lane 0 stores the
-    // head p .. p + 3 - sh and lane 31 the tail p + 4 - sh .. p + 3 as scalars.
-    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) >> 2) & 3u, lane = threadIdx.x & 31u;
-    const int nx = __shfl_down_sync(0xffffffffu, v.x, 1), ny = __shfl_down_sync(0xffffffffu, v.y, 1),
-              nz = __shfl_down_sync(0xffffffffu, v.z, 1);
-    if (lane < 31) {
-      const int4 w = sh == 1 ? make_int4(v.w, nx, ny, nz) : sh == 2 ? make_int4(v.z, v.w, nx, ny)
-                                                              : make_int4(v.y, v.z, v.w, nx);
-      st_stream4(reinterpret_cast<int4*>(out + p + 4 - sh), w);
-    } else {
-      if (sh == 3) out[p + 1] = v.y;
-      if (sh >= 2) out[p + 2] = v.z;
-      out[p + 3] = v.w;
-    }
-    if (lane == 0) {
-      out[p] = v.x;
-      if (sh <= 2) out[p + 1] = v.y;
-      if (sh == 1) out[p + 2] = v.z;
-    }
-    return;
-  }
-  if (full || (aligned && p >= lo && p + 4 <= hi)) {
+                                           bool aligned, bool full = false) {
+  const int4 v = make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w);
+  if (aligned && (full || (p >= lo && p + 4 <= hi))) {
     st_stream4(reinterpret_cast<int4*>(out + p), v);  // no L2 hint
   } else {
     if (p >= lo && p < hi) out[p] = v.x;
@@ -134,6 +106,14 @@ __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p
     if (p + 2 >= lo && p + 2 < hi) out[p + 2] = v.z;
     if (p + 3 >= lo && p + 3 < hi) out[p + 3] = v.w;
   }
+}
+
+// Coded domains (Proposition 2): the projection writes codes k; the CTA then rewrites
+// its own positions [lo, hi) with phi^-1(k) = dec[k] (just written: L2 hits).
+__device__ __forceinline__ void decode_range(int32_t* __restrict__ out, uint32_t lo, uint32_t hi,
+                                             const int32_t* __restrict__ dec) {
+  __syncthreads();  // (the CTA's projection stores of the range)
+  for (uint32_t p = lo + threadIdx.x; p < hi; p += blockDim.x) out[p] = __ldg(dec + out[p]);
 }
 
 // ---- table-driven projection (block-level) ----------------------------------------------
@@ -147,26 +127,36 @@ __device__ __forceinline__ void store_quad(int32_t* __restrict__ out, uint32_t p
 // its start's offset on — about 25 instructions per quad, a third of the ballot / REDUX /
 // shuffle projection it replaced.  A sub-block whose quads hold several starts (bins shorter
 // than 4 positions, empty bins) takes the count-mark path.
+// Positions are shifted by sh = (out / 4) mod 4 (out - sh is 16-byte aligned), so that every
+// quad store is aligned whatever the output's offset (a hierarchical block's output starts at
+// the block's offset; the warp-cooperative realigned stores this replaced cost ~25 instructions
+// a quad).
 constexpr uint32_t kFTblCap = kFSlot / 4;  // 4884 sub-blocks per window (one staging slot)
 __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
-                                            uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out,
-                                            bool aligned, uint64_t pol, const int32_t* __restrict__ dec = nullptr) {
+                                            uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out) {
   __shared__ uint32_t s_ib[2];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t ltmask = (1u << lane) - 1u;
+  // (positions < 2^32 - 4 after the shift; else unshifted, scalar stores when unaligned)
+  const uint32_t sh = hi <= 0xfffffff0u ? (uint32_t)(reinterpret_cast<uintptr_t>(out) >> 2) & 3u : 0u;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(out - sh)) & 15u) == 0;
+  out -= sh;
+  lo += sh;
+  hi += sh;
   const uint32_t jl = lo >> 7, jh = (hi + 127) >> 7;
   for (uint32_t jw = jl; jw < jh; jw += kFTblCap) {
     const uint32_t nsb = min(kFTblCap, jh - jw);
     for (uint32_t j = threadIdx.x; j < nsb; j += blockDim.x) T[j] = make_uint4(0, 0, 0, 0);
-    if (w == 0) {  // bins [ia, ib) start in the window
-      const uint32_t ia = count_below(Ps, m, 0, jw << 7);
-      const uint32_t ib = count_below(Ps, m, ia, (jw + nsb) << 7);
+    if (w == 0) {  // bins [ia, ib) start in the window (Ps[i] + sh < x  <=>  Ps[i] < x - sh)
+      const uint32_t xa = jw << 7, xb = (jw + nsb) << 7;
+      const uint32_t ia = xa > sh ? count_below(Ps, m, 0, xa - sh) : 0u;
+      const uint32_t ib = xb > sh ? count_below(Ps, m, ia, xb - sh) : 0u;
       if (lane == 0) s_ib[0] = ia, s_ib[1] = ib;
     }
     __syncthreads();
     const uint32_t ia = s_ib[0], ib = s_ib[1];
     for (uint32_t i = ia + threadIdx.x; i < ib; i += blockDim.x) {
-      const uint32_t p = Ps[i], j = (p >> 7) - jw, q = (p >> 2) & 31u;
+      const uint32_t p = Ps[i] + sh, j = (p >> 7) - jw, q = (p >> 2) & 31u;
       uint32_t* t = reinterpret_cast<uint32_t*>(T + j);
       const uint32_t old = atomicOr(t + 1, 1u << q);
       atomicAdd(t, 1u);
@@ -197,20 +187,20 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
       const uint4 e = T[j];
       const uint32_t c0 = e.x & 0x7fffffffu;
       if (!(e.x >> 31)) {
-        const bool full = b0 >= lo && hi - b0 >= 128;  // (any alignment: store_quad realigns)
+        const bool full = b0 >= lo && hi - b0 >= 128;
         const uint32_t below = __popc(e.y & ltmask), own = (e.y >> lane) & 1u;
         const uint32_t r = ((lane < 16 ? e.z : e.w) >> (2 * (lane & 15u))) & 3u;
         const uint32_t v = kbase + c0 + below;
         store_quad(out, b0 + 4 * lane, lo, hi,
                    make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own), aligned,
-                   pol, full, dec);
+                   full);
       } else {  // count marks of the sub-block's starts, then a warp scan
-        const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;
+        const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;  // (>= lo >= sh)
         uint32_t i1 = c0;
         for (;;) {
           const uint32_t sl = Ps[min(i1 + lane, m)];  // Ps[m] is a sentinel
-          const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= be));
-          if (lane < cnt) atomicAdd(&wc[sl - b0], 1u);
+          const uint32_t cnt = __popc(__ballot_sync(FULL, sl <= be - sh));
+          if (lane < cnt) atomicAdd(&wc[sl + sh - b0], 1u);
           i1 += cnt;
           if (cnt < 32) break;
         }
@@ -221,8 +211,7 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         mk.z += mk.y;
         mk.w += mk.z;
         const uint32_t v = kbase + c0 + warp_incl_scan(mk.w) - mk.w;
-        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned, pol,
-                   false, dec);
+        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned);
         __syncwarp();
       }
     }
@@ -657,8 +646,6 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
     return;
   }
 
-  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-  const uint64_t pol = l2_evict_first_policy();
   if (own) {
     // ---- projection of the own tiles' positions [oo[b], oo[b+1]) ∩ [0, nw) -----------------
     const uint32_t m = nown * kFTileBins;
@@ -666,10 +653,11 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
     __syncthreads();
     phase_mark(a.pt, 9);
     const uint32_t p0 = obase, p1 = (uint32_t)(oend < n_exp ? oend : n_exp);
-    if (nown && p0 < p1)  // (uniform per CTA) table in the second staging slot, dead after the merge
+    if (nown && p0 < p1) {  // (uniform per CTA) table in the second staging slot, dead after the merge
       project_tbl(Ps, m, (uint32_t)key_base + tb0 * kFTileBins - 1, p0, p1,
-                  reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
-                  reinterpret_cast<uint32_t*>(red64), out, aligned, pol, a.dec);
+                  reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc, reinterpret_cast<uint32_t*>(red64), out);
+      if (a.dec) decode_range(out, p0, p1, a.dec);
+    }
     phase_mark(a.pt, 7);
     return;
   }
@@ -720,10 +708,11 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
       }
       phase_mark(a.pt, 9);
       const uint32_t p0 = max(lo, ts[pt0 - x0]), p1 = min(hi, ts[pt1 - x0]);
-      if (p0 < p1)
+      if (p0 < p1) {
         project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
-                    reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc,
-                    reinterpret_cast<uint32_t*>(red64), out, aligned, pol, a.dec);
+                    reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc, reinterpret_cast<uint32_t*>(red64), out);
+        if (a.dec) decode_range(out, p0, p1, a.dec);
+      }
       __syncthreads();  // Pw is reused by the next pass
     }
   }
