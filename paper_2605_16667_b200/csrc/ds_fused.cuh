@@ -186,7 +186,10 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
       const uint32_t b0 = (jw + j) << 7;
       const uint4 e = T[j];
       const uint32_t c0 = e.x & 0x7fffffffu;
-      if (!(e.x >> 31)) {
+      if (e.y == 0u) {  // no bin starts in the sub-block: one key throughout (long runs: most sub-blocks)
+        const uint32_t v = kbase + c0;
+        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v, v, v, v), aligned, b0 >= lo && hi - b0 >= 128);
+      } else if (!(e.x >> 31)) {
         const bool full = b0 >= lo && hi - b0 >= 128;
         const uint32_t below = __popc(e.y & ltmask), own = (e.y >> lane) & 1u;
         const uint32_t r = ((lane < 16 ? e.z : e.w) >> (2 * (lane & 15u))) & 3u;
