@@ -287,18 +287,28 @@ __global__ void __launch_bounds__(1024) k_part_fin(uint32_t B, PartWs w) {
 #ifndef DIALSORT_PART_MINB
 #define DIALSORT_PART_MINB (2048 / DIALSORT_PART_THREADS)  // 4 CTAs per SM (32 registers): more loads in flight (c4 6.44 -> 6.19 ms)
 #endif
+// Ranking counters per (warp, block, lane parity): the 32 lanes of a ranking atomic spread over
+// 2 B words in distinct banks (B = 16), so same-address lanes — serialised by the atomic unit —
+// drop from ~2 to ~1 per word (ncu, one counter per (warp, block): 5.1 wavefronts per ranking
+// atomic).
+#ifndef DIALSORT_PART_SUBS
+#define DIALSORT_PART_SUBS 2
+#endif
+constexpr uint32_t kPartSubs = DIALSORT_PART_SUBS;
 template <bool EST>
 __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place(const int32_t* __restrict__ keys, uint64_t n,
                                                              uint32_t U, uint32_t B, PartWs w,
                                                              uint16_t* __restrict__ tmp, const uint32_t* gate,
                                                              uint32_t trash) {
-  constexpr uint32_t NW = kPartThreads / 32;
+  constexpr uint32_t NW = kPartThreads / 32, S = kPartSubs;
   constexpr uint32_t kBad = 0xffffffffu;
-  __shared__ uint32_t wcnt[NW][kPartMaxBlocks];   // per-warp block counts of the sub-tile
-  __shared__ uint32_t wbase[NW][kPartMaxBlocks];  // their slot bases in the staged sub-tile
-  __shared__ uint32_t bofs[2][kPartMaxBlocks + 1];  // run starts in the staged sub-tile, + total
-  __shared__ uint32_t delta[2][kPartMaxBlocks];     // staged slot j of block b goes to delta + j
-  __shared__ uint32_t gpos[kPartMaxBlocks];         // (exact) running output position of block b
+  // (static shared memory, 45 KB: as dynamic shared memory the kernel ran 5 % slower — the
+  //  driver then picks a larger shared-memory carveout, less L1)
+  __shared__ uint32_t wcnt[NW][kPartMaxBlocks * S];   // per-(warp, block, sub) counts of the sub-tile
+  __shared__ uint16_t wbase[NW][kPartMaxBlocks * S];  // their slot bases in the staged sub-tile (< 4096)
+  __shared__ uint32_t bofs[2][kPartMaxBlocks + 1];    // run starts in the staged sub-tile, + total
+  __shared__ uint32_t delta[2][kPartMaxBlocks];       // staged slot j of block b goes to delta + j
+  __shared__ uint32_t gpos[kPartMaxBlocks];           // (exact) running output position of block b
   __shared__ uint32_t stage[2][kPartTile];
   pdl_wait();
   if (!EST && part_gated_off(gate)) {
@@ -311,12 +321,13 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
   if (!EST && threadIdx.x < B) gpos[threadIdx.x] = w.cnt[(uint64_t)blockIdx.x * B + threadIdx.x];
   const bool vec = ((reinterpret_cast<uintptr_t>(keys + lo)) & 15u) == 0;
   unsigned short* const out = reinterpret_cast<unsigned short*>(tmp);
-  for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  for (uint32_t i = threadIdx.x; i < NW * kPartMaxBlocks * S; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   if (lo >= hi) {
     pdl_trigger();
     return;
   }
+  const uint32_t sub = lane & (S - 1);
   uint32_t k[kPartKPT], kn[kPartKPT];
   uint32_t pos0 = 0, pos1 = 0;  // (EST, warp 0) claims of blocks lane, lane + 32
 #define DS_PART_LOAD(T0, K)                                                                                 \
@@ -357,13 +368,13 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
     const bool allv = kmax < U;
     if (allv) {  // every key valid: no per-key test
 #pragma unroll
-      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] |= atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22;
+      for (uint32_t i = 0; i < kPartKPT; ++i) k[i] |= atomicAdd(&wcnt[warp][(k[i] >> kPartShift) * S + sub], 1u) << 22;
     } else {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i) {
         if (EST && k[i] >= U && t0 + (uint64_t)kPartKPT * threadIdx.x + i < hi)  // (past the end: kBad)
           record_bad(w.st, t0 + (uint64_t)kPartKPT * threadIdx.x + i, k[i]);
-        k[i] = k[i] < U ? k[i] | (atomicAdd(&wcnt[warp][k[i] >> kPartShift], 1u) << 22) : kBad;
+        k[i] = k[i] < U ? k[i] | (atomicAdd(&wcnt[warp][(k[i] >> kPartShift) * S + sub], 1u) << 22) : kBad;
       }
     }
     __syncthreads();  // B1: counts of sub-tile i complete
@@ -376,7 +387,9 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
         const uint32_t b = lane + 32 * h;
         if (b < B) {
 #pragma unroll
-          for (uint32_t q = 0; q < NW; ++q) t[h] += wcnt[q][b];
+          for (uint32_t q = 0; q < NW; ++q)
+#pragma unroll
+            for (uint32_t u = 0; u < S; ++u) t[h] += wcnt[q][b * S + u];
         }
       }
       const uint32_t i0 = warp_incl_scan(t[0]), i1 = nh > 1 ? warp_incl_scan(t[1]) : 0u;
@@ -397,12 +410,14 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
             gpos[b] += t[h];
           }
 #pragma unroll
-          for (uint32_t q = 0; q < NW; ++q) {
-            const uint32_t x = wcnt[q][b];
-            wbase[q][b] = base;
-            wcnt[q][b] = 0;
-            base += x;
-          }
+          for (uint32_t q = 0; q < NW; ++q)
+#pragma unroll
+            for (uint32_t u = 0; u < S; ++u) {
+              const uint32_t x = wcnt[q][b * S + u];
+              wbase[q][b * S + u] = (uint16_t)base;
+              wcnt[q][b * S + u] = 0;
+              base += x;
+            }
         }
       }
       if (lane == 31) bofs[p][B] = s0 + (nh > 1 ? i1 : 0u);  // lane 31 holds both totals
@@ -412,14 +427,14 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i) {
         const uint32_t key = k[i] & 0x3fffffu;
-        stage[p][wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+        stage[p][wbase[warp][(key >> kPartShift) * S + sub] + (k[i] >> 22)] = key;
       }
     } else {
 #pragma unroll
       for (uint32_t i = 0; i < kPartKPT; ++i)
         if (k[i] != kBad) {
           const uint32_t key = k[i] & 0x3fffffu;
-          stage[p][wbase[warp][key >> kPartShift] + (k[i] >> 22)] = key;
+          stage[p][wbase[warp][(key >> kPartShift) * S + sub] + (k[i] >> 22)] = key;
         }
     }
     if (t0 != lo) write_out(p ^ 1u);  // sub-tile i-1
