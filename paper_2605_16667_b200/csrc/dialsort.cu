@@ -1062,8 +1062,9 @@ int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const 
   for (uint32_t j0 = 0; j0 < nb; j0 += kBatchMax) {
     const uint32_t m = std::min<uint32_t>(kBatchMax, nb - j0);
     // groups: at most kGroups, and few enough that every group keeps its own-tile projection
-    // (ntiles <= kFPassTiles per CTA): smaller groups fall to the share mode (Zipf at 5 groups of
-    // 29 CTAs: 145 us per batch vs 22 us at 4 groups of 37)
+    // (ntiles <= kFPassTiles per CTA).  (5-6 groups measured slower for every order; Zipf at 5
+    // groups of 29 CTAs: 134 us per batch vs 22 us at 4 groups of 37 — its hottest key passes
+    // 65535 copies per CTA, the 16-bit counters' overflow fallback)
     const uint64_t ntl = cdiv(U, kFTileBins);
     const uint32_t Lown = (uint32_t)std::max<uint64_t>(1, (uint64_t)c->nsm * kFPassTiles / ntl);
     const uint32_t L = std::min<uint32_t>(std::min<uint32_t>(Lmax, Lown), m);

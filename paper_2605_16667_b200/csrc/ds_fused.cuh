@@ -52,7 +52,10 @@ template <int FMT> struct RowFmt {
 // Dynamic shared memory after the barrier (words); the ingestion histogram is dead by then.
 constexpr uint32_t kFSlot = kFMaxRows * kFRowStride;                 // one staging slot (19536 words)
 constexpr uint32_t kFOffStage = 0;                                   // 2 slots x C rows x 132 words
-constexpr uint32_t kFPassTiles = 32;                                 // own tiles per CTA (own-tile mode)
+#ifndef DIALSORT_FPASS_TILES
+#define DIALSORT_FPASS_TILES 32
+#endif
+constexpr uint32_t kFPassTiles = DIALSORT_FPASS_TILES;               // own tiles per CTA (own-tile mode)
 constexpr uint32_t kFSharePassTiles = (kFSlot - 32) / kFTileBins;    // share mode: 304 tiles per pass
 constexpr uint32_t kFOffPs = 2 * kFSlot;                             // own-mode P + 32 sentinels
 constexpr uint32_t kFOffHb = kFOffPs + kFPassTiles * kFTileBins + 32; // merged H of the batch (<= 1024)
@@ -62,6 +65,7 @@ constexpr uint32_t kFOffOwn = kFOffWc + 32 * 128;                    // oo[G + 1
 constexpr uint32_t kFOffTsh = kFOffOwn + kFMaxRows + 32 > kSmem16MaxBins / 2 ? kFOffOwn + kFMaxRows + 32
                                                                              : kSmem16MaxBins / 2;
 constexpr uint32_t kFSmemWords = kFOffTsh + kFTiles + 32;
+static_assert(kFOffOwn + kFMaxRows + 32 <= kSmem16MaxBins / 2, "own-mode P grows the fused kernel's shared memory");
 
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
