@@ -811,6 +811,7 @@ __global__ void __launch_bounds__(1024, 1) k_sort_batch(const __grid_constant__ 
   uint32_t k = 0;  // this group's steps so far
   for (uint32_t j = g; j < B.nb; j += B.L, ++k) {
     const ScanArgs& a = B.a[j];
+    phase_mark(a.pt, -1);  // (debug stamps: the group's last step survives)
     const unsigned long long bj = base + 3ull * B.Gg * k;
     sort_step<FMT, KB>(B.keys[j], B.n[j], a, B.out[j], B.key_base[j], vg, sh, red64, wsum, bj, seq + k,
                        k == 0 ? fs : nullptr, base + 3ull * B.Gg * steps, seq + steps);
