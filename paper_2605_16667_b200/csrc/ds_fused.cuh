@@ -186,21 +186,29 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
       }
     }
     __syncthreads();
+    // (per lane: the quad-offset shift and the word of the start offsets are loop constants; T is
+    //  read through its 32-bit shared address — the generic pointer's window base was otherwise
+    //  re-derived every iteration; a full aligned sub-block stores without per-lane bounds tests)
+    const uint32_t rsh = 2 * (lane & 15u);
+    uint32_t Ts;  // (an opaque mov keeps it in a register)
+    asm volatile("mov.b32 %0, %1;" : "=r"(Ts) : "r"(smem_addr(T) + 16u * w));
+    int4* __restrict__ o4 = reinterpret_cast<int4*>(out) + lane;
     for (uint32_t j = w; j < nsb; j += 32) {
       const uint32_t b0 = (jw + j) << 7;
-      const uint4 e = T[j];
+      uint4 e;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w) : "r"(Ts + 16u * (j - w)) : "memory");
       const uint32_t c0 = e.x & 0x7fffffffu;
+      const bool full = aligned && b0 >= lo && b0 + 128u <= hi;  // (warp-uniform)
+      uint4 q;
       if (e.y == 0u) {  // no bin starts in the sub-block: one key throughout (long runs: most sub-blocks)
         const uint32_t v = kbase + c0;
-        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v, v, v, v), aligned, b0 >= lo && hi - b0 >= 128);
+        q = make_uint4(v, v, v, v);
       } else if (!(e.x >> 31)) {
-        const bool full = b0 >= lo && hi - b0 >= 128;
         const uint32_t below = __popc(e.y & ltmask), own = (e.y >> lane) & 1u;
-        const uint32_t r = ((lane < 16 ? e.z : e.w) >> (2 * (lane & 15u))) & 3u;
+        const uint32_t r = ((lane < 16 ? e.z : e.w) >> rsh) & 3u;
         const uint32_t v = kbase + c0 + below;
-        store_quad(out, b0 + 4 * lane, lo, hi,
-                   make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own), aligned,
-                   full);
+        q = make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own);
       } else {  // count marks of the sub-block's starts, then a warp scan
         const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;  // (>= lo >= sh)
         uint32_t i1 = c0;
@@ -218,9 +226,11 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         mk.z += mk.y;
         mk.w += mk.z;
         const uint32_t v = kbase + c0 + warp_incl_scan(mk.w) - mk.w;
-        store_quad(out, b0 + 4 * lane, lo, hi, make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w), aligned);
+        q = make_uint4(v + mk.x, v + mk.y, v + mk.z, v + mk.w);
         __syncwarp();
       }
+      if (full) st_stream4(o4 + (b0 >> 2), make_int4((int)q.x, (int)q.y, (int)q.z, (int)q.w));
+      else store_quad(out, b0 + 4 * lane, lo, hi, q, aligned);
     }
     __syncthreads();  // T is reused by the next window
   }
