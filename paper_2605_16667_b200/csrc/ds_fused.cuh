@@ -383,7 +383,7 @@ __device__ __forceinline__ uint64_t tile_total_direct(const ScanArgs& a, uint32_
     if (FMT == kRowU32) s += __ldcg(row + k);
     else if (FMT == kRowP16) s += (__ldcg(row + (k >> 1)) >> ((k & 1u) << 4)) & 0xffffu;
     else s += (__ldcg(row + (k >> 3)) >> ((k & 7u) << 2)) & 0xfu;
-    if (r == 0) s += __ldcg(a.ovfH + k) + (FMT == kRowN4 ? __ldcg(a.Hx + k) : 0u);
+    if (r == 0) s += __ldcg(a.ovfH + k) + (FMT != kRowU32 ? __ldcg(a.Hx + k) : 0u);
   }
   return block_sum<uint64_t>(s, red);
 }
@@ -521,7 +521,9 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
   const uint32_t binend = min(tb1 * kFTileBins, U);  // bins of the own tiles end here
   auto hx_of = [&](uint32_t k) -> uint32_t {
     const uint32_t bin = (tb0 + k * tpb) * kFTileBins + batch_bin<FMT>(threadIdx.x >> 5, threadIdx.x & 31);
-    return FMT == kRowN4 && bin < binend ? __ldcg(a.Hx + bin) : 0u;
+    // (4-bit rows' exceptions and — 4-bit and 16-bit rows — the hot keys' counts, ds_hist.cuh)
+    const bool wr = FMT == kRowN4 || (FMT == kRowP16 && (threadIdx.x & 3u) == 0);
+    return FMT != kRowU32 && wr && bin < binend ? __ldcg(a.Hx + bin) : 0u;
   };
   uint32_t hx = hx_of(0);
   __syncthreads();  // s_pb

@@ -322,6 +322,34 @@ __device__ __noinline__ void hist_overflow_fallback16(const KeySpan16& s, uint4*
   }
 }
 
+// ---- hot keys (skew at scale) ------------------------------------------------------------
+// A packed 16-bit counter wraps when one CTA sees > 65535 copies of a key: possible once a CTA
+// ingests more than 65535 keys (n > 65000 G) and some key's share p exceeds 65535 G / n (Zipf
+// 1.2 at n = 1e8: p1 = 0.198 against 0.097).  The exact overflow fallback then re-ingests the
+// whole CTA through L2 (measured 15x slower: 2.46 ms vs 0.159 ms at n = 1e8).  Large launches
+// first sample each thread's first vector, find up to kHotK keys whose sampled share would put
+// more than 30000 copies in a CTA, and count those keys in per-thread registers (one compare per
+// hot key per key) instead of the packed histogram; the counts go whole into the exception
+// histogram Hx (32-bit, merged with the rows) and into the tile sums.  Candidates: the first key
+// of lanes 0 and 16 of every warp when it recurs >= 3 times in the warp's 128 sampled keys, in a
+// 128-slot open-addressing table; then every sampled key counts its candidate.
+constexpr uint32_t kHotK = 4, kHotTab = 128, kHotNone = 0xffffffffu;
+__device__ __forceinline__ uint32_t hot_hash(uint32_t k) { return (k * 0x9E3779B1u) >> 25; }  // 7 bits
+__device__ __forceinline__ void hot_tab_insert(uint32_t* tab, uint32_t k) {
+  for (uint32_t i = hot_hash(k), t = 0; t < kHotTab; ++t, i = (i + 1) & (kHotTab - 1)) {
+    const uint32_t old = atomicCAS(tab + i, kHotNone, k);
+    if (old == kHotNone || old == k) return;
+  }
+}
+__device__ __forceinline__ uint32_t hot_tab_find(const uint32_t* tab, uint32_t k) {
+  for (uint32_t i = hot_hash(k), t = 0; t < kHotTab; ++t, i = (i + 1) & (kHotTab - 1)) {
+    const uint32_t v = tab[i];
+    if (v == k) return i;
+    if (v == kHotNone) return kHotNone;
+  }
+  return kHotNone;
+}
+
 template <bool PACK16, int KB = 4>
 __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_v, uint64_t n, const ScanArgs& a,
                                                   uint32_t* sh_hist, uint64_t* red64, uint32_t* tsum_sh = nullptr,
@@ -342,6 +370,72 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   const KeySpan s = make_span(NARROW ? nullptr : static_cast<const int32_t*>(keys_v), NARROW ? 0 : n);
   const KeySpan16 s16 =
       make_span_narrow<NARROW ? KB : 2>(NARROW ? static_cast<const uint16_t*>(keys_v) : nullptr, NARROW ? n : 0);
+  const uint32_t lane0 = threadIdx.x & 31;
+  // hot keys of this launch (see kHotK); hot_on is uniform over the CTA
+  __shared__ uint32_t s_tab[kHotTab], s_tcnt[kHotTab], s_hot[kHotK], s_hotc[kHotK];
+  uint32_t hk[kHotK] = {kHotNone, kHotNone, kHotNone, kHotNone}, hc[kHotK] = {0u, 0u, 0u, 0u};
+  bool hot_on = false;
+  // (launches of > 131070 keys a CTA: below that only a key holding > half a CTA's keys can wrap
+  //  — rare, and the exact fallback still covers it — and the sampling (~2 us) would show in the
+  //  single-call c2 step, 67.6k keys a CTA)
+  if (PACK16 && a.fused && n > 131070ull * vg.G) {
+    uint32_t sk[4] = {kHotNone, kHotNone, kHotNone, kHotNone};  // this thread's first vector
+    const uint32_t iv = vg.b * blockDim.x + threadIdx.x;
+    if (NARROW) {
+      if (iv < s16.n8) {
+        const int4 x = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s16.keys) + KB * s16.head)[iv];
+        expand_narrow<NARROW ? KB : 2>(x, 0, a.enc, [&](int4 q, uint32_t g) {
+          if (g == 0) sk[0] = (uint32_t)q.x, sk[1] = (uint32_t)q.y, sk[2] = (uint32_t)q.z, sk[3] = (uint32_t)q.w;
+        });
+      }
+    } else if (iv < s.n4) {
+      const int4 x = s.body()[iv];
+      sk[0] = (uint32_t)x.x, sk[1] = (uint32_t)x.y, sk[2] = (uint32_t)x.z, sk[3] = (uint32_t)x.w;
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q)
+      if (sk[q] >= U) sk[q] = kHotNone;
+    for (uint32_t t = threadIdx.x; t < kHotTab; t += blockDim.x) s_tab[t] = kHotNone, s_tcnt[t] = 0;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {  // candidates: lanes 0 and 16's first key if it recurs
+      const uint32_t x = __shfl_sync(0xffffffffu, sk[0], 16 * h);
+      uint32_t c = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q) c += __popc(__ballot_sync(0xffffffffu, sk[q] == x));
+      if (lane0 == 16 * h && x != kHotNone && c >= 3) hot_tab_insert(s_tab, x);
+    }
+    const uint32_t nsamp = 4 * __syncthreads_count(sk[0] != kHotNone || iv < (NARROW ? s16.n8 : s.n4));
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q)
+      if (sk[q] != kHotNone) {
+        const uint32_t slot = hot_tab_find(s_tab, sk[q]);
+        if (slot != kHotNone) atomicAdd(s_tcnt + slot, 1u);
+      }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // the kHotK largest counts above the routing threshold
+      // count c of nsamp sampled keys -> ~ c n / (G nsamp) copies per CTA; route above 30000
+      const uint64_t thr = nsamp ? (30000ull * nsamp * vg.G + n - 1) / n : ~0ull;
+      uint32_t best[4];
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t t = 4 * lane0 + q;
+        best[q] = s_tab[t] != kHotNone && s_tcnt[t] >= thr ? (min(s_tcnt[t], 0x1ffffffu) << 7) | t : 0u;
+      }
+      for (uint32_t r = 0; r < kHotK; ++r) {
+        uint32_t mine = max(max(best[0], best[1]), max(best[2], best[3]));
+        const uint32_t top = __reduce_max_sync(0xffffffffu, mine);
+        if (lane0 == 0) s_hot[r] = top ? s_tab[top & (kHotTab - 1)] : kHotNone, s_hotc[r] = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          if (top && best[q] == top) best[q] = 0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t r = 0; r < kHotK; ++r) hk[r] = s_hot[r];
+    hot_on = hk[0] != kHotNone;
+  }
   DevStatus* st = a.st;
   uint32_t seen = 0, bad = 0, deferred = 0;
   // packed word of key k: k >> 1 at byte offset (k & ~1) * 2; increment 1 << 16 (k & 1) as a
@@ -373,8 +467,20 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   // per vector rules it out for the whole warp.
   constexpr uint32_t kRunMiss = 8;
   uint32_t run_state = 0;  // vectors since the last run; >= kRunMiss: detection off
+  // (hot keys counted in registers, the rest as usual; no run detection in such launches)
+  auto addh = [&](uint32_t k) {
+    if (k == hk[0]) ++hc[0];
+    else if (k == hk[1]) ++hc[1];
+    else if (k == hk[2]) ++hc[2];
+    else if (k == hk[3]) ++hc[3];
+    else add16(k);
+  };
   auto f4 = [&](int4 v, uint32_t) {
     if (umax4(v) < U) {
+      if (PACK16 && hot_on) {
+        addh((uint32_t)v.x); addh((uint32_t)v.y); addh((uint32_t)v.z); addh((uint32_t)v.w);
+        return;
+      }
       // Run detection adapts per warp: after kRunMiss vectors in a row without a run of 4 in
       // any lane it is switched off for the rest of the launch (it costs ~0.5 us at c2, where
       // runs never occur, and is what makes sorted inputs fast; a warp's first vectors decide)
@@ -446,9 +552,21 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
     if (NARROW) bad += ingest_deferred_narrow<PACK16, NARROW ? KB : 2>(sh_hist, s16, a.enc, U, st, vg);
     else bad += ingest_deferred<PACK16>(sh_hist, s, U, st, vg);
   }
+  if (PACK16 && hot_on) {  // the hot keys' register counts: a CTA total per key
+#pragma unroll
+    for (uint32_t r = 0; r < kHotK; ++r) {
+      const uint32_t c = __reduce_add_sync(0xffffffffu, hc[r]);
+      if (lane0 == 0 && c) atomicAdd(s_hotc + r, c);
+    }
+  }
   phase_mark(a.pt, 0);
   __syncthreads();
   phase_mark(a.pt, 1);
+  if (PACK16 && hot_on && threadIdx.x < kHotK && s_hot[threadIdx.x] != kHotNone && s_hotc[threadIdx.x]) {
+    // whole into Hx (32-bit, merged with the rows) and into the key's tile sum
+    red_add_u32(a.Hx + s_hot[threadIdx.x], s_hotc[threadIdx.x]);
+    atomicAdd(tsum_sh + s_hot[threadIdx.x] / kFTileBins, s_hotc[threadIdx.x]);
+  }
 
   // Flush the private histogram as partial row vg.b (4-, 16- or 32-bit counts) and this row's
   // 64-bin tile sums (tsum_sh) for the owner counters.
@@ -568,6 +686,9 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
             }
           }
         }
+        // (and the hot keys' counts: the fallback re-ingests every key of the CTA)
+        if (PACK16 && hot_on && threadIdx.x < kHotK && s_hot[threadIdx.x] != kHotNone && s_hotc[threadIdx.x])
+          red_add_u32(a.Hx + s_hot[threadIdx.x], 0u - s_hotc[threadIdx.x]);
         uint4* frow = reinterpret_cast<uint4*>(const_cast<uint32_t*>(a.partials) + (uint64_t)vg.b * a.ldr);
         if (K16) hist_overflow_fallback16(s16, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
         else hist_overflow_fallback(s, frow, a.ldr / 4, a.ovfH, U, st, a.epoch, vg);
