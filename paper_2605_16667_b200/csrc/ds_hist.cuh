@@ -48,8 +48,21 @@ __host__ __device__ inline KeySpan make_span(const int32_t* keys, uint64_t n) {
 
 // Visit this CTA's keys as int4 vectors f4(v, vector index), plus scalars f1(key, index) for
 // the unaligned head (CTA 0) and tail (last CTA).  32-bit vector indices (n4 < 2^30).
+// The first batch of a thread's vectors (a[u] = vector i + u stride, i = b T + t), loaded by the
+// caller before it zeroes its histogram (the loads' latency overlaps the zeroing and the hot-key
+// sampling, which reads a[0]).
+template <int NV>
+__device__ __forceinline__ void preload_vecs(const int4* __restrict__ body, uint32_t nv, VGrid vg, int4 (&a)[NV]) {
+  const uint64_t pol = l2_evict_first_policy();
+  const uint32_t stride = vg.G * blockDim.x, i = vg.b * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < NV; ++u)
+    a[u] = (i + u * stride < nv) ? ld_stream4(body + i + u * stride, pol) : make_int4(0, 0, 0, 0);
+}
+// (a: the thread's first batch, preload_vecs)
 template <typename F4, typename F1>
-__device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1, VGrid vg = vgrid_hw()) {
+__device__ __forceinline__ void for_each_key4(const KeySpan& s, int4 (&a)[kHistUnroll], F4&& f4, F1&& f1,
+                                              VGrid vg = vgrid_hw()) {
   const uint32_t T = blockDim.x, G = vg.G;
   if (vg.b == 0 && threadIdx.x < s.head) f1((uint32_t)s.keys[threadIdx.x], (uint64_t)threadIdx.x);
   if (vg.b == G - 1 && threadIdx.x < s.tail) {
@@ -64,10 +77,6 @@ __device__ __forceinline__ void for_each_key4(const KeySpan& s, F4&& f4, F1&& f1
   // (measured faster than ping-pong / refill-after-consume variants, 10 vs 14 us at c2).
   const uint32_t n4 = (uint32_t)s.n4, stride = G * T;
   uint32_t i = vg.b * T + threadIdx.x;
-  int4 a[kHistUnroll];
-#pragma unroll
-  for (int u = 0; u < kHistUnroll; ++u)
-    a[u] = (i + u * stride < n4) ? ld_stream4(body + i + u * stride, pol) : make_int4(0, 0, 0, 0);
   while (i < n4) {
     const uint32_t in = i + kHistUnroll * stride;
     int4 b[kHistUnroll];
@@ -245,10 +254,12 @@ __device__ __forceinline__ void expand_narrow(const int4& x, uint32_t v, const u
 #ifndef DIALSORT_NARROW_UNROLL
 #define DIALSORT_NARROW_UNROLL 3  // (c4 block steps: 2 -> 1.312 ms, 3 -> 1.294, 4 -> 1.335)
 #endif
+constexpr int kNarrowUnroll = DIALSORT_NARROW_UNROLL;  // vectors per batch (2 batches in flight)
+// (a: the thread's first batch, preload_vecs)
 template <int KB, typename F4, typename F1>
-__device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, const uint32_t* enc, F4&& f4, F1&& f1,
-                                                        VGrid vg) {
-  constexpr int NU = DIALSORT_NARROW_UNROLL;  // vectors per batch (2 batches in flight)
+__device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, int4 (&a)[kNarrowUnroll],
+                                                        const uint32_t* enc, F4&& f4, F1&& f1, VGrid vg) {
+  constexpr int NU = kNarrowUnroll;
   constexpr uint32_t per = 16 / KB;
   const uint32_t T = blockDim.x, G = vg.G;
   if (vg.b == 0 && threadIdx.x < s.head) f1(narrow_key<KB>(s.keys, threadIdx.x, enc), (uint64_t)threadIdx.x);
@@ -261,10 +272,6 @@ __device__ __forceinline__ uint32_t for_each_key_narrow(const KeySpan16& s, cons
   const uint32_t n8 = (uint32_t)s.n8, stride = G * T;
   uint32_t cnt = 0;
   uint32_t i = vg.b * T + threadIdx.x;
-  int4 a[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u)
-    a[u] = (i + u * stride < n8) ? ld_stream4(body + i + u * stride, pol) : make_int4(0, 0, 0, 0);
   while (i < n8) {
     const uint32_t in = i + (NU) * stride;
     int4 b[NU];
@@ -362,13 +369,6 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   constexpr bool NARROW = KB != 4;
   const uint32_t U = a.U, ldw = a.ldw;
 
-  // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
-  // merge may read whole uint4 groups).
-  const uint32_t W4 = ldw / 4;
-  uint4* h4 = reinterpret_cast<uint4*>(sh_hist);
-  for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-
   // Ingestion (eq:ingestion): one shared atomic per key; equal addresses inside one warp
   // instruction are merged by the shared-memory atomic unit (the CRN's equality merge).
   const KeySpan s = make_span(NARROW ? nullptr : static_cast<const int32_t*>(keys_v), NARROW ? 0 : n);
@@ -379,28 +379,52 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
   __shared__ uint32_t s_tab[kHotTab], s_tcnt[kHotTab], s_hot[kHotK], s_hotc[kHotK];
   uint32_t hk[kHotK] = {kHotNone, kHotNone, kHotNone, kHotNone}, hc[kHotK] = {0u, 0u, 0u, 0u};
   bool hot_on = false;
-  // (launches of > 131070 keys a CTA: below that only a key holding > half a CTA's keys can wrap
-  //  — rare, and the exact fallback still covers it — and the sampling (~2 us) would show in the
-  //  single-call c2 step, 67.6k keys a CTA)
-  if (PACK16 && a.fused && n > 131070ull * vg.G) {
-    uint32_t sk[4] = {kHotNone, kHotNone, kHotNone, kHotNone};  // this thread's first vector
-    const uint32_t iv = vg.b * blockDim.x + threadIdx.x;
-    if (NARROW) {
-      if (iv < s16.n8) {
+  // (launches of > 300000 keys a CTA: below that only a key holding > 22 % of a CTA's keys can
+  //  wrap — the exact fallback still covers it — and the sampling's ~1 us would show: batched c2
+  //  steps, 270k keys a CTA, 17.7 -> 18.3 us)
+#ifndef DIALSORT_HOT_GUARD_KEYS  // (A/B: a huge value turns the hot-key sampling off)
+#define DIALSORT_HOT_GUARD_KEYS 300000ull
+#endif
+  // (hierarchical block steps, 16-bit keys: from 65535 keys a CTA — their steps are long, and a
+  //  block concentrates its hot keys: Zipf(1.2) at n = 1e8, U = 2^20 had blocks of ~150k keys a
+  //  CTA with a key holding 60 % of them; 1.06 ms with the 300000 guard, 0.61 with this one)
+  const bool hot_guard = PACK16 && a.fused && n > (K16 ? 65535ull : DIALSORT_HOT_GUARD_KEYS) * vg.G;  // (uniform)
+  // the sample: the keys of the thread's first vector (loaded again by the ingestion loop)
+  uint32_t sk[4] = {kHotNone, kHotNone, kHotNone, kHotNone};
+  const uint32_t iv = vg.b * blockDim.x + threadIdx.x;
+  if (hot_guard) {  // (requested before the zeroing below)
+    if (iv < (NARROW ? (uint32_t)s16.n8 : (uint32_t)s.n4)) {
+      if constexpr (NARROW) {
         const int4 x = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s16.keys) + KB * s16.head)[iv];
         expand_narrow<NARROW ? KB : 2>(x, 0, a.enc, [&](int4 q, uint32_t g) {
           if (g == 0) sk[0] = (uint32_t)q.x, sk[1] = (uint32_t)q.y, sk[2] = (uint32_t)q.z, sk[3] = (uint32_t)q.w;
         });
+      } else {
+        const int4 x = s.body()[iv];
+        sk[0] = (uint32_t)x.x, sk[1] = (uint32_t)x.y, sk[2] = (uint32_t)x.z, sk[3] = (uint32_t)x.w;
       }
-    } else if (iv < s.n4) {
-      const int4 x = s.body()[iv];
-      sk[0] = (uint32_t)x.x, sk[1] = (uint32_t)x.y, sk[2] = (uint32_t)x.z, sk[3] = (uint32_t)x.w;
     }
+    for (uint32_t t = threadIdx.x; t < kHotTab; t += blockDim.x) s_tab[t] = kHotNone, s_tcnt[t] = 0;
+  }
+  // K1: zero the private histogram (ldw = W rounded up to 8 words; padding stays zero so the
+  // merge may read whole uint4 groups).
+  const uint32_t W4 = ldw / 4;
+  uint4* h4 = reinterpret_cast<uint4*>(sh_hist);
+  for (uint32_t i = threadIdx.x; i < W4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  // the thread's first batch of vectors (the loop's prologue; requesting it before the zeroing
+  // measured 1.3 us slower on the single-call c2 step)
+  constexpr int NV0 = NARROW ? kNarrowUnroll : kHistUnroll;
+  int4 a0[NV0];
+  if constexpr (NARROW)
+    preload_vecs<NV0>(reinterpret_cast<const int4*>(reinterpret_cast<const char*>(s16.keys) + KB * s16.head),
+                      (uint32_t)s16.n8, vg, a0);
+  else
+    preload_vecs<NV0>(s.body(), (uint32_t)s.n4, vg, a0);
+  if (hot_guard) {
 #pragma unroll
     for (uint32_t q = 0; q < 4; ++q)
       if (sk[q] >= U) sk[q] = kHotNone;
-    for (uint32_t t = threadIdx.x; t < kHotTab; t += blockDim.x) s_tab[t] = kHotNone, s_tcnt[t] = 0;
-    __syncthreads();
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {  // candidates: lanes 0 and 16's first key if it recurs
       const uint32_t x = __shfl_sync(0xffffffffu, sk[0], 16 * h);
@@ -542,10 +566,11 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
       ++bad;
     }
   };
-  if (NARROW) {
-    seen += (16 / KB) * for_each_key_narrow<NARROW ? KB : 2>(s16, a.enc, f4, f1, vg);
+  if constexpr (NARROW) {
+    seen += (16 / KB) * for_each_key_narrow<NARROW ? KB : 2>(s16, reinterpret_cast<int4(&)[kNarrowUnroll]>(a0), a.enc,
+                                                             f4, f1, vg);
   } else {
-    for_each_key4(s, f4, f1, vg);
+    for_each_key4(s, reinterpret_cast<int4(&)[kHistUnroll]>(a0), f4, f1, vg);
     // vectors of this thread: every grid-stride index < n4 (counted, not tallied in the loop)
     const uint32_t stride = vg.G * blockDim.x, i0 = vg.b * blockDim.x + threadIdx.x;
     const uint32_t n4 = (uint32_t)s.n4;
