@@ -326,7 +326,7 @@ int ctx_init(dialsort_ctx c) {
   int occ = 0;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass3, kRadixThreads, sizeof(Radix3Smem)));
   c->radix3_occ = occ > 0 ? occ : 1;
-  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass4, kRadixThreads, sizeof(Radix4Smem)));
+  DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass4, kR4Threads, sizeof(Radix4Smem)));
   c->radix4_occ = occ > 0 ? occ : 1;
   DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kExpandThreads, 0));
   c->expand_occ = occ > 0 ? occ : 1;
@@ -771,7 +771,7 @@ int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out,
   for (int p = 0; p < 4; ++p) {
     uint32_t* dst = pass_out ? pass_out + (uint64_t)p * n : bufs[p & 1];
     if (v == 4)
-      DS_CUDA(launch_k<true>(KID_RADIX_PASS, k_radix_pass4, dim3(G), dim3(kRadixThreads), sizeof(Radix4Smem), s, src,
+      DS_CUDA(launch_k<true>(KID_RADIX_PASS, k_radix_pass4, dim3(G), dim3(kR4Threads), sizeof(Radix4Smem), s, src,
                              dst, (uint32_t)n, p, w));
     else
       DS_CUDA(launch_k<true>(KID_RADIX_PASS, k_radix_pass3, dim3(G), dim3(kRadixThreads), sizeof(Radix3Smem), s, src,

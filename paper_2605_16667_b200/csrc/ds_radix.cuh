@@ -285,11 +285,19 @@ __global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass3(const uint32_t
 #define DIALSORT_R4_W16 1
 #endif
 
+#ifndef DIALSORT_R4_THREADS
+#define DIALSORT_R4_THREADS 512
+#endif
 constexpr int kR4KPT = DIALSORT_R4_KPT;
-constexpr int kR4Tile = kRadixThreads * kR4KPT;
+constexpr int kR4Threads = DIALSORT_R4_THREADS;  // 512, 768 or 1024
+constexpr int kR4Warps = kR4Threads / 32;
+constexpr int kR4TPD = kR4Threads / 256;         // threads per digit in the sub-tile scan
+constexpr int kR4WPT = kR4Warps / kR4TPD;        // warps per scan thread (8)
+static_assert(kR4Threads % 256 == 0 && kR4Warps % kR4TPD == 0, "pass4 thread count");
+constexpr int kR4Tile = kR4Threads * kR4KPT;
 constexpr bool kR4W16 = DIALSORT_R4_W16 != 0;  // per-warp digit counters as 16-bit halves
 struct Radix4Smem {
-  uint32_t wcur[kRadixWarps][kR4W16 ? 128 : 256];  // per-warp digit counts -> slot bases
+  uint32_t wcur[kR4Warps][kR4W16 ? 128 : 256];  // per-warp digit counts -> slot bases
   uint32_t sorted[kR4Tile];          // sub-tile sorted by digit
   uint32_t stage[kR4Tile + 4];       // staged sub-tile (+ alignment shift)
   uint32_t dstart[257];
@@ -316,7 +324,7 @@ __device__ __forceinline__ void r4_set(Radix4Smem& S, uint32_t w, uint32_t d, ui
   if (kR4W16) reinterpret_cast<uint16_t*>(&S.wcur[w][0])[d] = (uint16_t)v;
   else S.wcur[w][d] = v;
 }
-__global__ void __launch_bounds__(kRadixThreads, DIALSORT_R4_MINB) k_radix_pass4(const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(kR4Threads, DIALSORT_R4_MINB) k_radix_pass4(const uint32_t* __restrict__ src,
                                                                    uint32_t* __restrict__ dst, uint32_t n, int p,
                                                                    Radix2Ws w) {
   extern __shared__ __align__(16) unsigned char radix_smem_raw[];
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(kRadixThreads, DIALSORT_R4_MINB) k_radix_pass4
   for (uint32_t t0 = lo; t0 < hi; t0 += kR4Tile) {
     uint32_t tn, ab, ae;
     bounds(t0, tn, ab, ae);
-    for (int i = threadIdx.x; i < kRadixWarps * (kR4W16 ? 128 : 256); i += blockDim.x) (&S.wcur[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kR4Warps * (kR4W16 ? 128 : 256); i += blockDim.x) (&S.wcur[0][0])[i] = 0;
     const uint32_t sft = t0 & 3u;
     if (threadIdx.x < ab - t0) S.stage[sft + threadIdx.x] = __ldcs(src + t0 + threadIdx.x);
     if (threadIdx.x >= 8 && threadIdx.x - 8 < t0 + tn - ae)
@@ -457,20 +465,20 @@ __global__ void __launch_bounds__(kRadixThreads, DIALSORT_R4_MINB) k_radix_pass4
     }
     __syncthreads();  // counts complete; the stage buffer is free
     if (t0 + kR4Tile < hi) issue(t0 + kR4Tile);
-    {  // exclusive scan over (digit, warp): thread t has digit t >> 1, warps (t & 1) * 8 .. + 7
-      const uint32_t d = threadIdx.x >> 1, w0 = (threadIdx.x & 1u) * (kRadixWarps / 2);
-      uint32_t v[kRadixWarps / 2], s = 0;
+    {  // exclusive scan over (digit, warp): thread t has digit t / TPD, warps (t % TPD) * 8 .. + 7
+      const uint32_t d = threadIdx.x / kR4TPD, w0 = (threadIdx.x % kR4TPD) * kR4WPT;
+      uint32_t v[kR4WPT], s = 0;
 #pragma unroll
-      for (int j = 0; j < kRadixWarps / 2; ++j) {
+      for (int j = 0; j < kR4WPT; ++j) {
         v[j] = r4_get(S, w0 + j, d);
         s += v[j];
       }
       uint32_t tot;
       uint32_t ex = block_excl_scan<uint32_t>(s, tot, S.red);
-      if ((threadIdx.x & 1u) == 0) S.dstart[d] = ex;
+      if (threadIdx.x % kR4TPD == 0) S.dstart[d] = ex;
       if (threadIdx.x == 0) S.dstart[256] = tot;
 #pragma unroll
-      for (int j = 0; j < kRadixWarps / 2; ++j) {
+      for (int j = 0; j < kR4WPT; ++j) {
         r4_set(S, w0 + j, d, ex);
         ex += v[j];
       }
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kRadixThreads, DIALSORT_R4_MINB) k_radix_pass4
     if (tn == (uint32_t)kR4Tile) {  // full sub-tile: unrolled, 32-bit output index (n < 2^32)
 #pragma unroll
       for (int r = 0; r < kR4KPT; ++r) {
-        const uint32_t j = r * kRadixThreads + threadIdx.x, u = S.sorted[j];
+        const uint32_t j = r * kR4Threads + threadIdx.x, u = S.sorted[j];
         __stcs(dst + (uint32_t)(S.gdel[__byte_perm(u, 0, dsel)] + (int32_t)j), u ^ flip_out);
       }
     } else {
