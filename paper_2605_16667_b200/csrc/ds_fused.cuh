@@ -466,7 +466,7 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
     sum = block_sum<uint32_t>(sum, reinterpret_cast<uint32_t*>(red64));
     for (uint32_t o = b + threadIdx.x; o < G && sum; o += blockDim.x)
       red_add_u32(a.own_red + (uint64_t)(o + 1) * a.ctr_stride, sum);
-    if (threadIdx.x == 0 && 4ull * G * sum > 5ull * n_exp + 256ull * G)
+    if (threadIdx.x == 0 && 4ull * G * sum > 5ull * n_exp + kSkewSlack)
       red_add_u32(a.own_red + (uint64_t)kFOwnVote * a.ctr_stride, 1u);
     __syncthreads();
   } else {

@@ -186,6 +186,11 @@ __device__ __noinline__ void hist_overflow_fallback(const KeySpan& s, uint4* row
 // exceeds 5/4 of its even share of the row: the own-tile projection is then replaced by equal
 // position shares (no vote anywhere bounds every owner's positions by 5/4 n / G + 64 G, so own
 // tiles stay balanced).
+// Skew vote slack (flush_owner_totals): 32768 keys per owner, x 4.  With fewer 64-bin tiles
+// than CTAs (U = 256 on 25 CTAs at n = 1e5) four owners hold every key; below ~32k keys each,
+// projecting them in the own-tile mode beats the share mode's flag waits (c1 13.7 -> 11.8 us),
+// above it the share mode spreads them (n = 3e6, U = 256: 63 us own-tile vs 18.5 share).
+constexpr unsigned long long kSkewSlack = 4ull * 32768;
 __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint32_t* tsum_sh, uint32_t U,
                                                    uint32_t* red, VGrid vg) {
   const uint32_t ntf = (U + kFTileBins - 1) / kFTileBins, G = vg.G, b = threadIdx.x;
@@ -197,7 +202,10 @@ __device__ __forceinline__ void flush_owner_totals(const ScanArgs& a, const uint
   uint32_t tot;
   const uint32_t inc = block_excl_scan<uint32_t>(s, tot, red) + s;  // Σ_{o <= b} s_o
   if (b < G && inc) red_add_u32(a.own_red + (uint64_t)(b + 1) * a.ctr_stride, inc);
-  const bool skew = b < G && 4ull * G * s > 5ull * tot + 256ull * G;  // (tot = the row's keys)
+  // (tot = the row's keys: a row votes when an owner's share passes 5/4 of the even one plus a
+  //  slack of kSkewSlack / 4 projected keys over the whole step — what an owner projects in the
+  //  ~2 us the share mode's flags cost)
+  const bool skew = b < G && 4ull * G * s > 5ull * tot + kSkewSlack;
   if (__syncthreads_or(skew) && threadIdx.x == 0) red_add_u32(a.own_red + (uint64_t)(kFOwnVote)*a.ctr_stride, 1u);
 }
 
