@@ -193,6 +193,8 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
     uint32_t Ts;  // (an opaque mov keeps it in a register)
     asm volatile("mov.b32 %0, %1;" : "=r"(Ts) : "r"(smem_addr(T) + 16u * w));
     int4* __restrict__ o4 = reinterpret_cast<int4*>(out) + lane;
+    // starts before sub-block j + 1 (its c0; the window's end ib after the last one)
+    auto ib_next = [&](uint32_t j) -> uint32_t { return j + 1 < nsb ? T[j + 1].x & 0x7fffffffu : ib; };
     for (uint32_t j = w; j < nsb; j += 32) {
       const uint32_t b0 = (jw + j) << 7;
       uint4 e;
@@ -209,6 +211,25 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         const uint32_t r = ((lane < 16 ? e.z : e.w) >> rsh) & 3u;
         const uint32_t v = kbase + c0 + below;
         q = make_uint4(v + (own & (r == 0)), v + (own & (r <= 1)), v + (own & (r <= 2)), v + own);
+      } else if (ib_next(j) - c0 > 96u) {
+        // many starts in the sub-block (empty bins share their start with the next bin — a sparse
+        // stretch of the universe): per position a binary search over the sub-block's starts,
+        // key = kbase + #{i : P_i + sh <= p} (the marks loop below walks every start: one sparse
+        // share of n = 1e4, U = 65536 took 22 us)
+        const uint32_t cend = ib_next(j);
+        uint32_t v[4];
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+          const uint32_t pp = b0 + 4 * lane + u - sh;  // (b0 + 4 lane + u >= sh: b0 >= lo - 127 >= 0 ...)
+          uint32_t l = c0, r = cend;
+          while (l < r) {
+            const uint32_t mid = (l + r) >> 1;
+            if (Ps[mid] <= pp) l = mid + 1;
+            else r = mid;
+          }
+          v[u] = kbase + l;
+        }
+        q = make_uint4(v[0], v[1], v[2], v[3]);
       } else {  // count marks of the sub-block's starts, then a warp scan
         const uint32_t be = hi - b0 > 128 ? b0 + 127 : hi - 1;  // (>= lo >= sh)
         uint32_t i1 = c0;

@@ -15,9 +15,17 @@ import paper_2605_16667_b200 as ds  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 verbose = len(sys.argv) > 2
-cfg = bench.CONFIGS[cfgname]
+if cfgname in bench.CONFIGS:
+    cfg = bench.CONFIGS[cfgname]
+else:  # "n,U,dist" (a synth distribution)
+    n_, U_, d_ = cfgname.split(",")
+    cfg = dict(n=int(float(n_)), U=int(U_), dist=d_)
 dev = torch.device("cuda:0")
-keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
+if cfgname in bench.CONFIGS:
+    keys = [bench.make_device_input(cfg, 20260321, dev) for _ in range(5)]
+else:
+    import synth
+    keys = [torch.from_numpy(synth.make(cfg["dist"], cfg["n"], cfg["U"], 20260321 + i)).to(dev) for i in range(5)]
 outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = True
