@@ -137,7 +137,8 @@ __device__ __forceinline__ void decode_range(int32_t* __restrict__ out, uint32_t
 // a quad).
 constexpr uint32_t kFTblCap = kFSlot / 4;  // 4884 sub-blocks per window (one staging slot)
 __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint32_t kbase, uint32_t lo, uint32_t hi,
-                                            uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out) {
+                                            uint4* T, uint32_t* wc, uint32_t* red, int32_t* __restrict__ out,
+                                            PhaseTimes* pt = nullptr) {
   __shared__ uint32_t s_ib[2];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t ltmask = (1u << lane) - 1u;
@@ -179,13 +180,51 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
         continue;
       }
     }
-    for (uint32_t i = ia + threadIdx.x; i < ib; i += blockDim.x) {
-      const uint32_t p = Ps[i] + sh, j = (p >> 7) - jw, q = (p >> 2) & 31u;
-      uint32_t* t = reinterpret_cast<uint32_t*>(T + j);
-      const uint32_t old = atomicOr(t + 1, 1u << q);
-      atomicAdd(t, 1u);
-      if ((old >> q) & 1u) atomicOr(t, 0x80000000u);  // a second start in the quad
-      atomicOr(t + 2 + (q >> 4), (p & 3u) << (2 * (q & 15u)));
+    if (ib - ia <= 8u * nsb) {  // (uniform) few starts per sub-block: one set of atomics per start
+      for (uint32_t i = ia + threadIdx.x; i < ib; i += blockDim.x) {
+        const uint32_t p = Ps[i] + sh, j = (p >> 7) - jw, q = (p >> 2) & 31u;
+        uint32_t* t = reinterpret_cast<uint32_t*>(T + j);
+        const uint32_t old = atomicOr(t + 1, 1u << q);
+        atomicAdd(t, 1u);
+        if ((old >> q) & 1u) atomicOr(t, 0x80000000u);  // a second start in the quad
+        atomicOr(t + 2 + (q >> 4), (p & 3u) << (2 * (q & 15u)));
+      }
+    } else {
+      // many starts per sub-block (short bins): a warp takes 32 consecutive starts — ascending
+      // positions, so the starts of one sub-block are consecutive lanes — and reduces each
+      // sub-block's segment to its first lane (segmented shuffles), which does the atomics once:
+      // per-start atomics on a few entries serialised (n = 3e5, U = 65536 skewed: 7.5 us tables)
+      for (uint32_t base = ia + 32 * w; base < ib; base += 32 * (blockDim.x >> 5)) {
+        const uint32_t i = base + lane;
+        const bool v = i < ib;
+        const uint32_t p = v ? Ps[i] + sh : 0u, j = v ? (p >> 7) - jw : 0xffffffffu, q = (p >> 2) & 31u;
+        const uint32_t jp = __shfl_up_sync(FULL, j, 1), qp = __shfl_up_sync(FULL, q, 1);
+        const bool head = v && (lane == 0 || jp != j);
+        uint32_t occ = v ? 1u << q : 0u, cnt = v ? 1u : 0u;
+        uint32_t zb = v && q < 16 ? (p & 3u) << (2 * q) : 0u, wb = v && q >= 16 ? (p & 3u) << (2 * (q - 16)) : 0u;
+        uint32_t dq = v && lane > 0 && jp == j && qp == q ? 1u : 0u;  // shares its quad with the previous start
+#pragma unroll
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+          const uint32_t jd = __shfl_down_sync(FULL, j, d), od = __shfl_down_sync(FULL, occ, d);
+          const uint32_t cd = __shfl_down_sync(FULL, cnt, d), zd = __shfl_down_sync(FULL, zb, d);
+          const uint32_t wd = __shfl_down_sync(FULL, wb, d), dd = __shfl_down_sync(FULL, dq, d);
+          if (lane + d < 32 && jd == j) {
+            occ |= od;
+            cnt += cd;
+            zb |= zd;
+            wb |= wd;
+            dq |= dd;
+          }
+        }
+        if (head) {
+          uint32_t* t = reinterpret_cast<uint32_t*>(T + j);
+          const uint32_t old = atomicOr(t + 1, occ);
+          atomicAdd(t, cnt);
+          if (dq || (old & occ)) atomicOr(t, 0x80000000u);  // two starts in a quad
+          if (zb) atomicOr(t + 2, zb);
+          if (wb) atomicOr(t + 3, wb);
+        }
+      }
     }
     __syncthreads();
     {  // c0[j] = ia + Σ_{j' < j} #starts(j'): up to 5 consecutive entries per thread
@@ -206,6 +245,7 @@ __device__ __forceinline__ void project_tbl(const uint32_t* Ps, uint32_t m, uint
       }
     }
     __syncthreads();
+    phase_mark(pt, 13);  // (debug: table built)
     // (per lane: the quad-offset shift and the word of the start offsets are loop constants; T is
     //  read through its 32-bit shared address — the generic pointer's window base was otherwise
     //  re-derived every iteration; a full aligned sub-block stores without per-lane bounds tests)
@@ -770,7 +810,8 @@ __device__ __forceinline__ void sort_step(const void* __restrict__ keys, uint64_
       const uint32_t p0 = max(lo, ts[pt0 - x0]), p1 = min(hi, ts[pt1 - x0]);
       if (p0 < p1) {
         project_tbl(Pw, m, (uint32_t)key_base + pt0 * kFTileBins - 1, p0, p1,
-                    reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc, reinterpret_cast<uint32_t*>(red64), out);
+                    reinterpret_cast<uint4*>(sh + kFOffStage + kFSlot), wc, reinterpret_cast<uint32_t*>(red64), out,
+                    a.pt);
         if (a.dec) decode_range(out, p0, p1, a.dec);
       }
       __syncthreads();  // Pw is reused by the next pass

@@ -30,7 +30,7 @@ outs = [torch.empty_like(k) for k in keys]
 ctx = ds.Context(0, max_n=cfg["n"], max_U=max(cfg["U"], 256))
 fused = True
 names = ["ingest", "sync", "flush", "barrier1", "offsets", "batch_staged", "merged", "end", "flags_ready",
-         "proj_start", "m_reduced", "flush_loop", "r_rows", "r_synced", "m_scanned", "m_Pwritten"]
+         "proj_start", "m_reduced", "flush_loop", "r_rows", "tbl_built", "m_scanned", "m_Pwritten"]
 for rep in range(4):
     ctx.debug_phase_cta()
     for _ in range(int(os.environ.get("PHASE_BACK_TO_BACK", "1"))):  # stamps: the last launch
