@@ -635,7 +635,9 @@ __device__ __forceinline__ void hist_ingest_flush(const void* __restrict__ keys_
         if (g >= lim) break;  // (uint4 lim .. tot hold bins >= U: zero)
         const uint4 w = wv[u];
         uint32_t word, v = 0;
-        if (((w.x | w.y | w.z | w.w) & 0xFFF0FFF0u) == 0u) {
+        // (warp-uniform choice: a warp with one exception lane would otherwise run both paths —
+        //  under Zipf nearly every warp of the flush has one)
+        if (!__any_sync(__activemask(), ((w.x | w.y | w.z | w.w) & 0xFFF0FFF0u) != 0u)) {
           // fast path, all 8 counts <= 15: word j holds (c_{2j+1} << 16 | c_{2j}), so
           // (w | w >> 12) & 0xff = c_{2j} | c_{2j+1} << 4, and PRMT gathers the 4 bytes
           const uint32_t bx = w.x | (w.x >> 12), by = w.y | (w.y >> 12);
