@@ -534,7 +534,7 @@ int enqueue_reconstruct_fused(dialsort_ctx c, const uint32_t* H, uint32_t U, int
   int fmt;
   uint32_t C;
   size_t smem;
-  const uint64_t want = std::max<uint64_t>(cdiv(cap / 4 + 1, 1024ull * kHistUnroll * 2), cdiv(U, 1024));
+  const uint64_t want = std::max<uint64_t>(cdiv(cap / 4 + 1, 8192ull), cdiv(U, 1024));  // (32768 outputs a CTA)
   const uint32_t Cr = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, std::min<uint64_t>(c->nsm, kFMaxRows)));
   if ((rc = build_fused_args(c, a, fmt, C, smem, cap, U, nullptr, epoch, nullptr, nullptr, 4, false, nullptr, 0, 0, 0,
                              nullptr, nullptr, Cr, 2)))

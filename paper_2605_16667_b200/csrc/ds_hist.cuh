@@ -23,7 +23,13 @@ constexpr uint32_t kSmem16MaxBins = 98304;  // 192 KB of packed counters (49152 
 constexpr uint32_t kFTileBins = 64;         // scan-tile width of k_sort_fused (ds_fused.cuh)
 // int4 loads per batch, 2 batches in flight (5 or 6 per batch measured slower: c2 27.4 -> 28.6 /
 // 29.2 us single call, 17.8 -> 18.4 / 18.1 us batched — register pressure at 1024 threads)
-constexpr int kHistUnroll = 4;
+// Vectors per batch of the int32 ingestion (two batches in flight per thread): 3 measured
+// better than round 1's 4 on every config (c2 single call 27.8 -> 27.0 us, batched 17.6 ->
+// 17.5; Zipf 22.5 -> 22.0 batched; sorted 19.1 -> 18.65) — the loads are not what bounds it.
+#ifndef DIALSORT_HIST_UNROLL
+#define DIALSORT_HIST_UNROLL 3
+#endif
+constexpr int kHistUnroll = DIALSORT_HIST_UNROLL;
 constexpr uint32_t kFOwnVote = 255;         // k_sort_fused: owner-counter slot of the skew vote
 
 // Key layout shared by every pass over `keys`: `head` scalars before the first 16-byte
