@@ -56,14 +56,14 @@ enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
   KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
   KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
-  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_COUNT
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_PART_RING, KID_PART_COMPACT, KID_PART_MOVE, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {
     "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
     "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_place",
     "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
     "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch", "k_part_sample",
-    "k_part_place_est", "k_part_fin"};
+    "k_part_place_est", "k_part_fin", "k_part_place_ring", "k_part_ring_compact", "k_part_ring_move"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -213,7 +213,7 @@ struct dialsort_ctx_s {
   int nsm = 148;
   uint32_t epoch = 0;
   DBuf partials, P, tfb, ws_total, ovfH, status, stage, Hws, range_tot, gridbar, tsums, radix_tmp, radix_hist,
-      fused_tiles, Hx, part, htmp, qtmp, psamp;
+      fused_tiles, Hx, part, htmp, qtmp, psamp, ringws;
   DevStatus* host_status = nullptr;  // pinned mirror
   // gridbar layout: [0] GridBar of k_scan, [32] GridBarR of the radix passes, [64] FusedState of
   // the fused step, [128] GridBar of the query kernels (all zero at creation)
@@ -318,6 +318,8 @@ int ctx_init(dialsort_ctx c) {
   DS_CUDA(cudaFuncSetAttribute(k_reconstruct_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_part_scatter_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)part_wide_smem(kPartMaxBlocksWide)));
+  DS_CUDA(cudaFuncSetAttribute(k_part_place_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)part_ring_smem(kRpMaxB)));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -551,6 +553,14 @@ int enqueue_reconstruct_fused(dialsort_ctx c, const uint32_t* H, uint32_t U, int
   return DIALSORT_OK;
 }
 
+bool part_ring_enabled() {  // (DIALSORT_PART_RING=0: the sub-tile placement k_part_place<true>, A/B only)
+  static const bool v = [] {
+    const char* e = getenv("DIALSORT_PART_RING");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 bool hier_batched() {  // (DIALSORT_HIER_BATCH=0: one launch per block, A/B only)
   static const bool v = [] {
     const char* e = getenv("DIALSORT_HIER_BATCH");
@@ -577,8 +587,39 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
   // (+ a 4096-key trash area for the runs of an overflowed region; positions stay below 2^32)
   const uint64_t tcap = n + n / 4 + 512ull * B;
   const bool sampled = !wide && c->part_mode != 1 && tcap + kPartTile < (1ull << 32);
+  // ring placement (k_part_place_ring, B <= kRpMaxB): the regions also hold every warp's unused
+  // claimed units and tail remainder (part_ring_extra); the B tail pools follow them
+  RingWs rw;
+  memset(&rw, 0, sizeof rw);
+  uint64_t ring_extra = 0, tslots = sampled ? tcap + kPartTile : n;
+  uint32_t Gr = 0;
+  if (sampled && B <= kRpMaxB && part_ring_enabled()) {
+    int occ = 0;
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_part_place_ring, kRpThreads, part_ring_smem(B)));
+    const uint32_t g = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)c->nsm * std::max(occ, 1), cdiv(n, kRpWarps * 4096ull)));
+    const uint64_t W = (uint64_t)g * kRpWarps, extra = part_ring_extra((uint32_t)W);
+    const uint64_t tail0 = round_up(tcap + (uint64_t)B * (extra + kRpUnit), kRpUnit);
+    const uint64_t need = tail0 + (uint64_t)B * kRpUnit * W;
+    if (need < (1ull << 32)) {
+      if ((rc = c->ringws.ensure(4ull * ((uint64_t)B * (kRpSubs + 1) * kFillStride + 4ull * B * W +
+                                         2ull * B * kRpMaxHoles + 4ull * B))))
+        return rc;
+      Gr = g;
+      rw.W = (uint32_t)W;
+      rw.tailcap = (uint32_t)(kRpUnit * W);
+      rw.tail0 = tail0;
+      rw.sub = c->ringws.as<uint32_t>();
+      rw.tfill = rw.sub + (uint64_t)B * kRpSubs * kFillStride;
+      rw.holes = rw.tfill + (uint64_t)B * kFillStride;
+      rw.list = rw.holes + 4ull * B * W;
+      rw.meta = rw.list + 2ull * B * kRpMaxHoles;
+      ring_extra = extra;
+      tslots = need;
+    }
+  }
   if ((rc = c->part.ensure(4ull * Gp * B + 160ull * B + 64))) return rc;
-  if ((rc = c->htmp.ensure(2ull * (sampled ? tcap + kPartTile : n) + 16))) return rc;  // uint16 block keys
+  if ((rc = c->htmp.ensure(2ull * tslots + 16))) return rc;  // uint16 block keys
   PartWs w;
   w.bsz = c->part.as<uint64_t>();
   w.boff = w.bsz + B;
@@ -597,10 +638,20 @@ int enqueue_hier(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, ui
   } else {
     const uint32_t* gate = nullptr;
     if (sampled) {  // (part_mode 2: no margins — overflows, tests the exact schedule behind it)
+      // (part_mode 2: no margins — not even the ring's — so the regions overflow)
       DS_CUDA(launch_k(KID_PART_SAMPLE, k_part_sample, dim3(kSampleCtas), dim3(kSampleThreads), 0, s, keys, n, U, B,
-                       w, c->part_mode == 2 ? (uint64_t)0 : tcap, c->psamp.as<uint32_t>()));
-      DS_CUDA(launch_k(KID_PART_SCATTER_EST, k_part_place<true>, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B, w,
-                       tmp, (const uint32_t*)nullptr, (uint32_t)tcap));
+                       w, c->part_mode == 2 ? (uint64_t)0 : tcap, c->psamp.as<uint32_t>(),
+                       c->part_mode == 2 && ring_extra ? (uint64_t)kRpUnit : ring_extra, rw));
+      if (Gr) {
+        DS_CUDA(launch_k(KID_PART_RING, k_part_place_ring, dim3(Gr), dim3(kRpThreads), part_ring_smem(B), s, keys, n,
+                         U, B, w, rw, tmp));
+        DS_CUDA(launch_k(KID_PART_COMPACT, k_part_ring_compact, dim3(B), dim3(1024), 0, s, B, w, rw));
+        DS_CUDA(launch_k(KID_PART_MOVE, k_part_ring_move, dim3(B * kRpMoveCtas), dim3(512), 0, s, B, w, rw, tmp));
+        DS_CUDA(launch_k(KID_PART_MOVE, k_part_ring_tail, dim3(B * kRpMoveCtas), dim3(512), 0, s, B, w, rw, tmp));
+      } else {
+        DS_CUDA(launch_k(KID_PART_SCATTER_EST, k_part_place<true>, dim3(Gp), dim3(kPartThreads), 0, s, keys, n, U, B,
+                         w, tmp, (const uint32_t*)nullptr, (uint32_t)tcap));
+      }
       DS_CUDA(launch_k(KID_PART_FIN, k_part_fin, dim3(1), dim3(1024), 0, s, B, w));
       gate = w.ovf;  // the exact schedule below runs only after an overflow
     }
@@ -884,7 +935,7 @@ int dialsort_ctx_destroy(dialsort_ctx c) {
     }
   for (DBuf* b : {&c->partials, &c->P, &c->tfb, &c->ws_total, &c->ovfH, &c->status, &c->stage, &c->Hws,
                   &c->range_tot, &c->gridbar, &c->tsums, &c->radix_tmp, &c->radix_hist, &c->fused_tiles, &c->Hx,
-                  &c->part, &c->htmp, &c->qtmp, &c->psamp})
+                  &c->part, &c->htmp, &c->qtmp, &c->psamp, &c->ringws})
     b->release();
   if (c->host_status) cudaFreeHost(c->host_status);
   if (c->pt && c->owns_pt) cudaFree(c->pt);

@@ -50,6 +50,46 @@ struct PartWs {
   uint32_t* fill;  // [B * kFillStride] sampled schedule: keys placed per block so far
   uint32_t* ovf;   // sampled schedule: a region overflowed -> the exact schedule runs
 };
+// ---- ring placement constants (k_part_place_ring below; sampled schedule, B <= kRpMaxB) ----
+#ifndef DIALSORT_RP_THREADS
+#define DIALSORT_RP_THREADS 256
+#endif
+constexpr uint32_t kRpThreads = DIALSORT_RP_THREADS, kRpWarps = kRpThreads / 32;
+#ifndef DIALSORT_RP_UNIT
+#define DIALSORT_RP_UNIT 128
+#endif
+constexpr uint32_t kRpUnit = DIALSORT_RP_UNIT;  // keys a unit (128: 256 bytes of uint16)
+constexpr uint32_t kRpRing = 2 * kRpUnit;       // ring entries per (warp, block)
+constexpr uint32_t kRpCheck = kRpUnit / 32;     // key slots (32 keys each) between the flush checks
+constexpr uint32_t kRpKPL = kRpUnit / 32;       // keys a lane sends of a unit (8, 4 or 2: 16, 8 or 4 bytes)
+static_assert(kRpUnit == 64 || kRpUnit == 128 || kRpUnit == 256, "ring unit");
+static_assert(kRpUnit - 1 + 32 * kRpCheck <= kRpRing, "a ring holds what accumulates between checks");
+constexpr uint32_t kRpSubs = 16;          // unit counters per block
+constexpr uint32_t kRpClaim = 4;          // units per claim
+constexpr uint32_t kRpMaxB = 16;
+constexpr uint32_t kRpMaxHoles = 131072;  // hole units per block the compaction takes (more: ovf)
+#ifndef DIALSORT_RP_MINB
+#define DIALSORT_RP_MINB (DIALSORT_RP_UNIT == 128 ? 3 : 6)  // (shared memory: 66 / 33 KB a CTA at B = 16)
+#endif
+struct RingWs {
+  uint32_t* sub;    // [B][kRpSubs] units claimed per counter (kFillStride words apart)
+  uint32_t* tfill;  // [B] tail-pool fills (kFillStride words apart)
+  uint32_t* holes;  // [B][W] 2 x (first unit, count) of each warp's unused claimed units
+  uint32_t* list;   // [B][2][kRpMaxHoles] compaction scratch (hole units below F, filled units above)
+  uint32_t* meta;   // [B][4] compaction: moves, F
+  uint64_t tail0;   // first slot of the tail pools in tmp; pool b starts at tail0 + b * tailcap
+  uint32_t tailcap; // slots per tail pool (>= (kRpUnit - 1) W)
+  uint32_t W;       // warps of the placement grid
+};
+__host__ __device__ constexpr size_t part_ring_smem(uint32_t B) {
+  return 4ull * kRpWarps * 32 + 2ull * kRpWarps * B * kRpRing;
+}
+// Region slots a block needs beyond its keys (whole units): every warp's unused claimed units and
+// tail remainder, and the unit counters' imbalance.
+__host__ __device__ constexpr uint64_t part_ring_extra(uint32_t W) {
+  return (uint64_t)kRpUnit * ((uint64_t)W * (2 * kRpClaim + 1) + 64ull * kRpSubs);
+}
+
 // Gate of the exact schedule's kernels when they back up the sampled one: run only after an
 // overflow (nullptr: always run).
 __device__ __forceinline__ bool part_gated_off(const uint32_t* gate) {
@@ -174,9 +214,12 @@ __device__ __forceinline__ uint32_t part_hash(uint32_t x) {
   return x;
 }
 constexpr uint32_t kSampleCtas = 64, kSampleThreads = 256;  // 4 samples per thread
+// ring_extra > 0 (k_part_place_ring): capacities rounded to whole units plus ring_extra slots;
+// the ring's unit counters and tail fills are reset.
 __global__ void __launch_bounds__(kSampleThreads) k_part_sample(const int32_t* __restrict__ keys, uint64_t n,
                                                                 uint32_t U, uint32_t B, PartWs w, uint64_t tcap,
-                                                                uint32_t* __restrict__ sacc) {
+                                                                uint32_t* __restrict__ sacc, uint64_t ring_extra,
+                                                                RingWs r) {
   // sacc: [kPartMaxBlocks] sample counts of the whole grid, [kPartMaxBlocks] the CTA ticket —
   // zero between launches (the last CTA resets them)
   constexpr uint32_t kPer = kPartSample / (kSampleCtas * kSampleThreads);
@@ -233,7 +276,13 @@ __global__ void __launch_bounds__(kSampleThreads) k_part_sample(const int32_t* _
   __syncthreads();
   uint64_t cap = est + (uint64_t)((double)mar * s_scale);
   if (cap > n) cap = n;
+  if (ring_extra) cap = ((cap + kRpUnit - 1) & ~(uint64_t)(kRpUnit - 1)) + ring_extra;
   if (threadIdx.x >= B) cap = 0;
+  if (ring_extra)
+    for (uint32_t i = threadIdx.x; i < B * (kRpSubs + 1); i += blockDim.x) {
+      if (i < B * kRpSubs) r.sub[(uint64_t)i * kFillStride] = 0;
+      else r.tfill[(uint64_t)(i - B * kRpSubs) * kFillStride] = 0;
+    }
   unsigned long long tot_cap;
   const uint64_t start = block_excl_scan<unsigned long long>(cap, tot_cap, red);
   if (threadIdx.x < B) {
@@ -459,6 +508,291 @@ __global__ void __launch_bounds__(kPartThreads, DIALSORT_PART_MINB) k_part_place
   __syncthreads();  // the last sub-tile's staging and deltas
   write_out(p);
 #undef DS_PART_LOAD
+  pdl_trigger();
+}
+
+// ---- ring placement (sampled schedule, B <= 16: the c4 path) --------------------------------
+// The same MSD split without any CTA-wide step: order inside a universe block is free (its
+// histogram is order-free, eq:ingestion P:409-412), so every warp places its own keys alone.
+// A warp keeps, per block, a kRpRing-entry ring of low-16-bit keys in shared memory: a key
+// takes the next ring slot from the counting atomic (one ATOMS; no rank scan, no barrier), and
+// every kRpCheck key slots each ring holding a whole unit (kRpUnit keys) sends it as one
+// coalesced 256-byte store.  Units are claimed from the block's region by global atomics on
+// kRpSubs counters per block (unit k + kRpSubs j of counter k), kRpClaim units a claim; the
+// next claim is issued when the current one's first unit is used, so its round trip is hidden.
+// At the end a warp's ring remainders (< kRpUnit keys per block) go to the block's tail pool
+// (exact claims) and its unused claimed units are recorded as holes; k_part_ring_compact /
+// _move / _tail then make each region dense (the filled units above F fill the holes below
+// it, the tail pool follows at unit F).  A claim past the region's capacity raises ovf (the
+// exact schedule then redoes the placement, as for k_part_place<true>).  Bad keys are
+// recorded here.
+__device__ __forceinline__ uint32_t rp_atom_inc(uint32_t a) {
+  uint32_t v;
+  asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void rp_st16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint32_t rp_ld32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 rp_ld64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__global__ void __launch_bounds__(kRpThreads, DIALSORT_RP_MINB) k_part_place_ring(const int32_t* __restrict__ keys,
+                                                                                 uint64_t n, uint32_t U, uint32_t B,
+                                                                                 PartWs w, RingWs r,
+                                                                                 uint16_t* __restrict__ tmp) {
+  extern __shared__ __align__(16) unsigned char rp_smem[];
+  uint32_t* const cur_all = reinterpret_cast<uint32_t*>(rp_smem);          // [kRpWarps][32] ring fills
+  uint16_t* const ring_all = reinterpret_cast<uint16_t*>(cur_all + kRpWarps * 32);  // [kRpWarps][B][kRpRing]
+  pdl_wait();
+  const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5, gw = blockIdx.x * kRpWarps + wl;
+  for (uint32_t i = threadIdx.x; i < kRpWarps * 32; i += blockDim.x) cur_all[i] = 0;
+  __syncthreads();
+  const uint32_t cur_s = smem_addr(cur_all) + 128u * wl;               // this warp's fills
+  const uint32_t ring_s = smem_addr(ring_all) + 2u * kRpRing * B * wl;  // this warp's rings
+  const uint32_t my_cur = cur_s + 4u * lane;  // (lanes >= B: a fill that stays 0)
+  const bool own = lane < B;                  // lane b keeps the state of block b's ring
+  // (a lane sends kRpKPL keys of a unit: element e of tmp as uint2 / uint32 holds keys kRpKPL e ..)
+  const uint32_t koffe = own ? (uint32_t)(w.koff[lane] / kRpKPL) : 0u, capu = own ? (uint32_t)(w.cap[lane] / kRpUnit) : 0u;
+  uint32_t* const my_sub = r.sub + (uint64_t)(own ? lane : 0u) * kRpSubs * kFillStride;
+  uint32_t fl = 0;  // keys of the ring already sent (a multiple of kRpUnit)
+  // claims (unit k + kRpSubs j, j = jc .. jc + kRpClaim - 1 on counter k): the current one (kc,
+  // jc, cu used) and the next one (kn, jn); dst: element index of the next unit (~0u: past capacity)
+  uint32_t kc = (gw + lane) % kRpSubs, jc = 0, cu = 0, kn = 0, jn = 0, dst = ~0u;
+  bool started = false, has_next = false;
+  auto set_dst = [&]() {
+    const uint32_t unit = kc + kRpSubs * (jc + cu);
+    dst = unit < capu ? koffe + 32u * unit : ~0u;
+  };
+  auto first_claim = [&]() {
+    jc = atomicAdd(my_sub + kc * kFillStride, kRpClaim);
+    started = true;
+    set_dst();
+  };
+  auto advance = [&]() {  // (owner lane, after its unit left)
+    // (the switch reads jn before a new claim overwrites it: an instruction reading the
+    //  register of an atomic in flight waits for it, even predicated off)
+    fl += kRpUnit;
+    if (++cu == kRpClaim) {
+      kc = kn;
+      jc = jn;
+      cu = 0;
+      has_next = false;
+    } else if (cu == 1) {
+      kn = (kc + 1) & (kRpSubs - 1);
+      jn = atomicAdd(my_sub + kn * kFillStride, kRpClaim);
+      has_next = true;
+    }
+    set_dst();
+  };
+  auto flush = [&](uint32_t bb) {  // (whole warp) ring bb's next unit -> tmp
+    if (lane == bb && !started) first_claim();
+    const uint32_t d = __shfl_sync(FULL, dst, bb), f = __shfl_sync(FULL, fl, bb);
+    const uint32_t ra = ring_s + 2u * kRpRing * bb + 2u * ((f + kRpKPL * lane) & (kRpRing - 1));
+    if (d != ~0u) {
+      if constexpr (kRpKPL == 8) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra) : "memory");
+        __stcs(reinterpret_cast<uint4*>(tmp) + d + lane, v);
+      } else if constexpr (kRpKPL == 4) {
+        __stcs(reinterpret_cast<uint2*>(tmp) + d + lane, rp_ld64(ra));
+      } else {
+        __stcs(reinterpret_cast<unsigned int*>(tmp) + d + lane, rp_ld32(ra));
+      }
+    } else if (lane == 0) {
+      atomicOr(w.ovf, 1u);
+    }
+    if (lane == bb) advance();
+  };
+  auto check = [&]() {  // (whole warp) send every whole unit; first claims of rings holding keys
+    __syncwarp();
+    const uint32_t c = rp_ld32(my_cur) - fl;
+    if (own && !started && c) first_claim();
+    uint32_t need = __ballot_sync(FULL, c >= kRpUnit);
+    if (need) {
+      do {
+        flush(__ffs(need) - 1);
+        need &= need - 1;
+      } while (need);
+      __syncwarp();  // the flushes' ring reads before the next slots' writes
+    }
+  };
+  auto slot = [&](uint32_t key) {
+    const uint32_t b = key >> kPartShift;
+    const uint32_t sl = rp_atom_inc(cur_s + 4u * b);
+    rp_st16(ring_s + 2u * kRpRing * b + 2u * (sl & (kRpRing - 1)), key);
+  };
+  auto slot_checked = [&](uint32_t key, uint64_t idx, bool present) {
+    if (present) {
+      if (key < U) slot(key);
+      else record_bad(w.st, idx, key);
+    }
+  };
+  const KeySpan s = make_span(keys, n);
+  const int4* __restrict__ body = s.body();
+  const uint64_t v0 = s.n4 * gw / r.W, v1 = s.n4 * (gw + 1) / r.W;
+  if (gw == 0) slot_checked(lane < s.head ? (uint32_t)keys[lane] : 0u, lane, lane < s.head);
+  if (gw == r.W - 1) {
+    const uint64_t i = s.head + 4 * s.n4 + lane;
+    slot_checked(lane < s.tail ? (uint32_t)keys[i] : 0u, i, lane < s.tail);
+  }
+  check();
+  const uint64_t pol = l2_evict_first_policy();
+  int4 a0 = make_int4(0, 0, 0, 0), a1 = a0;
+  if (v0 + lane < v1) a0 = ld_stream4(body + v0 + lane, pol);
+  if (v0 + 32 + lane < v1) a1 = ld_stream4(body + v0 + 32 + lane, pol);
+  for (uint64_t vb = v0; vb < v1; vb += 64) {
+    const uint64_t vn = vb + 64 + lane;
+    int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+    if (vn < v1) b0 = ld_stream4(body + vn, pol);
+    if (vn + 32 < v1) b1 = ld_stream4(body + vn + 32, pol);
+    const uint32_t k8[8] = {(uint32_t)a0.x, (uint32_t)a0.y, (uint32_t)a0.z, (uint32_t)a0.w,
+                            (uint32_t)a1.x, (uint32_t)a1.y, (uint32_t)a1.z, (uint32_t)a1.w};
+    if (vb + 64 <= v1 && __all_sync(FULL, umax4(a0) < U && umax4(a1) < U)) {
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        slot(k8[q]);
+        if ((q + 1) % kRpCheck == 0) check();
+      }
+    } else {
+      const bool p0 = vb + lane < v1, p1 = vb + 32 + lane < v1;
+      const uint64_t i0 = s.head + 4 * (vb + lane), i1 = i0 + 128;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        slot_checked(k8[q], (q < 4 ? i0 : i1) + (q & 3), q < 4 ? p0 : p1);
+        if ((q + 1) % kRpCheck == 0) check();
+      }
+    }
+    a0 = b0;
+    a1 = b1;
+  }
+  // ring remainders -> the blocks' tail pools; unused claimed units -> holes
+  __syncwarp();
+  const uint32_t rem = rp_ld32(my_cur) - fl;  // (< kRpUnit; 0 on lanes >= B)
+  uint32_t t0 = 0;
+  if (rem) t0 = atomicAdd(r.tfill + (uint64_t)lane * kFillStride, rem);
+  uint32_t need = __ballot_sync(FULL, rem != 0);
+  while (need) {
+    const uint32_t bb = __ffs(need) - 1;
+    need &= need - 1;
+    const uint32_t rr = __shfl_sync(FULL, rem, bb), tt = __shfl_sync(FULL, t0, bb), f = __shfl_sync(FULL, fl, bb);
+    if (tt + rr > r.tailcap) {
+      if (lane == 0) atomicOr(w.ovf, 1u);
+      continue;
+    }
+    for (uint32_t i = lane; i < rr; i += 32)
+      tmp[r.tail0 + (uint64_t)bb * r.tailcap + tt + i] = ring_all[(wl * B + bb) * kRpRing + ((f + i) & (kRpRing - 1))];
+  }
+  if (own) {
+    uint4 h = make_uint4(0u, 0u, 0u, 0u);
+    if (started) h.x = kc + kRpSubs * (jc + cu), h.y = kRpClaim - cu;
+    if (has_next) h.z = kn + kRpSubs * jn, h.w = kRpClaim;
+    reinterpret_cast<uint4*>(r.holes)[(uint64_t)lane * r.W + gw] = h;
+  }
+  pdl_trigger();
+}
+
+// One CTA per block: the move lists of block b.  Units are claimed densely per counter, so the
+// units of [0, Utot = kRpSubs max_k f_k) all hold kRpUnit keys except the holes: the warps'
+// unused claimed units and, per counter k, the units k + kRpSubs j of f_k <= j < max f.  With
+// Hc holes, F = Utot - Hc units hold keys: the filled units of [F, Utot) (list sl) move into
+// the holes below F (list dl) — order inside a block is free — then the tail pool is
+// appended at unit F (k_part_ring_move, k_part_ring_tail: many CTAs per block).
+__global__ void __launch_bounds__(1024) k_part_ring_compact(uint32_t B, PartWs w, RingWs r) {
+  __shared__ uint32_t bits[kRpMaxHoles / 32];
+  __shared__ uint32_t s_f[kRpSubs];
+  __shared__ uint32_t red[34];
+  __shared__ uint32_t s_nd, s_ns;
+  pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(w.ovf)) {
+    pdl_trigger();
+    return;
+  }
+  const uint32_t b = blockIdx.x, T = blockDim.x;
+  if (threadIdx.x < kRpSubs) s_f[threadIdx.x] = r.sub[((uint64_t)b * kRpSubs + threadIdx.x) * kFillStride];
+  if (threadIdx.x == 0) s_nd = s_ns = 0;
+  __syncthreads();
+  uint32_t fmax = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kRpSubs; ++k) fmax = max(fmax, s_f[k]);
+  const uint2* hl = reinterpret_cast<const uint2*>(r.holes) + 2ull * b * r.W;  // 2 per warp
+  uint32_t h = threadIdx.x < kRpSubs ? fmax - s_f[threadIdx.x] : 0u;
+  for (uint32_t g = threadIdx.x; g < 2 * r.W; g += T) h += hl[g].y;
+  uint32_t Hc;
+  block_excl_scan<uint32_t>(h, Hc, red);
+  const uint32_t Utot = kRpSubs * fmax, F = Utot - Hc;
+  if (Hc > kRpMaxHoles) {
+    if (threadIdx.x == 0) atomicOr(w.ovf, 1u);
+    pdl_trigger();
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < (Hc + 31) / 32; i += T) bits[i] = 0;
+  __syncthreads();
+  uint32_t* const dl = r.list + (uint64_t)b * 2 * kRpMaxHoles;  // hole units below F
+  uint32_t* const sl = dl + kRpMaxHoles;                         // filled units of [F, Utot)
+  auto hole = [&](uint32_t u) {
+    if (u >= F) atomicOr(&bits[(u - F) >> 5], 1u << ((u - F) & 31));
+    else dl[atomicAdd(&s_nd, 1u)] = u;
+  };
+  for (uint32_t g = threadIdx.x; g < 2 * r.W; g += T) {
+    const uint2 e = hl[g];
+    for (uint32_t i = 0; i < e.y; ++i) hole(e.x + kRpSubs * i);
+  }
+  if (threadIdx.x < kRpSubs)
+    for (uint32_t j = s_f[threadIdx.x]; j < fmax; ++j) hole(threadIdx.x + kRpSubs * j);
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < Hc; p += T)
+    if (!((bits[p >> 5] >> (p & 31)) & 1u)) sl[atomicAdd(&s_ns, 1u)] = F + p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    r.meta[4 * b] = s_nd;  // (== s_ns)
+    r.meta[4 * b + 1] = F;
+  }
+  pdl_trigger();
+}
+constexpr uint32_t kRpMoveCtas = 16;  // CTAs per block of the moves (grid B x kRpMoveCtas)
+__global__ void __launch_bounds__(512) k_part_ring_move(uint32_t B, PartWs w, RingWs r, uint16_t* __restrict__ tmp) {
+  pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(w.ovf)) {
+    pdl_trigger();
+    return;
+  }
+  const uint32_t b = blockIdx.x / kRpMoveCtas, part = blockIdx.x % kRpMoveCtas;
+  const uint32_t nd = r.meta[4 * b];
+  const uint32_t* const dl = r.list + (uint64_t)b * 2 * kRpMaxHoles;
+  const uint32_t* const sl = dl + kRpMaxHoles;
+  constexpr uint32_t V = kRpUnit / 8;  // 16-byte vectors a unit
+  uint4* const reg4 = reinterpret_cast<uint4*>(tmp + w.koff[b]);
+  for (uint32_t q = part * blockDim.x + threadIdx.x; q < V * nd; q += kRpMoveCtas * blockDim.x)
+    reg4[V * dl[q / V] + (q % V)] = reg4[V * sl[q / V] + (q % V)];
+  pdl_trigger();
+}
+// (after the moves: the tail lands on units >= F, which the moves read)
+__global__ void __launch_bounds__(512) k_part_ring_tail(uint32_t B, PartWs w, RingWs r, uint16_t* __restrict__ tmp) {
+  pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(w.ovf)) {
+    pdl_trigger();
+    return;
+  }
+  const uint32_t b = blockIdx.x / kRpMoveCtas, part = blockIdx.x % kRpMoveCtas;
+  const uint32_t F = r.meta[4 * b + 1];
+  const uint32_t tl = r.tfill[(uint64_t)b * kFillStride];
+  if ((uint64_t)kRpUnit * F + tl > w.cap[b]) {
+    if (part == 0 && threadIdx.x == 0) atomicOr(w.ovf, 1u);
+    pdl_trigger();
+    return;
+  }
+  const uint16_t* pool = tmp + r.tail0 + (uint64_t)b * r.tailcap;
+  uint16_t* const dst = tmp + w.koff[b] + (uint64_t)kRpUnit * F;
+  for (uint32_t i = part * blockDim.x + threadIdx.x; i < tl; i += kRpMoveCtas * blockDim.x) dst[i] = pool[i];
+  if (part == 0 && threadIdx.x == 0) w.fill[(uint64_t)b * kFillStride] = kRpUnit * F + tl;
   pdl_trigger();
 }
 
