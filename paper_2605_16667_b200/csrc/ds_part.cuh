@@ -63,6 +63,11 @@ constexpr uint32_t kRpRing = 2 * kRpUnit;       // ring entries per (warp, block
 constexpr uint32_t kRpCheck = kRpUnit / 32;     // key slots (32 keys each) between the flush checks
 constexpr uint32_t kRpKPL = kRpUnit / 32;       // keys a lane sends of a unit (8, 4 or 2: 16, 8 or 4 bytes)
 static_assert(kRpUnit == 64 || kRpUnit == 128 || kRpUnit == 256, "ring unit");
+#ifndef DIALSORT_RP_NV
+#define DIALSORT_RP_NV 4  // (2: 1.514 ms at c4, 3: 1.451, 4: 1.449)
+#endif
+constexpr uint32_t kRpNV = DIALSORT_RP_NV;      // 16-byte key vectors a lane per batch
+static_assert((4 * kRpNV) % kRpCheck == 0, "a batch ends on a flush check");
 static_assert(kRpUnit - 1 + 32 * kRpCheck <= kRpRing, "a ring holds what accumulates between checks");
 constexpr uint32_t kRpSubs = 16;          // unit counters per block
 constexpr uint32_t kRpClaim = 4;          // units per claim
@@ -645,33 +650,44 @@ __global__ void __launch_bounds__(kRpThreads, DIALSORT_RP_MINB) k_part_place_rin
   }
   check();
   const uint64_t pol = l2_evict_first_policy();
-  int4 a0 = make_int4(0, 0, 0, 0), a1 = a0;
-  if (v0 + lane < v1) a0 = ld_stream4(body + v0 + lane, pol);
-  if (v0 + 32 + lane < v1) a1 = ld_stream4(body + v0 + 32 + lane, pol);
-  for (uint64_t vb = v0; vb < v1; vb += 64) {
-    const uint64_t vn = vb + 64 + lane;
-    int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
-    if (vn < v1) b0 = ld_stream4(body + vn, pol);
-    if (vn + 32 < v1) b1 = ld_stream4(body + vn + 32, pol);
-    const uint32_t k8[8] = {(uint32_t)a0.x, (uint32_t)a0.y, (uint32_t)a0.z, (uint32_t)a0.w,
-                            (uint32_t)a1.x, (uint32_t)a1.y, (uint32_t)a1.z, (uint32_t)a1.w};
-    if (vb + 64 <= v1 && __all_sync(FULL, umax4(a0) < U && umax4(a1) < U)) {
+  // batches of kRpNV vectors a lane (32 kRpNV vectors a warp); the next batch is in flight while
+  // one is placed
+  constexpr uint32_t NV = kRpNV, BV = 32 * NV;
+  int4 a[NV];
 #pragma unroll
-      for (uint32_t q = 0; q < 8; ++q) {
-        slot(k8[q]);
+  for (uint32_t q = 0; q < NV; ++q) {
+    a[q] = make_int4(0, 0, 0, 0);
+    if (v0 + 32 * q + lane < v1) a[q] = ld_stream4(body + v0 + 32 * q + lane, pol);
+  }
+  for (uint64_t vb = v0; vb < v1; vb += BV) {
+    int4 nx[NV];
+#pragma unroll
+    for (uint32_t q = 0; q < NV; ++q) {
+      nx[q] = make_int4(0, 0, 0, 0);
+      if (vb + BV + 32 * q + lane < v1) nx[q] = ld_stream4(body + vb + BV + 32 * q + lane, pol);
+    }
+    bool ok = vb + BV <= v1;
+#pragma unroll
+    for (uint32_t q = 0; q < NV; ++q) ok = ok && umax4(a[q]) < U;
+    if (__all_sync(FULL, ok)) {
+#pragma unroll
+      for (uint32_t q = 0; q < 4 * NV; ++q) {
+        const int4& x = a[q / 4];
+        slot((uint32_t)(q % 4 == 0 ? x.x : q % 4 == 1 ? x.y : q % 4 == 2 ? x.z : x.w));
         if ((q + 1) % kRpCheck == 0) check();
       }
     } else {
-      const bool p0 = vb + lane < v1, p1 = vb + 32 + lane < v1;
-      const uint64_t i0 = s.head + 4 * (vb + lane), i1 = i0 + 128;
 #pragma unroll
-      for (uint32_t q = 0; q < 8; ++q) {
-        slot_checked(k8[q], (q < 4 ? i0 : i1) + (q & 3), q < 4 ? p0 : p1);
+      for (uint32_t q = 0; q < 4 * NV; ++q) {
+        const int4& x = a[q / 4];
+        const uint64_t v = vb + 32 * (q / 4) + lane;
+        slot_checked((uint32_t)(q % 4 == 0 ? x.x : q % 4 == 1 ? x.y : q % 4 == 2 ? x.z : x.w), s.head + 4 * v + q % 4,
+                     v < v1);
         if ((q + 1) % kRpCheck == 0) check();
       }
     }
-    a0 = b0;
-    a1 = b1;
+#pragma unroll
+    for (uint32_t q = 0; q < NV; ++q) a[q] = nx[q];
   }
   // ring remainders -> the blocks' tail pools; unused claimed units -> holes
   __syncwarp();
