@@ -15,9 +15,12 @@
 //   sampled (default): 6 bytes per key, one pass over the keys
 //     k_part_sample   a stratified sample of 65536 keys -> each block's key-region capacity
 //                     (estimate + 6 sigma) and start in tmp
-//     k_part_place<true>  4096-key sub-tiles staged by block; each run claims its place in
-//                     its block's region with one global atomic (regions fill densely; a
-//                     region that would overflow sets ovf and drops the run)
+//     k_part_place_ring   (B <= 16) every warp alone: per-(warp, block) shared-memory rings,
+//                     whole 128-key units stored into units claimed from the block's region;
+//                     then k_part_ring_compact / _move / _tail make the regions dense
+//     k_part_place<true>  (16 < B <= 64) 4096-key sub-tiles staged by block; each run claims
+//                     its place in its block's region with one global atomic (regions fill
+//                     densely; a region that would overflow sets ovf and drops the run)
 //     k_part_fin      block sizes and output starts from the fills (skipped after ovf)
 //   exact (after ovf — gated on it, no host round trip — or DIALSORT_OPT_PART_MODE = 1):
 //     k_part_count    per-CTA chunk: block counts (per-warp shared counters)      [G][B]
