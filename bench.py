@@ -304,6 +304,7 @@ def main():
     ap.add_argument("--seed", type=int, default=20260321)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-streams", type=int, default=2, help="contexts / streams of the e2e host-buffer pipeline")
     ap.add_argument("--grid", action="store_true", help="NEXT-2: the paper's 48-config grid (one JSON line each)")
     ap.add_argument("--batch", type=int, default=32,
                     help="steps per dialsort_sort_batch_async call (U <= 98304 at N=1; 1 = one sort per call)")
@@ -633,14 +634,16 @@ def main():
         # a pipeline of host batches: two contexts on two streams, so batch i+1's host->device
         # copy runs while batch i sorts and copies back (PCIe is full duplex); every step still
         # copies its whole input in and its whole sorted output out
+        NS = max(2, args.e2e_streams)
         xh = torch.empty(n, dtype=torch.int32, pin_memory=True)
         xh.copy_(ins[0][:n].cpu())
-        ohs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        ctxs = [ctx, dsl.Context(local, max_n=n, max_U=max(U, 256))]
+        ohs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(NS)]
+        ctxs = [ctx] + [dsl.Context(local, max_n=n, max_U=max(U, 256)) for _ in range(NS - 1)]
         if args.part_mode:
-            ctxs[1].set_option(dsl._lib.OPT_PART_MODE, args.part_mode)
-        sts = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-        for c in range(2):  # warm-up (and the staging buffers)
+            for c in ctxs[1:]:
+                c.set_option(dsl._lib.OPT_PART_MODE, args.part_mode)
+        sts = [torch.cuda.Stream(dev) for _ in range(NS)]
+        for c in range(NS):  # warm-up (and the staging buffers)
             with torch.cuda.stream(sts[c]):
                 ctxs[c].sort_host(xh, U, ohs[c])
         # (best of 3 wall-clock blocks, as the device reps: host-side PCIe / scheduling noise
@@ -651,9 +654,9 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for i in range(k2):
-                with torch.cuda.stream(sts[i % 2]):
-                    ctxs[i % 2].sort_host(xh, U, ohs[i % 2], wait=False)
-            for c in range(2):
+                with torch.cuda.stream(sts[i % NS]):
+                    ctxs[i % NS].sort_host(xh, U, ohs[i % NS], wait=False)
+            for c in range(NS):
                 with torch.cuda.stream(sts[c]):
                     ctxs[c].sync()
             walls.append((time.perf_counter() - t0) / k2)
@@ -661,8 +664,8 @@ def main():
         e2e = {"value": n / wall, "unit": "keys/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                "ms_per_step": wall * 1e3, "mean_ms_per_step": sum(walls) / len(walls) * 1e3,
                "blocks": len(walls), "steps_per_block": k2, "api": "dialsort_sort_host_async",
-               "pipeline": "2 contexts x 2 streams: batch i+1's H2D overlaps batch i's sort + D2H (wall clock)"}
-        e2e["verified"] = bool(np.array_equal(ohs[(k2 - 1) % 2].numpy(), ref)) if ref is not None else None
+               "pipeline": f"{NS} contexts x {NS} streams: batch i+1's H2D overlaps batch i's sort + D2H (wall clock)"}
+        e2e["verified"] = bool(np.array_equal(ohs[(k2 - 1) % NS].numpy(), ref)) if ref is not None else None
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
