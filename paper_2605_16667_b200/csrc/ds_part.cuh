@@ -74,7 +74,10 @@ static_assert((4 * kRpNV) % kRpCheck == 0, "a batch ends on a flush check");
 static_assert(kRpUnit - 1 + 32 * kRpCheck <= kRpRing, "a ring holds what accumulates between checks");
 constexpr uint32_t kRpSubs = 16;          // unit counters per block
 constexpr uint32_t kRpClaim = 4;          // units per claim
-constexpr uint32_t kRpMaxB = 16;
+#ifndef DIALSORT_RP_MAXB
+#define DIALSORT_RP_MAXB 16
+#endif
+constexpr uint32_t kRpMaxB = DIALSORT_RP_MAXB;
 constexpr uint32_t kRpMaxHoles = 131072;  // hole units per block the compaction takes (more: ovf)
 #ifndef DIALSORT_RP_MINB
 #define DIALSORT_RP_MINB (DIALSORT_RP_UNIT == 128 ? 3 : 6)  // (shared memory: 66 / 33 KB a CTA at B = 16)
