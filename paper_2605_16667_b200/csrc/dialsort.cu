@@ -11,6 +11,7 @@
 #include "../../include/dialsort.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // (header-only NVTX v3: a no-op unless a profiler is attached)
 
 #include <cstdio>
 #include <cstdlib>
@@ -832,16 +833,19 @@ int radix_enqueue(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out,
   return DIALSORT_OK;
 }
 
-// Makes `c`'s profiler the active one for launches made by this thread during an API call.
-// (and its cooperative-launch option)
+// Makes `c`'s profiler the active one for launches made by this thread during an API call
+// (and its cooperative-launch option), and brackets the call in an NVTX range named after the
+// entry point (ncu --nvtx --nvtx-include "dialsort_sort_async/" selects one call's kernels).
 struct ProfScope {
   Profiler* prev;
   bool prev_coop;
-  explicit ProfScope(dialsort_ctx c) : prev(g_prof), prev_coop(g_coop_attr) {
+  explicit ProfScope(dialsort_ctx c, const char* api = "dialsort") : prev(g_prof), prev_coop(g_coop_attr) {
     g_prof = c ? &c->prof : nullptr;
     g_coop_attr = c ? c->coop_attr : false;
+    nvtxRangePushA(api);
   }
   ~ProfScope() {
+    nvtxRangePop();
     g_prof = prev;
     g_coop_attr = prev_coop;
   }
@@ -1032,7 +1036,7 @@ int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, ui
                              dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
   if (!H) return fail(DIALSORT_E_INVALID_ARG, "H is NULL");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1049,7 +1053,7 @@ int dialsort_reconstruct_async(dialsort_ctx c, const uint32_t* H, uint32_t U, in
                                uint64_t cap, int exact, uint64_t* d_total, dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(out, cap))) return rc;
   if (!H) return fail(DIALSORT_E_INVALID_ARG, "H is NULL");
   if ((int64_t)key_base + (int64_t)U - 1 > 0x7fffffffll)
@@ -1066,7 +1070,7 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
                         dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(out, n))) return rc;
   if (n && out != keys && ranges_overlap(keys, 4 * n, out, 4 * n))
     return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
@@ -1093,7 +1097,7 @@ int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const 
                               int32_t* const* out, uint32_t* const* H_out, uint32_t nb, dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U))) return rc;
   if (nb && (!keys || !n || !out)) return fail(DIALSORT_E_INVALID_ARG, "NULL batch arrays");
   for (uint32_t j = 0; j < nb; ++j) {
@@ -1182,7 +1186,7 @@ int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const 
 int dialsort_sort_int32_async(dialsort_ctx c, const int32_t* keys, uint64_t n, int32_t* out, dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(out, n))) return rc;
   if (n && out != keys && ranges_overlap(keys, 4 * n, out, 4 * n))
     return fail(DIALSORT_E_INVALID_ARG, "out partially overlaps keys (only out == keys is allowed)");
@@ -1197,7 +1201,7 @@ int dialsort_sort_domain_async(dialsort_ctx c, const void* items, int item_bytes
                                const uint32_t* encode, const int32_t* decode, int32_t* out, dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(out, n))) return rc;
   if (item_bytes != 1 && item_bytes != 2 && item_bytes != 4) return fail(DIALSORT_E_INVALID_ARG, "item_bytes: 1, 2 or 4");
   if (n > 0xffffffffull) return fail(DIALSORT_E_INVALID_ARG, "n exceeds 2^32-1");
@@ -1221,7 +1225,7 @@ int dialsort_debug_radix_passes(dialsort_ctx c, const int32_t* keys, uint64_t n,
                                 dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(keys, n)) || (rc = check_keys_arg(pass_out, 4 * n))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
@@ -1233,7 +1237,7 @@ int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, ui
                                uint64_t* d_result, dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U))) return rc;
   if (!H || !d_result) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
   if (a > b || b >= U) return fail(DIALSORT_E_INVALID_ARG, "need 0 <= a <= b < U");
@@ -1250,7 +1254,7 @@ int dialsort_range_count_async(dialsort_ctx c, const uint32_t* H, uint32_t U, ui
 int dialsort_query_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int op, const uint32_t* q, uint64_t m,
                          uint64_t* d_out, dialsort_stream_t stream) {
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   int rc;
   if ((rc = check_U(U))) return rc;
   if (op != DIALSORT_Q_FREQUENCY && op != DIALSORT_Q_PRESENCE && op != DIALSORT_Q_RANGE_COUNT)
@@ -1279,7 +1283,7 @@ int dialsort_query_async(dialsort_ctx c, const uint32_t* H, uint32_t U, int op, 
 int dialsort_support_set_async(dialsort_ctx c, const uint32_t* H, uint32_t U, uint32_t* D_out, uint64_t* d_count,
                                uint32_t* d_iso, dialsort_stream_t stream) {
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   int rc;
   if ((rc = check_U(U))) return rc;
   if (!H || !D_out || !d_count) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
@@ -1374,7 +1378,7 @@ int dialsort_debug_phase_cta(dialsort_ctx c, uint64_t* out, int max_ctas) {
 int dialsort_crn_resolve_async(dialsort_ctx c, const int32_t* lane_keys, const uint32_t* active, uint64_t n_batches,
                                int32_t* out_keys, uint32_t* out_counts, dialsort_stream_t stream) {
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if (n_batches == 0) return DIALSORT_OK;
   if (!lane_keys || !active || !out_keys || !out_counts) return fail(DIALSORT_E_INVALID_ARG, "NULL pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1514,7 +1518,7 @@ int dialsort_sharded_histogram_scatter_async(dialsort_ctx c, dialsort_comm m, co
                                              uint32_t U, dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(keys, n))) return rc;
   if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1544,7 +1548,7 @@ int dialsort_sharded_histogram_gather_async(dialsort_ctx c, dialsort_comm m, uin
                                             dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U))) return rc;
   if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1562,7 +1566,7 @@ int dialsort_sharded_project_async(dialsort_ctx c, dialsort_comm m, uint32_t U, 
                                    uint64_t cap, uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_U(U)) || (rc = check_keys_arg(out, cap))) return rc;
   if (U % m->G != 0 || U / m->G > m->lay.Lmax) return fail(DIALSORT_E_INVALID_ARG, "need U % G == 0 and U / G <= max_U / G");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1591,7 +1595,7 @@ int dialsort_sharded_radix_hist_async(dialsort_ctx c, dialsort_comm m, const int
                                       dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(keys, n))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
@@ -1606,7 +1610,7 @@ int dialsort_sharded_radix_split_async(dialsort_ctx c, dialsort_comm m, const in
                                        uint64_t* d_count, uint64_t* d_offset, dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(keys, n))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
@@ -1625,7 +1629,7 @@ int dialsort_sharded_radix_local_async(dialsort_ctx c, dialsort_comm m, int32_t*
                                        dialsort_stream_t stream) {
   int rc;
   if ((rc = check_comm(c, m))) return rc;
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(out, cap))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
@@ -1716,7 +1720,7 @@ int dialsort_sort_host_async(dialsort_ctx c, const int32_t* keys_host, uint64_t 
                              dialsort_stream_t stream) {
   int rc;
   if (!c) return fail(DIALSORT_E_INVALID_ARG, "ctx is NULL");
-  ProfScope prof_scope_(c);
+  ProfScope prof_scope_(c, __func__);
   if ((rc = check_keys_arg(keys_host, n)) || (rc = check_keys_arg(out_host, n))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
