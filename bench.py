@@ -599,6 +599,7 @@ def main():
         "k_part_count": 4 * n_loc, "k_part_place": 6 * n_loc, "k_part_scan": 0,
         "k_part_place_est": 6 * n_loc, "k_part_sample": 0, "k_part_fin": 0,
         "k_part_place_ring": 6 * n_loc, "k_part_ring_compact": 0, "k_part_ring_move": 0,
+        "k_sort_small": 8 * n_loc + 8 * U,
         # two-kernel pipeline: fused ingest+merge+scan (keys read + H and P written), expand
         "k_hist_smem32": 4 * n_loc + 8 * U, "k_hist_smem16": 4 * n_loc + 8 * U, "k_hist_global": 4 * n_loc,
         "k_expand": 4 * (n_loc if G == 1 else n // G) + 4 * (U // G), "k_scan": 8 * max(U // G, 1),

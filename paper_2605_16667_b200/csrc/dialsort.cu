@@ -32,6 +32,7 @@
 #include "ds_query.cuh"
 #include "ds_radix.cuh"
 #include "ds_scan.cuh"
+#include "ds_small.cuh"
 
 using namespace ds;
 
@@ -57,14 +58,14 @@ enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
   KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
   KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
-  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_PART_RING, KID_PART_COMPACT, KID_PART_MOVE, KID_COUNT
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_PART_RING, KID_PART_COMPACT, KID_PART_MOVE, KID_SORT_SMALL, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {
     "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
     "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_place",
     "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
     "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch", "k_part_sample",
-    "k_part_place_est", "k_part_fin", "k_part_place_ring", "k_part_ring_compact", "k_part_ring_move"};
+    "k_part_place_est", "k_part_fin", "k_part_place_ring", "k_part_ring_compact", "k_part_ring_move", "k_sort_small"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -1085,6 +1086,16 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
   if (!H) {
     if ((rc = c->Hws.ensure(4ull * U))) return rc;
     H = c->Hws.as<uint32_t>();
+  }
+  // small inputs: the whole step on one thread-block cluster (ds_small.cuh)
+  static const bool small_on = [] {  // (DIALSORT_SMALL=0: the fused co-resident grid instead, A/B)
+    const char* e = getenv("DIALSORT_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  if (small_on && n <= kSmallMaxN && U <= kSmallMaxU && c->nsm >= (int)kSmallCS) {
+    DS_CUDA(launch_k(KID_SORT_SMALL, k_sort_small, dim3(kSmallCS), dim3(kSmallThreads), 0, s, keys, n, U, out, H_out,
+                     c->status.as<DevStatus>()));
+    return DIALSORT_OK;
   }
   const HistPath path = choose_path(U);
   if (path == HistPath::Smem32 || path == HistPath::Smem16) return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);

@@ -10,6 +10,7 @@ the oracle's H and output bit for bit.
   DIALSORT_BATCH_GROUPS=2  the batched sort on 2 CTA groups
   DIALSORT_NO_FIFO=1       no FIFO between co-resident launches (single stream)
   DIALSORT_NO_PDL=1        launches without programmatic dependent launch
+  DIALSORT_SMALL=0         small inputs on the fused co-resident grid instead of one cluster
 """
 import os
 import subprocess
@@ -30,7 +31,8 @@ import paper_2605_16667_b200 as ds
 dev = torch.device("cuda:0")
 c = ds.Context(0, max_n=3_000_000, max_U=1 << 22)
 cases = [(3_000_001, 1 << 20, "uniform"), (2_000_003, 1 << 20, "zipf"), (1_000_000, (1 << 22) - 3, "uniform"),
-         (1_000_001, 65536, "uniform"), (999_999, 300_000, "sorted"), (70_000, 1 << 20, "uniform")]
+         (1_000_001, 65536, "uniform"), (999_999, 300_000, "sorted"), (70_000, 1 << 20, "uniform"),
+         (100_000, 256, "uniform"), (99_999, 8192, "zipf"), (5_001, 1000, "sorted")]
 for n, U, dist in cases:
     x = synth.make(dist, n, U, 11)
     k = torch.from_numpy(x).to(dev)
@@ -59,6 +61,7 @@ print("ok")
     {"DIALSORT_FUSED_KPC": "32768"},
     {"DIALSORT_BATCH_GROUPS": "2"},
     {"DIALSORT_NO_FIFO": "1", "DIALSORT_NO_PDL": "1"},
+    {"DIALSORT_SMALL": "0"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_parity(cuda_dev, env):
     r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], env={**os.environ, **env},
