@@ -96,7 +96,8 @@ struct CoopFifo {
 CoopFifo g_fifo[32];
 thread_local bool g_coop_attr = false;  // set per API call from the context's option
 
-template <bool COOP = false, typename... KArgs, typename... Args>
+// CLUSTER > 0: the grid runs as clusters of CLUSTER CTAs (launch attribute; k_sort_small)
+template <bool COOP = false, int CLUSTER = 0, typename... KArgs, typename... Args>
 cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -110,8 +111,14 @@ cudaError_t launch_k(int kid, void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].val.programmaticStreamSerializationAllowed = pdl;
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
+  if (CLUSTER) {
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = CLUSTER;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = (COOP && g_coop_attr) ? 2 : 1;
+  cfg.numAttrs = ((COOP && g_coop_attr) || CLUSTER) ? 2 : 1;
   std::unique_lock<std::mutex> lk;
   CoopFifo* fifo = nullptr;
   static const bool no_fifo = [] {  // (DIALSORT_NO_FIFO=1: experiments only)
@@ -224,6 +231,7 @@ struct dialsort_ctx_s {
   int expand_occ = 4, scan_occ = 2, radix3_occ = 1, radix4_occ = 1;
   long long probe_violations = -1;   // radix lane-order probe of this device
   int radix_force = 0;               // 0: auto (pass4 iff the probe passed), 3 / 4 forced
+  bool small16 = false;              // 16-CTA clusters of k_sort_small<16> can be launched here
   bool coop_attr = false;            // DIALSORT_OPT_COOPERATIVE
   uint32_t max_ctas = 0;             // DIALSORT_OPT_MAX_CTAS (0: every SM)
   int part_mode = 0;                 // DIALSORT_OPT_PART_MODE
@@ -322,6 +330,24 @@ int ctx_init(dialsort_ctx c) {
                                (int)part_wide_smem(kPartMaxBlocksWide)));
   DS_CUDA(cudaFuncSetAttribute(k_part_place_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)part_ring_smem(kRpMaxB)));
+  {  // non-portable 16-CTA clusters for k_sort_small<16> (where the device schedules them)
+    c->small16 = false;
+    if (cudaFuncSetAttribute(k_sort_small<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(kSmallThreads);
+      cudaLaunchAttribute ca;
+      ca.id = cudaLaunchAttributeClusterDimension;
+      ca.val.clusterDim.x = 16;
+      ca.val.clusterDim.y = 1;
+      ca.val.clusterDim.z = 1;
+      q.attrs = &ca;
+      q.numAttrs = 1;
+      int nclu = 0;
+      c->small16 = cudaOccupancyMaxActiveClusters(&nclu, k_sort_small<16>, &q) == cudaSuccess && nclu > 0;
+    }
+    cudaGetLastError();
+  }
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowN4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   DS_CUDA(cudaFuncSetAttribute(k_sort_batch<kRowP16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
@@ -1092,9 +1118,14 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     const char* e = getenv("DIALSORT_SMALL");
     return !(e && e[0] == '0');
   }();
-  if (small_on && n <= kSmallMaxN && U <= kSmallMaxU && c->nsm >= (int)kSmallCS) {
-    DS_CUDA(launch_k(KID_SORT_SMALL, k_sort_small, dim3(kSmallCS), dim3(kSmallThreads), 0, s, keys, n, U, out, H_out,
-                     c->status.as<DevStatus>()));
+  if (small_on && U <= kSmallMaxU && n <= (c->small16 ? kSmall8MaxN : kSmall8OnlyMaxN) && c->nsm >= 8) {
+    DS_CUDA((launch_k<false, 8>(KID_SORT_SMALL, k_sort_small<8>, dim3(8), dim3(kSmallThreads), 0, s, keys, n, U, out,
+                                H_out, c->status.as<DevStatus>())));
+    return DIALSORT_OK;
+  }
+  if (small_on && U <= kSmallMaxU && n <= small16_max_n(U) && c->small16) {
+    DS_CUDA((launch_k<false, 16>(KID_SORT_SMALL, k_sort_small<16>, dim3(16), dim3(kSmallThreads), 0, s, keys, n, U,
+                                 out, H_out, c->status.as<DevStatus>())));
     return DIALSORT_OK;
   }
   const HistPath path = choose_path(U);

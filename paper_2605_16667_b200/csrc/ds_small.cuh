@@ -1,6 +1,6 @@
 // ds_small.cuh — the whole DialSort step for small inputs on one thread-block cluster.
 //
-// For n <= kSmallMaxN keys and U <= kSmallMaxU bins the co-resident grid of k_sort_fused
+// For small n (below) and U <= kSmallMaxU bins the co-resident grid of k_sort_fused
 // (up to 148 CTAs, global-memory grid barriers, owner counters in L2) is latency-bound: ~11 us
 // for c1 (n = 10^5, U = 256) even replayed from a CUDA graph.  Here kSmallCS CTAs of one
 // cluster run the three steps of the method with cluster barriers and distributed shared
@@ -21,18 +21,45 @@
 #include "ds_common.cuh"
 
 namespace ds {
-constexpr uint32_t kSmallCS = 8;            // CTAs of the cluster
 constexpr uint32_t kSmallThreads = 1024;
 constexpr uint32_t kSmallMaxU = 8192;       // 32 KB of uint32 counters a CTA
-constexpr uint32_t kSmallOwn = kSmallMaxU / kSmallCS;  // bins a CTA owns at most
-#ifndef DIALSORT_SMALL_MAX_N
-#define DIALSORT_SMALL_MAX_N 120000  // (crossover with k_sort_fused: n = 1e5 8.0 vs 11.5 us, 1.5e5 U = 1024 14.0 vs 12.4)
-#endif
-constexpr uint64_t kSmallMaxN = DIALSORT_SMALL_MAX_N;
+// Sizes (CUDA-graph device time a sort; k_sort_fused beside): 8-CTA clusters up to n = 5·10^4
+// (n = 10^4: 4.6 us, 16 CTAs 5.0, fused 12.6), 16-CTA clusters (non-portable, where the device
+// schedules them) above it up to 4·10^5 for U <= 1024 (n = 10^5: 6.1 vs 11.5; 2·10^5: 9.5 vs
+// 10.9; 4·10^5: 10.7 vs 13.5; 10^6: 16.4 vs 14.1) and 1.5·10^5 for larger U; else the fused grid.
+// Without 16-CTA clusters the 8-CTA path runs up to 1.2·10^5 (n = 10^5: 8.0 vs 11.5; 1.5·10^5,
+// U = 1024: 14.0 vs 12.4).
+constexpr uint64_t kSmall8MaxN = 50000, kSmall8OnlyMaxN = 120000;
+__host__ __device__ constexpr uint64_t small16_max_n(uint32_t U) { return U <= 1024 ? 400000 : 150000; }
 
-__global__ void __cluster_dims__(kSmallCS, 1, 1) __launch_bounds__(kSmallThreads, 1)
+// Positions [p0, p1) of an output whose bin k (of nb, prefix pr[0..nb], pr[nb] = total) holds
+// the key k0 + k, T positions apart per thread (a warp's stores coalesce): a thread's next
+// position is mostly still in its bin — one test, else a binary search of the bins above.
+// (4 consecutive positions a thread, one search each, measured slower: 27.7 vs 16.4 us at
+//  n = 10^6 — a warp's stores then spread over 512 bytes per instruction)
+__device__ __forceinline__ void project_positions(const uint32_t* pr, uint32_t nb, uint32_t p0, uint32_t p1,
+                                                  int32_t* o, uint32_t k0) {
+  uint32_t j = 0;  // invariant: pr[j] <= p
+  for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    if (pr[j + 1] <= p) {
+      uint32_t hi = nb;
+      while (hi - j > 1) {
+        const uint32_t mid = (j + hi) >> 1;
+        if (pr[mid] <= p) j = mid;
+        else hi = mid;
+      }
+    }
+    __stcs(o + p, (int32_t)(k0 + j));
+  }
+}
+
+// kSmallCS CTAs a cluster: 8 (portable) or 16 (non-portable, larger inputs); the cluster
+// dimension is a launch attribute.
+template <uint32_t kSmallCS>
+__global__ void __launch_bounds__(kSmallThreads, 1)
     k_sort_small(const int32_t* __restrict__ keys, uint64_t n, uint32_t U, int32_t* out, uint32_t* __restrict__ H,
                  DevStatus* st) {
+  constexpr uint32_t kSmallOwn = (kSmallMaxU + kSmallCS - 1) / kSmallCS;  // bins a CTA owns at most
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ uint32_t h[kSmallMaxU + 1];   // this CTA's histogram of its keys (then P, skewed inputs)
@@ -115,19 +142,7 @@ __global__ void __cluster_dims__(kSmallCS, 1, 1) __launch_bounds__(kSmallThreads
   const bool even = (uint64_t)mx * kSmallCS > 2ull * tot + 16384;
   if (!even) {
     cl.sync();  // (no CTA leaves while another still reads its shared memory)
-    uint32_t j = 0;  // invariant: pre[j] <= p  (a thread's next position, T further, is mostly
-                     // still in its bin: one test, else a binary search of the bins above)
-    for (uint32_t p = threadIdx.x; p < own_tot; p += T) {
-      if (pre[j + 1] <= p) {
-        uint32_t hi = nb;
-        while (hi - j > 1) {
-          const uint32_t mid = (j + hi) >> 1;
-          if (pre[mid] <= p) j = mid;
-          else hi = mid;
-        }
-      }
-      __stcs(out + base + p, (int32_t)(b0 + j));
-    }
+    project_positions(pre, nb, 0, own_tot, out + base, b0);
   } else {
     for (uint32_t k = threadIdx.x; k < U; k += T) {
       uint32_t q = (uint32_t)(((uint64_t)k * kSmallCS) / U);  // owner: own_lo(q) <= k < own_lo(q + 1)
@@ -139,18 +154,7 @@ __global__ void __cluster_dims__(kSmallCS, 1, 1) __launch_bounds__(kSmallThreads
     if (threadIdx.x == 0) h[U] = tot;
     cl.sync();  // (no CTA leaves while another still reads its shared memory; h complete)
     const uint32_t p0 = (uint32_t)((uint64_t)tot * r / kSmallCS), p1 = (uint32_t)((uint64_t)tot * (r + 1) / kSmallCS);
-    uint32_t j = 0;  // invariant: h[j] <= p
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += T) {
-      if (h[j + 1] <= p) {
-        uint32_t hi = U;
-        while (hi - j > 1) {
-          const uint32_t mid = (j + hi) >> 1;
-          if (h[mid] <= p) j = mid;
-          else hi = mid;
-        }
-      }
-      __stcs(out + p, (int32_t)j);
-    }
+    project_positions(h, U, p0, p1, out, 0u);
   }
   pdl_trigger();
 }
