@@ -1059,6 +1059,29 @@ int dialsort_sync(dialsort_ctx c, dialsort_stream_t stream, dialsort_error_info*
   return DIALSORT_OK;
 }
 
+// Small inputs on one thread-block cluster (k_sort_small, ds_small.cuh): 8 CTAs up to
+// kSmall8MaxN keys, 16 (if the device schedules them) up to small16_max_n(U); out == nullptr:
+// histogram only.  done = false: not a small input (nothing enqueued).
+int enqueue_small(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, int32_t* out, uint32_t* H,
+                  cudaStream_t s, bool& done) {
+  static const bool small_on = [] {  // (DIALSORT_SMALL=0: the fused co-resident grid instead, A/B)
+    const char* e = getenv("DIALSORT_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  done = false;
+  if (!small_on || U > kSmallMaxU || c->nsm < 16) return DIALSORT_OK;
+  if (n <= (c->small16 ? kSmall8MaxN : kSmall8OnlyMaxN)) {
+    DS_CUDA((launch_k<false, 8>(KID_SORT_SMALL, k_sort_small<8>, dim3(8), dim3(kSmallThreads), 0, s, keys, n, U, out,
+                                H, c->status.as<DevStatus>())));
+    done = true;
+  } else if (c->small16 && n <= small16_max_n(U)) {
+    DS_CUDA((launch_k<false, 16>(KID_SORT_SMALL, k_sort_small<16>, dim3(16), dim3(kSmallThreads), 0, s, keys, n, U,
+                                 out, H, c->status.as<DevStatus>())));
+    done = true;
+  }
+  return DIALSORT_OK;
+}
+
 int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_t U, uint32_t* H,
                              dialsort_stream_t stream) {
   int rc;
@@ -1073,6 +1096,8 @@ int dialsort_histogram_async(dialsort_ctx c, const int32_t* keys, uint64_t n, ui
     DS_CUDA(launch_k(KID_ZERO, k_zero, dim3(c->nsm), dim3(256), 0, s, H, (uint64_t)U));
     return DIALSORT_OK;
   }
+  bool done = false;
+  if ((rc = enqueue_small(c, keys, n, U, nullptr, H, s, done)) || done) return rc;
   return enqueue_hist_scan(c, keys, n, U, H, false, 0, epoch, s);
 }
 
@@ -1114,20 +1139,8 @@ int dialsort_sort_async(dialsort_ctx c, const int32_t* keys, uint64_t n, uint32_
     H = c->Hws.as<uint32_t>();
   }
   // small inputs: the whole step on one thread-block cluster (ds_small.cuh)
-  static const bool small_on = [] {  // (DIALSORT_SMALL=0: the fused co-resident grid instead, A/B)
-    const char* e = getenv("DIALSORT_SMALL");
-    return !(e && e[0] == '0');
-  }();
-  if (small_on && U <= kSmallMaxU && n <= (c->small16 ? kSmall8MaxN : kSmall8OnlyMaxN) && c->nsm >= 8) {
-    DS_CUDA((launch_k<false, 8>(KID_SORT_SMALL, k_sort_small<8>, dim3(8), dim3(kSmallThreads), 0, s, keys, n, U, out,
-                                H_out, c->status.as<DevStatus>())));
-    return DIALSORT_OK;
-  }
-  if (small_on && U <= kSmallMaxU && n <= small16_max_n(U) && c->small16) {
-    DS_CUDA((launch_k<false, 16>(KID_SORT_SMALL, k_sort_small<16>, dim3(16), dim3(kSmallThreads), 0, s, keys, n, U,
-                                 out, H_out, c->status.as<DevStatus>())));
-    return DIALSORT_OK;
-  }
+  bool done = false;
+  if ((rc = enqueue_small(c, keys, n, U, out, H_out, s, done)) || done) return rc;
   const HistPath path = choose_path(U);
   if (path == HistPath::Smem32 || path == HistPath::Smem16) return enqueue_sort_fused(c, keys, n, U, H, out, epoch, s);
   if (path == HistPath::Hier) return enqueue_hier(c, keys, n, U, H, out, s);

@@ -14,7 +14,8 @@
 //   projection  eq:projection: out[P[k] .. P[k] + H[k]) = k by output position;
 //               owners write their bins, or — skewed inputs — every CTA an even share
 // Keys outside [0, U) are recorded (count, minimum index) and not counted; out may be keys
-// (in place: the projection starts after the cluster barrier that follows the ingestion).
+// (in place: the projection starts after the cluster barrier that follows the ingestion);
+// out == nullptr: histogram only (H).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -139,6 +140,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   // own bins' positions; when one owner holds much more than its share (skewed keys) every
   // CTA takes an even share of the positions instead, searching the whole prefix P (gathered
   // from the owners' prefixes into h).  The choice is the same on every CTA.
+  if (!out) {  // (histogram only)
+    cl.sync();  // (no CTA leaves while another still reads its shared memory)
+    pdl_trigger();
+    return;
+  }
   const bool even = (uint64_t)mx * kSmallCS > 2ull * tot + 16384;
   if (!even) {
     cl.sync();  // (no CTA leaves while another still reads its shared memory)
