@@ -140,14 +140,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   // own bins' positions; when one owner holds much more than its share (skewed keys) every
   // CTA takes an even share of the positions instead, searching the whole prefix P (gathered
   // from the owners' prefixes into h).  The choice is the same on every CTA.
+  // (the last cluster barrier only keeps this CTA's shared memory alive while the others read
+  //  it: arrived here, waited for at the end, so the projection runs in between)
   if (!out) {  // (histogram only)
-    cl.sync();  // (no CTA leaves while another still reads its shared memory)
+    cl.sync();
     pdl_trigger();
     return;
   }
   const bool even = (uint64_t)mx * kSmallCS > 2ull * tot + 16384;
   if (!even) {
-    cl.sync();  // (no CTA leaves while another still reads its shared memory)
+    cl.barrier_arrive();
     project_positions(pre, nb, 0, own_tot, out + base, b0);
   } else {
     for (uint32_t k = threadIdx.x; k < U; k += T) {
@@ -158,10 +160,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       h[k] = bq + cl.map_shared_rank(pre, q)[k - own_lo(q)];
     }
     if (threadIdx.x == 0) h[U] = tot;
-    cl.sync();  // (no CTA leaves while another still reads its shared memory; h complete)
+    cl.barrier_arrive();
+    __syncthreads();  // (h complete)
     const uint32_t p0 = (uint32_t)((uint64_t)tot * r / kSmallCS), p1 = (uint32_t)((uint64_t)tot * (r + 1) / kSmallCS);
     project_positions(h, U, p0, p1, out, 0u);
   }
+  cl.barrier_wait();
   pdl_trigger();
 }
 }  // namespace ds
