@@ -58,14 +58,14 @@ enum KernelId {
   KID_ZERO = 0, KID_HIST_SMEM32, KID_HIST_SMEM16, KID_HIST_GLOBAL, KID_SCAN, KID_EXPAND, KID_RADIX_PASS,
   KID_RANGE_COUNT, KID_CRN, KID_SORT_FUSED, KID_PART_COUNT, KID_PART_SCAN, KID_PART_SCATTER, KID_PUSH_SLICES,
   KID_SLICE_SUM, KID_COMM_SIGNAL, KID_COMM_SLICE_SUM, KID_COMM_OFFSETS, KID_COMM_RHIST, KID_COMM_RPLAN,
-  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_PART_RING, KID_PART_COMPACT, KID_PART_MOVE, KID_SORT_SMALL, KID_COUNT
+  KID_COMM_RSPLIT, KID_COMM_WAIT, KID_RADIX_PROBE, KID_QUERY, KID_SORT_BATCH, KID_PART_SAMPLE, KID_PART_SCATTER_EST, KID_PART_FIN, KID_PART_RING, KID_PART_COMPACT, KID_PART_MOVE, KID_SORT_SMALL, KID_SORT_SMALL_BATCH, KID_COUNT
 };
 const char* const kKernelNames[KID_COUNT] = {
     "k_zero", "k_hist_smem32", "k_hist_smem16", "k_hist_global", "k_scan", "k_expand", "k_radix_pass",
     "k_range_count", "k_crn_resolve", "k_sort_fused", "k_part_count", "k_part_scan", "k_part_place",
     "k_push_slices", "k_slice_sum", "k_comm_signal", "k_comm_slice_sum", "k_comm_offsets", "k_comm_rhist",
     "k_comm_rplan", "k_comm_rsplit", "k_comm_wait", "k_radix_lane_probe", "k_query", "k_sort_batch", "k_part_sample",
-    "k_part_place_est", "k_part_fin", "k_part_place_ring", "k_part_ring_compact", "k_part_ring_move", "k_sort_small"};
+    "k_part_place_est", "k_part_fin", "k_part_place_ring", "k_part_ring_compact", "k_part_ring_move", "k_sort_small", "k_sort_small_batch"};
 
 // Per-context launch profiler (off by default): an event pair around each launch.
 struct Profiler {
@@ -332,7 +332,8 @@ int ctx_init(dialsort_ctx c) {
                                (int)part_ring_smem(kRpMaxB)));
   {  // non-portable 16-CTA clusters for k_sort_small<16> (where the device schedules them)
     c->small16 = false;
-    if (cudaFuncSetAttribute(k_sort_small<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    if (cudaFuncSetAttribute(k_sort_small<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(k_sort_small_batch<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(16);
       q.blockDim = dim3(kSmallThreads);
@@ -1162,6 +1163,36 @@ int dialsort_sort_batch_async(dialsort_ctx c, const int32_t* const* keys, const 
   }
   cudaStream_t s = (cudaStream_t)stream;
   DS_CUDA(cudaSetDevice(c->device));
+  {  // small batches: one thread-block cluster per batch, all in one launch (ds_small.cuh)
+    static const bool small_on = [] {
+      const char* e = getenv("DIALSORT_SMALL");
+      return !(e && e[0] == '0');
+    }();
+    uint64_t nmax = 0, nmin = ~0ull;
+    for (uint32_t j = 0; j < nb; ++j) nmax = std::max(nmax, n[j]), nmin = std::min(nmin, n[j]);
+    const bool use16 = c->small16 && nmax > kSmallBatch8MaxN;
+    if (small_on && nb > 1 && nmin > 0 && U <= kSmallMaxU && c->nsm >= 16 &&
+        nmax <= (c->small16 ? small16_max_n(U) : kSmallBatch8MaxN)) {
+      for (uint32_t j0 = 0; j0 < nb; j0 += kSmallBatchMax) {
+        const uint32_t m = std::min<uint32_t>(kSmallBatchMax, nb - j0);
+        SmallBatch B;
+        memset(&B, 0, sizeof B);
+        for (uint32_t j = 0; j < m; ++j) {
+          B.keys[j] = keys[j0 + j];
+          B.out[j] = out[j0 + j];
+          B.H[j] = H_out ? H_out[j0 + j] : nullptr;
+          B.n[j] = n[j0 + j];
+        }
+        if (use16)
+          DS_CUDA((launch_k<false, 16>(KID_SORT_SMALL_BATCH, k_sort_small_batch<16>, dim3(16 * m), dim3(kSmallThreads),
+                                       0, s, B, U, c->status.as<DevStatus>())));
+        else
+          DS_CUDA((launch_k<false, 8>(KID_SORT_SMALL_BATCH, k_sort_small_batch<8>, dim3(8 * m), dim3(kSmallThreads), 0,
+                                      s, B, U, c->status.as<DevStatus>())));
+      }
+      return DIALSORT_OK;
+    }
+  }
   const HistPath path = choose_path(U);
   static const uint32_t kGroups = [] {  // CTA groups per launch (DIALSORT_BATCH_GROUPS: experiments)
     const char* e = getenv("DIALSORT_BATCH_GROUPS");

@@ -31,6 +31,10 @@ constexpr uint32_t kSmallMaxU = 8192;       // 32 KB of uint32 counters a CTA
 // Without 16-CTA clusters the 8-CTA path runs up to 1.2·10^5 (n = 10^5: 8.0 vs 11.5; 1.5·10^5,
 // U = 1024: 14.0 vs 12.4).
 constexpr uint64_t kSmall8MaxN = 50000, kSmall8OnlyMaxN = 120000;
+#ifndef DIALSORT_SMALL_BATCH8_MAX_N
+#define DIALSORT_SMALL_BATCH8_MAX_N 120000
+#endif
+constexpr uint64_t kSmallBatch8MaxN = DIALSORT_SMALL_BATCH8_MAX_N;  // batches: 8-CTA clusters up to here
 __host__ __device__ constexpr uint64_t small16_max_n(uint32_t U) { return U <= 1024 ? 400000 : 150000; }
 
 // Positions [p0, p1) of an output whose bin k (of nb, prefix pr[0..nb], pr[nb] = total) holds
@@ -57,9 +61,8 @@ __device__ __forceinline__ void project_positions(const uint32_t* pr, uint32_t n
 // kSmallCS CTAs a cluster: 8 (portable) or 16 (non-portable, larger inputs); the cluster
 // dimension is a launch attribute.
 template <uint32_t kSmallCS>
-__global__ void __launch_bounds__(kSmallThreads, 1)
-    k_sort_small(const int32_t* __restrict__ keys, uint64_t n, uint32_t U, int32_t* out, uint32_t* __restrict__ H,
-                 DevStatus* st) {
+__device__ __forceinline__ void small_step(const int32_t* __restrict__ keys, uint64_t n, uint32_t U, int32_t* out,
+                                           uint32_t* __restrict__ H, DevStatus* st) {
   constexpr uint32_t kSmallOwn = (kSmallMaxU + kSmallCS - 1) / kSmallCS;  // bins a CTA owns at most
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -67,7 +70,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   __shared__ uint32_t pre[kSmallOwn + 1];  // exclusive prefix of the owned bins' totals (+ their total)
   __shared__ uint32_t red[34];
   __shared__ uint32_t s_sum, s_all[kSmallCS];  // owned total; every owner's total
-  pdl_wait();
   const uint32_t r = cl.block_rank(), T = blockDim.x;
   for (uint32_t i = threadIdx.x; i < U; i += T) h[i] = 0;
   __syncthreads();
@@ -144,7 +146,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   //  it: arrived here, waited for at the end, so the projection runs in between)
   if (!out) {  // (histogram only)
     cl.sync();
-    pdl_trigger();
     return;
   }
   const bool even = (uint64_t)mx * kSmallCS > 2ull * tot + 16384;
@@ -166,6 +167,33 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     project_positions(h, U, p0, p1, out, 0u);
   }
   cl.barrier_wait();
+}
+
+template <uint32_t kSmallCS>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_sort_small(const int32_t* __restrict__ keys, uint64_t n, uint32_t U, int32_t* out, uint32_t* __restrict__ H,
+                 DevStatus* st) {
+  pdl_wait();
+  small_step<kSmallCS>(keys, n, U, out, H, st);
+  pdl_trigger();
+}
+
+// Independent small sorts (dialsort_sort_batch_async): cluster j of the grid sorts batch j; the
+// hardware runs as many clusters at once as the SMs hold (9 of 16 CTAs, 18 of 8) and starts the
+// next ones as they finish.
+constexpr uint32_t kSmallBatchMax = 64;
+struct SmallBatch {
+  const int32_t* keys[kSmallBatchMax];
+  int32_t* out[kSmallBatchMax];
+  uint32_t* H[kSmallBatchMax];
+  uint64_t n[kSmallBatchMax];
+};
+template <uint32_t kSmallCS>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_sort_small_batch(const __grid_constant__ SmallBatch B, uint32_t U,
+                                                                       DevStatus* st) {
+  pdl_wait();
+  const uint32_t j = blockIdx.x / kSmallCS;
+  small_step<kSmallCS>(B.keys[j], B.n[j], U, B.out[j], B.H[j], st);
   pdl_trigger();
 }
 }  // namespace ds

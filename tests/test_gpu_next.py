@@ -253,6 +253,34 @@ def test_sort_batch_vs_oracle(ds, cuda_dev, U, nb):
             assert np.array_equal(outs[j].cpu().numpy(), oracle.project(Hr)), (call, j)
 
 
+@pytest.mark.parametrize("U,nb,lo,hi", [(256, 2, 1, 5000), (256, 9, 10_000, 120_000), (8192, 64, 1, 60_000),
+                                          (7, 70, 100, 30_000), (1024, 12, 120_001, 400_000),
+                                          (8192, 5, 60_000, 150_000)])
+def test_sort_batch_small_clusters(ds, cuda_dev, U, nb, lo, hi):
+    """Batches of small sorts (U <= 8192, n <= 4e5): one thread-block cluster per batch in one
+    launch (k_sort_small_batch — 8-CTA clusters up to 120000 keys, 16-CTA above; more than 64
+    batches in several launches): ragged sizes, uniform / Zipf / one key / sorted, some in place,
+    every batch's H and output vs the oracle."""
+    c = ds.Context(0, max_n=hi, max_U=U)
+    rng = np.random.default_rng(U * nb + lo)
+    xs = []
+    for j in range(nb):
+        n = int(rng.integers(lo, hi + 1))
+        kind = j % 4
+        x = (synth.uniform(n, U, seed=j) if kind == 0 else synth.zipf(n, U, seed=j) if kind == 1 else
+             np.full(n, (j * 31) % U, dtype=np.int32) if kind == 2 else synth.make("sorted", n, U, seed=j))
+        xs.append(x)
+    ks = [to_dev(x) for x in xs]
+    outs = [k if j % 3 == 2 else torch.empty_like(k) for j, k in enumerate(ks)]
+    Hs = [torch.empty(U, dtype=torch.int32, device=cuda_dev) for _ in range(nb)]
+    c.sort_batch(ks, U, outs, Hs)
+    c.sync()
+    for j in range(nb):
+        Hr = oracle.histogram(xs[j], U)
+        assert np.array_equal(Hs[j].cpu().numpy().view(np.uint32).astype(np.uint64), Hr), j
+        assert np.array_equal(outs[j].cpu().numpy(), oracle.project(Hr)), j
+
+
 def test_sort_batch_range_error(ds, cuda_dev):
     """A bad key in one batch of a batched launch is reported by dialsort_sync of the context."""
     c = ds.Context(0)
